@@ -1,0 +1,45 @@
+// Internal (non-ABI) interfaces shared by the translation units of
+// libvabft_b200.so.
+#pragma once
+
+#include <cstdint>
+#include <stdexcept>
+#include <string>
+
+#include <cuda_runtime.h>
+
+#include "vabft_c.h"
+
+namespace vabft_dev {
+
+// Exception carrying a vabft_status; converted at the C-ABI boundary.
+struct Error : std::runtime_error {
+    vabft_status status;
+    Error(vabft_status s, const std::string& msg) : std::runtime_error(msg), status(s) {}
+};
+
+[[noreturn]] inline void fail(vabft_status s, const std::string& msg) { throw Error(s, msg); }
+
+inline void check_cuda(cudaError_t e, const char* what) {
+    if (e != cudaSuccess)
+        fail(VABFT_CUDA_ERROR, std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+int sm_count();
+size_t elem_size(int fmt);
+
+// ---- tcgen05 GEMM (tc_gemm.cu)
+struct TcEpilogue {
+    int abft = 0;             // 0 none, 1 online (FP32 accum), 2 offline (quantized C)
+    float* part1 = nullptr;   // [ceil(N/128)][M] row partials of C r1
+    float* part2 = nullptr;   // [ceil(N/128)][M] row partials of C r2
+    const int32_t* fault_col = nullptr;
+    const int32_t* fault_bit = nullptr;
+    const int32_t* fault_dir = nullptr;
+    vabft_fault_record* fault_records = nullptr;
+};
+void tc_gemm_launch(int fmt, bool b_kmajor, int64_t M, int64_t N, int64_t K, const void* A,
+                    const void* B, void* C, const TcEpilogue& epi, cudaStream_t stream);
+bool tc_gemm_supported(int fmt, int64_t M, int64_t N, int64_t K);
+
+}  // namespace vabft_dev

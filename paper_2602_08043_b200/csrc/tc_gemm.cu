@@ -1,0 +1,397 @@
+// tcgen05 fused ABFT-GEMM for BF16/FP16 inputs with FP32 accumulation in
+// TMEM — the B200 replacement of gemm_emulated_with_accum's 16-bit path
+// (proj/src/precision.cpp:238-338) plus the epilogue half of row_sums
+// (proj/src/checksum.cpp:160-187) and the accumulator/output fault injector
+// (proj/src/faults.cpp:104-168).
+//
+// Structure (one CTA per SM, persistent over 128 x 256 output tiles):
+//   warp 0      TMA producer: A tile 128x64 (K-major, SW128) and B tile
+//               64x256 (N-major 4 x [64k x 64n] boxes, or K-major 256x64)
+//               into a 4-stage smem ring guarded by full/empty mbarriers.
+//   warp 1      TMEM allocator (512 cols = 2 accumulators of 256 FP32 cols)
+//               and single-thread tcgen05.mma issuer (M=128, N=256, K=16).
+//   warps 2..5  epilogue: tcgen05.ld 32x32b -> registers; saturate; optional
+//               bit-flip injection; quantize (RNE, satfinite); store C; row
+//               partials r1 = sum_j v, r2 = sum_j (j+1) v in FP32, one
+//               partial per 128-column block (the reference's blocked:128
+//               reduction order), written as [block][M] for the verify tail.
+#include <cuda.h>
+#include <cuda_bf16.h>
+#include <cuda_fp16.h>
+#include <cudaTypedefs.h>
+
+#include <mutex>
+
+#include "internal.hpp"
+#include "numerics.cuh"
+#include "ptx.cuh"
+
+namespace vabft_dev {
+
+namespace {
+
+constexpr int kBM = 128;
+constexpr int kBN = 256;
+constexpr int kBK = 64;
+constexpr int kStages = 4;
+constexpr int kThreads = 192;
+constexpr uint32_t kABytes = kBM * kBK * 2;  // 16 KiB
+constexpr uint32_t kBBytes = kBN * kBK * 2;  // 32 KiB
+constexpr uint32_t kStageBytes = kABytes + kBBytes;
+constexpr uint32_t kTmemCols = 512;
+constexpr size_t kSmemBytes = size_t(kStages) * kStageBytes + 1024 /*align*/ + 256 /*barriers*/;
+
+struct TcParams {
+    int M, N, K;
+    int num_m_blk, num_n_blk, num_k_blk, num_tiles;
+    uint16_t* C;
+    TcEpilogue epi;
+};
+
+template <int kFmt, bool kBKMajor, int kAbft, bool kInject>
+__global__ void __launch_bounds__(kThreads, 1)
+    tc_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                   const TcParams p) {
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                               ~uintptr_t(1023));
+    uint8_t* smA = smem;
+    uint8_t* smB = smem + kStages * kABytes;
+    uint64_t* bars = reinterpret_cast<uint64_t*>(smem + kStages * kStageBytes);
+    uint64_t* full_bar = bars;
+    uint64_t* empty_bar = bars + kStages;
+    uint64_t* tfull_bar = bars + 2 * kStages;
+    uint64_t* tempty_bar = bars + 2 * kStages + 2;
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * kStages + 4);
+
+    const int warp = threadIdx.x >> 5;
+    const int lane = threadIdx.x & 31;
+
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < kStages; ++s) {
+            mbar_init(smem_u32(&full_bar[s]), 1);
+            mbar_init(smem_u32(&empty_bar[s]), 1);
+        }
+        for (int a = 0; a < 2; ++a) {
+            mbar_init(smem_u32(&tfull_bar[a]), 1);
+            mbar_init(smem_u32(&tempty_bar[a]), 4);
+        }
+        fence_mbar_init();
+        tma_prefetch_desc(&tmA);
+        tma_prefetch_desc(&tmB);
+    }
+    if (warp == 1) tmem_alloc(smem_u32(tmem_slot), kTmemCols);
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem_base = *tmem_slot;
+
+    if (warp == 0) {
+        if (lane == 0) {
+            // ------------------------------------------------ TMA producer
+            int stage = 0;
+            uint32_t phase = 0;
+            for (int tile = blockIdx.x; tile < p.num_tiles; tile += gridDim.x) {
+                const int m_blk = tile % p.num_m_blk;
+                const int n_blk = tile / p.num_m_blk;
+                for (int kb = 0; kb < p.num_k_blk; ++kb) {
+                    mbar_wait(smem_u32(&empty_bar[stage]), phase ^ 1);
+                    const uint32_t fb = smem_u32(&full_bar[stage]);
+                    mbar_arrive_expect_tx(fb, kStageBytes);
+                    tma_load_2d(smem_u32(smA + stage * kABytes), &tmA, fb, kb * kBK, m_blk * kBM);
+                    const uint32_t bdst = smem_u32(smB + stage * kBBytes);
+                    if constexpr (kBKMajor) {
+                        tma_load_2d(bdst, &tmB, fb, kb * kBK, n_blk * kBN);
+                    } else {
+#pragma unroll
+                        for (int c = 0; c < kBN / 64; ++c)
+                            tma_load_2d(bdst + c * 8192, &tmB, fb, n_blk * kBN + c * 64, kb * kBK);
+                    }
+                    if (++stage == kStages) {
+                        stage = 0;
+                        phase ^= 1;
+                    }
+                }
+            }
+        }
+    } else if (warp == 1) {
+        if (lane == 0) {
+            // --------------------------------------------------- MMA issuer
+            constexpr uint32_t idesc =
+                umma_idesc_f16(kFmt == VABFT_BF16 ? 1u : 0u, !kBKMajor, kBM, kBN);
+            int stage = 0;
+            uint32_t phase = 0;
+            int acc = 0;
+            uint32_t acc_phase = 0;
+            for (int tile = blockIdx.x; tile < p.num_tiles; tile += gridDim.x) {
+                mbar_wait(smem_u32(&tempty_bar[acc]), acc_phase ^ 1);
+                tc_fence_after();
+                const uint32_t d_tmem = tmem_base + uint32_t(acc * kBN);
+                for (int kb = 0; kb < p.num_k_blk; ++kb) {
+                    mbar_wait(smem_u32(&full_bar[stage]), phase);
+                    tc_fence_after();
+                    const uint64_t adesc = umma_desc_sw128(smem_u32(smA + stage * kABytes), 16, 1024);
+                    const uint64_t bdesc =
+                        kBKMajor ? umma_desc_sw128(smem_u32(smB + stage * kBBytes), 16, 1024)
+                                 : umma_desc_sw128(smem_u32(smB + stage * kBBytes), 8192, 1024);
+#pragma unroll
+                    for (int k = 0; k < kBK / 16; ++k) {
+                        // K-major: +32 bytes per 16 elements inside the 128B swizzle row.
+                        // N-major: +16 k-rows = 2 swizzle atoms = 2048 bytes.
+                        const uint64_t a_off = uint64_t((k * 32) >> 4);
+                        const uint64_t b_off = kBKMajor ? uint64_t((k * 32) >> 4) : uint64_t((k * 2048) >> 4);
+                        umma_f16(d_tmem, adesc + a_off, bdesc + b_off, idesc,
+                                 (kb > 0 || k > 0) ? 1u : 0u);
+                    }
+                    umma_commit(smem_u32(&empty_bar[stage]));
+                    if (++stage == kStages) {
+                        stage = 0;
+                        phase ^= 1;
+                    }
+                }
+                umma_commit(smem_u32(&tfull_bar[acc]));
+                if (++acc == 2) {
+                    acc = 0;
+                    acc_phase ^= 1;
+                }
+            }
+        }
+    } else {
+        // ------------------------------------------------------- epilogue
+        const int quad = warp & 3;  // TMEM lanes [32*quad, 32*quad+32) are addressable by this warp
+        const int row_in_tile = quad * 32 + lane;
+        int acc = 0;
+        uint32_t acc_phase = 0;
+        for (int tile = blockIdx.x; tile < p.num_tiles; tile += gridDim.x) {
+            const int m_blk = tile % p.num_m_blk;
+            const int n_blk = tile / p.num_m_blk;
+            const int row = m_blk * kBM + row_in_tile;
+            const bool row_ok = row < p.M;
+            const int n0 = n_blk * kBN;
+
+            int fcol = -1, fbit = 0, fdir = 0;
+            if constexpr (kInject) {
+                if (row_ok) {
+                    fcol = p.epi.fault_col[row];
+                    if (fcol >= n0 && fcol < n0 + kBN) {
+                        fbit = p.epi.fault_bit[row];
+                        fdir = p.epi.fault_dir[row];
+                    } else {
+                        fcol = -1;
+                    }
+                }
+            }
+
+            mbar_wait(smem_u32(&tfull_bar[acc]), acc_phase);
+            tc_fence_after();
+
+            float s1 = 0.0f, s2 = 0.0f;
+#pragma unroll 1
+            for (int c = 0; c < kBN; c += 32) {
+                uint32_t v[32];
+                tmem_ld32(tmem_base + (uint32_t(quad * 32) << 16) + uint32_t(acc * kBN + c), v);
+                tmem_wait_ld();
+                uint32_t packed[16];
+#pragma unroll
+                for (int e = 0; e < 32; ++e) {
+                    const int col = n0 + c + e;
+                    float x = saturate_accum<kFmt>(__uint_as_float(v[e]));
+                    uint16_t q;
+                    if constexpr (kAbft == 2) {
+                        q = quantize16_bits<kFmt>(x);
+                        if constexpr (kInject) {
+                            if (col == fcol) {
+                                const bool ok = bit_eligible(q, fbit, fdir);
+                                const uint16_t q2 = ok ? uint16_t(q ^ (1u << fbit)) : q;
+                                if (p.epi.fault_records) {
+                                    vabft_fault_record r;
+                                    r.value_before = double(bits16_to_float<kFmt>(q));
+                                    r.value_after = double(bits16_to_float<kFmt>(q2));
+                                    r.applied = ok ? 1 : 0;
+                                    r.reserved = 0;
+                                    p.epi.fault_records[row] = r;
+                                }
+                                q = q2;
+                            }
+                        }
+                        const float f = bits16_to_float<kFmt>(q);
+                        if (col < p.N) {
+                            s1 = __fadd_rn(s1, f);
+                            s2 = __fadd_rn(s2, __fmul_rn(float(col + 1), f));
+                        }
+                    } else {
+                        if constexpr (kAbft == 1 && kInject) {
+                            if (col == fcol) {
+                                const uint32_t b = __float_as_uint(x);
+                                const bool ok = bit_eligible(b, fbit, fdir);
+                                const uint32_t b2 = ok ? (b ^ (1u << fbit)) : b;
+                                if (p.epi.fault_records) {
+                                    vabft_fault_record r;
+                                    r.value_before = double(x);
+                                    r.value_after = double(__uint_as_float(b2));
+                                    r.applied = ok ? 1 : 0;
+                                    r.reserved = 0;
+                                    p.epi.fault_records[row] = r;
+                                }
+                                x = __uint_as_float(b2);
+                            }
+                        }
+                        if constexpr (kAbft == 1) {
+                            if (col < p.N) {
+                                s1 = __fadd_rn(s1, x);
+                                s2 = __fadd_rn(s2, __fmul_rn(float(col + 1), x));
+                            }
+                        }
+                        q = quantize16_bits<kFmt>(x);
+                    }
+                    if (e & 1)
+                        packed[e >> 1] |= uint32_t(q) << 16;
+                    else
+                        packed[e >> 1] = uint32_t(q);
+                }
+                if (row_ok) {
+                    uint16_t* dst = p.C + size_t(row) * p.N + n0 + c;
+#pragma unroll
+                    for (int g = 0; g < 4; ++g) {
+                        if (n0 + c + g * 8 + 8 <= p.N) {
+                            uint4 w = make_uint4(packed[4 * g], packed[4 * g + 1], packed[4 * g + 2],
+                                                 packed[4 * g + 3]);
+                            *reinterpret_cast<uint4*>(dst + g * 8) = w;
+                        }
+                    }
+                }
+                if constexpr (kAbft != 0) {
+                    if ((c + 32) % 128 == 0) {
+                        const int blk = (n0 + c) / 128;
+                        if (row_ok && blk * 128 < p.N) {
+                            p.epi.part1[size_t(blk) * p.M + row] = s1;
+                            p.epi.part2[size_t(blk) * p.M + row] = s2;
+                        }
+                        s1 = 0.0f;
+                        s2 = 0.0f;
+                    }
+                }
+            }
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(smem_u32(&tempty_bar[acc]));
+            if (++acc == 2) {
+                acc = 0;
+                acc_phase ^= 1;
+            }
+        }
+    }
+
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 1) {
+        __syncwarp();
+        tc_fence_after();
+        tmem_dealloc(tmem_base, kTmemCols);
+    }
+}
+
+// ---------------------------------------------------------- host helpers
+PFN_cuTensorMapEncodeTiled_v12000 get_encode_fn() {
+    static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+    static std::once_flag once;
+    std::call_once(once, [] {
+        void* ptr = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &ptr, cudaEnableDefault, &q) ==
+                cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(ptr);
+    });
+    if (!fn) fail(VABFT_CUDA_ERROR, "cuTensorMapEncodeTiled unavailable");
+    return fn;
+}
+
+// 2D row-major tensor [rows][cols] of 16-bit elements, box {box_cols, box_rows}.
+CUtensorMap make_map_2d(int fmt, const void* base, uint64_t rows, uint64_t cols, uint32_t box_cols,
+                        uint32_t box_rows) {
+    CUtensorMap m;
+    cuuint64_t dims[2] = {cols, rows};
+    cuuint64_t strides[1] = {cols * 2};
+    cuuint32_t box[2] = {box_cols, box_rows};
+    cuuint32_t estr[2] = {1, 1};
+    const CUtensorMapDataType dt =
+        fmt == VABFT_BF16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT16;
+    CUresult r = get_encode_fn()(&m, dt, 2, const_cast<void*>(base), dims, strides, box, estr,
+                                 CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                                 CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                                 CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) fail(VABFT_CUDA_ERROR, "cuTensorMapEncodeTiled failed");
+    return m;
+}
+
+template <int kFmt, bool kBKMajor, int kAbft, bool kInject>
+void launch_inst(const CUtensorMap& ta, const CUtensorMap& tb, const TcParams& p,
+                 cudaStream_t stream) {
+    auto kern = tc_gemm_kernel<kFmt, kBKMajor, kAbft, kInject>;
+    static bool attr_set = false;  // per instantiation
+    if (!attr_set) {
+        check_cuda(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                        int(kSmemBytes)),
+                   "cudaFuncSetAttribute(tc_gemm)");
+        attr_set = true;
+    }
+    const int grid = p.num_tiles < sm_count() ? p.num_tiles : sm_count();
+    kern<<<grid, kThreads, kSmemBytes, stream>>>(ta, tb, p);
+    check_cuda(cudaGetLastError(), "tc_gemm launch");
+}
+
+template <int kFmt, bool kBKMajor>
+void dispatch_epi(const CUtensorMap& ta, const CUtensorMap& tb, const TcParams& p,
+                  cudaStream_t stream) {
+    const bool inj = p.epi.fault_col != nullptr;
+    switch (p.epi.abft) {
+        case 0: launch_inst<kFmt, kBKMajor, 0, false>(ta, tb, p, stream); break;
+        case 1:
+            if (inj) launch_inst<kFmt, kBKMajor, 1, true>(ta, tb, p, stream);
+            else launch_inst<kFmt, kBKMajor, 1, false>(ta, tb, p, stream);
+            break;
+        default:
+            if (inj) launch_inst<kFmt, kBKMajor, 2, true>(ta, tb, p, stream);
+            else launch_inst<kFmt, kBKMajor, 2, false>(ta, tb, p, stream);
+            break;
+    }
+}
+
+}  // namespace
+
+bool tc_gemm_supported(int fmt, int64_t M, int64_t N, int64_t K) {
+    if (fmt != VABFT_BF16 && fmt != VABFT_FP16) return false;
+    if (M < 1 || N < 1 || K < 1) return false;
+    if (N % 8 != 0 || K % 8 != 0) return false;  // 16-byte TMA global strides
+    if (M > (int64_t(1) << 31) - 1 || N > (int64_t(1) << 24) || K > (int64_t(1) << 31) - 1) return false;
+    return true;
+}
+
+void tc_gemm_launch(int fmt, bool b_kmajor, int64_t M, int64_t N, int64_t K, const void* A,
+                    const void* B, void* C, const TcEpilogue& epi, cudaStream_t stream) {
+    if (!tc_gemm_supported(fmt, M, N, K))
+        fail(VABFT_UNSUPPORTED, "tcgen05 GEMM: needs BF16/FP16 with N % 8 == 0 and K % 8 == 0");
+    TcParams p;
+    p.M = int(M);
+    p.N = int(N);
+    p.K = int(K);
+    p.num_m_blk = int((M + kBM - 1) / kBM);
+    p.num_n_blk = int((N + kBN - 1) / kBN);
+    p.num_k_blk = int((K + kBK - 1) / kBK);
+    p.num_tiles = p.num_m_blk * p.num_n_blk;
+    p.C = static_cast<uint16_t*>(C);
+    p.epi = epi;
+    const CUtensorMap ta = make_map_2d(fmt, A, uint64_t(M), uint64_t(K), kBK, kBM);
+    const CUtensorMap tb = b_kmajor ? make_map_2d(fmt, B, uint64_t(N), uint64_t(K), kBK, kBN)
+                                    : make_map_2d(fmt, B, uint64_t(K), uint64_t(N), 64, kBK);
+    if (fmt == VABFT_BF16) {
+        if (b_kmajor) dispatch_epi<VABFT_BF16, true>(ta, tb, p, stream);
+        else dispatch_epi<VABFT_BF16, false>(ta, tb, p, stream);
+    } else {
+        if (b_kmajor) dispatch_epi<VABFT_FP16, true>(ta, tb, p, stream);
+        else dispatch_epi<VABFT_FP16, false>(ta, tb, p, stream);
+    }
+}
+
+}  // namespace vabft_dev
