@@ -37,6 +37,7 @@ struct TcEpilogue {
     const int32_t* fault_bit = nullptr;
     const int32_t* fault_dir = nullptr;
     vabft_fault_record* fault_records = nullptr;
+    float* accum_out = nullptr;  // optional M x N FP32 accumulator dump (parity API)
 };
 void tc_gemm_launch(int fmt, bool b_kmajor, int64_t M, int64_t N, int64_t K, const void* A,
                     const void* B, void* C, const TcEpilogue& epi, cudaStream_t stream);

@@ -249,6 +249,21 @@ __global__ void __launch_bounds__(kThreads, 1)
                     else
                         packed[e >> 1] = uint32_t(q);
                 }
+                if (p.epi.accum_out != nullptr && row_ok) {
+                    // parity dump of the (saturated, post-injection) FP32 accumulator
+                    float* dst = p.epi.accum_out + size_t(row) * p.N + n0 + c;
+#pragma unroll
+                    for (int e = 0; e < 32; ++e) {
+                        if (n0 + c + e < p.N) {
+                            float x = saturate_accum<kFmt>(__uint_as_float(v[e]));
+                            if constexpr (kAbft == 1 && kInject) {
+                                if (n0 + c + e == fcol && bit_eligible(__float_as_uint(x), fbit, fdir))
+                                    x = __uint_as_float(__float_as_uint(x) ^ (1u << fbit));
+                            }
+                            dst[e] = x;
+                        }
+                    }
+                }
                 if (row_ok) {
                     uint16_t* dst = p.C + size_t(row) * p.N + n0 + c;
 #pragma unroll

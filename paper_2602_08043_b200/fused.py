@@ -1,0 +1,132 @@
+"""The hot path on device tensors: the tcgen05 fused V-ABFT GEMM.
+
+    g = FusedAbftGemm(B, mode="online")          # per-weight B-side state
+    r = g(A)                                     # C, thresholds, verdicts, counts
+
+One call = A-side statistics (row stats -> V-ABFT thresholds, A (B r)
+checksums), the tcgen05 GEMM with the ABFT epilogue, and the verify tail —
+all stream-ordered on the current torch stream, no host synchronization.
+"""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass
+from typing import Optional
+
+import torch
+
+from . import _capi
+from ._capi import check, lib
+from .device import ptr, stream_ptr
+
+_FMT = {torch.bfloat16: _capi.BF16, torch.float16: _capi.FP16}
+_METHOD = {"vabft": 0, "aabft-fixed-y": 1, "aabft-computed-y": 2}
+
+# e_max for online (FP32-accumulator) verification of the tcgen05 kernel:
+# the calibrate() protocol (proj/src/calibration.cpp:88-150) run on B200 —
+# see calibration.py / DESIGN.md. Overridable per call.
+DEFAULT_ONLINE_EMAX = 2.0e-6
+
+
+@dataclass
+class FusedResult:
+    C: torch.Tensor
+    T: Optional[torch.Tensor]
+    diff1: Optional[torch.Tensor]
+    diff2: Optional[torch.Tensor]
+    detected: Optional[torch.Tensor]
+    location: Optional[torch.Tensor]
+    residual: Optional[torch.Tensor]
+    counts: Optional[torch.Tensor]
+
+
+class FusedAbftGemm:
+    """Fault-tolerant C = A B for a fixed BF16/FP16 weight B (K x N, row-major)."""
+
+    def __init__(self, B: torch.Tensor, mode: str = "online", threshold: str = "vabft",
+                 e_max: Optional[float] = None, c_sigma: float = 2.5, floor_scale: float = 1e-3,
+                 aabft_mantissa_bits: int = 0, aabft_fixed_y: float = 21.0, aabft_confidence: float = 3.0):
+        if B.dtype not in _FMT or not B.is_cuda or B.dim() != 2:
+            raise _capi.InvalidArgument("FusedAbftGemm: B must be a 2-D BF16/FP16 CUDA tensor")
+        self.B = B.contiguous()
+        self.fmt = _FMT[B.dtype]
+        self.k, self.n = self.B.shape
+        self.mode = _capi.ONLINE if mode == "online" else _capi.OFFLINE
+        if e_max is None:
+            if self.mode == _capi.ONLINE:
+                e_max = DEFAULT_ONLINE_EMAX
+            else:
+                e_max = 8e-3 if self.fmt == _capi.BF16 else 1e-3  # format defaults (precision.cpp:44-62)
+        self.opts = _capi.FusedOpts()
+        self.opts.mode = self.mode
+        self.opts.threshold_method = _METHOD[threshold]
+        self.opts.e_max = e_max
+        self.opts.c_sigma = c_sigma
+        self.opts.floor_scale = floor_scale
+        self.opts.aabft_mantissa_bits = aabft_mantissa_bits
+        self.opts.b_kmajor = 0
+        self.opts.aabft_fixed_y = aabft_fixed_y
+        self.opts.aabft_confidence = aabft_confidence
+        self.h = C.c_void_p()
+        check(lib.vabft_bside_create(self.fmt, self.mode, self.k, self.n, ptr(self.B), C.byref(self.h),
+                                     stream_ptr()))
+        self._ws = None
+
+    def update_weight(self, B: torch.Tensor) -> None:
+        self.B = B.contiguous()
+        check(lib.vabft_bside_update(self.h, ptr(self.B), stream_ptr()))
+
+    def workspace(self, m: int) -> torch.Tensor:
+        sz = C.c_size_t()
+        check(lib.vabft_fused_workspace_size(m, self.n, self.k, C.byref(sz)))
+        if self._ws is None or self._ws.numel() < sz.value:
+            self._ws = torch.empty(sz.value, dtype=torch.uint8, device=self.B.device)
+        return self._ws
+
+    def __call__(self, A: torch.Tensor, out: Optional[torch.Tensor] = None, *, verdicts: bool = True,
+                 thresholds: bool = True, counts: Optional[torch.Tensor] = None,
+                 faults: Optional[dict] = None) -> FusedResult:
+        if A.dtype != self.B.dtype or A.dim() != 2 or A.shape[1] != self.k:
+            raise _capi.InvalidArgument("FusedAbftGemm: A must be M x K with B's dtype")
+        m = A.shape[0]
+        dev = A.device
+        C_ = out if out is not None else torch.empty((m, self.n), dtype=A.dtype, device=dev)
+        T = torch.empty(m, dtype=torch.float64, device=dev) if thresholds else None
+        if verdicts:
+            d1, d2, res = (torch.empty(m, dtype=torch.float64, device=dev) for _ in range(3))
+            det = torch.empty(m, dtype=torch.uint8, device=dev)
+            loc = torch.empty(m, dtype=torch.int64, device=dev)
+        else:
+            d1 = d2 = res = det = loc = None
+        v = _capi.Verdicts(ptr(d1), ptr(d2), ptr(det), ptr(loc), ptr(res))
+        opts = self.opts
+        if faults is not None:
+            opts = _capi.FusedOpts.from_buffer_copy(self.opts)
+            opts.fault_col = ptr(faults["col"])
+            opts.fault_bit = ptr(faults["bit"])
+            opts.fault_dir = ptr(faults["dir"])
+            opts.fault_records = ptr(faults.get("records"))
+        ws = self.workspace(m)
+        check(lib.vabft_fused_gemm(C.byref(opts), self.h, m, ptr(A.contiguous()), ptr(C_), ptr(T), v, ptr(counts),
+                                   ptr(ws), ws.numel(), stream_ptr()))
+        return FusedResult(C_, T, d1, d2, det, loc, res, counts)
+
+    def close(self) -> None:
+        if self.h:
+            check(lib.vabft_bside_destroy(self.h))
+            self.h = C.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def plain_gemm(A: torch.Tensor, B: torch.Tensor, out: Optional[torch.Tensor] = None, b_kmajor: bool = False):
+    """The same tcgen05 kernel with the ABFT epilogue compiled out (overhead baseline)."""
+    m, k = A.shape
+    n = B.shape[0] if b_kmajor else B.shape[1]
+    C_ = out if out is not None else torch.empty((m, n), dtype=A.dtype, device=A.device)
+    check(lib.vabft_gemm_plain(_FMT[A.dtype], int(b_kmajor), m, n, k, ptr(A), ptr(B), ptr(C_), stream_ptr()))
+    return C_
