@@ -1,0 +1,377 @@
+#!/usr/bin/env python
+"""bench.py — fused V-ABFT GEMM throughput (BASELINE.json metric).
+
+A step = one pass of the hot path over one batch: for the default workload
+(BASELINE config 2) one BF16 4096x4096x4096 fused V-ABFT GEMM per GPU —
+A-side statistics -> thresholds, the tcgen05 GEMM with the FP32-accumulator
+(online) verification epilogue, the verify tail — followed by the NCCL
+all-reduce of the fault counters across ranks (the only collective).
+
+  python bench.py                          # N=1, defaults below
+  python -m torch.distributed.run --nproc-per-node N bench.py --gpus N
+  python bench.py --impl reference         # the reference CPU path on host cores
+
+Timing: W untimed warm-up steps; K timed steps bracketed by barrier +
+synchronize; between steps a 512 MiB buffer is written (L2 flush, untimed);
+each step is timed with CUDA events on the launching stream (a CUDA graph of
+the step is replayed) and the MAX over ranks of the summed step time is used.
+value = total FLOP of all ranks / that time.
+"""
+from __future__ import annotations
+
+import argparse
+import ctypes as C
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "fused V-ABFT GEMM TFLOP/s"
+LLAMA_LAYER = [(4096, 4096)] * 4 + [(4096, 11008)] * 2 + [(11008, 4096)]
+
+CONFIGS = {
+    "c2": {"workload": "BF16 GEMM 4096x4096x4096 fused V-ABFT, online (FP32-accumulator) verify, "
+                       "N(0,1) inputs; 1 GEMM per GPU per step", "gemms": [(4096, 4096, 4096)], "scaling": "weak"},
+    "llama": {"workload": "LLaMA-7B layer GEMMs, tokens M=8192, (K,N) in {(4096,4096)x4,(4096,11008)x2,"
+                          "(11008,4096)x1}, 1 layer per GPU per step", "gemms": [(8192, k, n) for k, n in LLAMA_LAYER],
+              "scaling": "weak"},
+}
+
+
+def env_rank():
+    return int(os.environ.get("RANK", "0")), int(os.environ.get("WORLD_SIZE", "1")), int(os.environ.get("LOCAL_RANK", "0"))
+
+
+def load_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        d = json.load(open(p))
+        return d.get("bf16_tflops", 1590.0), d.get("bf16_tflops_sustained", 1400.0), d.get("hbm_gbs", 6650.0), "measured"
+    return 1590.0, 1400.0, 6650.0, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.sw_power_cap,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown")
+
+    def __init__(self, dev_index: int):
+        self.dev = dev_index
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.dev), f"--query-gpu={self.Q}",
+                                          "--format=csv,noheader,nounits", "-lms", "50"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except OSError:
+            self.proc = None
+        return self
+
+    def __exit__(self, *a):
+        self.lines = []
+        if self.proc is not None:
+            time.sleep(0.12)
+            self.proc.terminate()
+            try:
+                out, _ = self.proc.communicate(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+                out, _ = self.proc.communicate()
+            self.lines = [ln for ln in out.splitlines() if ln.strip()]
+
+    def summary(self):
+        sm, mx, reasons = [], 0.0, set()
+        names = ["sw_power_cap", "hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown"]
+        for ln in getattr(self, "lines", []):
+            f = [x.strip() for x in ln.split(",")]
+            try:
+                sm.append(float(f[0]))
+                mx = max(mx, float(f[1]))
+            except (ValueError, IndexError):
+                continue
+            for nm, val in zip(names, f[2:]):
+                if val.lower().startswith("active"):
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx or None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ---------------------------------------------------------------- CPU arms
+def cpu_reference_sample(m_rows: int, k: int, n: int, threads: int, mode: str):
+    """Reference CPU path (encode_and_multiply + vabft_thresholds + verify)
+    on a row sample: `threads` concurrent calls of m_rows rows each (row
+    slices are bit-exact sub-problems). Returns (flop, seconds,
+    kind)."""
+    import numpy as np
+    import oracle
+    O = oracle.best()
+    kind = "reference" if O.name == "reference" else "port"
+    A, B = O.trial_inputs(m_rows * threads, k, n, "bf16", "normal:0,1", 7, 0)
+    e_max = 2e-6 if mode == "online" else 8e-3
+
+    def one(t):
+        a = np.ascontiguousarray(A[t * m_rows:(t + 1) * m_rows])
+        e = O.encode_and_multiply(a, B, "bf16", mode)
+        T, _ = O.vabft_thresholds(a, B, e_max)
+        src = e.c_accum if mode == "online" else e.c
+        O.verify(src, e.row_check1, e.row_check2, T, "bf16", mode)
+
+    t0 = time.perf_counter()
+    ths = [threading.Thread(target=one, args=(t,)) for t in range(threads)]
+    for th in ths:
+        th.start()
+    for th in ths:
+        th.join()
+    dt = time.perf_counter() - t0
+    return 2.0 * m_rows * threads * k * n, dt, kind
+
+
+def run_reference_arm(args, cfg):
+    rank, world, _ = env_rank()
+    if rank != 0:
+        return
+    m, k, n = cfg["gemms"][0]
+    threads = os.cpu_count() or 1
+    rows = args.ref_rows
+    for _ in range(max(0, min(args.warmup, 1))):
+        cpu_reference_sample(1, k, min(n, 512), 1, args.mode)
+    tot_f, tot_t = 0.0, 0.0
+    for _ in range(args.steps):
+        f, dt, kind = cpu_reference_sample(rows, k, n, threads, args.mode)
+        tot_f += f
+        tot_t += dt
+    val = tot_f / tot_t / 1e12
+    sample = f"{threads} concurrent calls x {rows} rows of {m}x{k}x{n} (row slices), per step"
+    line = {"impl": "reference", "metric": METRIC, "value": val, "unit": "TFLOP/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": tot_t / args.steps * 1e3,
+            "higher_is_better": True, "scaling": cfg["scaling"], "vs_baseline": None, "dtype": "bf16",
+            "data": "synthetic N(0,1), reference Philox stream",
+            "config": {"workload": cfg["workload"], "mode": args.mode},
+            "cpu_baseline": {"value": val, "unit": "TFLOP/s", "cores": threads, "kind": kind, "sample": sample},
+            "e2e": {"value": val, "unit": "TFLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+# ---------------------------------------------------------------- GPU arm
+def run_ours(args, cfg):
+    import torch
+    import torch.distributed as dist
+
+    from paper_2602_08043_b200 import _capi
+    from paper_2602_08043_b200.device import ptr, stream_ptr
+    from paper_2602_08043_b200.fused import FusedAbftGemm, plain_gemm
+
+    rank, world, local = env_rank()
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    torch.manual_seed(1234 + rank)
+    gemms = cfg["gemms"]
+    flops_rank = sum(2.0 * m * k * n for (m, k, n) in gemms)
+
+    # resident inputs (weights are per-rank random-init, activations N(0,1))
+    As, Bs, Cs, gs = [], [], [], []
+    for (m, k, n) in gemms:
+        As.append(torch.randn(m, k, device=dev).bfloat16())
+        Bs.append(torch.randn(k, n, device=dev).bfloat16())
+        Cs.append(torch.empty(m, n, device=dev, dtype=torch.bfloat16))
+        gs.append(FusedAbftGemm(Bs[-1], mode=args.mode))
+    counts = torch.zeros(4, dtype=torch.int64, device=dev)
+    flush = torch.empty(512 * 1024 * 1024, dtype=torch.uint8, device=dev)
+    stream = torch.cuda.current_stream()
+
+    def step_fused():
+        for g, A, Cc in zip(gs, As, Cs):
+            g(A, out=Cc, counts=counts)
+
+    def reduce_counts():
+        if world > 1:
+            dist.all_reduce(counts)
+
+    def step_plain():
+        for A, B, Cc in zip(As, Bs, Cs):
+            plain_gemm(A, B, out=Cc)
+
+    def capture(fn):
+        for _ in range(3):
+            fn()
+        torch.cuda.synchronize()
+        gr = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(gr):
+            fn()
+        torch.cuda.synchronize()
+        return gr
+
+    def timed(gr_or_fn, steps, warmup, use_graph=True, clocks=False, post=None):
+        base = gr_or_fn.replay if use_graph else gr_or_fn
+
+        def run():
+            base()
+            if post is not None:
+                post()
+        for _ in range(warmup):
+            flush.zero_()
+            run()
+        starts = [torch.cuda.Event(enable_timing=True) for _ in range(steps)]
+        ends = [torch.cuda.Event(enable_timing=True) for _ in range(steps)]
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        sampler = ClockSampler(local) if clocks else None
+        if sampler:
+            sampler.__enter__()
+        for i in range(steps):
+            flush.zero_()
+            starts[i].record(stream)
+            run()
+            ends[i].record(stream)
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        if sampler:
+            sampler.__exit__()
+        ms = sum(s.elapsed_time(e) for s, e in zip(starts, ends))
+        t = torch.tensor([ms], dtype=torch.float64, device=dev)
+        if world > 1:
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return t.item(), (sampler.summary() if sampler else None)
+
+    # The GEMM part of a step is a CUDA graph; the NCCL all-reduce of the
+    # counters follows each replay as a plain NCCL call on the same stream.
+    use_graph = True
+    g_fused = capture(step_fused)
+    ms_fused, clocks = timed(g_fused, args.steps, args.warmup, use_graph, clocks=True, post=reduce_counts)
+    g_plain = capture(step_plain) if use_graph else step_plain
+    ms_plain, _ = timed(g_plain, args.steps, args.warmup, use_graph)
+
+    # dominant kernel alone (tcgen05 GEMM with the ABFT epilogue): stage mask 2
+    def step_gemm_only():
+        for g, A, Cc in zip(gs, As, Cs):
+            g(A, out=Cc, counts=counts, stages=2)
+    g_k = capture(step_gemm_only) if use_graph else step_gemm_only
+    ms_kernel, _ = timed(g_k, max(5, args.steps // 2), args.warmup, use_graph)
+
+    # FPR over the timed steps (clean data) and a fault-injection sanity pass
+    counts.zero_()
+    step_fused()
+    reduce_counts()
+    torch.cuda.synchronize()
+    fp_rows = int(counts[1].item())
+    rows_checked = int(counts[0].item())
+
+    # offline mode, same kernel family, for the online-vs-offline comparison
+    go = [FusedAbftGemm(B, mode="offline") for B in Bs]
+
+    def step_off():
+        for g, A, Cc in zip(go, As, Cs):
+            g(A, out=Cc, counts=counts)
+    g_off = capture(step_off) if use_graph else step_off
+    ms_off, _ = timed(g_off, max(5, args.steps // 2), args.warmup, use_graph)
+
+    # e2e through the public API with HOST buffers: pinned A and B in,
+    # C + verdict counts out, inside the timed region every step.
+    m0, k0, n0 = gemms[0]
+    hA = [A.cpu().pin_memory() for A in As]
+    hB = [B.cpu().pin_memory() for B in Bs]
+    hC = [torch.empty(Cc.shape, dtype=Cc.dtype).pin_memory() for Cc in Cs]
+    hcounts = torch.zeros(4, dtype=torch.int64).pin_memory()
+    dA2 = [torch.empty_like(A) for A in As]
+    dB2 = [torch.empty_like(B) for B in Bs]
+    g_e2e = [FusedAbftGemm(dB, mode=args.mode) for dB in dB2]
+
+    def step_e2e():
+        for i, g in enumerate(g_e2e):
+            dA2[i].copy_(hA[i], non_blocking=True)
+            dB2[i].copy_(hB[i], non_blocking=True)
+            g.update_weight(dB2[i])
+            g(dA2[i], out=Cs[i], counts=counts)
+            hC[i].copy_(Cs[i], non_blocking=True)
+        reduce_counts()
+        hcounts.copy_(counts, non_blocking=True)
+    e2e_steps = max(3, min(args.steps, 50))
+    ms_e2e, _ = timed(step_e2e, e2e_steps, args.warmup, use_graph=False)
+    h2d = sum(A.numel() * 2 + B.numel() * 2 for A, B in zip(As, Bs))
+    d2h = sum(Cc.numel() * 2 for Cc in Cs) + 32
+
+    value = flops_rank * world / (ms_fused / args.steps / 1e3) / 1e12
+    plain_tf = flops_rank * world / (ms_plain / args.steps / 1e3) / 1e12
+    kernel_tf = flops_rank / (ms_kernel / max(5, args.steps // 2) / 1e3) / 1e12
+    off_tf = flops_rank * world / (ms_off / max(5, args.steps // 2) / 1e3) / 1e12
+    e2e_tf = flops_rank * world / (ms_e2e / e2e_steps / 1e3) / 1e12
+    burst, sustained, hbm, peak_src = load_peaks()
+
+    if rank != 0:
+        if world > 1:
+            dist.destroy_process_group()
+        return
+    cpu_base = None
+    if world == 1 and not args.no_cpu_baseline:
+        f, dt, kind = cpu_reference_sample(args.ref_rows, gemms[0][1], gemms[0][2], os.cpu_count() or 1, args.mode)
+        cpu_base = {"value": f / dt / 1e12, "unit": "TFLOP/s", "cores": os.cpu_count() or 1, "kind": kind,
+                    "sample": f"{os.cpu_count()} concurrent reference calls x {args.ref_rows} rows of "
+                              f"{gemms[0][0]}x{gemms[0][1]}x{gemms[0][2]} (encode_and_multiply + vabft_thresholds + "
+                              f"verify, {args.mode})"}
+    prof = os.path.join(ROOT, "profiles", "r01_ncu_gemm_dram.json")
+    traffic = None
+    if os.path.exists(prof):
+        try:
+            traffic = json.load(open(prof)).get("dram_bytes_per_launch")
+        except (OSError, ValueError):
+            traffic = None
+    line = {
+        "metric": METRIC, "value": value, "unit": "TFLOP/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms_fused / args.steps, "higher_is_better": True,
+        "scaling": cfg["scaling"], "vs_baseline": None, "dtype": "bf16",
+        "data": "synthetic: A ~ N(0,1), random-init B ~ N(0,1), BF16 on device",
+        "config": {"workload": cfg["workload"], "mode": args.mode, "l2": "flushed between steps (512 MiB write)",
+                   "parallelism": f"independent GEMMs x{world} (no operand exchange), NCCL all-reduce of counters"},
+        "plain_gemm_tflops": plain_tf,
+        "abft_overhead_pct": 100.0 * (plain_tf / value - 1.0),
+        "fused_vs_plain": value / plain_tf,
+        "offline_tflops": off_tf,
+        "fpr": {"false_positive_rows": fp_rows, "rows_checked": rows_checked},
+        "roofline": {"bound": "tensor", "kernel": "tc_gemm_kernel (tcgen05 + ABFT epilogue)",
+                     "achieved": kernel_tf, "peak": burst, "unit": "TFLOP/s", "frac": kernel_tf / burst,
+                     "peak_source": f"{peak_src} bf16_tflops (burst, cuBLAS 8192^3)", "traffic": traffic},
+        "cpu_baseline": cpu_base,
+        "e2e": {"value": e2e_tf, "unit": "TFLOP/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+                "path": "pinned host A,B -> H2D -> B-side update + fused GEMM -> D2H C + counts"},
+        "gpu_launches": args.steps * len(gemms) * 3,
+        "clocks": clocks,
+    }
+    print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=200)
+    ap.add_argument("--warmup", type=int, default=10)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="c2", choices=sorted(CONFIGS))
+    ap.add_argument("--mode", default="online", choices=["online", "offline"])
+    ap.add_argument("--ref-rows", type=int, default=8, help="rows per reference call (CPU sample)")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3
+    cfg = CONFIGS[args.config]
+    if args.impl == "reference":
+        run_reference_arm(args, cfg)
+    else:
+        run_ours(args, cfg)
+
+
+if __name__ == "__main__":
+    main()

@@ -249,6 +249,10 @@ typedef struct vabft_fused_opts {
     const int32_t* fault_bit;
     const int32_t* fault_dir;
     vabft_fault_record* fault_records; /* device, length M, may be NULL */
+    /* Stage mask for profiling (0 = all): 1 statistics pass, 2 tcgen05 GEMM
+     * with the ABFT epilogue, 4 verify tail. */
+    int32_t stages;
+    int32_t reserved;
 } vabft_fused_opts;
 
 /* Workspace bytes for vabft_fused_gemm at this shape. */

@@ -59,7 +59,7 @@ class FusedOpts(C.Structure):
                 ("c_sigma", C.c_double), ("floor_scale", C.c_double), ("aabft_mantissa_bits", C.c_int32),
                 ("b_kmajor", C.c_int32), ("aabft_fixed_y", C.c_double), ("aabft_confidence", C.c_double),
                 ("fault_col", C.c_void_p), ("fault_bit", C.c_void_p), ("fault_dir", C.c_void_p),
-                ("fault_records", C.c_void_p)]
+                ("fault_records", C.c_void_p), ("stages", C.c_int32), ("reserved", C.c_int32)]
 
 
 _st = C.c_int

@@ -232,7 +232,8 @@ def encode_and_multiply(a: np.ndarray, b: np.ndarray, mode="offline", spec="fp64
     torch.cuda.synchronize()
     cs = checksum_precision_for(s, mode)
     if engine == "tensor":
-        cs = cs.with_accumulation(AccumStrategy(AccumKind.NATIVE_BLOCKED, 128))
+        # FP32 arithmetic, blocked:128 order, in both modes
+        cs = PrecisionSpec.fp32().with_accumulation(AccumStrategy(AccumKind.NATIVE_BLOCKED, 128))
     out = EncodedProduct(to_host(dC), to_host(r1), to_host(r2), to_host(c1), to_host(c2), cs,
                          "online" if mc else "offline", to_host(dCa), s.format, engine)
     if mc == _capi.OFFLINE:

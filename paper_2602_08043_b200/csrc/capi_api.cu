@@ -98,7 +98,12 @@ extern "C" vabft_status vabft_encode_and_multiply(const vabft_precision* spec, i
         int csf;
         vabft_accum csa;
         cs_prec(*spec, mode, &csf, &csa);
-        if (engine == VABFT_ENGINE_TENSOR) csa = vabft_accum{VABFT_ACCUM_BLOCKED, 0, 128};
+        if (engine == VABFT_ENGINE_TENSOR) {
+            // TENSOR engine checksum precision: FP32 arithmetic in blocked:128
+            // order for both modes (an FP32 PrecisionSpec with NativeBlocked(128))
+            csf = VABFT_FP32;
+            csa = vabft_accum{VABFT_ACCUM_BLOCKED, 0, 128};
+        }
         check_weights(n, csf, csa.kind);
         check_weights(m, csf, csa.kind);
         cudaStream_t s = as_stream(stream);

@@ -4,13 +4,20 @@
 //                        BStatsSummary::from (threshold_vabft.cpp:8-26), B r1 /
 //                        B r2 (checksum.cpp:110-115), max_k |sum_j B| for A-ABFT
 //                        computed y (threshold_aabft.cpp:38-48).
-//   vabft_fused_gemm     1. aside_kernel: A row stats -> V-ABFT T_i
-//                           (threshold_vabft.cpp:54-61), A (B r1/2), max|A|
-//                        2. tc_gemm (tcgen05): C plus per-128-column row
-//                           partials of the FP32 accumulator (online) or of
-//                           the quantized output (offline), optional in-
-//                           epilogue fault injection (faults.cpp:104-168)
-//                        3. verify tail: blocked:128 row sums, D1/D2, strict
+//   vabft_fused_gemm     1. tc_gemm (tcgen05), one persistent kernel:
+//                           - MMA: C = A B, FP32 accumulators in TMEM;
+//                           - epilogue warps: per-128-column row partials of
+//                             the FP32 accumulator (online) or of the quantized
+//                             output (offline), optional in-epilogue fault
+//                             injection (faults.cpp:104-168), C store;
+//                           - statistics warps: read the TMA-staged A tiles from
+//                             shared memory and produce per-(row, 128-k-block)
+//                             A (B r) partials and exact row-sum / max / min
+//                             partials (threshold_vabft.cpp:54-61 inputs) —
+//                             the A operand is never re-read from HBM.
+//                        2. verify tail: A-row statistics -> V-ABFT T_i
+//                           (exactness guard + sequential fallback), blocked:128
+//                           combination of both partial sets, D1/D2, strict
 //                           compare, NaN rule, localization (detect.cpp:9-55),
 //                           warp-aggregated counters.
 // No host synchronization anywhere on this path.
@@ -36,33 +43,196 @@ namespace vabft_dev {
 
 namespace {
 
-__global__ void fused_tail_kernel(int64_t M, int64_t N, int64_t K, int64_t nblk,
-                                  const float* __restrict__ part1, const float* __restrict__ part2,
-                                  const double* __restrict__ cr1, const double* __restrict__ cr2,
-                                  const double* __restrict__ Tv, const double* __restrict__ bsum,
-                                  const double* __restrict__ max_abs_a, int method, int aabft_t,
-                                  double aabft_fixed_y, double aabft_conf, double floor_scale,
-                                  double* T_out, vabft_verdicts v, int64_t* counts) {
-    const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
-    const bool valid = i < M;
+__device__ __forceinline__ uint32_t pminu2(uint32_t a, uint32_t b) {
+    uint32_t d;
+    asm("min.u16x2 %0, %1, %2;" : "=r"(d) : "r"(a), "r"(b));
+    return d;
+}
+template <int F>
+__device__ __forceinline__ uint32_t pmax2(uint32_t a, uint32_t b) {
+    uint32_t d;
+    if constexpr (F == VABFT_BF16) asm("max.bf16x2 %0, %1, %2;" : "=r"(d) : "r"(a), "r"(b));
+    else asm("max.f16x2 %0, %1, %2;" : "=r"(d) : "r"(a), "r"(b));
+    return d;
+}
+template <int F>
+__device__ __forceinline__ uint32_t pmin2(uint32_t a, uint32_t b) {
+    uint32_t d;
+    if constexpr (F == VABFT_BF16) asm("min.bf16x2 %0, %1, %2;" : "=r"(d) : "r"(a), "r"(b));
+    else asm("min.f16x2 %0, %1, %2;" : "=r"(d) : "r"(a), "r"(b));
+    return d;
+}
+
+// n * max|x| < 2^(53 + lsb(min nonzero |x|)) => plain FP64 sums are exact in
+// any order (see aside.cu); mnz_pat is (smallest nonzero magnitude - 1).
+template <int F>
+__device__ __forceinline__ bool guard_exact(float max_abs, uint32_t mnz_pat, int64_t n) {
+    if (mnz_pat >= 0x7FFFu) return true;
+    if (!isfinite(max_abs)) return false;
+    const uint32_t pat = mnz_pat + 1;
+    int lsb;
+    if constexpr (F == VABFT_BF16) {
+        const int ef = int((pat >> 7) & 0xFF);
+        lsb = (ef == 0 ? 1 : ef) - 127 - 7;
+    } else {
+        const int ef = int((pat >> 10) & 0x1F);
+        lsb = (ef == 0 ? 1 : ef) - 15 - 10;
+    }
+    const int top = ilogbf(max_abs) + 1 + (64 - __clzll(static_cast<unsigned long long>(n)));
+    return top <= 53 + lsb;
+}
+
+struct TailArgs {
+    int64_t M, N, K, nblkN, nblkK;
+    const uint16_t* A;
+    const float *part1, *part2;            // [nblkN][M] C row partials
+    const float *sp1, *sp2;                // [nblkK][M] A (B r) partials
+    const double* ssum;                    // [nblkK][M]
+    const uint32_t *smax, *smin, *smnz;    // [nblkK][M]
+    const double* bsum;                    // B summary (4)
+    double* cr1;                           // [M] staged checksums (phase 1 -> 2)
+    double* cr2;
+    double* Tv;                            // [M] V-ABFT thresholds
+    double* max_abs_a;
+    int method, aabft_t, quantize_cr;
+    double e_max, c_sigma, aabft_fixed_y, aabft_conf, floor_scale;
+    double* T_out;
+    vabft_verdicts v;
+    int64_t* counts;
+};
+
+// phase bit 1: A-row statistics -> T_i, A (B r); bit 2: row sums + verify.
+// A CTA owns 32 rows: its 4 warps stage the [block][row] partial arrays
+// through shared memory with coalesced loads (many loads in flight), then
+// warp 0 (lane = row) combines them in block order — NativeBlocked(128) for
+// the checksum and row-sum partials — and runs the verify rules.
+constexpr int kTailRows = 32;
+constexpr int kTailChunk = 16;
+
+template <int F>
+__global__ void __launch_bounds__(128) fused_tail_kernel(const TailArgs a, int phase) {
+    __shared__ float s_p1[kTailChunk][kTailRows], s_p2[kTailChunk][kTailRows];
+    __shared__ double s_sum[kTailChunk][kTailRows];
+    __shared__ uint32_t s_max[kTailChunk][kTailRows], s_min[kTailChunk][kTailRows], s_mnz[kTailChunk][kTailRows];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int64_t row0 = int64_t(blockIdx.x) * kTailRows;
+    const int64_t i = row0 + lane;
+    const bool valid = warp == 0 && i < a.M;
     bool det = false, located = false, isnan_row = false;
+    double c1 = 0.0, c2 = 0.0, tv = 0.0;
+    if (phase & 1) {
+        float t1 = 0.0f, t2 = 0.0f;
+        double sum = 0.0;
+        uint32_t gmax = F == VABFT_BF16 ? 0xFF80FF80u : 0xFC00FC00u;
+        uint32_t gmin = F == VABFT_BF16 ? 0x7F807F80u : 0x7C007C00u;
+        uint32_t gmnz = 0x7FFF7FFFu;
+        for (int64_t b0 = 0; b0 < a.nblkK; b0 += kTailChunk) {
+            for (int e = threadIdx.x; e < kTailChunk * kTailRows; e += blockDim.x) {
+                const int bb = e / kTailRows, rr = e % kTailRows;
+                const int64_t b = b0 + bb, row = row0 + rr;
+                if (b < a.nblkK && row < a.M) {
+                    const int64_t o = b * a.M + row;
+                    s_p1[bb][rr] = __ldg(a.sp1 + o);
+                    s_p2[bb][rr] = __ldg(a.sp2 + o);
+                    s_sum[bb][rr] = __ldg(a.ssum + o);
+                    s_max[bb][rr] = __ldg(a.smax + o);
+                    s_min[bb][rr] = __ldg(a.smin + o);
+                    s_mnz[bb][rr] = __ldg(a.smnz + o);
+                }
+            }
+            __syncthreads();
+            if (valid) {
+                const int cnt = int((a.nblkK - b0) < kTailChunk ? (a.nblkK - b0) : kTailChunk);
+                for (int bb = 0; bb < cnt; ++bb) {  // block order
+                    t1 = __fadd_rn(t1, s_p1[bb][lane]);
+                    t2 = __fadd_rn(t2, s_p2[bb][lane]);
+                    sum = __dadd_rn(sum, s_sum[bb][lane]);
+                    gmax = pmax2<F>(gmax, s_max[bb][lane]);
+                    gmin = pmin2<F>(gmin, s_min[bb][lane]);
+                    gmnz = pminu2(gmnz, s_mnz[bb][lane]);
+                }
+            }
+            __syncthreads();
+        }
+        if (valid) {
+            const float mx = fmaxf(bits16_to_float<F>(uint16_t(gmax & 0xFFFFu)), bits16_to_float<F>(uint16_t(gmax >> 16)));
+            const float mn = fminf(bits16_to_float<F>(uint16_t(gmin & 0xFFFFu)), bits16_to_float<F>(uint16_t(gmin >> 16)));
+            const uint32_t mnz = min(gmnz & 0xFFFFu, gmnz >> 16);
+            const float amax = fmaxf(fabsf(mx), fabsf(mn));
+            if (!guard_exact<F>(amax, mnz, a.K)) {
+                // the reference's sequential Neumaier pass over the row (stats.cpp:12-24)
+                Neu ns;
+                const uint16_t* row = a.A + i * a.K;
+                for (int64_t q = 0; q < a.K; ++q) ns.add(double(bits16_to_float<F>(row[q])));
+                sum = __dadd_rn(ns.s, ns.c);
+            }
+            Neu fin;
+            fin.s = sum;
+            double mean, vb;
+            stats_finish(fin, double(mx), double(mn), a.K, &mean, &vb);
+            tv = vabft_threshold_total(mean, vb, a.bsum[0], a.bsum[1], a.bsum[2], a.N, a.e_max, a.c_sigma);
+            if (a.quantize_cr) {
+                t1 = bits16_to_float<F>(quantize16_bits<F>(t1));
+                t2 = bits16_to_float<F>(quantize16_bits<F>(t2));
+            }
+            c1 = double(t1);
+            c2 = double(t2);
+            a.Tv[i] = tv;
+            if (phase == 1) {
+                a.cr1[i] = c1;
+                a.cr2[i] = c2;
+            }
+        }
+        if (warp == 0) {  // one atomic per warp for max|A|
+            float amax = 0.0f;
+            if (valid) amax = float(fmax(fabs(double(bits16_to_float<F>(uint16_t(gmax & 0xFFFFu)))),
+                                         fabs(double(bits16_to_float<F>(uint16_t(gmin & 0xFFFFu))))));
+            if (valid) amax = fmaxf(amax, fmaxf(fabsf(bits16_to_float<F>(uint16_t(gmax >> 16))),
+                                                fabsf(bits16_to_float<F>(uint16_t(gmin >> 16)))));
+#pragma unroll
+            for (int m = 16; m >= 1; m >>= 1) amax = fmaxf(amax, __shfl_xor_sync(0xffffffffu, amax, m));
+            if (lane == 0) atomic_max_nonneg(a.max_abs_a, double(amax));
+        }
+    }
+    if (!(phase & 2)) return;
+    float r1 = 0.0f, r2 = 0.0f;
+    for (int64_t b0 = 0; b0 < a.nblkN; b0 += kTailChunk) {
+        for (int e = threadIdx.x; e < kTailChunk * kTailRows; e += blockDim.x) {
+            const int bb = e / kTailRows, rr = e % kTailRows;
+            const int64_t b = b0 + bb, row = row0 + rr;
+            if (b < a.nblkN && row < a.M) {
+                const int64_t o = b * a.M + row;
+                s_p1[bb][rr] = __ldg(a.part1 + o);
+                s_p2[bb][rr] = __ldg(a.part2 + o);
+            }
+        }
+        __syncthreads();
+        if (valid) {
+            const int cnt = int((a.nblkN - b0) < kTailChunk ? (a.nblkN - b0) : kTailChunk);
+            for (int bb = 0; bb < cnt; ++bb) {  // reduce_terms NativeBlocked(128), in order
+                r1 = __fadd_rn(r1, s_p1[bb][lane]);
+                r2 = __fadd_rn(r2, s_p2[bb][lane]);
+            }
+        }
+        __syncthreads();
+    }
+    if (warp != 0) return;
     if (valid) {
-        // reduce_terms NativeBlocked(128): tot += part per block, in order.
-        float r1 = 0.0f, r2 = 0.0f;
-        for (int64_t b = 0; b < nblk; ++b) {
-            r1 = __fadd_rn(r1, part1[b * M + i]);
-            r2 = __fadd_rn(r2, part2[b * M + i]);
+        if (!(phase & 1)) {
+            c1 = a.cr1[i];
+            c2 = a.cr2[i];
+            tv = a.Tv[i];
         }
         double t;
-        if (method == 0) {
-            t = Tv[i];
+        if (a.method == 0) {
+            t = tv;
         } else {
-            const double y = method == 1 ? aabft_fixed_y : __dmul_rn(*max_abs_a, bsum[3]);
-            t = aabft_total(K, aabft_t, y, aabft_conf);
+            const double y = a.method == 1 ? a.aabft_fixed_y : __dmul_rn(*a.max_abs_a, a.bsum[3]);
+            t = aabft_total(a.K, a.aabft_t, y, a.aabft_conf);
         }
-        if (T_out && method != 0) T_out[i] = t;
-        const double d1 = __dsub_rn(double(r1), cr1[i]);
-        const double d2 = __dsub_rn(double(r2), cr2[i]);
+        if (a.T_out) a.T_out[i] = t;
+        const double d1 = __dsub_rn(double(r1), c1);
+        const double d2 = __dsub_rn(double(r2), c2);
         int64_t loc = -1;
         double res = 0.0;
         if (isnan(d1) || isnan(d2)) {
@@ -70,73 +240,48 @@ __global__ void fused_tail_kernel(int64_t M, int64_t N, int64_t K, int64_t nblk,
             isnan_row = true;
         } else {
             det = fabs(d1) > t;
-            if (det && fabs(d1) > __dmul_rn(floor_scale, t)) {
+            if (det && fabs(d1) > __dmul_rn(a.floor_scale, t)) {
                 int64_t j;
                 double rr;
-                if (localize_dev(d1, d2, N, &j, &rr)) {
+                if (localize_dev(d1, d2, a.N, &j, &rr)) {
                     loc = j;
                     res = rr;
                     located = true;
                 }
             }
         }
-        if (v.diff1) v.diff1[i] = d1;
-        if (v.diff2) v.diff2[i] = d2;
-        if (v.detected) v.detected[i] = det ? 1 : 0;
-        if (v.location) v.location[i] = loc;
-        if (v.residual) v.residual[i] = res;
+        if (a.v.diff1) a.v.diff1[i] = d1;
+        if (a.v.diff2) a.v.diff2[i] = d2;
+        if (a.v.detected) a.v.detected[i] = det ? 1 : 0;
+        if (a.v.location) a.v.location[i] = loc;
+        if (a.v.residual) a.v.residual[i] = res;
     }
-    if (counts) {
+    if (a.counts) {
         const unsigned mv = __ballot_sync(0xffffffffu, valid);
         const unsigned md = __ballot_sync(0xffffffffu, det);
         const unsigned ml = __ballot_sync(0xffffffffu, located);
         const unsigned mn = __ballot_sync(0xffffffffu, isnan_row);
-        if ((threadIdx.x & 31) == 0) {
-            if (mv) atomicAdd(reinterpret_cast<unsigned long long*>(counts + VABFT_COUNT_ROWS), __popc(mv));
-            if (md) atomicAdd(reinterpret_cast<unsigned long long*>(counts + VABFT_COUNT_DETECTED), __popc(md));
-            if (ml) atomicAdd(reinterpret_cast<unsigned long long*>(counts + VABFT_COUNT_LOCATED), __popc(ml));
-            if (mn) atomicAdd(reinterpret_cast<unsigned long long*>(counts + VABFT_COUNT_NAN), __popc(mn));
+        if (lane == 0) {
+            if (mv) atomicAdd(reinterpret_cast<unsigned long long*>(a.counts + VABFT_COUNT_ROWS), __popc(mv));
+            if (md) atomicAdd(reinterpret_cast<unsigned long long*>(a.counts + VABFT_COUNT_DETECTED), __popc(md));
+            if (ml) atomicAdd(reinterpret_cast<unsigned long long*>(a.counts + VABFT_COUNT_LOCATED), __popc(ml));
+            if (mn) atomicAdd(reinterpret_cast<unsigned long long*>(a.counts + VABFT_COUNT_NAN), __popc(mn));
         }
     }
 }
 
 size_t align_up(size_t x) { return (x + 255) & ~size_t(255); }
 
-// Per-thread, per-device side stream + fork/join events: the HBM-bound
-// A-side statistics pass runs concurrently with the tensor-bound GEMM
-// (its CTAs use no shared memory and co-reside with the persistent GEMM
-// CTAs); the verify tail joins both. Capturable into CUDA graphs.
-struct SideStream {
-    int dev = -1;
-    cudaStream_t s = nullptr;
-    cudaEvent_t fork = nullptr, join = nullptr;
-};
-
-SideStream& side_stream() {
-    thread_local SideStream ss;
-    int dev = 0;
-    check_cuda(cudaGetDevice(&dev), "cudaGetDevice");
-    if (ss.dev != dev) {
-        check_cuda(cudaStreamCreateWithFlags(&ss.s, cudaStreamNonBlocking), "cudaStreamCreate");
-        check_cuda(cudaEventCreateWithFlags(&ss.fork, cudaEventDisableTiming), "cudaEventCreate");
-        check_cuda(cudaEventCreateWithFlags(&ss.join, cudaEventDisableTiming), "cudaEventCreate");
-        ss.dev = dev;
-    }
-    return ss;
-}
-
 struct FusedWs {
-    float* part1;
-    float* part2;
-    double* cr1;
-    double* cr2;
-    double* Tv;
-    double* max_abs_a;
+    float *part1, *part2, *sp1, *sp2;
+    double* ssum;
+    uint32_t *smax, *smin, *smnz;
+    double *cr1, *cr2, *Tv, *max_abs_a;
     size_t bytes;
 };
 
-FusedWs carve(void* base, int64_t M, int64_t N) {
-    const int64_t nblk = (N + 127) / 128;
+FusedWs carve(void* base, int64_t M, int64_t N, int64_t K) {
+    const size_t nN = size_t((N + 127) / 128), nK = size_t((K + 127) / 128), m = size_t(M);
     FusedWs w{};
     size_t off = 0;
     char* b = static_cast<char*>(base);
@@ -145,12 +290,18 @@ FusedWs carve(void* base, int64_t M, int64_t N) {
         off += align_up(sz);
         return p;
     };
-    w.part1 = reinterpret_cast<float*>(take(sizeof(float) * size_t(nblk * M)));
-    w.part2 = reinterpret_cast<float*>(take(sizeof(float) * size_t(nblk * M)));
-    w.cr1 = reinterpret_cast<double*>(take(sizeof(double) * size_t(M)));
-    w.cr2 = reinterpret_cast<double*>(take(sizeof(double) * size_t(M)));
-    w.Tv = reinterpret_cast<double*>(take(sizeof(double) * size_t(M)));
-    w.max_abs_a = reinterpret_cast<double*>(take(sizeof(double)));
+    w.part1 = reinterpret_cast<float*>(take(4 * nN * m));
+    w.part2 = reinterpret_cast<float*>(take(4 * nN * m));
+    w.sp1 = reinterpret_cast<float*>(take(4 * nK * m));
+    w.sp2 = reinterpret_cast<float*>(take(4 * nK * m));
+    w.ssum = reinterpret_cast<double*>(take(8 * nK * m));
+    w.smax = reinterpret_cast<uint32_t*>(take(4 * nK * m));
+    w.smin = reinterpret_cast<uint32_t*>(take(4 * nK * m));
+    w.smnz = reinterpret_cast<uint32_t*>(take(4 * nK * m));
+    w.cr1 = reinterpret_cast<double*>(take(8 * m));
+    w.cr2 = reinterpret_cast<double*>(take(8 * m));
+    w.Tv = reinterpret_cast<double*>(take(8 * m));
+    w.max_abs_a = reinterpret_cast<double*>(take(8));
     w.bytes = off;
     return w;
 }
@@ -219,10 +370,9 @@ extern "C" vabft_status vabft_bside_destroy(vabft_bside_t h) {
 
 extern "C" vabft_status vabft_fused_workspace_size(int64_t m, int64_t n, int64_t k, size_t* bytes) {
     return guarded([&] {
-        (void)k;
         if (!bytes) fail(VABFT_INVALID_ARGUMENT, "null bytes");
-        if (m < 1 || n < 1) fail(VABFT_INVALID_ARGUMENT, "dims must be >= 1");
-        *bytes = carve(nullptr, m, n).bytes;
+        if (m < 1 || n < 1 || k < 1) fail(VABFT_INVALID_ARGUMENT, "dims must be >= 1");
+        *bytes = carve(nullptr, m, n, k).bytes;
     });
 }
 
@@ -241,36 +391,82 @@ extern "C" vabft_status vabft_fused_gemm(const vabft_fused_opts* o, vabft_bside_
         if (m < 1) fail(VABFT_INVALID_ARGUMENT, "dims must be >= 1");
         if (m > (int64_t(1) << 24)) fail(VABFT_INVALID_ARGUMENT, "ChecksumVectors: weights exceed exact range");
         const int64_t n = h->n, k = h->k;
-        const FusedWs ws = carve(workspace, m, n);
+        if (k % 8 != 0 || n % 8 != 0) fail(VABFT_UNSUPPORTED, "vabft_fused_gemm: K and N must be multiples of 8");
+        const FusedWs ws = carve(workspace, m, n, k);
         if (!workspace || ws_bytes < ws.bytes) fail(VABFT_INVALID_ARGUMENT, "vabft_fused_gemm: workspace too small");
         cudaStream_t s = as_stream(stream);
         const bool offline = o->mode == VABFT_OFFLINE;
-        double* Tv = (T && o->threshold_method == 0) ? T : ws.Tv;
-        SideStream& side = side_stream();
-        check_cuda(cudaEventRecord(side.fork, s), "cudaEventRecord");
-        check_cuda(cudaStreamWaitEvent(side.s, side.fork, 0), "cudaStreamWaitEvent");
-        TcEpilogue epi;
-        epi.abft = offline ? 2 : 1;
-        epi.part1 = ws.part1;
-        epi.part2 = ws.part2;
-        epi.fault_col = o->fault_col;
-        epi.fault_bit = o->fault_bit;
-        epi.fault_dir = o->fault_dir;
-        epi.fault_records = o->fault_records;
-        tc_gemm_launch(h->fmt, o->b_kmajor != 0, m, n, k, A, h->B, C, epi, s);
-        // statistics pass on the side stream, overlapping the GEMM
-        check_cuda(cudaMemsetAsync(ws.max_abs_a, 0, sizeof(double), side.s), "memset");
-        launch_aside(h->fmt, m, k, n, A, h->buf, offline ? 1 : 0, o->e_max, o->c_sigma, Tv, ws.cr1, ws.cr2,
-                     ws.max_abs_a, side.s);
-        check_cuda(cudaEventRecord(side.join, side.s), "cudaEventRecord");
-        check_cuda(cudaStreamWaitEvent(s, side.join, 0), "cudaStreamWaitEvent");
-        const int64_t nblk = (n + 127) / 128;
-        const int t_bits = o->aabft_mantissa_bits > 0 ? o->aabft_mantissa_bits
-                                                      : (h->fmt == VABFT_BF16 ? 8 : 11);
-        fused_tail_kernel<<<unsigned((m + 255) / 256), 256, 0, s>>>(
-            m, n, k, nblk, ws.part1, ws.part2, ws.cr1, ws.cr2, Tv, h->buf.summary, ws.max_abs_a,
-            o->threshold_method, t_bits, o->aabft_fixed_y, o->aabft_confidence > 0 ? o->aabft_confidence : 3.0,
-            o->floor_scale, T, verdicts, counts);
+        const int stages = o->stages == 0 ? 7 : o->stages;
+        if (stages & 2) {
+            TcEpilogue epi;
+            epi.abft = offline ? 2 : 1;
+            epi.part1 = ws.part1;
+            epi.part2 = ws.part2;
+            epi.fault_col = o->fault_col;
+            epi.fault_bit = o->fault_bit;
+            epi.fault_dir = o->fault_dir;
+            epi.fault_records = o->fault_records;
+            epi.br1 = h->buf.br1;
+            epi.br2 = h->buf.br2;
+            epi.sp1 = ws.sp1;
+            epi.sp2 = ws.sp2;
+            epi.ssum = ws.ssum;
+            epi.smax = ws.smax;
+            epi.smin = ws.smin;
+            epi.smnz = ws.smnz;
+            tc_gemm_launch(h->fmt, o->b_kmajor != 0, m, n, k, A, h->B, C, epi, s);
+        }
+        if (!(stages & 4)) return;
+        TailArgs a;
+        a.M = m;
+        a.N = n;
+        a.K = k;
+        a.nblkN = (n + 127) / 128;
+        a.nblkK = (k + 127) / 128;
+        a.A = static_cast<const uint16_t*>(A);
+        a.part1 = ws.part1;
+        a.part2 = ws.part2;
+        a.sp1 = ws.sp1;
+        a.sp2 = ws.sp2;
+        a.ssum = ws.ssum;
+        a.smax = ws.smax;
+        a.smin = ws.smin;
+        a.smnz = ws.smnz;
+        a.bsum = h->buf.summary;
+        a.cr1 = ws.cr1;
+        a.cr2 = ws.cr2;
+        a.Tv = (T && o->threshold_method == 0) ? T : ws.Tv;
+        a.max_abs_a = ws.max_abs_a;
+        a.method = o->threshold_method;
+        a.aabft_t = o->aabft_mantissa_bits > 0 ? o->aabft_mantissa_bits : (h->fmt == VABFT_BF16 ? 8 : 11);
+        a.quantize_cr = offline ? 1 : 0;
+        a.e_max = o->e_max;
+        a.c_sigma = o->c_sigma;
+        a.aabft_fixed_y = o->aabft_fixed_y;
+        a.aabft_conf = o->aabft_confidence > 0 ? o->aabft_confidence : 3.0;
+        a.floor_scale = o->floor_scale;
+        a.T_out = T;
+        a.v = verdicts;
+        a.counts = counts;
+        const unsigned grid = unsigned((m + kTailRows - 1) / kTailRows);
+        check_cuda(cudaMemsetAsync(ws.max_abs_a, 0, sizeof(double), s), "memset");
+        // computed-y A-ABFT needs the global max|A| before any verdict
+        const bool two_phase = o->threshold_method == 2;
+        if (h->fmt == VABFT_BF16) {
+            if (two_phase) {
+                fused_tail_kernel<VABFT_BF16><<<grid, 128, 0, s>>>(a, 1);
+                fused_tail_kernel<VABFT_BF16><<<grid, 128, 0, s>>>(a, 2);
+            } else {
+                fused_tail_kernel<VABFT_BF16><<<grid, 128, 0, s>>>(a, 3);
+            }
+        } else {
+            if (two_phase) {
+                fused_tail_kernel<VABFT_FP16><<<grid, 128, 0, s>>>(a, 1);
+                fused_tail_kernel<VABFT_FP16><<<grid, 128, 0, s>>>(a, 2);
+            } else {
+                fused_tail_kernel<VABFT_FP16><<<grid, 128, 0, s>>>(a, 3);
+            }
+        }
         check_cuda(cudaGetLastError(), "fused tail launch");
     });
 }

@@ -38,6 +38,16 @@ struct TcEpilogue {
     const int32_t* fault_dir = nullptr;
     vabft_fault_record* fault_records = nullptr;
     float* accum_out = nullptr;  // optional M x N FP32 accumulator dump (parity API)
+    // In-GEMM A-side statistics (stats warps read the TMA-staged A tiles):
+    // per (128-column block b of K, row i), stored [b][M]. Enabled when sp1 != nullptr.
+    const float* br1 = nullptr;  // [K] B r1 (FP32, quantized for offline)
+    const float* br2 = nullptr;  // [K] B r2
+    float* sp1 = nullptr;        // partial sum_k br1[k] A[i][k] over block b (FP32, in order)
+    float* sp2 = nullptr;
+    double* ssum = nullptr;      // exact FP64 partial sum of A[i][k] over block b (see aside.cu guard)
+    uint32_t* smax = nullptr;    // packed 16x2 running max / min / min-nonzero-magnitude-1
+    uint32_t* smin = nullptr;
+    uint32_t* smnz = nullptr;
 };
 void tc_gemm_launch(int fmt, bool b_kmajor, int64_t M, int64_t N, int64_t K, const void* A,
                     const void* B, void* C, const TcEpilogue& epi, cudaStream_t stream);

@@ -5,21 +5,16 @@
 //   precompute_b_stats/BStatsSummary proj/src/threshold_vabft.cpp:8-26
 //   threshold_row/vabft_thresholds   proj/src/threshold_vabft.cpp:28-61
 //   aabft_computed_y                 proj/src/threshold_aabft.cpp:38-48
-//   encode's B r1 / B r2 and A (B r) (blocked:128 order, TENSOR engine)
+//   encode's B r1 / B r2 (blocked:128 order, TENSOR engine)
 //                                    proj/src/checksum.cpp:103-146
+// (the per-GEMM A-side pass lives in aside.cu)
 //
 // One warp per matrix row. Per-lane Neumaier sums merged across lanes with
 // TwoSum (the compensated FP64 mean equals the reference's sequential
 // Neumaier result except in pathological near-tie cases), warp-shuffle
-// max/min, FP32 checksum dot products in the reference's NativeBlocked(128)
-// order: lane l owns 128-element blocks l, l+32, ... (sequential inside a
-// block) and block partials are combined sequentially in block order.
-//
-// The per-weight B r1 / B r2 vectors are stored INTERLEAVED for the A pass:
-// element k lives at ((k%128)/8 * nblk + k/128) * 8 + k%8, so when lane b
-// consumes the 8-element granule v of its block b, the warp reads one
-// contiguous 1 KiB span (coalesced, L1/L2-resident) instead of 32 scattered
-// lines.
+// max/min, FP32 checksum sums in the reference's NativeBlocked(128) order:
+// lane l owns 128-element blocks l, l+32, ... (sequential inside a block)
+// and block partials are combined sequentially in block order.
 #include "devcommon.cuh"
 #include "internal.hpp"
 #include "numerics.cuh"
@@ -30,10 +25,6 @@ namespace vabft_dev {
 namespace {
 
 constexpr int kWarpsPerBlock = 8;
-
-__host__ __device__ __forceinline__ int64_t br_index(int64_t k, int64_t nblk) {
-    return ((k % 128) / 8 * nblk + k / 128) * 8 + (k % 8);
-}
 
 // ---------------------------------------------------------------- row stats
 template <int F>
@@ -126,7 +117,7 @@ __global__ void bside_rows_kernel(const typename Elem<F>::T* __restrict__ B, int
                 t2 = bits16_to_float<F>(quantize16_bits<F>(t2));
             }
         }
-        const int64_t idx = br_index(k, (K + 127) / 128);
+        const int64_t idx = k;  // plain layout: A-side reads are warp-uniform broadcasts
         br1[idx] = t1;
         br2[idx] = t2;
         // aabft_computed_y's FP64 row sum: the compensated sum rounded once
@@ -138,96 +129,38 @@ __global__ void bside_rows_kernel(const typename Elem<F>::T* __restrict__ B, int
 
 // BStatsSummary::from: sequential FP64 sums over k (bit-exact order) and
 // max_k |sum_j B[k][j]|. Independent chains, one thread each.
-__global__ void bside_summary_kernel(const double* mean, const double* vb, const double* rowsum_abs,
-                                     int64_t K, double* summary) {
+// Chunks of 1024 are staged through shared memory with coalesced loads so the
+// four serial chains run at add latency instead of global-load latency.
+__global__ void __launch_bounds__(1024) bside_summary_kernel(const double* mean, const double* vb,
+                                                             const double* rowsum_abs, int64_t K,
+                                                             double* summary) {
+    __shared__ double sm[3][1024];
     const int t = threadIdx.x;
     double acc = 0.0;
-    if (t == 0) {
-        for (int64_t k = 0; k < K; ++k) acc = __dadd_rn(acc, fabs(mean[k]));
-        summary[0] = acc;
-    } else if (t == 1) {
-        for (int64_t k = 0; k < K; ++k) acc = __dadd_rn(acc, __dmul_rn(mean[k], mean[k]));
-        summary[1] = acc;
-    } else if (t == 2) {
-        for (int64_t k = 0; k < K; ++k) acc = __dadd_rn(acc, vb[k]);
-        summary[2] = acc;
-    } else if (t == 3) {
-        for (int64_t k = 0; k < K; ++k) acc = fmax(acc, rowsum_abs[k]);
-        summary[3] = acc;
-    }
-}
-
-// ------------------------------------------------------ A-side (per GEMM)
-// One warp per row of 16-bit A (K % 8 == 0, the TENSOR-engine envelope):
-// row stats -> V-ABFT T_i; A (B r1), A (B r2) in FP32 blocked:128
-// (quantized for offline mode); max|A| for A-ABFT computed y. No shared
-// memory, so these CTAs co-reside with the persistent tcgen05 GEMM.
-template <int F>
-__global__ void __launch_bounds__(256) aside_kernel(const uint16_t* __restrict__ A, int64_t M,
-                                                    int64_t K, int64_t N, const float* __restrict__ br1,
-                                                    const float* __restrict__ br2,
-                                                    const double* __restrict__ bsum, int quantize_cr,
-                                                    double e_max, double c_sigma, double* T, double* cr1,
-                                                    double* cr2, double* max_abs_a) {
-    const int64_t i = int64_t(blockIdx.x) * kWarpsPerBlock + (threadIdx.x >> 5);
-    const int lane = threadIdx.x & 31;
-    if (i >= M) return;
-    const uint16_t* row = A + i * K;
-    const int64_t nblk = (K + 127) / 128;
-    Neu n;
-    float mx = -INFINITY, mn = INFINITY;
-    float t1 = 0.0f, t2 = 0.0f;
-    for (int64_t b0 = 0; b0 < nblk; b0 += 32) {
-        const int64_t b = b0 + lane;
-        float p1 = 0.0f, p2 = 0.0f;
-        if (b < nblk) {
-            const int64_t k0 = b * 128;
-            const int nv = int((K - k0) >= 128 ? 16 : (K - k0) / 8);
-#pragma unroll 2
-            for (int v = 0; v < nv; ++v) {
-                const uint4 w = __ldg(reinterpret_cast<const uint4*>(row + k0 + v * 8));
-                const float4* g1 = reinterpret_cast<const float4*>(br1 + (int64_t(v) * nblk + b) * 8);
-                const float4* g2 = reinterpret_cast<const float4*>(br2 + (int64_t(v) * nblk + b) * 8);
-                const float4 u0 = __ldg(g1), u1 = __ldg(g1 + 1), q0 = __ldg(g2), q1 = __ldg(g2 + 1);
-                const float w1[8] = {u0.x, u0.y, u0.z, u0.w, u1.x, u1.y, u1.z, u1.w};
-                const float w2[8] = {q0.x, q0.y, q0.z, q0.w, q1.x, q1.y, q1.z, q1.w};
-                const uint32_t ws[4] = {w.x, w.y, w.z, w.w};
-#pragma unroll
-                for (int h = 0; h < 8; ++h) {
-                    const uint16_t e = uint16_t(h & 1 ? ws[h >> 1] >> 16 : ws[h >> 1] & 0xFFFFu);
-                    const float xf = Elem<F>::f(e);
-                    n.add(double(xf));
-                    mx = fmaxf(mx, xf);
-                    mn = fminf(mn, xf);
-                    p1 = __fadd_rn(p1, __fmul_rn(w1[h], xf));
-                    p2 = __fadd_rn(p2, __fmul_rn(w2[h], xf));
-                }
-            }
+    for (int64_t c0 = 0; c0 < K; c0 += 1024) {
+        const int64_t k = c0 + t;
+        if (k < K) {
+            sm[0][t] = mean[k];
+            sm[1][t] = vb[k];
+            sm[2][t] = rowsum_abs[k];
         }
-        const int cnt = (nblk - b0 < 32) ? int(nblk - b0) : 32;
-        for (int l = 0; l < cnt; ++l) {
-            t1 = __fadd_rn(t1, __shfl_sync(0xffffffffu, p1, l));
-            t2 = __fadd_rn(t2, __shfl_sync(0xffffffffu, p2, l));
+        __syncthreads();
+        const int cnt = int((K - c0) < 1024 ? (K - c0) : 1024);
+        if (t == 0) {
+            for (int q = 0; q < cnt; ++q) acc = __dadd_rn(acc, fabs(sm[0][q]));
+        } else if (t == 32) {
+            for (int q = 0; q < cnt; ++q) acc = __dadd_rn(acc, __dmul_rn(sm[0][q], sm[0][q]));
+        } else if (t == 64) {
+            for (int q = 0; q < cnt; ++q) acc = __dadd_rn(acc, sm[1][q]);
+        } else if (t == 96) {
+            for (int q = 0; q < cnt; ++q) acc = fmax(acc, sm[2][q]);
         }
+        __syncthreads();
     }
-    n = warp_merge(n);
-#pragma unroll
-    for (int m = 16; m >= 1; m >>= 1) {
-        mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, m));
-        mn = fminf(mn, __shfl_xor_sync(0xffffffffu, mn, m));
-    }
-    if (lane == 0) {
-        double m, vb;
-        stats_finish(n, double(mx), double(mn), K, &m, &vb);
-        T[i] = vabft_threshold_total(m, vb, bsum[0], bsum[1], bsum[2], N, e_max, c_sigma);
-        if (quantize_cr) {
-            t1 = bits16_to_float<F>(quantize16_bits<F>(t1));
-            t2 = bits16_to_float<F>(quantize16_bits<F>(t2));
-        }
-        cr1[i] = double(t1);
-        cr2[i] = double(t2);
-        atomic_max_nonneg(max_abs_a, double(fmaxf(fabsf(mx), fabsf(mn))));
-    }
+    if (t == 0) summary[0] = acc;
+    if (t == 32) summary[1] = acc;
+    if (t == 64) summary[2] = acc;
+    if (t == 96) summary[3] = acc;
 }
 
 }  // namespace
@@ -262,22 +195,8 @@ void launch_bside(int fmt, int64_t K, int64_t N, const void* B, int quantize_br,
         default: fail(VABFT_INVALID_ARGUMENT, "bad format");
     }
     check_cuda(cudaGetLastError(), "bside launch");
-    bside_summary_kernel<<<1, 32, 0, s>>>(buf.mean, buf.vb, buf.rowsum_abs, K, buf.summary);
+    bside_summary_kernel<<<1, 1024, 0, s>>>(buf.mean, buf.vb, buf.rowsum_abs, K, buf.summary);
     check_cuda(cudaGetLastError(), "bside summary launch");
-}
-
-void launch_aside(int fmt, int64_t M, int64_t K, int64_t N, const void* A, const BsideBuffers& buf,
-                  int quantize_cr, double e_max, double c_sigma, double* T, double* cr1, double* cr2,
-                  double* max_abs_a, cudaStream_t s) {
-    if (K % 8 != 0) fail(VABFT_UNSUPPORTED, "A-side stats: K must be a multiple of 8");
-    const dim3 grid(unsigned((M + kWarpsPerBlock - 1) / kWarpsPerBlock)), block(32 * kWarpsPerBlock);
-    const uint16_t* a = static_cast<const uint16_t*>(A);
-    switch (fmt) {
-        case VABFT_BF16: aside_kernel<VABFT_BF16><<<grid, block, 0, s>>>(a, M, K, N, buf.br1, buf.br2, buf.summary, quantize_cr, e_max, c_sigma, T, cr1, cr2, max_abs_a); break;
-        case VABFT_FP16: aside_kernel<VABFT_FP16><<<grid, block, 0, s>>>(a, M, K, N, buf.br1, buf.br2, buf.summary, quantize_cr, e_max, c_sigma, T, cr1, cr2, max_abs_a); break;
-        default: fail(VABFT_UNSUPPORTED, "A-side stats: BF16/FP16 only");
-    }
-    check_cuda(cudaGetLastError(), "aside launch");
 }
 
 }  // namespace vabft_dev

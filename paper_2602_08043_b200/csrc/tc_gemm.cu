@@ -1,8 +1,10 @@
 // tcgen05 fused ABFT-GEMM for BF16/FP16 inputs with FP32 accumulation in
 // TMEM — the B200 replacement of gemm_emulated_with_accum's 16-bit path
 // (proj/src/precision.cpp:238-338) plus the epilogue half of row_sums
-// (proj/src/checksum.cpp:160-187) and the accumulator/output fault injector
-// (proj/src/faults.cpp:104-168).
+// (proj/src/checksum.cpp:160-187), the accumulator/output fault injector
+// (proj/src/faults.cpp:104-168) and, fused into the operand stream, the A-side
+// statistics of vabft_thresholds / encode (threshold_vabft.cpp:54-61,
+// checksum.cpp:103-146).
 //
 // Structure (one CTA per SM, persistent over 128 x 256 output tiles):
 //   warp 0      TMA producer: A tile 128x64 (K-major, SW128) and B tile
@@ -15,6 +17,7 @@
 //               partials r1 = sum_j v, r2 = sum_j (j+1) v in FP32, one
 //               partial per 128-column block (the reference's blocked:128
 //               reduction order), written as [block][M] for the verify tail.
+//   warps 6..9  (fused path only) A statistics: see stats_warps below.
 #include <cuda.h>
 #include <cuda_bf16.h>
 #include <cuda_fp16.h>
@@ -33,13 +36,21 @@ namespace {
 constexpr int kBM = 128;
 constexpr int kBN = 256;
 constexpr int kBK = 64;
-constexpr int kStages = 4;
-constexpr int kThreads = 192;
+#ifndef VABFT_STAGES
+#define VABFT_STAGES 4
+#endif
+constexpr int kStages = VABFT_STAGES;
+constexpr int kThreads = 192;       // TMA, MMA, 4 epilogue warps
+constexpr int kThreadsStats = 352;  // + 4 A-statistics warps + 1 statistics producer
 constexpr uint32_t kABytes = kBM * kBK * 2;  // 16 KiB
 constexpr uint32_t kBBytes = kBN * kBK * 2;  // 32 KiB
 constexpr uint32_t kStageBytes = kABytes + kBBytes;
 constexpr uint32_t kTmemCols = 512;
 constexpr size_t kSmemBytes = size_t(kStages) * kStageBytes + 1024 /*align*/ + 256 /*barriers*/;
+static_assert(size_t(kStages) * kStageBytes + 2 * (kABytes + 2 * kBK * 4) + 1024 + 256 <= 232448, "smem budget");
+// + the statistics warps' private 2-slot A ring (fused path)
+constexpr uint32_t kSlotBytes = kABytes + 2 * kBK * 4;  // A tile + B r1/B r2 segments
+constexpr size_t kSmemBytesStats = kSmemBytes + 2 * size_t(kSlotBytes);
 
 struct TcParams {
     int M, N, K;
@@ -48,8 +59,151 @@ struct TcParams {
     TcEpilogue epi;
 };
 
-template <int kFmt, bool kBKMajor, int kAbft, bool kInject>
-__global__ void __launch_bounds__(kThreads, 1)
+// ------------------------------------------------ in-GEMM A statistics
+// Four statistics warps (thread = row of the 128-row A tile). The 128-column
+// K blocks b are spread over the N tiles: the CTA computing tile
+// (m_blk, n_blk) owns the blocks with b % num_n_blk == n_blk, so each
+// (row, block) is processed exactly once and the work is balanced. For an
+// owned k-stage the TMA producer issues a second load of the same A tile
+// into the statistics warps' private 2-slot ring (own full/empty barriers),
+// so the MMA ring never waits on statistics; the next owned pair of stages
+// is ~2*num_n_blk stages away, far more than the arithmetic needs. Per
+// (row, b) the warps write the blocked:128 checksum partials
+// sum_k fl(br[k] A[i][k]) (sequential in k) and the exact FP64 row-sum
+// partial with packed max / min / min-nonzero trackers (the order-independent
+// exactness guard, see aside.cu). A tile row r lives at byte r*128 of a slot
+// with 16-byte chunk c stored at chunk c ^ (r & 7) (SWIZZLE_128B), so 8
+// consecutive threads hit 8 distinct bank groups.
+__device__ __forceinline__ uint32_t pminu2_(uint32_t a, uint32_t b) {
+    uint32_t d;
+    asm("min.u16x2 %0, %1, %2;" : "=r"(d) : "r"(a), "r"(b));
+    return d;
+}
+template <int F>
+__device__ __forceinline__ uint32_t pmax2_(uint32_t a, uint32_t b) {
+    uint32_t d;
+    if constexpr (F == VABFT_BF16) asm("max.bf16x2 %0, %1, %2;" : "=r"(d) : "r"(a), "r"(b));
+    else asm("max.f16x2 %0, %1, %2;" : "=r"(d) : "r"(a), "r"(b));
+    return d;
+}
+template <int F>
+__device__ __forceinline__ uint32_t pmin2_(uint32_t a, uint32_t b) {
+    uint32_t d;
+    if constexpr (F == VABFT_BF16) asm("min.bf16x2 %0, %1, %2;" : "=r"(d) : "r"(a), "r"(b));
+    else asm("min.f16x2 %0, %1, %2;" : "=r"(d) : "r"(a), "r"(b));
+    return d;
+}
+
+template <int F>
+struct StatsAcc {
+    float p1, p2;
+    double s0, s1;
+    uint32_t vmax, vmin, vmnz;
+    __device__ __forceinline__ void reset() {
+        p1 = p2 = 0.0f;
+        s0 = s1 = 0.0;
+        vmax = F == VABFT_BF16 ? 0xFF80FF80u : 0xFC00FC00u;
+        vmin = F == VABFT_BF16 ? 0x7F807F80u : 0x7C007C00u;
+        vmnz = 0x7FFF7FFFu;
+    }
+    // 8 consecutive elements k .. k+7 (one 16-byte granule)
+    __device__ __forceinline__ void granule(const uint4 w, const float* br1, const float* br2, int k) {
+        const float4* g1 = reinterpret_cast<const float4*>(br1 + k);  // shared memory (broadcast)
+        const float4* g2 = reinterpret_cast<const float4*>(br2 + k);
+        const float4 u0 = g1[0], u1 = g1[1], v0 = g2[0], v1 = g2[1];
+        const float b1[8] = {u0.x, u0.y, u0.z, u0.w, u1.x, u1.y, u1.z, u1.w};
+        const float b2[8] = {v0.x, v0.y, v0.z, v0.w, v1.x, v1.y, v1.z, v1.w};
+        const uint32_t ws[4] = {w.x, w.y, w.z, w.w};
+#pragma unroll
+        for (int h = 0; h < 4; ++h) {
+            vmax = pmax2_<F>(vmax, ws[h]);
+            vmin = pmin2_<F>(vmin, ws[h]);
+            vmnz = pminu2_(vmnz, (((ws[h] & 0x7FFF7FFFu) | 0x80008000u) - 0x00010001u) & 0x7FFF7FFFu);
+            const float xa = bits16_to_float<F>(uint16_t(ws[h] & 0xFFFFu));
+            const float xb = bits16_to_float<F>(uint16_t(ws[h] >> 16));
+            s0 = __dadd_rn(s0, double(xa));
+            s1 = __dadd_rn(s1, double(xb));
+            p1 = __fadd_rn(p1, __fmul_rn(b1[2 * h], xa));
+            p2 = __fadd_rn(p2, __fmul_rn(b2[2 * h], xa));
+            p1 = __fadd_rn(p1, __fmul_rn(b1[2 * h + 1], xb));
+            p2 = __fadd_rn(p2, __fmul_rn(b2[2 * h + 1], xb));
+        }
+    }
+};
+
+// Statistics producer (one thread): walks the CTA's owned (tile, 128-block,
+// k-stage) sequence and TMA-loads each A tile + its B r segments into the
+// 2-slot statistics ring, independently of the main MMA ring.
+__device__ __forceinline__ void stats_producer(const TcParams& p, const CUtensorMap* tmA, uint8_t* smS,
+                                               uint64_t* sfull_bar, uint64_t* sempty_bar) {
+    uint32_t cnt = 0;
+    const int nblk = (p.K + 127) / 128;
+    for (int tile = blockIdx.x; tile < p.num_tiles; tile += gridDim.x) {
+        const int m_blk = tile % p.num_m_blk;
+        const int n_blk = tile / p.num_m_blk;
+        for (int b = n_blk; b < nblk; b += p.num_n_blk) {
+            for (int kb = 2 * b; kb < 2 * b + 2 && kb < p.num_k_blk; ++kb, ++cnt) {
+                const int slot = int(cnt & 1u);
+                mbar_wait(smem_u32(&sempty_bar[slot]), ((cnt >> 1) & 1u) ^ 1u);
+                const uint32_t sb = smem_u32(&sfull_bar[slot]);
+                // slot layout: [A tile 0][A tile 1] (1024-aligned for SW128), then the
+                // [B r1 | B r2] segments; the br arrays are padded to 128 entries
+                const uint32_t adst = smem_u32(smS + slot * kABytes);
+                const uint32_t bdst = smem_u32(smS + 2 * kABytes + slot * (2 * kBK * 4));
+                mbar_arrive_expect_tx(sb, kSlotBytes);
+                tma_load_2d(adst, tmA, sb, kb * kBK, m_blk * kBM);
+                bulk_load(bdst, p.epi.br1 + kb * kBK, kBK * 4, sb);
+                bulk_load(bdst + kBK * 4, p.epi.br2 + kb * kBK, kBK * 4, sb);
+            }
+        }
+    }
+}
+
+template <int kFmt>
+__device__ __forceinline__ void stats_warps(const TcParams& p, const uint8_t* smS, uint64_t* sfull_bar,
+                                            uint64_t* sempty_bar, int sw, int lane) {
+    const int r = sw * 32 + lane;  // row within the 128-row tile
+    StatsAcc<kFmt> acc;
+    acc.reset();
+    uint32_t cnt = 0;  // statistics stages consumed: slot = cnt & 1, phase = (cnt >> 1) & 1
+    const int nblk = (p.K + 127) / 128;
+    for (int tile = blockIdx.x; tile < p.num_tiles; tile += gridDim.x) {
+        const int m_blk = tile % p.num_m_blk;
+        const int n_blk = tile / p.num_m_blk;
+        const int row = m_blk * kBM + r;
+        for (int b = n_blk; b < nblk; b += p.num_n_blk) {
+            for (int kb = 2 * b; kb < 2 * b + 2 && kb < p.num_k_blk; ++kb, ++cnt) {
+                const int slot = int(cnt & 1u);
+                mbar_wait(smem_u32(&sfull_bar[slot]), (cnt >> 1) & 1u);
+                const uint8_t* trow = smS + slot * kABytes + r * 128;
+                const float* sbr1 = reinterpret_cast<const float*>(smS + 2 * kABytes + slot * (2 * kBK * 4));
+                const float* sbr2 = sbr1 + kBK;
+                const int kbase = kb * kBK;
+#pragma unroll 2
+                for (int c = 0; c < 8; ++c) {
+                    if (kbase + c * 8 >= p.K) break;  // K % 8 == 0: whole granules only
+                    const uint4 w = *reinterpret_cast<const uint4*>(trow + ((c ^ (r & 7)) << 4));
+                    acc.granule(w, sbr1, sbr2, c * 8);
+                }
+                __syncwarp();
+                if (lane == 0) mbar_arrive(smem_u32(&sempty_bar[slot]));
+            }
+            if (row < p.M) {  // end of the 128-column block b
+                const size_t o = size_t(b) * p.M + row;
+                p.epi.sp1[o] = acc.p1;
+                p.epi.sp2[o] = acc.p2;
+                p.epi.ssum[o] = __dadd_rn(acc.s0, acc.s1);
+                p.epi.smax[o] = acc.vmax;
+                p.epi.smin[o] = acc.vmin;
+                p.epi.smnz[o] = acc.vmnz;
+            }
+            acc.reset();
+        }
+    }
+}
+
+template <int kFmt, bool kBKMajor, int kAbft, bool kInject, bool kStats>
+__global__ void __launch_bounds__(kThreadsStats, 1)
     tc_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                    const TcParams p) {
     extern __shared__ uint8_t smem_raw[];
@@ -57,12 +211,15 @@ __global__ void __launch_bounds__(kThreads, 1)
                                                ~uintptr_t(1023));
     uint8_t* smA = smem;
     uint8_t* smB = smem + kStages * kABytes;
-    uint64_t* bars = reinterpret_cast<uint64_t*>(smem + kStages * kStageBytes);
+    uint8_t* smS = smem + kStages * kStageBytes;  // statistics ring (kStats only)
+    uint64_t* bars = reinterpret_cast<uint64_t*>(smS + (kStats ? 2 * kSlotBytes : 0));
     uint64_t* full_bar = bars;
     uint64_t* empty_bar = bars + kStages;
     uint64_t* tfull_bar = bars + 2 * kStages;
     uint64_t* tempty_bar = bars + 2 * kStages + 2;
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * kStages + 4);
+    uint64_t* sfull_bar = bars + 2 * kStages + 4;
+    uint64_t* sempty_bar = bars + 2 * kStages + 6;
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * kStages + 8);
 
     const int warp = threadIdx.x >> 5;
     const int lane = threadIdx.x & 31;
@@ -70,11 +227,13 @@ __global__ void __launch_bounds__(kThreads, 1)
     if (threadIdx.x == 0) {
         for (int s = 0; s < kStages; ++s) {
             mbar_init(smem_u32(&full_bar[s]), 1);
-            mbar_init(smem_u32(&empty_bar[s]), 1);
+            mbar_init(smem_u32(&empty_bar[s]), 1);  // MMA commit
         }
         for (int a = 0; a < 2; ++a) {
             mbar_init(smem_u32(&tfull_bar[a]), 1);
             mbar_init(smem_u32(&tempty_bar[a]), 4);
+            mbar_init(smem_u32(&sfull_bar[a]), 1);
+            mbar_init(smem_u32(&sempty_bar[a]), 4);  // the 4 statistics warps
         }
         fence_mbar_init();
         tma_prefetch_desc(&tmA);
@@ -156,6 +315,12 @@ __global__ void __launch_bounds__(kThreads, 1)
                 }
             }
         }
+    } else if (warp == 10) {
+        if constexpr (kStats) {
+            if (lane == 0) stats_producer(p, &tmA, smS, sfull_bar, sempty_bar);
+        }
+    } else if (warp >= 6) {
+        if constexpr (kStats) stats_warps<kFmt>(p, smS, sfull_bar, sempty_bar, warp - 6, lane);
     } else {
         // ------------------------------------------------------- epilogue
         const int quad = warp & 3;  // TMEM lanes [32*quad, 32*quad+32) are addressable by this warp
@@ -204,12 +369,12 @@ __global__ void __launch_bounds__(kThreads, 1)
                                 const bool ok = bit_eligible(q, fbit, fdir);
                                 const uint16_t q2 = ok ? uint16_t(q ^ (1u << fbit)) : q;
                                 if (p.epi.fault_records) {
-                                    vabft_fault_record r;
-                                    r.value_before = double(bits16_to_float<kFmt>(q));
-                                    r.value_after = double(bits16_to_float<kFmt>(q2));
-                                    r.applied = ok ? 1 : 0;
-                                    r.reserved = 0;
-                                    p.epi.fault_records[row] = r;
+                                    vabft_fault_record rr;
+                                    rr.value_before = double(bits16_to_float<kFmt>(q));
+                                    rr.value_after = double(bits16_to_float<kFmt>(q2));
+                                    rr.applied = ok ? 1 : 0;
+                                    rr.reserved = 0;
+                                    p.epi.fault_records[row] = rr;
                                 }
                                 q = q2;
                             }
@@ -222,16 +387,16 @@ __global__ void __launch_bounds__(kThreads, 1)
                     } else {
                         if constexpr (kAbft == 1 && kInject) {
                             if (col == fcol) {
-                                const uint32_t b = __float_as_uint(x);
-                                const bool ok = bit_eligible(b, fbit, fdir);
-                                const uint32_t b2 = ok ? (b ^ (1u << fbit)) : b;
+                                const uint32_t bb = __float_as_uint(x);
+                                const bool ok = bit_eligible(bb, fbit, fdir);
+                                const uint32_t b2 = ok ? (bb ^ (1u << fbit)) : bb;
                                 if (p.epi.fault_records) {
-                                    vabft_fault_record r;
-                                    r.value_before = double(x);
-                                    r.value_after = double(__uint_as_float(b2));
-                                    r.applied = ok ? 1 : 0;
-                                    r.reserved = 0;
-                                    p.epi.fault_records[row] = r;
+                                    vabft_fault_record rr;
+                                    rr.value_before = double(x);
+                                    rr.value_after = double(__uint_as_float(b2));
+                                    rr.applied = ok ? 1 : 0;
+                                    rr.reserved = 0;
+                                    p.epi.fault_records[row] = rr;
                                 }
                                 x = __uint_as_float(b2);
                             }
@@ -340,19 +505,19 @@ CUtensorMap make_map_2d(int fmt, const void* base, uint64_t rows, uint64_t cols,
     return m;
 }
 
-template <int kFmt, bool kBKMajor, int kAbft, bool kInject>
+template <int kFmt, bool kBKMajor, int kAbft, bool kInject, bool kStats = false>
 void launch_inst(const CUtensorMap& ta, const CUtensorMap& tb, const TcParams& p,
                  cudaStream_t stream) {
-    auto kern = tc_gemm_kernel<kFmt, kBKMajor, kAbft, kInject>;
+    auto kern = tc_gemm_kernel<kFmt, kBKMajor, kAbft, kInject, kStats>;
     static bool attr_set = false;  // per instantiation
     if (!attr_set) {
         check_cuda(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                        int(kSmemBytes)),
+                                        int(kStats ? kSmemBytesStats : kSmemBytes)),
                    "cudaFuncSetAttribute(tc_gemm)");
         attr_set = true;
     }
     const int grid = p.num_tiles < sm_count() ? p.num_tiles : sm_count();
-    kern<<<grid, kThreads, kSmemBytes, stream>>>(ta, tb, p);
+    kern<<<grid, kStats ? kThreadsStats : kThreads, kStats ? kSmemBytesStats : kSmemBytes, stream>>>(ta, tb, p);
     check_cuda(cudaGetLastError(), "tc_gemm launch");
 }
 
@@ -360,15 +525,26 @@ template <int kFmt, bool kBKMajor>
 void dispatch_epi(const CUtensorMap& ta, const CUtensorMap& tb, const TcParams& p,
                   cudaStream_t stream) {
     const bool inj = p.epi.fault_col != nullptr;
+    const bool st = p.epi.sp1 != nullptr;
     switch (p.epi.abft) {
         case 0: launch_inst<kFmt, kBKMajor, 0, false>(ta, tb, p, stream); break;
         case 1:
-            if (inj) launch_inst<kFmt, kBKMajor, 1, true>(ta, tb, p, stream);
-            else launch_inst<kFmt, kBKMajor, 1, false>(ta, tb, p, stream);
+            if (st) {
+                if (inj) launch_inst<kFmt, kBKMajor, 1, true, true>(ta, tb, p, stream);
+                else launch_inst<kFmt, kBKMajor, 1, false, true>(ta, tb, p, stream);
+            } else {
+                if (inj) launch_inst<kFmt, kBKMajor, 1, true>(ta, tb, p, stream);
+                else launch_inst<kFmt, kBKMajor, 1, false>(ta, tb, p, stream);
+            }
             break;
         default:
-            if (inj) launch_inst<kFmt, kBKMajor, 2, true>(ta, tb, p, stream);
-            else launch_inst<kFmt, kBKMajor, 2, false>(ta, tb, p, stream);
+            if (st) {
+                if (inj) launch_inst<kFmt, kBKMajor, 2, true, true>(ta, tb, p, stream);
+                else launch_inst<kFmt, kBKMajor, 2, false, true>(ta, tb, p, stream);
+            } else {
+                if (inj) launch_inst<kFmt, kBKMajor, 2, true>(ta, tb, p, stream);
+                else launch_inst<kFmt, kBKMajor, 2, false>(ta, tb, p, stream);
+            }
             break;
     }
 }

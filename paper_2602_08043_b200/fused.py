@@ -71,6 +71,7 @@ class FusedAbftGemm:
         check(lib.vabft_bside_create(self.fmt, self.mode, self.k, self.n, ptr(self.B), C.byref(self.h),
                                      stream_ptr()))
         self._ws = None
+        self._bufs = {}
 
     def update_weight(self, B: torch.Tensor) -> None:
         self.B = B.contiguous()
@@ -85,23 +86,36 @@ class FusedAbftGemm:
 
     def __call__(self, A: torch.Tensor, out: Optional[torch.Tensor] = None, *, verdicts: bool = True,
                  thresholds: bool = True, counts: Optional[torch.Tensor] = None,
-                 faults: Optional[dict] = None) -> FusedResult:
+                 faults: Optional[dict] = None, stages: int = 0) -> FusedResult:
         if A.dtype != self.B.dtype or A.dim() != 2 or A.shape[1] != self.k:
             raise _capi.InvalidArgument("FusedAbftGemm: A must be M x K with B's dtype")
         m = A.shape[0]
-        dev = A.device
-        C_ = out if out is not None else torch.empty((m, self.n), dtype=A.dtype, device=dev)
-        T = torch.empty(m, dtype=torch.float64, device=dev) if thresholds else None
+        # output buffers are cached per M (valid until the next call with the
+        # same M) so the hot loop allocates nothing
+        bufs = self._bufs.get(m)
+        if bufs is None:
+            dev = A.device
+            bufs = {"C": torch.empty((m, self.n), dtype=A.dtype, device=dev),
+                    "T": torch.empty(m, dtype=torch.float64, device=dev),
+                    "d1": torch.empty(m, dtype=torch.float64, device=dev),
+                    "d2": torch.empty(m, dtype=torch.float64, device=dev),
+                    "res": torch.empty(m, dtype=torch.float64, device=dev),
+                    "det": torch.empty(m, dtype=torch.uint8, device=dev),
+                    "loc": torch.empty(m, dtype=torch.int64, device=dev)}
+            self._bufs[m] = bufs
+        C_ = out if out is not None else bufs["C"]
+        T = bufs["T"] if thresholds else None
         if verdicts:
-            d1, d2, res = (torch.empty(m, dtype=torch.float64, device=dev) for _ in range(3))
-            det = torch.empty(m, dtype=torch.uint8, device=dev)
-            loc = torch.empty(m, dtype=torch.int64, device=dev)
+            d1, d2, res, det, loc = bufs["d1"], bufs["d2"], bufs["res"], bufs["det"], bufs["loc"]
         else:
             d1 = d2 = res = det = loc = None
         v = _capi.Verdicts(ptr(d1), ptr(d2), ptr(det), ptr(loc), ptr(res))
         opts = self.opts
-        if faults is not None:
+        if stages:
             opts = _capi.FusedOpts.from_buffer_copy(self.opts)
+            opts.stages = stages
+        if faults is not None:
+            opts = _capi.FusedOpts.from_buffer_copy(opts)
             opts.fault_col = ptr(faults["col"])
             opts.fault_bit = ptr(faults["bit"])
             opts.fault_dir = ptr(faults["dir"])

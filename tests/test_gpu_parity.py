@@ -169,15 +169,24 @@ def test_tensor_engine_parity(api, port, fmt, mode, shape):
     # C is the quantized accumulator (RNE, saturating)
     q = np.array([port.quantize(x, fmt) for x in e.c_accum.ravel()]).reshape(e.c.shape)
     assert same(e.c, q)
-    # checksums: blocked:128 order, bit-exact against the oracle restatement
-    ob = port.encode_and_multiply(A, B, "fp32" if fmt == "fp32" else fmt, mode)  # noqa: F841 (shape/mode check)
+    # checksums: FP32 blocked:128 order, bit-exact against the restatement
     blk = _blocked_checksums(port, A, B, fmt, mode)
     assert same(e.row_check1, blk[0]) and same(e.row_check2, blk[1])
-    # row sums of the device accumulator in blocked:128 == reference row_sums(blocked:128)
+    # row sums of the device accumulator / output == reference row_sums with
+    # an FP32 NativeBlocked(128) sum precision
     src = e.verification_source()
     r1, r2 = api.row_sums(src, e.checksum_precision, e.verification_format())
-    p1, p2 = port.row_sums(src, fmt, mode, accum=(2, 128))
+    p1, p2 = port.row_sums(src, "fp32", "offline", accum=(2, 128))
     assert same(r1, p1) and same(r2, p2)
+    # verdicts on planted faults: device verify == oracle verify (same inputs)
+    src2 = src.copy()
+    src2[1, 3] += 7.0
+    src2[5, n - 1] = -src2[5, n - 1] * 9.0 + 1.0
+    T = np.full(m, 1e-3)
+    v = api.verify_arrays(src2, "fp32", e.row_check1, e.row_check2, T, e.checksum_precision)
+    o = port.verify(src2, e.row_check1, e.row_check2, T, "fp32", "offline", accum=(2, 128))
+    assert same(v["diff1"], o["diff1"]) and same(v["diff2"], o["diff2"])
+    assert np.array_equal(v["detected"], o["detected"]) and np.array_equal(v["location"], o["location"])
 
 
 def _blocked_checksums(port, A, B, fmt, mode):
