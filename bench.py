@@ -185,7 +185,7 @@ def run_ours(args, cfg):
         Bs.append(torch.randn(k, n, device=dev).bfloat16())
         Cs.append(torch.empty(m, n, device=dev, dtype=torch.bfloat16))
         gs.append(FusedAbftGemm(Bs[-1], mode=args.mode))
-    counts = torch.zeros(4, dtype=torch.int64, device=dev)
+    counts = torch.zeros(5, dtype=torch.int64, device=dev)
     flush = torch.empty(512 * 1024 * 1024, dtype=torch.uint8, device=dev)
     stream = torch.cuda.current_stream()
 
@@ -283,7 +283,7 @@ def run_ours(args, cfg):
     hA = [A.cpu().pin_memory() for A in As]
     hB = [B.cpu().pin_memory() for B in Bs]
     hC = [torch.empty(Cc.shape, dtype=Cc.dtype).pin_memory() for Cc in Cs]
-    hcounts = torch.zeros(4, dtype=torch.int64).pin_memory()
+    hcounts = torch.zeros(5, dtype=torch.int64).pin_memory()
     dA2 = [torch.empty_like(A) for A in As]
     dB2 = [torch.empty_like(B) for B in Bs]
     g_e2e = [FusedAbftGemm(dB, mode=args.mode) for dB in dB2]

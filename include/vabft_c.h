@@ -97,6 +97,8 @@ typedef struct vabft_verdicts {
     uint8_t* detected;
     int64_t* location;
     double* residual;
+    double* row_check1; /* EncodedProduct::row_check1/2 (fused path only; may be NULL) */
+    double* row_check2;
 } vabft_verdicts;
 
 /* Aggregate counters written by the verify tails (device, int64). Layout of
@@ -106,7 +108,8 @@ typedef struct vabft_verdicts {
 #define VABFT_COUNT_DETECTED 1
 #define VABFT_COUNT_LOCATED 2
 #define VABFT_COUNT_NAN 3
-#define VABFT_NUM_COUNTS 4
+#define VABFT_COUNT_SLOW_STATS 4 /* rows whose A-row mean needed the sequential fallback */
+#define VABFT_NUM_COUNTS 5
 
 /* One planned fault (InjectionRecord inputs, faults.hpp:21-35). */
 typedef struct vabft_fault {

@@ -25,7 +25,7 @@ ACCUM_FP32_ROUND_OUTPUT, ACCUM_SEQUENTIAL, ACCUM_BLOCKED, ACCUM_PAIRWISE = range
 OFFLINE, ONLINE = 0, 1
 FLIP, SET0TO1, SET1TO0, ANY = range(4)
 ENGINE_EXACT, ENGINE_TENSOR = 0, 1
-COUNT_ROWS, COUNT_DETECTED, COUNT_LOCATED, COUNT_NAN, NUM_COUNTS = 0, 1, 2, 3, 4
+COUNT_ROWS, COUNT_DETECTED, COUNT_LOCATED, COUNT_NAN, COUNT_SLOW_STATS, NUM_COUNTS = 0, 1, 2, 3, 4, 5
 
 FORMAT_CODES = {"bf16": BF16, "fp16": FP16, "fp32": FP32, "fp64": FP64}
 
@@ -42,7 +42,8 @@ class Precision(C.Structure):
 
 class Verdicts(C.Structure):
     _fields_ = [("diff1", C.c_void_p), ("diff2", C.c_void_p), ("detected", C.c_void_p),
-                ("location", C.c_void_p), ("residual", C.c_void_p)]
+                ("location", C.c_void_p), ("residual", C.c_void_p), ("row_check1", C.c_void_p),
+                ("row_check2", C.c_void_p)]
 
 
 class Fault(C.Structure):

@@ -480,7 +480,7 @@ def verify_arrays(source: np.ndarray, src_format: str, row_check1, row_check2, t
     det = torch.empty(m, dtype=torch.uint8, device="cuda")
     loc = torch.empty(m, dtype=torch.int64, device="cuda")
     counts = torch.zeros(_capi.NUM_COUNTS, dtype=torch.int64, device="cuda")
-    v = _capi.Verdicts(ptr(d1), ptr(d2), ptr(det), ptr(loc), ptr(res))
+    v = _capi.Verdicts(ptr(d1), ptr(d2), ptr(det), ptr(loc), ptr(res), None, None)
     check(lib.vabft_verify(C.byref(checksum_precision.to_c()), _capi.FORMAT_CODES[src_format], m, n, ptr(dS),
                            ptr(rc1), ptr(rc2), ptr(T), opts.localization_floor_scale, v, ptr(counts),
                            stream_ptr()))

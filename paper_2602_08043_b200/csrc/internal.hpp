@@ -28,10 +28,35 @@ inline void check_cuda(cudaError_t e, const char* what) {
 int sm_count();
 size_t elem_size(int fmt);
 
+// ---- verify tail (tail.cuh): inputs of one fused launch
+struct TailArgs {
+    int64_t M, N, K, nblkN, nblkK;
+    const uint16_t* A;
+    const float *part1, *part2;          // C row partials (part_index, nb = nblkN)
+    const float *sp1, *sp2;              // A (B r) partials (nb = nblkK)
+    // per-row order-independent A statistics, accumulated with atomics by the
+    // statistics warps and reset to their identities by the tail after use:
+    double* rsum;                        // exact FP64 row sum (identity 0.0)
+    uint32_t *rmax, *rmin, *rmnz;        // order keys of max / min (identities 0 / ~0),
+                                         // smallest nonzero magnitude - 1 (identity ~0)
+    const double* bsum;                  // B summary (4)
+    double *cr1, *cr2, *Tv;              // [M] staged between two-phase passes
+    double* max_abs_a;
+    int method, aabft_t, quantize_cr;
+    double e_max, c_sigma, aabft_fixed_y, aabft_conf, floor_scale;
+    double* T_out;
+    vabft_verdicts v;
+    int64_t* counts;
+};
+
 // ---- tcgen05 GEMM (tc_gemm.cu)
 struct TcEpilogue {
     int abft = 0;             // 0 none, 1 online (FP32 accum), 2 offline (quantized C)
-    float* part1 = nullptr;   // [ceil(N/128)][M] row partials of C r1
+    // Every partial array is row-group-major: element (block b, row i) of an
+    // array with nb blocks lives at ((i / 32) * nb + b) * 32 + i % 32, so a
+    // warp's 32 rows write 128 contiguous bytes and the verify tail fetches
+    // one row group's whole array with a single bulk copy (see part_index).
+    float* part1 = nullptr;   // C r1 row partials, nb = ceil(N/128)
     float* part2 = nullptr;   // [ceil(N/128)][M] row partials of C r2
     const int32_t* fault_col = nullptr;
     const int32_t* fault_bit = nullptr;
@@ -44,11 +69,21 @@ struct TcEpilogue {
     const float* br2 = nullptr;  // [K] B r2
     float* sp1 = nullptr;        // partial sum_k br1[k] A[i][k] over block b (FP32, in order)
     float* sp2 = nullptr;
-    double* ssum = nullptr;      // exact FP64 partial sum of A[i][k] over block b (see aside.cu guard)
-    uint32_t* smax = nullptr;    // packed 16x2 running max / min / min-nonzero-magnitude-1
-    uint32_t* smin = nullptr;
-    uint32_t* smnz = nullptr;
+    double* rsum = nullptr;      // per-row atomics, see TailArgs
+    uint32_t* rmax = nullptr;
+    uint32_t* rmin = nullptr;
+    uint32_t* rmnz = nullptr;
+    int debug = 0;  // profiling ablations (VABFT_DEBUG_STATS): 1 = no stats loads, 2 = no stats math
+    // In-kernel verify tail after a grid barrier (cooperative launch):
+    // 0 = none, 3 = single pass, 1|2 = two passes with a second barrier.
+    int tail_phases = 0;
+    unsigned int* gbar = nullptr;  // [count, generation], zero-initialised once
+    TailArgs tail;
 };
+__host__ __device__ inline size_t part_index(int64_t b, int64_t row, int64_t nb) {
+    return size_t(((row >> 5) * nb + b) * 32 + (row & 31));
+}
+
 void tc_gemm_launch(int fmt, bool b_kmajor, int64_t M, int64_t N, int64_t K, const void* A,
                     const void* B, void* C, const TcEpilogue& epi, cudaStream_t stream);
 bool tc_gemm_supported(int fmt, int64_t M, int64_t N, int64_t K);

@@ -1,0 +1,218 @@
+// Verify tail of the fused V-ABFT GEMM, as a warp-level device function so it
+// runs both inside the persistent tcgen05 kernel (after a grid barrier) and as
+// a standalone kernel (profiling stage mask).
+//
+//   A-row statistics -> V-ABFT T_i   threshold_vabft.cpp:28-61, stats.cpp:9-32
+//   A (B r) checksums, C r row sums  checksum.cpp:103-187 (FP32, blocked:128)
+//   D1/D2, strict compare, NaN rule, localization, correction
+//                                    detect.cpp:9-55
+//
+// One warp owns a 32-row group (lane = row). The ordered FP32 partials are
+// row-group-major (part_index), so the group's segment of each array is one
+// contiguous span: lane 0 fetches them with cp.async.bulk into the warp's
+// shared-memory slice (one memory round trip per chunk) and every lane then
+// combines its row's partials in block order. The order-independent A-row
+// statistics come from per-row atomics, which the tail resets after use.
+#pragma once
+
+#include "devcommon.cuh"
+#include "internal.hpp"
+#include "numerics.cuh"
+#include "ptx.cuh"
+
+namespace vabft_dev {
+
+constexpr int kTailChunkBlocks = 96;                        // blocks per bulk round trip
+constexpr uint32_t kTailWarpSmem = 2u * kTailChunkBlocks * 32 * 4;  // 24 KiB per warp
+
+// order-preserving uint32 keys of floats (for atomicMax / atomicMin)
+__device__ __forceinline__ uint32_t fkey(float f) {
+    const uint32_t u = __float_as_uint(f);
+    return (u & 0x80000000u) ? ~u : (u | 0x80000000u);
+}
+__device__ __forceinline__ float fkey_decode(uint32_t k) {
+    return __uint_as_float((k & 0x80000000u) ? (k & 0x7FFFFFFFu) : ~k);
+}
+
+// n * max|x| < 2^(53 + lsb(min nonzero |x|)) => plain FP64 sums of the row are
+// exact in any order (so they equal the reference's sequential Neumaier
+// result); mnz_pat is (smallest nonzero magnitude - 1), >= 0x7FFF if none.
+template <int F>
+__device__ __forceinline__ bool guard_exact(float max_abs, uint32_t mnz_pat, int64_t n) {
+    if (mnz_pat >= 0x7FFFu) return true;
+    if (!isfinite(max_abs)) return false;
+    const uint32_t pat = mnz_pat + 1;
+    int lsb;
+    if constexpr (F == VABFT_BF16) {
+        const int ef = int((pat >> 7) & 0xFF);
+        lsb = (ef == 0 ? 1 : ef) - 127 - 7;
+    } else {
+        const int ef = int((pat >> 10) & 0x1F);
+        lsb = (ef == 0 ? 1 : ef) - 15 - 10;
+    }
+    const int top = ilogbf(max_abs) + 1 + (64 - __clzll(static_cast<unsigned long long>(n)));
+    return top <= 53 + lsb;
+}
+
+// Sequentially accumulate arrays x1/x2 (blocks [0, nb) of row group g) in
+// block order, fetching chunks through the warp's smem slice.
+__device__ __forceinline__ void ordered_sums(const float* x1, const float* x2, int64_t nb, int64_t g,
+                                             float* sbuf, uint32_t bar, uint32_t& bar_phase,
+                                             float& r1, float& r2) {
+    const int lane = threadIdx.x & 31;
+    const size_t base = part_index(0, g * 32, nb);
+    for (int64_t b0 = 0; b0 < nb; b0 += kTailChunkBlocks) {
+        const int64_t cnt = (nb - b0) < kTailChunkBlocks ? (nb - b0) : kTailChunkBlocks;
+        const uint32_t bytes = uint32_t(cnt * 32 * 4);
+        __syncwarp();
+        if (lane == 0) {
+            mbar_arrive_expect_tx(bar, 2 * bytes);
+            bulk_load(smem_u32(sbuf), x1 + base + b0 * 32, bytes, bar);
+            bulk_load(smem_u32(sbuf + kTailChunkBlocks * 32), x2 + base + b0 * 32, bytes, bar);
+        }
+        mbar_wait(bar, bar_phase);
+        bar_phase ^= 1u;
+        for (int64_t b = 0; b < cnt; ++b) {  // reduce_terms NativeBlocked(128), in order
+            r1 = __fadd_rn(r1, sbuf[b * 32 + lane]);
+            r2 = __fadd_rn(r2, sbuf[kTailChunkBlocks * 32 + b * 32 + lane]);
+        }
+    }
+}
+
+// phase bit 1: statistics -> T_i and A (B r); bit 2: row sums + verify.
+// Phase 1 alone stages cr1/cr2/Tv for a later phase-2 pass (A-ABFT computed y
+// needs the global max|A| first).
+template <int F>
+__device__ void verify_rowgroup(const TailArgs& a, int64_t g, int phase, float* sbuf, uint32_t bar,
+                                uint32_t& bar_phase) {
+    const int lane = threadIdx.x & 31;
+    const int64_t i = g * 32 + lane;
+    const bool valid = i < a.M;
+    bool det = false, located = false, isnan_row = false;
+    double c1 = 0.0, c2 = 0.0, tv = 0.0;
+    if (phase & 1) {
+        float t1 = 0.0f, t2 = 0.0f;
+        ordered_sums(a.sp1, a.sp2, a.nblkK, g, sbuf, bar, bar_phase, t1, t2);
+        float amax = 0.0f;
+        if (valid) {
+            double sum = __ldcg(a.rsum + i);
+            const float mx = fkey_decode(__ldcg(a.rmax + i));
+            const float mn = fkey_decode(__ldcg(a.rmin + i));
+            const uint32_t mnz = __ldcg(a.rmnz + i);
+            // reset to the identities for the next launch
+            a.rsum[i] = 0.0;
+            a.rmax[i] = 0u;
+            a.rmin[i] = 0xFFFFFFFFu;
+            a.rmnz[i] = 0xFFFFFFFFu;
+            amax = fmaxf(fabsf(mx), fabsf(mn));
+            if (!guard_exact<F>(amax, mnz, a.K)) {
+                // the reference's sequential Neumaier pass over the row (stats.cpp:12-24)
+                if (a.counts) atomicAdd(reinterpret_cast<unsigned long long*>(a.counts + VABFT_COUNT_SLOW_STATS), 1ull);
+                Neu ns;
+                const uint16_t* row = a.A + i * a.K;
+                for (int64_t q = 0; q < a.K; ++q) ns.add(double(bits16_to_float<F>(row[q])));
+                sum = __dadd_rn(ns.s, ns.c);
+            }
+            Neu fin;
+            fin.s = sum;
+            double mean, vb;
+            stats_finish(fin, double(mx), double(mn), a.K, &mean, &vb);
+            tv = vabft_threshold_total(mean, vb, a.bsum[0], a.bsum[1], a.bsum[2], a.N, a.e_max, a.c_sigma);
+            if (a.quantize_cr) {
+                t1 = bits16_to_float<F>(quantize16_bits<F>(t1));
+                t2 = bits16_to_float<F>(quantize16_bits<F>(t2));
+            }
+            c1 = double(t1);
+            c2 = double(t2);
+            if (phase == 1) {
+                a.cr1[i] = c1;
+                a.cr2[i] = c2;
+                a.Tv[i] = tv;
+            }
+        }
+        if (a.method == 2) {  // one atomic per warp for max|A| (A-ABFT computed y)
+            float wmax = amax;
+#pragma unroll
+            for (int m = 16; m >= 1; m >>= 1) wmax = fmaxf(wmax, __shfl_xor_sync(0xffffffffu, wmax, m));
+            if (lane == 0) atomic_max_nonneg(a.max_abs_a, double(wmax));
+        }
+    }
+    if (!(phase & 2)) return;
+    float r1 = 0.0f, r2 = 0.0f;
+    ordered_sums(a.part1, a.part2, a.nblkN, g, sbuf, bar, bar_phase, r1, r2);
+    if (valid) {
+        if (!(phase & 1)) {
+            c1 = a.cr1[i];
+            c2 = a.cr2[i];
+            tv = a.Tv[i];
+        }
+        double t;
+        if (a.method == 0) {
+            t = tv;
+        } else {
+            const double y = a.method == 1 ? a.aabft_fixed_y : __dmul_rn(*a.max_abs_a, a.bsum[3]);
+            t = aabft_total(a.K, a.aabft_t, y, a.aabft_conf);
+        }
+        if (a.T_out) a.T_out[i] = t;
+        const double d1 = __dsub_rn(double(r1), c1);
+        const double d2 = __dsub_rn(double(r2), c2);
+        int64_t loc = -1;
+        double res = 0.0;
+        if (isnan(d1) || isnan(d2)) {
+            det = true;
+            isnan_row = true;
+        } else {
+            det = fabs(d1) > t;
+            if (det && fabs(d1) > __dmul_rn(a.floor_scale, t)) {
+                int64_t j;
+                double rr;
+                if (localize_dev(d1, d2, a.N, &j, &rr)) {
+                    loc = j;
+                    res = rr;
+                    located = true;
+                }
+            }
+        }
+        if (a.v.diff1) a.v.diff1[i] = d1;
+        if (a.v.diff2) a.v.diff2[i] = d2;
+        if (a.v.detected) a.v.detected[i] = det ? 1 : 0;
+        if (a.v.location) a.v.location[i] = loc;
+        if (a.v.residual) a.v.residual[i] = res;
+        if (a.v.row_check1) a.v.row_check1[i] = c1;
+        if (a.v.row_check2) a.v.row_check2[i] = c2;
+    }
+    if (a.counts) {
+        const unsigned mv = __ballot_sync(0xffffffffu, valid);
+        const unsigned md = __ballot_sync(0xffffffffu, det);
+        const unsigned ml = __ballot_sync(0xffffffffu, located);
+        const unsigned mn = __ballot_sync(0xffffffffu, isnan_row);
+        if (lane == 0) {
+            if (mv) atomicAdd(reinterpret_cast<unsigned long long*>(a.counts + VABFT_COUNT_ROWS), __popc(mv));
+            if (md) atomicAdd(reinterpret_cast<unsigned long long*>(a.counts + VABFT_COUNT_DETECTED), __popc(md));
+            if (ml) atomicAdd(reinterpret_cast<unsigned long long*>(a.counts + VABFT_COUNT_LOCATED), __popc(ml));
+            if (mn) atomicAdd(reinterpret_cast<unsigned long long*>(a.counts + VABFT_COUNT_NAN), __popc(mn));
+        }
+    }
+}
+
+// Self-resetting grid barrier for a co-resident (cooperative) grid: the last
+// arriving CTA resets the count and bumps the generation, so the same state
+// works across launches and CUDA-graph replays.
+__device__ __forceinline__ void grid_barrier(unsigned int* count, volatile unsigned int* gen) {
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        const unsigned int my_gen = *gen;
+        __threadfence();
+        if (atomicAdd(count, 1u) == gridDim.x - 1) {
+            *count = 0;
+            __threadfence();
+            atomicAdd(const_cast<unsigned int*>(gen), 1u);
+        } else {
+            while (*gen == my_gen) __nanosleep(64);
+        }
+        __threadfence();
+    }
+    __syncthreads();
+}
+
+}  // namespace vabft_dev

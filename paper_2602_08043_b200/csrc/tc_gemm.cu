@@ -28,6 +28,7 @@
 #include "internal.hpp"
 #include "numerics.cuh"
 #include "ptx.cuh"
+#include "tail.cuh"
 
 namespace vabft_dev {
 
@@ -51,6 +52,11 @@ static_assert(size_t(kStages) * kStageBytes + 2 * (kABytes + 2 * kBK * 4) + 1024
 // + the statistics warps' private 2-slot A ring (fused path)
 constexpr uint32_t kSlotBytes = kABytes + 2 * kBK * 4;  // A tile + B r1/B r2 segments
 constexpr size_t kSmemBytesStats = kSmemBytes + 2 * size_t(kSlotBytes);
+// warps running the in-kernel verify tail, each with a 24 KiB slice of the
+// (then idle) pipeline shared memory
+constexpr int kTailWarps = 9;
+static_assert(kTailWarps * kTailWarpSmem <= kStages * kStageBytes + 2 * kSlotBytes, "tail smem slices");
+static_assert((2 * kStages + 9 + kTailWarps) * 8 <= 256, "barrier area");
 
 struct TcParams {
     int M, N, K;
@@ -150,6 +156,10 @@ __device__ __forceinline__ void stats_producer(const TcParams& p, const CUtensor
                 // [B r1 | B r2] segments; the br arrays are padded to 128 entries
                 const uint32_t adst = smem_u32(smS + slot * kABytes);
                 const uint32_t bdst = smem_u32(smS + 2 * kABytes + slot * (2 * kBK * 4));
+                if (p.epi.debug == 1) {  // ablation: no statistics loads
+                    mbar_arrive(sb);
+                    continue;
+                }
                 mbar_arrive_expect_tx(sb, kSlotBytes);
                 tma_load_2d(adst, tmA, sb, kb * kBK, m_blk * kBM);
                 bulk_load(bdst, p.epi.br1 + kb * kBK, kBK * 4, sb);
@@ -183,19 +193,26 @@ __device__ __forceinline__ void stats_warps(const TcParams& p, const uint8_t* sm
                 for (int c = 0; c < 8; ++c) {
                     if (kbase + c * 8 >= p.K) break;  // K % 8 == 0: whole granules only
                     const uint4 w = *reinterpret_cast<const uint4*>(trow + ((c ^ (r & 7)) << 4));
-                    acc.granule(w, sbr1, sbr2, c * 8);
+                    if (p.epi.debug != 2) acc.granule(w, sbr1, sbr2, c * 8);  // 2: ablation, no math
                 }
                 __syncwarp();
                 if (lane == 0) mbar_arrive(smem_u32(&sempty_bar[slot]));
             }
             if (row < p.M) {  // end of the 128-column block b
-                const size_t o = size_t(b) * p.M + row;
+                const size_t o = part_index(b, row, nblk);
                 p.epi.sp1[o] = acc.p1;
                 p.epi.sp2[o] = acc.p2;
-                p.epi.ssum[o] = __dadd_rn(acc.s0, acc.s1);
-                p.epi.smax[o] = acc.vmax;
-                p.epi.smin[o] = acc.vmin;
-                p.epi.smnz[o] = acc.vmnz;
+                // order-independent statistics: per-row atomics (exact sum under
+                // the guard; max / min / min-nonzero via order keys)
+                atomicAdd(p.epi.rsum + row, __dadd_rn(acc.s0, acc.s1));
+                const float hx = fmaxf(bits16_to_float<kFmt>(uint16_t(acc.vmax & 0xFFFFu)),
+                                       bits16_to_float<kFmt>(uint16_t(acc.vmax >> 16)));
+                const float hn = fminf(bits16_to_float<kFmt>(uint16_t(acc.vmin & 0xFFFFu)),
+                                       bits16_to_float<kFmt>(uint16_t(acc.vmin >> 16)));
+                atomicMax(p.epi.rmax + row, fkey(hx));
+                atomicMin(p.epi.rmin + row, fkey(hn));
+                const uint32_t mz = min(acc.vmnz & 0xFFFFu, acc.vmnz >> 16);
+                if (mz < 0x7FFFu) atomicMin(p.epi.rmnz + row, mz);
             }
             acc.reset();
         }
@@ -220,6 +237,7 @@ __global__ void __launch_bounds__(kThreadsStats, 1)
     uint64_t* sfull_bar = bars + 2 * kStages + 4;
     uint64_t* sempty_bar = bars + 2 * kStages + 6;
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * kStages + 8);
+    uint64_t* tail_bar = bars + 2 * kStages + 9;  // kTailWarps verify-tail barriers
 
     const int warp = threadIdx.x >> 5;
     const int lane = threadIdx.x & 31;
@@ -234,6 +252,9 @@ __global__ void __launch_bounds__(kThreadsStats, 1)
             mbar_init(smem_u32(&tempty_bar[a]), 4);
             mbar_init(smem_u32(&sfull_bar[a]), 1);
             mbar_init(smem_u32(&sempty_bar[a]), 4);  // the 4 statistics warps
+        }
+        if constexpr (kStats) {
+            for (int w = 0; w < kTailWarps; ++w) mbar_init(smem_u32(&tail_bar[w]), 1);
         }
         fence_mbar_init();
         tma_prefetch_desc(&tmA);
@@ -444,8 +465,9 @@ __global__ void __launch_bounds__(kThreadsStats, 1)
                     if ((c + 32) % 128 == 0) {
                         const int blk = (n0 + c) / 128;
                         if (row_ok && blk * 128 < p.N) {
-                            p.epi.part1[size_t(blk) * p.M + row] = s1;
-                            p.epi.part2[size_t(blk) * p.M + row] = s2;
+                            const size_t o = part_index(blk, row, (p.N + 127) / 128);
+                            p.epi.part1[o] = s1;
+                            p.epi.part2[o] = s2;
                         }
                         s1 = 0.0f;
                         s2 = 0.0f;
@@ -468,6 +490,33 @@ __global__ void __launch_bounds__(kThreadsStats, 1)
         __syncwarp();
         tc_fence_after();
         tmem_dealloc(tmem_base, kTmemCols);
+    }
+    if constexpr (kStats) {
+        // ---------------------------------------------- in-kernel verify tail
+        // every tile's C partials and statistics partials are in global memory
+        // once all CTAs pass the barrier; then all warps of the grid verify
+        // 32-row groups (lane = row).
+        if (p.epi.tail_phases) {
+            unsigned int* gcount = p.epi.gbar;
+            volatile unsigned int* ggen = p.epi.gbar + 1;
+            grid_barrier(gcount, ggen);
+            const int64_t ngroups = (int64_t(p.M) + 31) / 32;
+            const int64_t g0 = int64_t(blockIdx.x) * kTailWarps + warp, gs = int64_t(gridDim.x) * kTailWarps;
+            const bool tw = warp < kTailWarps;
+            float* sbuf = reinterpret_cast<float*>(smem + size_t(warp) * kTailWarpSmem);
+            const uint32_t tb = smem_u32(&tail_bar[tw ? warp : 0]);
+            uint32_t tph = 0;
+            if (p.epi.tail_phases == 3) {
+                if (tw)
+                    for (int64_t g = g0; g < ngroups; g += gs) verify_rowgroup<kFmt>(p.epi.tail, g, 3, sbuf, tb, tph);
+            } else {
+                if (tw)
+                    for (int64_t g = g0; g < ngroups; g += gs) verify_rowgroup<kFmt>(p.epi.tail, g, 1, sbuf, tb, tph);
+                grid_barrier(gcount, ggen);
+                if (tw)
+                    for (int64_t g = g0; g < ngroups; g += gs) verify_rowgroup<kFmt>(p.epi.tail, g, 2, sbuf, tb, tph);
+            }
+        }
     }
 }
 
@@ -517,7 +566,23 @@ void launch_inst(const CUtensorMap& ta, const CUtensorMap& tb, const TcParams& p
         attr_set = true;
     }
     const int grid = p.num_tiles < sm_count() ? p.num_tiles : sm_count();
-    kern<<<grid, kStats ? kThreadsStats : kThreads, kStats ? kSmemBytesStats : kSmemBytes, stream>>>(ta, tb, p);
+    if (kStats && p.epi.tail_phases) {
+        // the in-kernel verify tail synchronizes the grid: cooperative launch
+        // guarantees every CTA is co-resident (grid <= #SMs, 1 CTA/SM)
+        cudaLaunchConfig_t cfg{};
+        cfg.gridDim = dim3(unsigned(grid));
+        cfg.blockDim = dim3(kStats ? kThreadsStats : kThreads);
+        cfg.dynamicSmemBytes = kStats ? kSmemBytesStats : kSmemBytes;
+        cfg.stream = stream;
+        cudaLaunchAttribute attr[1];
+        attr[0].id = cudaLaunchAttributeCooperative;
+        attr[0].val.cooperative = 1;
+        cfg.attrs = attr;
+        cfg.numAttrs = 1;
+        check_cuda(cudaLaunchKernelEx(&cfg, kern, ta, tb, p), "tc_gemm cooperative launch");
+    } else {
+        kern<<<grid, kStats ? kThreadsStats : kThreads, kStats ? kSmemBytesStats : kSmemBytes, stream>>>(ta, tb, p);
+    }
     check_cuda(cudaGetLastError(), "tc_gemm launch");
 }
 

@@ -38,6 +38,8 @@ class FusedResult:
     location: Optional[torch.Tensor]
     residual: Optional[torch.Tensor]
     counts: Optional[torch.Tensor]
+    row_check1: Optional[torch.Tensor] = None
+    row_check2: Optional[torch.Tensor] = None
 
 
 class FusedAbftGemm:
@@ -86,7 +88,7 @@ class FusedAbftGemm:
 
     def __call__(self, A: torch.Tensor, out: Optional[torch.Tensor] = None, *, verdicts: bool = True,
                  thresholds: bool = True, counts: Optional[torch.Tensor] = None,
-                 faults: Optional[dict] = None, stages: int = 0) -> FusedResult:
+                 faults: Optional[dict] = None, stages: int = 0, checksums: bool = False) -> FusedResult:
         if A.dtype != self.B.dtype or A.dim() != 2 or A.shape[1] != self.k:
             raise _capi.InvalidArgument("FusedAbftGemm: A must be M x K with B's dtype")
         m = A.shape[0]
@@ -101,7 +103,9 @@ class FusedAbftGemm:
                     "d2": torch.empty(m, dtype=torch.float64, device=dev),
                     "res": torch.empty(m, dtype=torch.float64, device=dev),
                     "det": torch.empty(m, dtype=torch.uint8, device=dev),
-                    "loc": torch.empty(m, dtype=torch.int64, device=dev)}
+                    "loc": torch.empty(m, dtype=torch.int64, device=dev),
+                    "rc1": torch.empty(m, dtype=torch.float64, device=dev),
+                    "rc2": torch.empty(m, dtype=torch.float64, device=dev)}
             self._bufs[m] = bufs
         C_ = out if out is not None else bufs["C"]
         T = bufs["T"] if thresholds else None
@@ -109,7 +113,8 @@ class FusedAbftGemm:
             d1, d2, res, det, loc = bufs["d1"], bufs["d2"], bufs["res"], bufs["det"], bufs["loc"]
         else:
             d1 = d2 = res = det = loc = None
-        v = _capi.Verdicts(ptr(d1), ptr(d2), ptr(det), ptr(loc), ptr(res))
+        rc1, rc2 = (bufs["rc1"], bufs["rc2"]) if checksums else (None, None)
+        v = _capi.Verdicts(ptr(d1), ptr(d2), ptr(det), ptr(loc), ptr(res), ptr(rc1), ptr(rc2))
         opts = self.opts
         if stages:
             opts = _capi.FusedOpts.from_buffer_copy(self.opts)
@@ -123,7 +128,7 @@ class FusedAbftGemm:
         ws = self.workspace(m)
         check(lib.vabft_fused_gemm(C.byref(opts), self.h, m, ptr(A.contiguous()), ptr(C_), ptr(T), v, ptr(counts),
                                    ptr(ws), ws.numel(), stream_ptr()))
-        return FusedResult(C_, T, d1, d2, det, loc, res, counts)
+        return FusedResult(C_, T, d1, d2, det, loc, res, counts, rc1, rc2)
 
     def close(self) -> None:
         if self.h:

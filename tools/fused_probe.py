@@ -40,7 +40,7 @@ def main():
         flops = 2 * m * n * k
         for mode in ("online", "offline"):
             g = FusedAbftGemm(B, mode=mode)
-            counts = torch.zeros(4, dtype=torch.int64, device="cuda")
+            counts = torch.zeros(5, dtype=torch.int64, device="cuda")
             t = {}
             t["plain"] = graph_time(lambda: plain_gemm(A, B, out=C))
             t["all"] = graph_time(lambda: g(A, out=C, counts=counts))
