@@ -78,6 +78,13 @@ struct TcEpilogue {
     // 0 = none, 3 = single pass, 1|2 = two passes with a second barrier.
     int tail_phases = 0;
     unsigned int* gbar = nullptr;  // [count, generation], zero-initialised once
+    // Streamed verification (threshold methods without a global dependency):
+    // per-32-row-group arrival counters, zero-initialised once and reset by
+    // their verifier. Every tile adds one arrival from the epilogue warp and
+    // one from the statistics warp covering the group; the warp making the
+    // last arrival verifies the group at once, inside the GEMM.
+    int stream_verify = 0;
+    unsigned int* group_cnt = nullptr;
     TailArgs tail;
 };
 __host__ __device__ inline size_t part_index(int64_t b, int64_t row, int64_t nb) {

@@ -79,10 +79,39 @@ __device__ __forceinline__ void ordered_sums(const float* x1, const float* x2, i
     }
 }
 
+// Same combination reading the partials straight from L2 (no shared memory:
+// used inside the GEMM, whose shared memory is all pipeline). Lane = row; for
+// each block the warp's 32 loads are one coalesced 128-byte line; batches of
+// kDirectBatch blocks are in flight before the in-order FP32 adds.
+constexpr int kDirectBatch = 16;
+__device__ __forceinline__ void ordered_sums_direct(const float* x1, const float* x2, int64_t nb, int64_t g,
+                                                    float& r1, float& r2) {
+    const int lane = threadIdx.x & 31;
+    const float* p1 = x1 + part_index(0, g * 32, nb) + lane;
+    const float* p2 = x2 + part_index(0, g * 32, nb) + lane;
+    for (int64_t b0 = 0; b0 < nb; b0 += kDirectBatch) {
+        float v1[kDirectBatch], v2[kDirectBatch];
+#pragma unroll
+        for (int j = 0; j < kDirectBatch; ++j) {
+            const bool ok = b0 + j < nb;
+            v1[j] = ok ? __ldcg(p1 + (b0 + j) * 32) : 0.0f;
+            v2[j] = ok ? __ldcg(p2 + (b0 + j) * 32) : 0.0f;
+        }
+#pragma unroll
+        for (int j = 0; j < kDirectBatch; ++j) {
+            if (b0 + j < nb) {  // reduce_terms NativeBlocked(128), in order
+                r1 = __fadd_rn(r1, v1[j]);
+                r2 = __fadd_rn(r2, v2[j]);
+            }
+        }
+    }
+}
+
 // phase bit 1: statistics -> T_i and A (B r); bit 2: row sums + verify.
 // Phase 1 alone stages cr1/cr2/Tv for a later phase-2 pass (A-ABFT computed y
 // needs the global max|A| first).
-template <int F>
+// kDirect: partials read with ordered_sums_direct (sbuf / bar unused).
+template <int F, bool kDirect = false>
 __device__ void verify_rowgroup(const TailArgs& a, int64_t g, int phase, float* sbuf, uint32_t bar,
                                 uint32_t& bar_phase) {
     const int lane = threadIdx.x & 31;
@@ -92,7 +121,8 @@ __device__ void verify_rowgroup(const TailArgs& a, int64_t g, int phase, float* 
     double c1 = 0.0, c2 = 0.0, tv = 0.0;
     if (phase & 1) {
         float t1 = 0.0f, t2 = 0.0f;
-        ordered_sums(a.sp1, a.sp2, a.nblkK, g, sbuf, bar, bar_phase, t1, t2);
+        if constexpr (kDirect) ordered_sums_direct(a.sp1, a.sp2, a.nblkK, g, t1, t2);
+        else ordered_sums(a.sp1, a.sp2, a.nblkK, g, sbuf, bar, bar_phase, t1, t2);
         float amax = 0.0f;
         if (valid) {
             double sum = __ldcg(a.rsum + i);
@@ -139,7 +169,8 @@ __device__ void verify_rowgroup(const TailArgs& a, int64_t g, int phase, float* 
     }
     if (!(phase & 2)) return;
     float r1 = 0.0f, r2 = 0.0f;
-    ordered_sums(a.part1, a.part2, a.nblkN, g, sbuf, bar, bar_phase, r1, r2);
+    if constexpr (kDirect) ordered_sums_direct(a.part1, a.part2, a.nblkN, g, r1, r2);
+    else ordered_sums(a.part1, a.part2, a.nblkN, g, sbuf, bar, bar_phase, r1, r2);
     if (valid) {
         if (!(phase & 1)) {
             c1 = a.cr1[i];

@@ -23,6 +23,7 @@
 #include <cuda_fp16.h>
 #include <cudaTypedefs.h>
 
+#include <cstdlib>
 #include <mutex>
 
 #include "internal.hpp"
@@ -61,9 +62,49 @@ static_assert((2 * kStages + 9 + kTailWarps) * 8 <= 256, "barrier area");
 struct TcParams {
     int M, N, K;
     int num_m_blk, num_n_blk, num_k_blk, num_tiles;
+    int group_m;  // tile raster: groups of group_m row blocks, n-major inside a group
     uint16_t* C;
     TcEpilogue epi;
 };
+
+// Grouped raster: tiles run through groups of group_m consecutive 128-row
+// blocks; inside a group the row block varies fastest, so the CTAs of one
+// wave share B tiles across the group and every row block of a group
+// completes (all N tiles done) at the same time, group after group, which is
+// what lets streamed verification run while later groups are still in the
+// tensor cores. group_m = num_m_blk is the plain n-major order.
+__device__ __forceinline__ void tile_coords(const TcParams& p, int tile, int& m_blk, int& n_blk) {
+    const int per_group = p.group_m * p.num_n_blk;
+    const int grp = tile / per_group;
+    const int rem = tile - grp * per_group;
+    const int m0 = grp * p.group_m;
+    const int gm = p.num_m_blk - m0 < p.group_m ? p.num_m_blk - m0 : p.group_m;
+    m_blk = m0 + rem % gm;
+    n_blk = rem / gm;
+}
+
+// Streamed verification arrival (see TcEpilogue::stream_verify): publish this
+// warp's partials of row group g, count the arrival, and verify the group if
+// it was the last one (2 per N tile: epilogue + statistics warp).
+template <int F>
+__device__ __forceinline__ void group_arrive(const TcParams& p, int64_t g) {
+    if (g * 32 >= p.M) return;
+    const int lane = threadIdx.x & 31;
+    // __syncwarp orders every lane's partial / atomic writes before lane 0's
+    // acq_rel RMW at GPU scope (release is cumulative); the last arriver's
+    // acquire side orders the verifier's L2 reads after all other arrivals.
+    // (A full __threadfence per lane is fence.sc + L1 invalidate: measured
+    // to cost tensor-pipe time when issued once per tile per warp.)
+    __syncwarp();
+    unsigned int old = 0;
+    if (lane == 0) old = atom_add_acq_rel_gpu(p.epi.group_cnt + g, 1u);
+    old = __shfl_sync(0xffffffffu, old, 0);
+    if (old != 2u * unsigned(p.num_n_blk) - 1u || p.epi.debug == 7) return;  // 7: ablation, no verify
+    uint32_t unused_phase = 0;
+    verify_rowgroup<F, true>(p.epi.tail, g, 3, nullptr, 0u, unused_phase);
+    __syncwarp();
+    if (lane == 0) p.epi.group_cnt[g] = 0u;  // ready for the next launch
+}
 
 // ------------------------------------------------ in-GEMM A statistics
 // Four statistics warps (thread = row of the 128-row A tile). The 128-column
@@ -85,6 +126,11 @@ __device__ __forceinline__ uint32_t pminu2_(uint32_t a, uint32_t b) {
     asm("min.u16x2 %0, %1, %2;" : "=r"(d) : "r"(a), "r"(b));
     return d;
 }
+__device__ __forceinline__ uint32_t pmaxu2_(uint32_t a, uint32_t b) {
+    uint32_t d;
+    asm("max.u16x2 %0, %1, %2;" : "=r"(d) : "r"(a), "r"(b));
+    return d;
+}
 template <int F>
 __device__ __forceinline__ uint32_t pmax2_(uint32_t a, uint32_t b) {
     uint32_t d;
@@ -100,20 +146,67 @@ __device__ __forceinline__ uint32_t pmin2_(uint32_t a, uint32_t b) {
     return d;
 }
 
+// Exact row sums without FP64 arithmetic. FP64 instructions issued next to a
+// running tcgen05 pipeline cost tensor-pipe cycles on B200 (measured: an FP64
+// add per element in these warps cut the GEMM's flops/cycle by ~12%, the
+// same work in integer/FP32 ~3%), so each 64-element stage of a row is summed
+// as an integer: element = m * 2^(e - bias) with the stage anchored at
+// ebase = (stage max exponent) - 48, i.e. m << (e - ebase) < 2^56 and 64 terms
+// < 2^62. Under the exactness guard (tail.cuh guard_exact: every nonzero
+// element's lsb is within 45 bits of the row maximum) no element falls below
+// the anchor and the stage sum is exactly representable in FP64, so the one
+// int64 -> double conversion per stage is exact and equals the reference's
+// Neumaier sum once all stages are added. Rows that fail the guard take the
+// sequential fallback, so what this computes for them is irrelevant.
+// FP16's exponent range is narrow enough for a fixed anchor (ebase = 1).
 template <int F>
 struct StatsAcc {
+    static constexpr int kFracBits = F == VABFT_BF16 ? 7 : 10;
+    static constexpr int kExpMask = F == VABFT_BF16 ? 0xFF : 0x1F;
+    static constexpr int kBias = F == VABFT_BF16 ? 127 + 7 : 15 + 10;  // value = m * 2^(e - kBias)
     float p1, p2;
-    double s0, s1;
+    double s;  // exact FP64 sum of the finished stages
     uint32_t vmax, vmin, vmnz;
     __device__ __forceinline__ void reset() {
         p1 = p2 = 0.0f;
-        s0 = s1 = 0.0;
+        s = 0.0;
         vmax = F == VABFT_BF16 ? 0xFF80FF80u : 0xFC00FC00u;
         vmin = F == VABFT_BF16 ? 0x7F807F80u : 0x7C007C00u;
         vmnz = 0x7FFF7FFFu;
     }
-    // 8 consecutive elements k .. k+7 (one 16-byte granule)
-    __device__ __forceinline__ void granule(const uint4 w, const float* br1, const float* br2, int k) {
+    // pass 1 over a granule: max / min / min-nonzero trackers and the stage's
+    // largest magnitude pattern (packed u16 max)
+    __device__ __forceinline__ void track(const uint4 w, uint32_t& amx) {
+        const uint32_t ws[4] = {w.x, w.y, w.z, w.w};
+#pragma unroll
+        for (int h = 0; h < 4; ++h) {
+            vmax = pmax2_<F>(vmax, ws[h]);
+            vmin = pmin2_<F>(vmin, ws[h]);
+            const uint32_t mag = ws[h] & 0x7FFF7FFFu;
+            vmnz = pminu2_(vmnz, ((mag | 0x80008000u) - 0x00010001u) & 0x7FFF7FFFu);
+            if constexpr (F == VABFT_BF16) amx = pmaxu2_(amx, mag);
+        }
+    }
+    __device__ __forceinline__ static int anchor(uint32_t amx) {
+        if constexpr (F == VABFT_BF16) {
+            const int e0 = int((amx >> 7) & 0xFFu), e1 = int((amx >> 23) & 0xFFu);
+            return (e0 > e1 ? e0 : e1) - 48;
+        } else {
+            return 1;  // m < 2^11, shift <= 30: 64 terms < 2^47
+        }
+    }
+    __device__ __forceinline__ static void isum(uint32_t x, int ebase, uint64_t& pos, uint64_t& neg) {
+        const uint32_t e = (x >> kFracBits) & uint32_t(kExpMask);
+        const uint32_t m = (x & ((1u << kFracBits) - 1u)) | (e ? (1u << kFracBits) : 0u);
+        const int sh = int(e ? e : 1u) - ebase;
+        const uint64_t t = sh >= 0 ? (uint64_t(m) << sh) : 0ull;  // sh < 0 only for guard failures
+        if (x & 0x8000u) neg += t;
+        else pos += t;
+    }
+    // pass 2 over a granule (8 consecutive elements k .. k+7): blocked:128
+    // checksum partials in FP32 (reference order, no FMA) and the integer sum
+    __device__ __forceinline__ void sums(const uint4 w, const float* br1, const float* br2, int k, int ebase,
+                                         uint64_t& pos, uint64_t& neg) {
         const float4* g1 = reinterpret_cast<const float4*>(br1 + k);  // shared memory (broadcast)
         const float4* g2 = reinterpret_cast<const float4*>(br2 + k);
         const float4 u0 = g1[0], u1 = g1[1], v0 = g2[0], v1 = g2[1];
@@ -122,18 +215,20 @@ struct StatsAcc {
         const uint32_t ws[4] = {w.x, w.y, w.z, w.w};
 #pragma unroll
         for (int h = 0; h < 4; ++h) {
-            vmax = pmax2_<F>(vmax, ws[h]);
-            vmin = pmin2_<F>(vmin, ws[h]);
-            vmnz = pminu2_(vmnz, (((ws[h] & 0x7FFF7FFFu) | 0x80008000u) - 0x00010001u) & 0x7FFF7FFFu);
+            isum(ws[h] & 0xFFFFu, ebase, pos, neg);
+            isum(ws[h] >> 16, ebase, pos, neg);
             const float xa = bits16_to_float<F>(uint16_t(ws[h] & 0xFFFFu));
             const float xb = bits16_to_float<F>(uint16_t(ws[h] >> 16));
-            s0 = __dadd_rn(s0, double(xa));
-            s1 = __dadd_rn(s1, double(xb));
             p1 = __fadd_rn(p1, __fmul_rn(b1[2 * h], xa));
             p2 = __fadd_rn(p2, __fmul_rn(b2[2 * h], xa));
             p1 = __fadd_rn(p1, __fmul_rn(b1[2 * h + 1], xb));
             p2 = __fadd_rn(p2, __fmul_rn(b2[2 * h + 1], xb));
         }
+    }
+    // close a stage: s += (pos - neg) * 2^(ebase - kBias), exact under the guard
+    __device__ __forceinline__ void close_stage(uint64_t pos, uint64_t neg, int ebase) {
+        const double scale = __longlong_as_double(static_cast<long long>(ebase - kBias + 1023) << 52);
+        s = __dadd_rn(s, __dmul_rn(__ll2double_rn(static_cast<long long>(pos - neg)), scale));
     }
 };
 
@@ -145,8 +240,8 @@ __device__ __forceinline__ void stats_producer(const TcParams& p, const CUtensor
     uint32_t cnt = 0;
     const int nblk = (p.K + 127) / 128;
     for (int tile = blockIdx.x; tile < p.num_tiles; tile += gridDim.x) {
-        const int m_blk = tile % p.num_m_blk;
-        const int n_blk = tile / p.num_m_blk;
+        int m_blk, n_blk;
+        tile_coords(p, tile, m_blk, n_blk);
         for (int b = n_blk; b < nblk; b += p.num_n_blk) {
             for (int kb = 2 * b; kb < 2 * b + 2 && kb < p.num_k_blk; ++kb, ++cnt) {
                 const int slot = int(cnt & 1u);
@@ -178,8 +273,8 @@ __device__ __forceinline__ void stats_warps(const TcParams& p, const uint8_t* sm
     uint32_t cnt = 0;  // statistics stages consumed: slot = cnt & 1, phase = (cnt >> 1) & 1
     const int nblk = (p.K + 127) / 128;
     for (int tile = blockIdx.x; tile < p.num_tiles; tile += gridDim.x) {
-        const int m_blk = tile % p.num_m_blk;
-        const int n_blk = tile / p.num_m_blk;
+        int m_blk, n_blk;
+        tile_coords(p, tile, m_blk, n_blk);
         const int row = m_blk * kBM + r;
         for (int b = n_blk; b < nblk; b += p.num_n_blk) {
             for (int kb = 2 * b; kb < 2 * b + 2 && kb < p.num_k_blk; ++kb, ++cnt) {
@@ -189,11 +284,19 @@ __device__ __forceinline__ void stats_warps(const TcParams& p, const uint8_t* sm
                 const float* sbr1 = reinterpret_cast<const float*>(smS + 2 * kABytes + slot * (2 * kBK * 4));
                 const float* sbr2 = sbr1 + kBK;
                 const int kbase = kb * kBK;
+                const int ng = (p.K - kbase) >= kBK ? 8 : (p.K - kbase) / 8;  // K % 8 == 0: whole granules
+                if (p.epi.debug != 2) {  // 2: ablation, no math
+                    uint32_t amx = 0;
+#pragma unroll 4
+                    for (int c = 0; c < ng; ++c)
+                        acc.track(*reinterpret_cast<const uint4*>(trow + ((c ^ (r & 7)) << 4)), amx);
+                    const int ebase = StatsAcc<kFmt>::anchor(amx);
+                    uint64_t pos = 0, neg = 0;
 #pragma unroll 2
-                for (int c = 0; c < 8; ++c) {
-                    if (kbase + c * 8 >= p.K) break;  // K % 8 == 0: whole granules only
-                    const uint4 w = *reinterpret_cast<const uint4*>(trow + ((c ^ (r & 7)) << 4));
-                    if (p.epi.debug != 2) acc.granule(w, sbr1, sbr2, c * 8);  // 2: ablation, no math
+                    for (int c = 0; c < ng; ++c)
+                        acc.sums(*reinterpret_cast<const uint4*>(trow + ((c ^ (r & 7)) << 4)), sbr1, sbr2, c * 8,
+                                 ebase, pos, neg);
+                    acc.close_stage(pos, neg, ebase);
                 }
                 __syncwarp();
                 if (lane == 0) mbar_arrive(smem_u32(&sempty_bar[slot]));
@@ -204,7 +307,7 @@ __device__ __forceinline__ void stats_warps(const TcParams& p, const uint8_t* sm
                 p.epi.sp2[o] = acc.p2;
                 // order-independent statistics: per-row atomics (exact sum under
                 // the guard; max / min / min-nonzero via order keys)
-                atomicAdd(p.epi.rsum + row, __dadd_rn(acc.s0, acc.s1));
+                atomicAdd(p.epi.rsum + row, acc.s);
                 const float hx = fmaxf(bits16_to_float<kFmt>(uint16_t(acc.vmax & 0xFFFFu)),
                                        bits16_to_float<kFmt>(uint16_t(acc.vmax >> 16)));
                 const float hn = fminf(bits16_to_float<kFmt>(uint16_t(acc.vmin & 0xFFFFu)),
@@ -216,6 +319,7 @@ __device__ __forceinline__ void stats_warps(const TcParams& p, const uint8_t* sm
             }
             acc.reset();
         }
+        if (p.epi.stream_verify) group_arrive<kFmt>(p, int64_t(m_blk) * 4 + sw);
     }
 }
 
@@ -272,8 +376,8 @@ __global__ void __launch_bounds__(kThreadsStats, 1)
             int stage = 0;
             uint32_t phase = 0;
             for (int tile = blockIdx.x; tile < p.num_tiles; tile += gridDim.x) {
-                const int m_blk = tile % p.num_m_blk;
-                const int n_blk = tile / p.num_m_blk;
+                int m_blk, n_blk;
+                tile_coords(p, tile, m_blk, n_blk);
                 for (int kb = 0; kb < p.num_k_blk; ++kb) {
                     mbar_wait(smem_u32(&empty_bar[stage]), phase ^ 1);
                     const uint32_t fb = smem_u32(&full_bar[stage]);
@@ -349,8 +453,8 @@ __global__ void __launch_bounds__(kThreadsStats, 1)
         int acc = 0;
         uint32_t acc_phase = 0;
         for (int tile = blockIdx.x; tile < p.num_tiles; tile += gridDim.x) {
-            const int m_blk = tile % p.num_m_blk;
-            const int n_blk = tile / p.num_m_blk;
+            int m_blk, n_blk;
+            tile_coords(p, tile, m_blk, n_blk);
             const int row = m_blk * kBM + row_in_tile;
             const bool row_ok = row < p.M;
             const int n0 = n_blk * kBN;
@@ -481,6 +585,9 @@ __global__ void __launch_bounds__(kThreadsStats, 1)
                 acc = 0;
                 acc_phase ^= 1;
             }
+            if constexpr (kStats) {
+                if (p.epi.stream_verify) group_arrive<kFmt>(p, int64_t(m_blk) * 4 + quad);
+            }
         }
     }
 
@@ -590,7 +697,7 @@ template <int kFmt, bool kBKMajor>
 void dispatch_epi(const CUtensorMap& ta, const CUtensorMap& tb, const TcParams& p,
                   cudaStream_t stream) {
     const bool inj = p.epi.fault_col != nullptr;
-    const bool st = p.epi.sp1 != nullptr;
+    const bool st = p.epi.sp1 != nullptr && p.epi.debug != 3;  // 3: ablation, ABFT epilogue only
     switch (p.epi.abft) {
         case 0: launch_inst<kFmt, kBKMajor, 0, false>(ta, tb, p, stream); break;
         case 1:
@@ -636,6 +743,11 @@ void tc_gemm_launch(int fmt, bool b_kmajor, int64_t M, int64_t N, int64_t K, con
     p.num_n_blk = int((N + kBN - 1) / kBN);
     p.num_k_blk = int((K + kBK - 1) / kBK);
     p.num_tiles = p.num_m_blk * p.num_n_blk;
+    static const int raster = [] {
+        const char* e = std::getenv("VABFT_RASTER_GROUP");  // developer override
+        return e ? std::atoi(e) : 8;
+    }();
+    p.group_m = raster <= 0 || raster > p.num_m_blk ? p.num_m_blk : raster;
     p.C = static_cast<uint16_t*>(C);
     p.epi = epi;
     const CUtensorMap ta = make_map_2d(fmt, A, uint64_t(M), uint64_t(K), kBK, kBM);

@@ -71,10 +71,10 @@ def test_fused_injection_matches_oracle_per_trial(torch_cuda, port, mode, bit):
 def test_campaign_rates(torch_cuda):
     from paper_2602_08043_b200.campaign import DeviceCampaign
     c = DeviceCampaign(256, 1024, 256, dist="normal:1e-6,1", mode="online", seed=5)
-    hi = c.run(30, 512, reduce=False)   # FP32 exponent MSB: always catastrophic
+    hi = c.run(29, 512, reduce=False)   # FP32 exponent bit 6: |x| in [2^-62, 2) -> x 2^64
     lo = c.run(0, 512, reduce=False)    # FP32 mantissa LSB: below every threshold
     mid = c.run(24, 512, reduce=False)  # exponent LSB: doubles/halves the value
     c.close()
-    assert hi.applicable > 200 and hi.detection_rate() == 1.0
+    assert hi.applicable > 200 and hi.detection_rate() == 1.0 and hi.localization_accuracy() > 0.99
     assert lo.applicable > 100 and lo.detection_rate() == 0.0
     assert mid.detection_rate() > 0.99 and mid.localization_accuracy() > 0.99
