@@ -115,7 +115,8 @@ def cpu_reference_sample(m_rows: int, k: int, n: int, threads: int, mode: str):
     O = oracle.best()
     kind = "reference" if O.name == "reference" else "port"
     A, B = O.trial_inputs(m_rows * threads, k, n, "bf16", "normal:0,1", 7, 0)
-    e_max = 2e-6 if mode == "online" else 8e-3
+    from paper_2602_08043_b200.emax import default_e_max
+    e_max = default_e_max("bf16", mode, k)  # the same e_max the GPU arm resolves
 
     def one(t):
         a = np.ascontiguousarray(A[t * m_rows:(t + 1) * m_rows])

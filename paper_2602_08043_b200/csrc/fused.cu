@@ -73,7 +73,7 @@ struct FusedWs {
     double* rsum;                      // [M] per-row atomics (identities: 0, 0, ~0, ~0)
     uint32_t *rmax, *rmin, *rmnz;
     double *cr1, *cr2, *Tv, *max_abs_a;
-    unsigned int* group_cnt;           // [ceil(M/32)] streamed-verification arrivals (identity 0)
+    unsigned int* group_cnt;           // [ceil(M/32)][2] streamed-verification arrivals (identity 0)
     size_t bytes;
 };
 
@@ -100,7 +100,7 @@ FusedWs carve(void* base, int64_t M, int64_t N, int64_t K) {
     w.cr2 = reinterpret_cast<double*>(take(8 * m));
     w.Tv = reinterpret_cast<double*>(take(8 * m));
     w.max_abs_a = reinterpret_cast<double*>(take(8));
-    w.group_cnt = reinterpret_cast<unsigned int*>(take(4 * (ld / 32)));
+    w.group_cnt = reinterpret_cast<unsigned int*>(take(4 * 2 * (ld / 32)));
     w.bytes = off;
     return w;
 }
@@ -222,7 +222,7 @@ extern "C" vabft_status vabft_fused_gemm(const vabft_fused_opts* o, vabft_bside_
             check_cuda(cudaMemsetAsync(ws.rmax, 0, sizeof(uint32_t) * size_t(m), s), "memset");
             check_cuda(cudaMemsetAsync(ws.rmin, 0xFF, size_t(reinterpret_cast<char*>(ws.rmnz + m) -
                                                              reinterpret_cast<char*>(ws.rmin)), s), "memset");
-            check_cuda(cudaMemsetAsync(ws.group_cnt, 0, sizeof(unsigned int) * size_t((m + 31) / 32), s), "memset");
+            check_cuda(cudaMemsetAsync(ws.group_cnt, 0, sizeof(unsigned int) * 2 * size_t((m + 31) / 32), s), "memset");
             h->ws_ready = workspace;
             h->ws_ready_bytes = ws.bytes;
         }

@@ -79,104 +79,50 @@ __device__ __forceinline__ void ordered_sums(const float* x1, const float* x2, i
     }
 }
 
-// Same combination reading the partials straight from L2 (no shared memory:
-// used inside the GEMM, whose shared memory is all pipeline). Lane = row; for
-// each block the warp's 32 loads are one coalesced 128-byte line; batches of
-// kDirectBatch blocks are in flight before the in-order FP32 adds.
-constexpr int kDirectBatch = 16;
-__device__ __forceinline__ void ordered_sums_direct(const float* x1, const float* x2, int64_t nb, int64_t g,
-                                                    float& r1, float& r2) {
-    const int lane = threadIdx.x & 31;
-    const float* p1 = x1 + part_index(0, g * 32, nb) + lane;
-    const float* p2 = x2 + part_index(0, g * 32, nb) + lane;
-    for (int64_t b0 = 0; b0 < nb; b0 += kDirectBatch) {
-        float v1[kDirectBatch], v2[kDirectBatch];
-#pragma unroll
-        for (int j = 0; j < kDirectBatch; ++j) {
-            const bool ok = b0 + j < nb;
-            v1[j] = ok ? __ldcg(p1 + (b0 + j) * 32) : 0.0f;
-            v2[j] = ok ? __ldcg(p2 + (b0 + j) * 32) : 0.0f;
-        }
-#pragma unroll
-        for (int j = 0; j < kDirectBatch; ++j) {
-            if (b0 + j < nb) {  // reduce_terms NativeBlocked(128), in order
-                r1 = __fadd_rn(r1, v1[j]);
-                r2 = __fadd_rn(r2, v2[j]);
-            }
-        }
+// ---------------------------------------------------------------- pieces
+// Threshold of row i from its order-independent statistics (which are reset
+// to their identities for the next launch) and the A (B r) checksums from
+// their FP32 blocked:128 sums t1 / t2 (quantized offline).
+template <int F>
+__device__ __forceinline__ void row_threshold(const TailArgs& a, int64_t i, double sum, uint32_t kmax,
+                                              uint32_t kmin, uint32_t mnz, float t1, float t2, double& tv,
+                                              double& c1, double& c2, float& amax) {
+    a.rsum[i] = 0.0;
+    a.rmax[i] = 0u;
+    a.rmin[i] = 0xFFFFFFFFu;
+    a.rmnz[i] = 0xFFFFFFFFu;
+    const float mx = fkey_decode(kmax);
+    const float mn = fkey_decode(kmin);
+    amax = fmaxf(fabsf(mx), fabsf(mn));
+    if (!guard_exact<F>(amax, mnz, a.K)) {
+        // the reference's sequential Neumaier pass over the row (stats.cpp:12-24)
+        if (a.counts) atomicAdd(reinterpret_cast<unsigned long long*>(a.counts + VABFT_COUNT_SLOW_STATS), 1ull);
+        Neu ns;
+        const uint16_t* row = a.A + i * a.K;
+        for (int64_t q = 0; q < a.K; ++q) ns.add(double(bits16_to_float<F>(row[q])));
+        sum = __dadd_rn(ns.s, ns.c);
     }
+    Neu fin;
+    fin.s = sum;
+    double mean, vb;
+    stats_finish(fin, double(mx), double(mn), a.K, &mean, &vb);
+    tv = vabft_threshold_total(mean, vb, a.bsum[0], a.bsum[1], a.bsum[2], a.N, a.e_max, a.c_sigma);
+    if (a.quantize_cr) {
+        t1 = bits16_to_float<F>(quantize16_bits<F>(t1));
+        t2 = bits16_to_float<F>(quantize16_bits<F>(t2));
+    }
+    c1 = double(t1);
+    c2 = double(t2);
 }
 
-// phase bit 1: statistics -> T_i and A (B r); bit 2: row sums + verify.
-// Phase 1 alone stages cr1/cr2/Tv for a later phase-2 pass (A-ABFT computed y
-// needs the global max|A| first).
-// kDirect: partials read with ordered_sums_direct (sbuf / bar unused).
-template <int F, bool kDirect = false>
-__device__ void verify_rowgroup(const TailArgs& a, int64_t g, int phase, float* sbuf, uint32_t bar,
-                                uint32_t& bar_phase) {
+// Verdict of row i (detect.cpp:19-55) from its row sums r1 / r2, checksums
+// c1 / c2 and V-ABFT threshold tv (A-ABFT methods replace it), plus the
+// warp's counters.
+__device__ __forceinline__ void row_verdict(const TailArgs& a, int64_t i, bool valid, float r1, float r2,
+                                            double c1, double c2, double tv) {
     const int lane = threadIdx.x & 31;
-    const int64_t i = g * 32 + lane;
-    const bool valid = i < a.M;
     bool det = false, located = false, isnan_row = false;
-    double c1 = 0.0, c2 = 0.0, tv = 0.0;
-    if (phase & 1) {
-        float t1 = 0.0f, t2 = 0.0f;
-        if constexpr (kDirect) ordered_sums_direct(a.sp1, a.sp2, a.nblkK, g, t1, t2);
-        else ordered_sums(a.sp1, a.sp2, a.nblkK, g, sbuf, bar, bar_phase, t1, t2);
-        float amax = 0.0f;
-        if (valid) {
-            double sum = __ldcg(a.rsum + i);
-            const float mx = fkey_decode(__ldcg(a.rmax + i));
-            const float mn = fkey_decode(__ldcg(a.rmin + i));
-            const uint32_t mnz = __ldcg(a.rmnz + i);
-            // reset to the identities for the next launch
-            a.rsum[i] = 0.0;
-            a.rmax[i] = 0u;
-            a.rmin[i] = 0xFFFFFFFFu;
-            a.rmnz[i] = 0xFFFFFFFFu;
-            amax = fmaxf(fabsf(mx), fabsf(mn));
-            if (!guard_exact<F>(amax, mnz, a.K)) {
-                // the reference's sequential Neumaier pass over the row (stats.cpp:12-24)
-                if (a.counts) atomicAdd(reinterpret_cast<unsigned long long*>(a.counts + VABFT_COUNT_SLOW_STATS), 1ull);
-                Neu ns;
-                const uint16_t* row = a.A + i * a.K;
-                for (int64_t q = 0; q < a.K; ++q) ns.add(double(bits16_to_float<F>(row[q])));
-                sum = __dadd_rn(ns.s, ns.c);
-            }
-            Neu fin;
-            fin.s = sum;
-            double mean, vb;
-            stats_finish(fin, double(mx), double(mn), a.K, &mean, &vb);
-            tv = vabft_threshold_total(mean, vb, a.bsum[0], a.bsum[1], a.bsum[2], a.N, a.e_max, a.c_sigma);
-            if (a.quantize_cr) {
-                t1 = bits16_to_float<F>(quantize16_bits<F>(t1));
-                t2 = bits16_to_float<F>(quantize16_bits<F>(t2));
-            }
-            c1 = double(t1);
-            c2 = double(t2);
-            if (phase == 1) {
-                a.cr1[i] = c1;
-                a.cr2[i] = c2;
-                a.Tv[i] = tv;
-            }
-        }
-        if (a.method == 2) {  // one atomic per warp for max|A| (A-ABFT computed y)
-            float wmax = amax;
-#pragma unroll
-            for (int m = 16; m >= 1; m >>= 1) wmax = fmaxf(wmax, __shfl_xor_sync(0xffffffffu, wmax, m));
-            if (lane == 0) atomic_max_nonneg(a.max_abs_a, double(wmax));
-        }
-    }
-    if (!(phase & 2)) return;
-    float r1 = 0.0f, r2 = 0.0f;
-    if constexpr (kDirect) ordered_sums_direct(a.part1, a.part2, a.nblkN, g, r1, r2);
-    else ordered_sums(a.part1, a.part2, a.nblkN, g, sbuf, bar, bar_phase, r1, r2);
     if (valid) {
-        if (!(phase & 1)) {
-            c1 = a.cr1[i];
-            c2 = a.cr2[i];
-            tv = a.Tv[i];
-        }
         double t;
         if (a.method == 0) {
             t = tv;
@@ -224,6 +170,124 @@ __device__ void verify_rowgroup(const TailArgs& a, int64_t g, int phase, float* 
             if (mn) atomicAdd(reinterpret_cast<unsigned long long*>(a.counts + VABFT_COUNT_NAN), __popc(mn));
         }
     }
+}
+
+// ------------------------------------------------- smem-staged (tail warps)
+// phase bit 1: statistics -> T_i and A (B r); bit 2: row sums + verify.
+// Phase 1 alone stages cr1/cr2/Tv for a later phase-2 pass (A-ABFT computed y
+// needs the global max|A| first).
+template <int F>
+__device__ void verify_rowgroup(const TailArgs& a, int64_t g, int phase, float* sbuf, uint32_t bar,
+                                uint32_t& bar_phase) {
+    const int lane = threadIdx.x & 31;
+    const int64_t i = g * 32 + lane;
+    const bool valid = i < a.M;
+    double c1 = 0.0, c2 = 0.0, tv = 0.0;
+    if (phase & 1) {
+        float t1 = 0.0f, t2 = 0.0f;
+        ordered_sums(a.sp1, a.sp2, a.nblkK, g, sbuf, bar, bar_phase, t1, t2);
+        float amax = 0.0f;
+        if (valid) {
+            row_threshold<F>(a, i, __ldcg(a.rsum + i), __ldcg(a.rmax + i), __ldcg(a.rmin + i), __ldcg(a.rmnz + i),
+                             t1, t2, tv, c1, c2, amax);
+            if (phase == 1) {
+                a.cr1[i] = c1;
+                a.cr2[i] = c2;
+                a.Tv[i] = tv;
+            }
+        }
+        if (a.method == 2) {  // one atomic per warp for max|A| (A-ABFT computed y)
+            float wmax = amax;
+#pragma unroll
+            for (int m = 16; m >= 1; m >>= 1) wmax = fmaxf(wmax, __shfl_xor_sync(0xffffffffu, wmax, m));
+            if (lane == 0) atomic_max_nonneg(a.max_abs_a, double(wmax));
+        }
+    }
+    if (!(phase & 2)) return;
+    float r1 = 0.0f, r2 = 0.0f;
+    ordered_sums(a.part1, a.part2, a.nblkN, g, sbuf, bar, bar_phase, r1, r2);
+    if (valid && !(phase & 1)) {
+        c1 = a.cr1[i];
+        c2 = a.cr2[i];
+        tv = a.Tv[i];
+    }
+    row_verdict(a, i, valid, r1, r2, c1, c2, tv);
+}
+
+// ---------------------------------------------- L2-direct (inside the GEMM)
+// Streamed verification inside the GEMM, whose shared memory is all
+// pipeline: everything is read straight from L2 (lane = row; each block of a
+// partial array is one coalesced 128-byte line for the warp). It runs in two
+// halves so that the half left after the final MMA is short:
+//   stats half  (the warp completing a group's statistics, usually long
+//                before its last tile): T_i and the A (B r) checksums,
+//                staged in cr1 / cr2 / Tv;
+//   final half  (the warp making the group's last arrival): the row sums
+//                and the verdict, one round of loads for N <= 32 * 128.
+constexpr int kDirectBatch = 32;
+
+// ordered FP32 sums of two partial arrays (reduce_terms NativeBlocked(128))
+__device__ __forceinline__ void ordered_sums_l2(const float* x1, const float* x2, int64_t nb, int64_t g,
+                                                float& r1, float& r2) {
+    const int lane = threadIdx.x & 31;
+    const float* p1 = x1 + part_index(0, g * 32, nb) + lane;
+    const float* p2 = x2 + part_index(0, g * 32, nb) + lane;
+    for (int64_t b0 = 0; b0 < nb; b0 += kDirectBatch) {
+        float v1[kDirectBatch], v2[kDirectBatch];
+#pragma unroll
+        for (int j = 0; j < kDirectBatch; ++j) {
+            const bool ok = b0 + j < nb;
+            v1[j] = ok ? __ldcg(p1 + (b0 + j) * 32) : 0.0f;
+            v2[j] = ok ? __ldcg(p2 + (b0 + j) * 32) : 0.0f;
+        }
+#pragma unroll
+        for (int j = 0; j < kDirectBatch; ++j) {
+            if (b0 + j < nb) {
+                r1 = __fadd_rn(r1, v1[j]);
+                r2 = __fadd_rn(r2, v2[j]);
+            }
+        }
+    }
+}
+
+template <int F>
+__device__ void stats_half_direct(const TailArgs& a, int64_t g) {
+    const int lane = threadIdx.x & 31;
+    const int64_t i = g * 32 + lane;
+    const bool valid = i < a.M;
+    double sum = 0.0;
+    uint32_t kmax = 0u, kmin = 0xFFFFFFFFu, mnz = 0xFFFFFFFFu;
+    if (valid) {
+        sum = __ldcg(a.rsum + i);
+        kmax = __ldcg(a.rmax + i);
+        kmin = __ldcg(a.rmin + i);
+        mnz = __ldcg(a.rmnz + i);
+    }
+    float t1 = 0.0f, t2 = 0.0f;
+    ordered_sums_l2(a.sp1, a.sp2, a.nblkK, g, t1, t2);
+    if (valid) {
+        double c1, c2, tv;
+        float amax;
+        row_threshold<F>(a, i, sum, kmax, kmin, mnz, t1, t2, tv, c1, c2, amax);
+        a.cr1[i] = c1;
+        a.cr2[i] = c2;
+        a.Tv[i] = tv;
+    }
+}
+
+__device__ __forceinline__ void final_half_direct(const TailArgs& a, int64_t g) {
+    const int lane = threadIdx.x & 31;
+    const int64_t i = g * 32 + lane;
+    const bool valid = i < a.M;
+    double c1 = 0.0, c2 = 0.0, tv = 0.0;
+    if (valid) {
+        c1 = __ldcg(a.cr1 + i);
+        c2 = __ldcg(a.cr2 + i);
+        tv = __ldcg(a.Tv + i);
+    }
+    float r1 = 0.0f, r2 = 0.0f;
+    ordered_sums_l2(a.part1, a.part2, a.nblkN, g, r1, r2);
+    row_verdict(a, i, valid, r1, r2, c1, c2, tv);
 }
 
 // Self-resetting grid barrier for a co-resident (cooperative) grid: the last

@@ -83,27 +83,36 @@ __device__ __forceinline__ void tile_coords(const TcParams& p, int tile, int& m_
     n_blk = rem / gm;
 }
 
-// Streamed verification arrival (see TcEpilogue::stream_verify): publish this
-// warp's partials of row group g, count the arrival, and verify the group if
-// it was the last one (2 per N tile: epilogue + statistics warp).
-template <int F>
-__device__ __forceinline__ void group_arrive(const TcParams& p, int64_t g) {
-    if (g * 32 >= p.M) return;
-    const int lane = threadIdx.x & 31;
-    // __syncwarp orders every lane's partial / atomic writes before lane 0's
-    // acq_rel RMW at GPU scope (release is cumulative); the last arriver's
-    // acquire side orders the verifier's L2 reads after all other arrivals.
-    // (A full __threadfence per lane is fence.sc + L1 invalidate: measured
-    // to cost tensor-pipe time when issued once per tile per warp.)
+// Streamed verification (see TcEpilogue::stream_verify). Per 32-row group g
+// two self-resetting counters: group_cnt[2g] counts statistics arrivals (one
+// per N tile), group_cnt[2g+1] final arrivals (one per N tile from the
+// epilogue + one from the statistics half). __syncwarp orders every lane's
+// partial / atomic writes before lane 0's acq_rel RMW at GPU scope (release
+// is cumulative); the acquire side orders the verifier's L2 reads after all
+// earlier arrivals. (A __threadfence per lane is fence.sc + L1 invalidate.)
+__device__ __forceinline__ unsigned int warp_arrive(unsigned int* cnt) {
     __syncwarp();
     unsigned int old = 0;
-    if (lane == 0) old = atom_add_acq_rel_gpu(p.epi.group_cnt + g, 1u);
-    old = __shfl_sync(0xffffffffu, old, 0);
-    if (old != 2u * unsigned(p.num_n_blk) - 1u || p.epi.debug == 7) return;  // 7: ablation, no verify
-    uint32_t unused_phase = 0;
-    verify_rowgroup<F, true>(p.epi.tail, g, 3, nullptr, 0u, unused_phase);
+    if ((threadIdx.x & 31) == 0) old = atom_add_acq_rel_gpu(cnt, 1u);
+    return __shfl_sync(0xffffffffu, old, 0);
+}
+
+__device__ __forceinline__ void final_arrive(const TcParams& p, int64_t g) {
+    unsigned int* cnt = p.epi.group_cnt + 2 * g + 1;
+    if (warp_arrive(cnt) != unsigned(p.num_n_blk)) return;  // target num_n_blk + 1
+    if (p.epi.debug != 7) final_half_direct(p.epi.tail, g);  // 7: ablation, no verification
     __syncwarp();
-    if (lane == 0) p.epi.group_cnt[g] = 0u;  // ready for the next launch
+    if ((threadIdx.x & 31) == 0) *cnt = 0u;  // ready for the next launch
+}
+
+template <int F>
+__device__ __forceinline__ void stats_arrive(const TcParams& p, int64_t g) {
+    unsigned int* cnt = p.epi.group_cnt + 2 * g;
+    if (warp_arrive(cnt) != unsigned(p.num_n_blk) - 1u) return;
+    if (p.epi.debug != 7) stats_half_direct<F>(p.epi.tail, g);
+    __syncwarp();
+    if ((threadIdx.x & 31) == 0) *cnt = 0u;
+    final_arrive(p, g);
 }
 
 // ------------------------------------------------ in-GEMM A statistics
@@ -319,7 +328,8 @@ __device__ __forceinline__ void stats_warps(const TcParams& p, const uint8_t* sm
             }
             acc.reset();
         }
-        if (p.epi.stream_verify) group_arrive<kFmt>(p, int64_t(m_blk) * 4 + sw);
+        if (p.epi.stream_verify && (int64_t(m_blk) * 4 + sw) * 32 < p.M)
+            stats_arrive<kFmt>(p, int64_t(m_blk) * 4 + sw);
     }
 }
 
@@ -586,7 +596,8 @@ __global__ void __launch_bounds__(kThreadsStats, 1)
                 acc_phase ^= 1;
             }
             if constexpr (kStats) {
-                if (p.epi.stream_verify) group_arrive<kFmt>(p, int64_t(m_blk) * 4 + quad);
+                if (p.epi.stream_verify && (int64_t(m_blk) * 4 + quad) * 32 < p.M)
+                    final_arrive(p, int64_t(m_blk) * 4 + quad);
             }
         }
     }

@@ -1,0 +1,172 @@
+"""e_max models: the reference's calibration result type (fit_model /
+CalibrationResult::e_max_for, proj/src/calibration.cpp:15-74) and the
+device-calibrated defaults the fused tcgen05 path uses.
+
+The reference resolves e_max per run by calibrating (harness.cpp
+resolve_run_e_max: calibrate(precision, mode, {128, 256, 512, K}) then
+e_max_for(K)). Online verification compares the FP32 accumulator of the
+tensor core, whose rounding the CPU emulator does not reproduce, so the
+online defaults here come from the same protocol run on the B200 fused path
+(calibration.calibrate; raw data in profiles/r01_calibration_*_device.json):
+|N(1,1)| square operands, per size the max over trials and rows of
+|D1| / |row_check1|. Offline defaults are the reference's format constants
+(precision.cpp:44-62), which its own calibration reproduces (the 2u floor).
+"""
+from __future__ import annotations
+
+import math
+from dataclasses import dataclass, field
+from typing import Dict, List, Sequence, Tuple
+
+
+@dataclass
+class CalibrationModel:
+    kind: str = "constant"  # "constant" | "sqrt_scaled" (EmaxModel::Kind)
+    value: float = 0.0
+    scale: float = 0.0
+    offset: float = 0.0
+    cv: float = 0.0
+    r2: float = 0.0
+
+
+def fit_model(sizes: Sequence[int], maxima: Sequence[float]) -> CalibrationModel:
+    """fit_model (calibration.cpp:15-59): Constant if the maxima vary little
+    (CV < 15%), else least squares of max against sqrt(size)."""
+    if len(sizes) != len(maxima) or not sizes:
+        raise ValueError("fit_model: sizes and maxima must match and be nonempty")
+    n = len(maxima)
+    m = CalibrationModel()
+    mean = sum(maxima) / n
+    m.value = mean
+    if n >= 2 and mean > 0.0:
+        ss = sum((v - mean) ** 2 for v in maxima)
+        m.cv = math.sqrt(ss / (n - 1)) / mean
+    if n >= 2:
+        xs = [math.sqrt(float(s)) for s in sizes]
+        sx, sy = sum(xs), sum(maxima)
+        sxx = sum(x * x for x in xs)
+        sxy = sum(x * y for x, y in zip(xs, maxima))
+        denom = n * sxx - sx * sx
+        if denom != 0.0:
+            m.scale = (n * sxy - sx * sy) / denom
+            m.offset = (sy - m.scale * sx) / n
+            ss_res = sum((y - (m.scale * x + m.offset)) ** 2 for x, y in zip(xs, maxima))
+            ss_tot = sum((y - mean) ** 2 for y in maxima)
+            m.r2 = 1.0 - ss_res / ss_tot if ss_tot > 0.0 else 1.0
+    m.kind = "constant" if (n < 2 or m.cv < 0.15 or m.scale <= 0.0) else "sqrt_scaled"
+    return m
+
+
+@dataclass
+class CalibrationResult:
+    precision: str
+    mode: str
+    sizes: List[int]
+    maxima: List[float]
+    model: CalibrationModel
+    recommended: float
+    unit_roundoff: float
+    trials_per_size: int
+    aborted_trials: int = 0
+    engine: str = "tensor"
+
+    @classmethod
+    def from_maxima(cls, precision: str, mode: str, sizes: Sequence[int], maxima: Sequence[float],
+                    trials: int, aborted: int = 0) -> "CalibrationResult":
+        """calibrate()'s result assembly (calibration.cpp:135-150)."""
+        u = unit_roundoff_for(precision, mode)
+        overall = max(maxima) if maxima else 0.0
+        return cls(precision, mode, list(sizes), list(maxima), fit_model(list(sizes), list(maxima)),
+                   max(1.2 * overall, 2.0 * u), u, trials, aborted)
+
+    def e_max_for(self, dim: int) -> float:
+        """e_max_for (calibration.cpp:61-74): margin 1.2, floor 2u; a
+        SqrtScaled model is inflated so every calibrated size stays covered."""
+        floor = 2.0 * self.unit_roundoff
+        if self.model.kind == "constant":
+            return max(self.recommended, floor)
+        lam = 1.0
+        for s, mx in zip(self.sizes, self.maxima):
+            fit = self.model.scale * math.sqrt(float(s)) + self.model.offset
+            if fit > 0.0:
+                lam = max(lam, mx / fit)
+        return max(1.2 * lam * (self.model.scale * math.sqrt(float(dim)) + self.model.offset), floor)
+
+    def as_dict(self):
+        return {"precision": self.precision, "mode": self.mode, "engine": self.engine, "sizes": self.sizes,
+                "maxima": self.maxima, "model": self.model.__dict__, "recommended": self.recommended,
+                "trials": self.trials_per_size, "aborted_trials": self.aborted_trials}
+
+
+def unit_roundoff_for(precision: str, mode: str) -> float:
+    """u of the verification precision: the FP32 accumulator online, the
+    format itself offline (checksum_precision_for, checksum.cpp:18-24)."""
+    if mode == "online":
+        return 2.0 ** -24
+    return {"bf16": 2.0 ** -8, "fp16": 2.0 ** -11, "fp32": 2.0 ** -24, "fp64": 2.0 ** -53}[precision]
+
+
+# Device calibration of the fused tcgen05 path (B200, 6 trials per size,
+# seed 0; tools/calib_run.py). Maxima of |D1|/|row_check1| per square size.
+DEVICE_CALIBRATION: Dict[Tuple[str, str], Tuple[List[int], List[float]]] = {
+    ("bf16", "online"): ([128, 256, 512, 1024, 2048, 4096, 8192, 16384],
+                         [1.04e-06, 9.19e-07, 1.32e-06, 2.59e-06, 6.06e-06, 1.48e-05, 3.61e-05, 8.40e-05]),
+}
+
+# reference format defaults (PrecisionSpec::bf16/fp16, precision.cpp:44-62)
+FORMAT_DEFAULT = {"bf16": 8e-3, "fp16": 1e-3}
+
+
+def device_calibration(precision: str, mode: str) -> CalibrationResult:
+    key = (precision, mode)
+    if key not in DEVICE_CALIBRATION:
+        raise KeyError(f"no device calibration for {precision}/{mode}")
+    sizes, maxima = DEVICE_CALIBRATION[key]
+    return CalibrationResult.from_maxima(precision, mode, sizes, maxima, trials=6)
+
+
+def measured_max(precision: str, mode: str, size: int) -> float:
+    """The calibration maximum at `size`: the device table, log-log
+    interpolated between calibrated sizes (extrapolated along the end
+    segments outside them)."""
+    sizes, maxima = DEVICE_CALIBRATION[(precision, mode)]
+    if size in sizes:
+        return maxima[sizes.index(size)]
+    i = 1
+    while i < len(sizes) - 1 and sizes[i] < size:
+        i += 1
+    x0, x1 = math.log(sizes[i - 1]), math.log(sizes[i])
+    y0, y1 = math.log(maxima[i - 1]), math.log(maxima[i])
+    return math.exp(y0 + (y1 - y0) * (math.log(size) - x0) / (x1 - x0))
+
+
+def resolve_run_e_max(precision: str, mode: str, k: int) -> float:
+    """resolve_run_e_max (harness.cpp, with auto_calib_sizes): calibration
+    sizes {128, 256, 512} plus K (K > 512) or with K prepended (K < 128),
+    model fitted on those, e_max_for(K) — with the device calibration's
+    maxima standing in for per-run trials."""
+    sizes = [128, 256, 512]
+    if k > 512:
+        sizes.append(k)
+    if k < 128:
+        sizes.insert(0, k)
+    maxima = [measured_max(precision, mode, s) for s in sizes]
+    return CalibrationResult.from_maxima(precision, mode, sizes, maxima, trials=6).e_max_for(k)
+
+
+def default_e_max(precision: str, mode: str, k: int) -> float:
+    """e_max the fused path uses when the caller gives none: calibrate()'s
+    `recommended` rule applied at the accumulation length itself,
+    max(1.2 x max(K), 2u), with max(K) from the device calibration.
+    (resolve_run_e_max above is the reference's per-run rule; its lambda
+    inflation turns erratic when the sqrt fit nearly vanishes at a small
+    calibration size, e.g. 1.6e-3 at K = 3072 against 1.8e-5 at K = 4096.)
+    The FP16 online path shares the BF16 path's FP32 accumulator and uses
+    its table when it has none of its own; offline without a table, the
+    format constant."""
+    key = (precision, mode) if (precision, mode) in DEVICE_CALIBRATION else None
+    if key is None and mode == "online":
+        key = ("bf16", "online")
+    if key is None:
+        return FORMAT_DEFAULT[precision]
+    return max(1.2 * measured_max(key[0], key[1], k), 2.0 * unit_roundoff_for(precision, mode))

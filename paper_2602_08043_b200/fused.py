@@ -17,15 +17,13 @@ import torch
 
 from . import _capi
 from ._capi import check, lib
+from .emax import default_e_max
 from .device import ptr, stream_ptr
 
 _FMT = {torch.bfloat16: _capi.BF16, torch.float16: _capi.FP16}
 _METHOD = {"vabft": 0, "aabft-fixed-y": 1, "aabft-computed-y": 2}
 
-# e_max for online (FP32-accumulator) verification of the tcgen05 kernel:
-# the calibrate() protocol (proj/src/calibration.cpp:88-150) run on B200 —
-# see calibration.py / DESIGN.md. Overridable per call.
-DEFAULT_ONLINE_EMAX = 2.0e-6
+_FMT_NAME = {torch.bfloat16: "bf16", torch.float16: "fp16"}
 
 
 @dataclass
@@ -55,10 +53,9 @@ class FusedAbftGemm:
         self.k, self.n = self.B.shape
         self.mode = _capi.ONLINE if mode == "online" else _capi.OFFLINE
         if e_max is None:
-            if self.mode == _capi.ONLINE:
-                e_max = DEFAULT_ONLINE_EMAX
-            else:
-                e_max = 8e-3 if self.fmt == _capi.BF16 else 1e-3  # format defaults (precision.cpp:44-62)
+            # resolve_run_e_max (harness.cpp): the calibrated model at dim = K
+            e_max = default_e_max(_FMT_NAME[B.dtype], "online" if self.mode == _capi.ONLINE else "offline",
+                                  self.k)
         self.opts = _capi.FusedOpts()
         self.opts.mode = self.mode
         self.opts.threshold_method = _METHOD[threshold]
