@@ -281,6 +281,19 @@ class Oracle:
         return X, {"i": int(rec[0]), "j": int(rec[1]), "applied": bool(rec[2]), "direction_taken": int(rec[3]),
                    "value_before": vals[0], "value_after": vals[1]}
 
+    def calibrate(self, fmt, sizes, trials, seed, mode="offline", dim=None):
+        """Reference calibrate (calibration.cpp:88-150); reference library only.
+        Returns (maxima, {kind, value, scale, offset, recommended, e_max_at_dim})."""
+        if self.name != "reference":
+            raise OracleError(5, "calibrate: reference library only")
+        sz = np.asarray(sizes, dtype=np.int64)
+        mx = np.zeros(len(sizes))
+        out = np.zeros(6)
+        self._call("calibrate", FORMATS[fmt], 1 if mode == "online" else 0, sz.ctypes.data_as(_I64), len(sizes), trials, seed,
+                   int(dim if dim is not None else sizes[-1]), _dp(mx), _dp(out))
+        return mx, {"kind": "constant" if out[0] == 0.0 else "sqrt_scaled", "value": out[1], "scale": out[2],
+                    "offset": out[3], "recommended": out[4], "e_max_at_dim": out[5]}
+
     def campaign_trial(self, m, k, n, fmt, dist, bit, seed, trial, mode="offline", method=0, e_max=8e-3,
                        c_sigma=2.5, direction=1):
         kind, p0, p1, lo, hi = parse_dist(dist)

@@ -109,8 +109,15 @@ def unit_roundoff_for(precision: str, mode: str) -> float:
 # Device calibration of the fused tcgen05 path (B200, 6 trials per size,
 # seed 0; tools/calib_run.py). Maxima of |D1|/|row_check1| per square size.
 DEVICE_CALIBRATION: Dict[Tuple[str, str], Tuple[List[int], List[float]]] = {
+    # 10 trials per size (profiles/r01_calibration_bf16_device_10trials.json)
     ("bf16", "online"): ([128, 256, 512, 1024, 2048, 4096, 8192, 16384],
-                         [1.04e-06, 9.19e-07, 1.32e-06, 2.59e-06, 6.06e-06, 1.48e-05, 3.61e-05, 8.40e-05]),
+                         [1.04e-06, 9.20e-07, 1.41e-06, 2.55e-06, 6.05e-06, 1.49e-05, 3.61e-05, 8.41e-05]),
+    # profiles/r01_calibration_fp16_device.json. (FP16 OFFLINE is not tabled:
+    # with |N(1,1)| operands the FP16-quantized checksums saturate at 65504
+    # from size 256 on, so the protocol measures overflow, not rounding; the
+    # format constant stays.)
+    ("fp16", "online"): ([128, 256, 512, 1024, 2048, 4096, 8192, 16384],
+                         [1.48e-06, 1.88e-06, 3.39e-06, 6.62e-06, 1.35e-05, 2.73e-05, 5.45e-05, 1.10e-04]),
 }
 
 # reference format defaults (PrecisionSpec::bf16/fp16, precision.cpp:44-62)
