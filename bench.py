@@ -40,7 +40,7 @@ CONFIGS = {
                        "N(0,1) inputs; 1 GEMM per GPU per step", "gemms": [(4096, 4096, 4096)], "scaling": "weak"},
     "llama": {"workload": "LLaMA-7B layer GEMMs, tokens M=8192, (K,N) in {(4096,4096)x4,(4096,11008)x2,"
                           "(11008,4096)x1}, 1 layer per GPU per step", "gemms": [(8192, k, n) for k, n in LLAMA_LAYER],
-              "scaling": "weak"},
+              "scaling": "weak", "weights": "linear"},
 }
 
 
@@ -183,7 +183,10 @@ def run_ours(args, cfg):
     As, Bs, Cs, gs = [], [], [], []
     for (m, k, n) in gemms:
         As.append(torch.randn(m, k, device=dev).bfloat16())
-        Bs.append(torch.randn(k, n, device=dev).bfloat16())
+        if cfg.get("weights") == "linear":  # nn.Linear default init, U(-1/sqrt(K), 1/sqrt(K))
+            Bs.append(((torch.rand(k, n, device=dev) * 2 - 1) / k ** 0.5).bfloat16())
+        else:
+            Bs.append(torch.randn(k, n, device=dev).bfloat16())
         Cs.append(torch.empty(m, n, device=dev, dtype=torch.bfloat16))
         gs.append(FusedAbftGemm(Bs[-1], mode=args.mode))
     counts = torch.zeros(5, dtype=torch.int64, device=dev)
@@ -334,7 +337,8 @@ def run_ours(args, cfg):
         "metric": METRIC, "value": value, "unit": "TFLOP/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms_fused / args.steps, "higher_is_better": True,
         "scaling": cfg["scaling"], "vs_baseline": None, "dtype": "bf16",
-        "data": "synthetic: A ~ N(0,1), random-init B ~ N(0,1), BF16 on device",
+        "data": "synthetic: A ~ N(0,1), random-init B ~ " + ("U(-1/sqrt(K), 1/sqrt(K))" if cfg.get("weights") == "linear"
+                                                              else "N(0,1)") + ", BF16 on device",
         "config": {"workload": cfg["workload"], "mode": args.mode, "l2": "flushed between steps (512 MiB write)",
                    "parallelism": f"independent GEMMs x{world} (no operand exchange), NCCL all-reduce of counters"},
         "plain_gemm_tflops": plain_tf,
