@@ -294,6 +294,19 @@ class Oracle:
         return mx, {"kind": "constant" if out[0] == 0.0 else "sqrt_scaled", "value": out[1], "scale": out[2],
                     "offset": out[3], "recommended": out[4], "e_max_at_dim": out[5]}
 
+    def injection_campaign(self, m, k, n, fmt, dist, bit, trials, seed, mode="offline", method=0, e_max=8e-3,
+                           c_sigma=2.5, direction=1):
+        """Reference injection_campaign (faults.cpp:170-216), multithreaded over
+        trials; reference library only. Returns [trials, applicable, detected,
+        located_correctly, nonfinite_after]."""
+        if self.name != "reference":
+            raise OracleError(5, "injection_campaign: reference library only")
+        kind, p0, p1, lo, hi = parse_dist(dist)
+        out = np.zeros(5, dtype=np.int64)
+        self._call("injection_campaign", m, k, n, FORMATS[fmt], kind, p0, p1, lo, hi, bit, direction, trials, seed,
+                   1 if mode == "online" else 0, method, e_max, c_sigma, out.ctypes.data_as(_I64))
+        return out
+
     def campaign_trial(self, m, k, n, fmt, dist, bit, seed, trial, mode="offline", method=0, e_max=8e-3,
                        c_sigma=2.5, direction=1):
         kind, p0, p1, lo, hi = parse_dist(dist)
