@@ -128,7 +128,8 @@ extern "C" vabft_status vabft_bside_create(int32_t format, int32_t mode, int64_t
         h->B = B;
         const size_t K = size_t(k);
         const size_t KB = size_t(br_storage_floats(k));
-        const size_t bytes = align_up(8 * K) * 3 + align_up(4 * KB) * 2 + align_up(8 * 4) + align_up(4) + align_up(8);
+        const size_t bytes = align_up(8 * K) * 3 + align_up(4 * KB) * 2 + align_up(8 * 4) + align_up(4) + align_up(8) +
+                             align_up(4);
         cudaError_t e = cudaMalloc(&h->storage, bytes);
         if (e != cudaSuccess) {
             delete h;
@@ -142,8 +143,10 @@ extern "C" vabft_status vabft_bside_create(int32_t format, int32_t mode, int64_t
         h->buf.br2 = reinterpret_cast<float*>(p); p += align_up(4 * KB);
         h->buf.summary = reinterpret_cast<double*>(p); p += align_up(32);
         h->buf.nonfinite = reinterpret_cast<int*>(p); p += align_up(4);
-        h->gbar = reinterpret_cast<unsigned int*>(p);
+        h->gbar = reinterpret_cast<unsigned int*>(p); p += align_up(8);
+        h->buf.done = reinterpret_cast<unsigned int*>(p);
         check_cuda(cudaMemset(h->gbar, 0, 2 * sizeof(unsigned int)), "memset(grid barrier)");
+        check_cuda(cudaMemset(h->buf.done, 0, sizeof(unsigned int)), "memset(bside counter)");
         *out = h;
         if (B) {
             check_cuda(cudaMemsetAsync(h->buf.nonfinite, 0, sizeof(int), as_stream(stream)), "memset");

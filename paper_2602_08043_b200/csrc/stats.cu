@@ -15,10 +15,13 @@
 // max/min, FP32 checksum sums in the reference's NativeBlocked(128) order:
 // lane l owns 128-element blocks l, l+32, ... (sequential inside a block)
 // and block partials are combined sequentially in block order.
+#include <cstdlib>
+
 #include "devcommon.cuh"
 #include "internal.hpp"
 #include "numerics.cuh"
 #include "stats.hpp"
+#include "tail.cuh"
 
 namespace vabft_dev {
 
@@ -163,6 +166,203 @@ __global__ void __launch_bounds__(1024) bside_summary_kernel(const double* mean,
     if (t == 96) summary[3] = acc;
 }
 
+// ----------------------------------------- B side, 16-bit formats (HBM pass)
+// One warp per B row; the row streams through a per-warp 8 KiB shared-memory
+// stage (32 blocks of 128 elements) with coalesced 16-byte loads, written
+// with a 16-byte-chunk XOR swizzle (chunk c of block b at c ^ (b & 15)) so
+// that lane l then walks its own block l (the reference's sequential order
+// inside a 128-element block) without bank conflicts. Per element: FP32
+// B r1 / B r2 block partials (no FMA), an FP64 partial of the row sum (plain
+// adds: exact under the guard below), packed max / min / min-nonzero
+// trackers. The row sum is exact in any order when
+// n max|x| < 2^(53 + lsb(min nonzero |x|)) (tail.cuh guard_exact), and then
+// equals both the reference's Neumaier sum (row_stats) and its plain
+// sequential sum (aabft_computed_y); rows failing the guard are redone
+// sequentially by lane 0. The last CTA to finish computes the summary
+// (BStatsSummary::from's sequential FP64 sums and max_k |sum_j B|).
+constexpr int kB16Warps = 8;
+constexpr int kB16StageGranules = 32 * 16;  // 32 blocks x 16 granules of 8 elements
+
+template <int F>
+__device__ __forceinline__ float b16_f(uint32_t bits) {
+    return bits16_to_float<F>(uint16_t(bits));
+}
+
+// BStatsSummary::from's sequential FP64 sums (threshold_vabft.cpp:15-26) and
+// max_k |sum_j B| (threshold_aabft.cpp:38-48), by the whole CTA: chunks of
+// the inputs are staged into shared memory with coalesced loads, then thread
+// 0 runs the four independent serial chains out of shared memory.
+__device__ void bside_summary_cta(const double* mean, const double* vb, const double* rowsum_abs, int64_t K,
+                                  double* summary, double* sm, int sm_doubles) {
+    const int chunk = sm_doubles / 3;
+    double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+    for (int64_t c0 = 0; c0 < K; c0 += chunk) {
+        const int cnt = int(K - c0 < chunk ? K - c0 : chunk);
+        __syncthreads();
+        for (int i = threadIdx.x; i < cnt; i += blockDim.x) {
+            sm[i] = __ldcg(mean + c0 + i);
+            sm[chunk + i] = __ldcg(vb + c0 + i);
+            sm[2 * chunk + i] = __ldcg(rowsum_abs + c0 + i);
+        }
+        __syncthreads();
+        if (threadIdx.x == 0) {
+#pragma unroll 8
+            for (int i = 0; i < cnt; ++i) {
+                const double m = sm[i];
+                a0 = __dadd_rn(a0, fabs(m));
+                a1 = __dadd_rn(a1, __dmul_rn(m, m));
+                a2 = __dadd_rn(a2, sm[chunk + i]);
+                a3 = fmax(a3, sm[2 * chunk + i]);
+            }
+        }
+    }
+    if (threadIdx.x == 0) {
+        summary[0] = a0;
+        summary[1] = a1;
+        summary[2] = a2;
+        summary[3] = a3;
+    }
+}
+
+template <int F>
+__global__ void __launch_bounds__(32 * kB16Warps) bside_rows16_kernel(const uint16_t* __restrict__ B, int64_t K,
+                                                                      int64_t N, int quantize_br, BsideBuffers buf,
+                                                                      unsigned int* done) {
+    extern __shared__ uint4 b16_stage[];
+    const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int64_t k = int64_t(blockIdx.x) * kB16Warps + w;
+    if (k < K) {
+        uint4* st = b16_stage + w * kB16StageGranules;
+        const uint4* row = reinterpret_cast<const uint4*>(B + k * N);
+        const int64_t ng = N / 8, nblk = (N + 127) / 128;
+        // four independent FP64 partials per lane (the sum is order-free under
+        // the guard; one chain would serialize on FP64 add latency)
+        double sp[4] = {0.0, 0.0, 0.0, 0.0};
+        float t1 = 0.0f, t2 = 0.0f;
+        uint32_t vmax = F == VABFT_BF16 ? 0xFF80FF80u : 0xFC00FC00u;
+        uint32_t vmin = F == VABFT_BF16 ? 0x7F807F80u : 0x7C007C00u;
+        uint32_t vmnz = 0x7FFF7FFFu, vmag = 0u;
+        for (int64_t b0 = 0; b0 < nblk; b0 += 32) {
+            const int64_t g0 = b0 * 16;
+            const int gcnt = int(ng - g0 < kB16StageGranules ? ng - g0 : kB16StageGranules);
+            __syncwarp();
+            for (int q = lane; q < gcnt; q += 32) {
+                const int blk = q >> 4, c = q & 15;
+                st[blk * 16 + (c ^ (blk & 15))] = __ldcs(row + g0 + q);  // streamed: read once
+            }
+            __syncwarp();
+            float p1 = 0.0f, p2 = 0.0f;
+            const int64_t blk = b0 + lane;
+            if (blk < nblk) {
+                const int nc = int(ng - blk * 16 < 16 ? ng - blk * 16 : 16);
+                for (int c = 0; c < nc; ++c) {
+                    const uint4 v = st[lane * 16 + (c ^ (lane & 15))];
+                    const uint32_t ws[4] = {v.x, v.y, v.z, v.w};
+                    const float jb = float(blk * 128 + c * 8 + 1);  // weight of element 0 (exact: N <= 2^24)
+#pragma unroll
+                    for (int h = 0; h < 4; ++h) {
+                        uint32_t d;
+                        if constexpr (F == VABFT_BF16) {
+                            asm("max.bf16x2 %0, %1, %2;" : "=r"(d) : "r"(vmax), "r"(ws[h]));
+                            vmax = d;
+                            asm("min.bf16x2 %0, %1, %2;" : "=r"(d) : "r"(vmin), "r"(ws[h]));
+                            vmin = d;
+                        } else {
+                            asm("max.f16x2 %0, %1, %2;" : "=r"(d) : "r"(vmax), "r"(ws[h]));
+                            vmax = d;
+                            asm("min.f16x2 %0, %1, %2;" : "=r"(d) : "r"(vmin), "r"(ws[h]));
+                            vmin = d;
+                        }
+                        const uint32_t mag = ws[h] & 0x7FFF7FFFu;
+                        asm("max.u16x2 %0, %1, %2;" : "=r"(d) : "r"(vmag), "r"(mag));
+                        vmag = d;
+                        asm("min.u16x2 %0, %1, %2;" : "=r"(d) : "r"(vmnz),
+                            "r"(((mag | 0x80008000u) - 0x00010001u) & 0x7FFF7FFFu));
+                        vmnz = d;
+                        const float xa = b16_f<F>(ws[h] & 0xFFFFu), xb = b16_f<F>(ws[h] >> 16);
+                        sp[h] = __dadd_rn(sp[h], __dadd_rn(double(xa), double(xb)));  // exact under the guard
+                        p1 = __fadd_rn(p1, xa);
+                        p2 = __fadd_rn(p2, __fmul_rn(__fadd_rn(jb, float(2 * h)), xa));
+                        p1 = __fadd_rn(p1, xb);
+                        p2 = __fadd_rn(p2, __fmul_rn(__fadd_rn(jb, float(2 * h + 1)), xb));
+                    }
+                }
+            }
+            const int cnt = int(nblk - b0 < 32 ? nblk - b0 : 32);
+            for (int l = 0; l < cnt; ++l) {  // block partials in block order
+                t1 = __fadd_rn(t1, __shfl_sync(0xffffffffu, p1, l));
+                t2 = __fadd_rn(t2, __shfl_sync(0xffffffffu, p2, l));
+            }
+        }
+        // combine lanes: the FP64 partials (exact under the guard), trackers
+        double s = __dadd_rn(__dadd_rn(sp[0], sp[1]), __dadd_rn(sp[2], sp[3]));
+        vmag = max(vmag & 0xFFFFu, vmag >> 16);
+#pragma unroll
+        for (int m = 16; m >= 1; m >>= 1) {
+            s = __dadd_rn(s, __shfl_xor_sync(0xffffffffu, s, m));
+            uint32_t o = __shfl_xor_sync(0xffffffffu, vmax, m), d;
+            if constexpr (F == VABFT_BF16) asm("max.bf16x2 %0, %1, %2;" : "=r"(d) : "r"(vmax), "r"(o));
+            else asm("max.f16x2 %0, %1, %2;" : "=r"(d) : "r"(vmax), "r"(o));
+            vmax = d;
+            o = __shfl_xor_sync(0xffffffffu, vmin, m);
+            if constexpr (F == VABFT_BF16) asm("min.bf16x2 %0, %1, %2;" : "=r"(d) : "r"(vmin), "r"(o));
+            else asm("min.f16x2 %0, %1, %2;" : "=r"(d) : "r"(vmin), "r"(o));
+            vmin = d;
+            vmag = max(vmag, __shfl_xor_sync(0xffffffffu, vmag, m));
+            o = __shfl_xor_sync(0xffffffffu, vmnz, m);
+            asm("min.u16x2 %0, %1, %2;" : "=r"(d) : "r"(vmnz), "r"(o));
+            vmnz = d;
+        }
+        if (lane == 0) {
+            const bool finite = vmag < (F == VABFT_BF16 ? 0x7F80u : 0x7C00u);
+            if (!finite) atomicExch(buf.nonfinite, 1);
+            const double mx = double(fmaxf(b16_f<F>(vmax & 0xFFFFu), b16_f<F>(vmax >> 16)));
+            const double mn = double(fminf(b16_f<F>(vmin & 0xFFFFu), b16_f<F>(vmin >> 16)));
+            const uint32_t mz = min(vmnz & 0xFFFFu, vmnz >> 16);
+            Neu n;
+            double plain;
+            if (finite && guard_exact<F>(float(fmax(fabs(mx), fabs(mn))), mz, N)) {
+                n.s = s;
+                plain = s;
+            } else {  // the reference's sequential loops over the row
+                const uint16_t* r = B + k * N;
+                plain = 0.0;
+                for (int64_t j = 0; j < N; ++j) {
+                    const double x = double(b16_f<F>(r[j]));
+                    n.add(x);
+                    plain = __dadd_rn(plain, x);
+                }
+            }
+            double m, v;
+            stats_finish(n, mx, mn, N, &m, &v);
+            buf.mean[k] = m;
+            buf.vb[k] = v;
+            if (quantize_br) {
+                t1 = bits16_to_float<F>(quantize16_bits<F>(t1));
+                t2 = bits16_to_float<F>(quantize16_bits<F>(t2));
+            }
+            buf.br1[k] = t1;
+            buf.br2[k] = t2;
+            buf.rowsum_abs[k] = fabs(plain);
+        }
+    }
+    if (done == nullptr) return;
+    // last CTA: the summary (self-resetting counter)
+    __syncthreads();
+    __shared__ unsigned int last;
+    if (threadIdx.x == 0) {
+        __threadfence();
+        last = atomicAdd(done, 1u) == gridDim.x - 1 ? 1u : 0u;
+    }
+    __syncthreads();
+    if (last) {  // CTA-uniform
+        __threadfence();
+        bside_summary_cta(buf.mean, buf.vb, buf.rowsum_abs, K, buf.summary, reinterpret_cast<double*>(b16_stage),
+                          kB16Warps * kB16StageGranules * 2);
+        if (threadIdx.x == 0) *done = 0u;
+    }
+}
+
 }  // namespace
 
 int64_t br_storage_floats(int64_t K) { return ((K + 127) / 128) * 128; }
@@ -187,6 +387,31 @@ void launch_bside(int fmt, int64_t K, int64_t N, const void* B, int quantize_br,
     // padding lanes of the interleaved B r vectors must read as zero
     check_cuda(cudaMemsetAsync(buf.br1, 0, sizeof(float) * size_t(br_storage_floats(K)), s), "memset");
     check_cuda(cudaMemsetAsync(buf.br2, 0, sizeof(float) * size_t(br_storage_floats(K)), s), "memset");
+    if ((fmt == VABFT_BF16 || fmt == VABFT_FP16) && N % 8 == 0 && N <= (int64_t(1) << 24)) {
+        const unsigned grid16 = unsigned((K + kB16Warps - 1) / kB16Warps);
+        const size_t smem = size_t(kB16Warps) * kB16StageGranules * sizeof(uint4);  // 64 KiB
+        static bool attr_set[2] = {false, false};  // per format (both kernels share one pointer type)
+        auto run = [&](auto kern) {
+            bool& attr = attr_set[fmt == VABFT_BF16 ? 0 : 1];
+            if (!attr) {
+                check_cuda(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)),
+                           "attr(bside_rows16)");
+                attr = true;
+            }
+            static const bool split = std::getenv("VABFT_BSIDE_SPLIT") != nullptr;  // developer: time the parts
+            kern<<<grid16, 32 * kB16Warps, smem, s>>>(static_cast<const uint16_t*>(B), K, N, quantize_br, buf,
+                                                       split ? nullptr : buf.done);
+            if (split) buf.done = nullptr;
+        };
+        if (fmt == VABFT_BF16) run(bside_rows16_kernel<VABFT_BF16>);
+        else run(bside_rows16_kernel<VABFT_FP16>);
+        check_cuda(cudaGetLastError(), "bside16 launch");
+        if (buf.done == nullptr) {
+            bside_summary_kernel<<<1, 1024, 0, s>>>(buf.mean, buf.vb, buf.rowsum_abs, K, buf.summary);
+            check_cuda(cudaGetLastError(), "bside summary launch");
+        }
+        return;
+    }
     switch (fmt) {
         case VABFT_BF16: bside_rows_kernel<VABFT_BF16><<<grid, block, 0, s>>>(static_cast<const uint16_t*>(B), K, N, quantize_br, buf.mean, buf.vb, buf.br1, buf.br2, buf.rowsum_abs, buf.nonfinite); break;
         case VABFT_FP16: bside_rows_kernel<VABFT_FP16><<<grid, block, 0, s>>>(static_cast<const uint16_t*>(B), K, N, quantize_br, buf.mean, buf.vb, buf.br1, buf.br2, buf.rowsum_abs, buf.nonfinite); break;

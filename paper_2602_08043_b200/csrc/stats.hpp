@@ -16,6 +16,8 @@ struct BsideBuffers {
     double* rowsum_abs = nullptr;  // [K] |sum_j B[k][j]|
     double* summary = nullptr;     // [4] sum|mu|, sum mu^2, sum var, max_k |sum_j B|
     int* nonfinite = nullptr;      // [1] set when B holds NaN/Inf
+    unsigned int* done = nullptr;  // [1] zero-initialised CTA counter: the last CTA of the
+                                   // 16-bit row pass computes the summary (else a 2nd launch)
 };
 
 // Floats of storage for one interleaved B r vector (K padded to 128).
