@@ -205,23 +205,43 @@ __device__ void bside_summary_cta(const double* mean, const double* vb, const do
             sm[2 * chunk + i] = __ldcg(rowsum_abs + c0 + i);
         }
         __syncthreads();
-        if (threadIdx.x == 0) {
+        // one chain per warp (lane 0 of warps 0..3): the chains run
+        // concurrently at FP64 add latency (~8 cycles on B200) instead of
+        // sharing one thread's issue slots
+        if ((threadIdx.x & 31) == 0) {
+            switch (threadIdx.x >> 5) {
+                case 0:
 #pragma unroll 8
-            for (int i = 0; i < cnt; ++i) {
-                const double m = sm[i];
-                a0 = __dadd_rn(a0, fabs(m));
-                a1 = __dadd_rn(a1, __dmul_rn(m, m));
-                a2 = __dadd_rn(a2, sm[chunk + i]);
-                a3 = fmax(a3, sm[2 * chunk + i]);
+                    for (int i = 0; i < cnt; ++i) a0 = __dadd_rn(a0, fabs(sm[i]));
+                    break;
+                case 1:
+#pragma unroll 8
+                    for (int i = 0; i < cnt; ++i) a1 = __dadd_rn(a1, __dmul_rn(sm[i], sm[i]));
+                    break;
+                case 2:
+#pragma unroll 8
+                    for (int i = 0; i < cnt; ++i) a2 = __dadd_rn(a2, sm[chunk + i]);
+                    break;
+                case 3:
+#pragma unroll 8
+                    for (int i = 0; i < cnt; ++i) a3 = fmax(a3, sm[2 * chunk + i]);
+                    break;
+                default: break;
             }
         }
     }
-    if (threadIdx.x == 0) {
-        summary[0] = a0;
-        summary[1] = a1;
-        summary[2] = a2;
-        summary[3] = a3;
+    if ((threadIdx.x & 31) == 0 && (threadIdx.x >> 5) < 4) {
+        const int c = threadIdx.x >> 5;
+        summary[c] = c == 0 ? a0 : c == 1 ? a1 : c == 2 ? a2 : a3;
     }
+}
+
+__global__ void __launch_bounds__(32 * kB16Warps) bside_summary_cta_kernel(const double* mean, const double* vb,
+                                                                           const double* rowsum_abs, int64_t K,
+                                                                           double* summary) {
+    extern __shared__ uint4 sum_stage[];
+    bside_summary_cta(mean, vb, rowsum_abs, K, summary, reinterpret_cast<double*>(sum_stage),
+                      kB16Warps * kB16StageGranules * 2);
 }
 
 template <int F>
@@ -407,7 +427,14 @@ void launch_bside(int fmt, int64_t K, int64_t N, const void* B, int quantize_br,
         else run(bside_rows16_kernel<VABFT_FP16>);
         check_cuda(cudaGetLastError(), "bside16 launch");
         if (buf.done == nullptr) {
-            bside_summary_kernel<<<1, 1024, 0, s>>>(buf.mean, buf.vb, buf.rowsum_abs, K, buf.summary);
+            static bool sattr = false;
+            if (!sattr) {
+                check_cuda(cudaFuncSetAttribute(bside_summary_cta_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                int(smem)), "attr(bside_summary)");
+                sattr = true;
+            }
+            bside_summary_cta_kernel<<<1, 32 * kB16Warps, smem, s>>>(buf.mean, buf.vb, buf.rowsum_abs, K,
+                                                                     buf.summary);
             check_cuda(cudaGetLastError(), "bside summary launch");
         }
         return;
