@@ -189,7 +189,7 @@ def run_ours(args, cfg):
             Bs.append(torch.randn(k, n, device=dev).bfloat16())
         Cs.append(torch.empty(m, n, device=dev, dtype=torch.bfloat16))
         gs.append(FusedAbftGemm(Bs[-1], mode=args.mode))
-    counts = torch.zeros(5, dtype=torch.int64, device=dev)
+    counts = torch.zeros(6, dtype=torch.int64, device=dev)
     flush = torch.empty(512 * 1024 * 1024, dtype=torch.uint8, device=dev)
     stream = torch.cuda.current_stream()
 
@@ -288,7 +288,7 @@ def run_ours(args, cfg):
     hA = [A.cpu().pin_memory() for A in As]
     hB = [B.cpu().pin_memory() for B in Bs]
     hC = [torch.empty(Cc.shape, dtype=Cc.dtype).pin_memory() for Cc in Cs]
-    hcounts = torch.zeros(5, dtype=torch.int64).pin_memory()
+    hcounts = torch.zeros(6, dtype=torch.int64).pin_memory()
     dA2 = [torch.empty_like(A) for A in As]
     dB2 = [torch.empty_like(B) for B in Bs]
     g_e2e = [FusedAbftGemm(dB, mode=args.mode) for dB in dB2]
@@ -305,7 +305,7 @@ def run_ours(args, cfg):
     e2e_steps = max(3, min(args.steps, 50))
     ms_e2e, _ = timed(step_e2e, e2e_steps, args.warmup, use_graph=False)
     h2d = sum(A.numel() * 2 + B.numel() * 2 for A, B in zip(As, Bs))
-    d2h = sum(Cc.numel() * 2 for Cc in Cs) + 32
+    d2h = sum(Cc.numel() * 2 for Cc in Cs) + hcounts.numel() * 8
 
     value = flops_rank * world / (ms_fused / args.steps / 1e3) / 1e12
     plain_tf = flops_rank * world / (ms_plain / args.steps / 1e3) / 1e12

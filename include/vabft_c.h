@@ -109,7 +109,8 @@ typedef struct vabft_verdicts {
 #define VABFT_COUNT_LOCATED 2
 #define VABFT_COUNT_NAN 3
 #define VABFT_COUNT_SLOW_STATS 4 /* rows whose A-row mean needed the sequential fallback */
-#define VABFT_NUM_COUNTS 5
+#define VABFT_COUNT_CORRECTED 5  /* rows corrected in the kernel (vabft_fused_opts.correct) */
+#define VABFT_NUM_COUNTS 6
 
 /* One planned fault (InjectionRecord inputs, faults.hpp:21-35). */
 typedef struct vabft_fault {
@@ -255,7 +256,25 @@ typedef struct vabft_fused_opts {
     /* Stage mask for profiling (0 = all): 1 statistics pass, 2 tcgen05 GEMM
      * with the ABFT epilogue, 4 verify tail. */
     int32_t stages;
-    int32_t reserved;
+    /* Where the planned faults land (FaultTarget, faults.hpp:15):
+     *  0 OutputC: fault_col/bit/dir per row as above (accumulator online,
+     *    output bits offline);
+     *  1 InputA: fault_col[i] = k — bit fault_bit[i] of A[i][k] is flipped in
+     *    the shared-memory operand tiles the tensor cores read (every N tile
+     *    of row i), while the checksums and statistics use the clean A;
+     *  2 InputB: operand_faults[t] = {i = k, j = column, bit, direction} —
+     *    B[k][j] flipped in the operand tiles of every M tile; the checksums
+     *    come from the clean B of the B-side handle.
+     * Operand bits are the BF16/FP16 patterns (0..15). Records: fault_records
+     * per row for InputA, operand_fault_records per fault for InputB. */
+    int32_t fault_target;
+    int32_t n_operand_faults;
+    int32_t correct;  /* 1: rows with a located single error (residual < 0.5 - 0.1,
+                         DetectOptions::residual_margin) get C[i][j] = quantize(C[i][j] - diff1)
+                         in the kernel (correct, detect.cpp:57-64); counted in
+                         counts[VABFT_COUNT_CORRECTED] */
+    const vabft_fault* operand_faults;
+    vabft_fault_record* operand_fault_records;
 } vabft_fused_opts;
 
 /* Workspace bytes for vabft_fused_gemm at this shape. */

@@ -25,7 +25,8 @@ ACCUM_FP32_ROUND_OUTPUT, ACCUM_SEQUENTIAL, ACCUM_BLOCKED, ACCUM_PAIRWISE = range
 OFFLINE, ONLINE = 0, 1
 FLIP, SET0TO1, SET1TO0, ANY = range(4)
 ENGINE_EXACT, ENGINE_TENSOR = 0, 1
-COUNT_ROWS, COUNT_DETECTED, COUNT_LOCATED, COUNT_NAN, COUNT_SLOW_STATS, NUM_COUNTS = 0, 1, 2, 3, 4, 5
+COUNT_ROWS, COUNT_DETECTED, COUNT_LOCATED, COUNT_NAN, COUNT_SLOW_STATS, COUNT_CORRECTED, NUM_COUNTS = \
+    0, 1, 2, 3, 4, 5, 6
 
 FORMAT_CODES = {"bf16": BF16, "fp16": FP16, "fp32": FP32, "fp64": FP64}
 
@@ -60,7 +61,9 @@ class FusedOpts(C.Structure):
                 ("c_sigma", C.c_double), ("floor_scale", C.c_double), ("aabft_mantissa_bits", C.c_int32),
                 ("b_kmajor", C.c_int32), ("aabft_fixed_y", C.c_double), ("aabft_confidence", C.c_double),
                 ("fault_col", C.c_void_p), ("fault_bit", C.c_void_p), ("fault_dir", C.c_void_p),
-                ("fault_records", C.c_void_p), ("stages", C.c_int32), ("reserved", C.c_int32)]
+                ("fault_records", C.c_void_p), ("stages", C.c_int32), ("fault_target", C.c_int32),
+                ("n_operand_faults", C.c_int32), ("correct", C.c_int32), ("operand_faults", C.c_void_p),
+                ("operand_fault_records", C.c_void_p)]
 
 
 _st = C.c_int

@@ -245,6 +245,13 @@ extern "C" vabft_status vabft_fused_gemm(const vabft_fused_opts* o, vabft_bside_
         a.T_out = T;
         a.v = verdicts;
         a.counts = counts;
+        a.C = static_cast<uint16_t*>(C);
+        a.correct = o->correct;
+        if (o->fault_target < 0 || o->fault_target > 2) fail(VABFT_INVALID_ARGUMENT, "bad fault target");
+        if (o->fault_target == 1 && (!o->fault_col || !o->fault_bit || !o->fault_dir))
+            fail(VABFT_INVALID_ARGUMENT, "InputA faults need fault_col / fault_bit / fault_dir");
+        if (o->fault_target == 2 && o->n_operand_faults > 0 && !o->operand_faults)
+            fail(VABFT_INVALID_ARGUMENT, "InputB faults need operand_faults");
         // computed-y A-ABFT needs the global max|A| before any verdict: two passes
         const bool two_phase = o->threshold_method == 2;
         if (two_phase && (stages & 4)) check_cuda(cudaMemsetAsync(ws.max_abs_a, 0, sizeof(double), s), "memset");
@@ -258,6 +265,10 @@ extern "C" vabft_status vabft_fused_gemm(const vabft_fused_opts* o, vabft_bside_
             epi.fault_bit = o->fault_bit;
             epi.fault_dir = o->fault_dir;
             epi.fault_records = o->fault_records;
+            epi.fault_target = o->fault_target;
+            epi.n_operand_faults = o->n_operand_faults;
+            epi.operand_faults = o->operand_faults;
+            epi.operand_fault_records = o->operand_fault_records;
             epi.br1 = h->buf.br1;
             epi.br2 = h->buf.br2;
             epi.sp1 = ws.sp1;

@@ -47,6 +47,9 @@ struct TailArgs {
     double* T_out;
     vabft_verdicts v;
     int64_t* counts;
+    // in-kernel correction (detect.cpp:57-64): C[i][j] = quantize(C[i][j] - diff1)
+    uint16_t* C = nullptr;
+    int correct = 0;
 };
 
 // ---- tcgen05 GEMM (tc_gemm.cu)
@@ -62,6 +65,12 @@ struct TcEpilogue {
     const int32_t* fault_bit = nullptr;
     const int32_t* fault_dir = nullptr;
     vabft_fault_record* fault_records = nullptr;
+    // fault target (vabft_fused_opts.fault_target): 0 accumulator / output
+    // (epilogue), 1 A operand, 2 B operand (shared-memory tiles of the MMAs)
+    int fault_target = 0;
+    int n_operand_faults = 0;
+    const vabft_fault* operand_faults = nullptr;
+    vabft_fault_record* operand_fault_records = nullptr;
     float* accum_out = nullptr;  // optional M x N FP32 accumulator dump (parity API)
     // In-GEMM A-side statistics (stats warps read the TMA-staged A tiles):
     // per (128-column block b of K, row i), stored [b][M]. Enabled when sp1 != nullptr.

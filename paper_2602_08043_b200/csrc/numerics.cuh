@@ -36,6 +36,21 @@ __device__ __forceinline__ uint16_t quantize16_bits(float v) {
     }
 }
 
+// quantize (precision.cpp:129-159) of an FP64 value to a 16-bit format: one
+// RNE rounding from double (no intermediate float), saturating.
+template <int kFmt>
+__device__ __forceinline__ uint16_t quantize16_bits_d(double v) {
+    if constexpr (kFmt == VABFT_BF16) {
+        uint16_t b = __bfloat16_as_ushort(__double2bfloat16(v));
+        if ((b & 0x7FFFu) == 0x7F80u) b = static_cast<uint16_t>((b & 0x8000u) | 0x7F7Fu);
+        return b;
+    } else {
+        uint16_t b = __half_as_ushort(__double2half(v));
+        if ((b & 0x7FFFu) == 0x7C00u) b = static_cast<uint16_t>((b & 0x8000u) | 0x7BFFu);
+        return b;
+    }
+}
+
 template <int kFmt>
 __device__ __forceinline__ float bits16_to_float(uint16_t b) {
     if constexpr (kFmt == VABFT_BF16) {

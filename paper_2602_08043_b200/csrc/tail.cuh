@@ -118,10 +118,11 @@ __device__ __forceinline__ void row_threshold(const TailArgs& a, int64_t i, doub
 // Verdict of row i (detect.cpp:19-55) from its row sums r1 / r2, checksums
 // c1 / c2 and V-ABFT threshold tv (A-ABFT methods replace it), plus the
 // warp's counters.
+template <int F>
 __device__ __forceinline__ void row_verdict(const TailArgs& a, int64_t i, bool valid, float r1, float r2,
                                             double c1, double c2, double tv) {
     const int lane = threadIdx.x & 31;
-    bool det = false, located = false, isnan_row = false;
+    bool det = false, located = false, isnan_row = false, corrected = false;
     if (valid) {
         double t;
         if (a.method == 0) {
@@ -147,6 +148,13 @@ __device__ __forceinline__ void row_verdict(const TailArgs& a, int64_t i, bool v
                     loc = j;
                     res = rr;
                     located = true;
+                    // correct (detect.cpp:57-64) for a confidently located single
+                    // error (residual < 0.5 - DetectOptions::residual_margin)
+                    if (a.correct && a.C != nullptr && rr < 0.4) {
+                        uint16_t* cij = a.C + i * a.N + j;
+                        *cij = quantize16_bits_d<F>(__dsub_rn(double(bits16_to_float<F>(*cij)), d1));
+                        corrected = true;
+                    }
                 }
             }
         }
@@ -163,7 +171,9 @@ __device__ __forceinline__ void row_verdict(const TailArgs& a, int64_t i, bool v
         const unsigned md = __ballot_sync(0xffffffffu, det);
         const unsigned ml = __ballot_sync(0xffffffffu, located);
         const unsigned mn = __ballot_sync(0xffffffffu, isnan_row);
+        const unsigned mc = __ballot_sync(0xffffffffu, corrected);
         if (lane == 0) {
+            if (mc) atomicAdd(reinterpret_cast<unsigned long long*>(a.counts + VABFT_COUNT_CORRECTED), __popc(mc));
             if (mv) atomicAdd(reinterpret_cast<unsigned long long*>(a.counts + VABFT_COUNT_ROWS), __popc(mv));
             if (md) atomicAdd(reinterpret_cast<unsigned long long*>(a.counts + VABFT_COUNT_DETECTED), __popc(md));
             if (ml) atomicAdd(reinterpret_cast<unsigned long long*>(a.counts + VABFT_COUNT_LOCATED), __popc(ml));
@@ -211,7 +221,7 @@ __device__ void verify_rowgroup(const TailArgs& a, int64_t g, int phase, float* 
         c2 = a.cr2[i];
         tv = a.Tv[i];
     }
-    row_verdict(a, i, valid, r1, r2, c1, c2, tv);
+    row_verdict<F>(a, i, valid, r1, r2, c1, c2, tv);
 }
 
 // ---------------------------------------------- L2-direct (inside the GEMM)
@@ -275,6 +285,7 @@ __device__ void stats_half_direct(const TailArgs& a, int64_t g) {
     }
 }
 
+template <int F>
 __device__ __forceinline__ void final_half_direct(const TailArgs& a, int64_t g) {
     const int lane = threadIdx.x & 31;
     const int64_t i = g * 32 + lane;
@@ -287,7 +298,7 @@ __device__ __forceinline__ void final_half_direct(const TailArgs& a, int64_t g) 
     }
     float r1 = 0.0f, r2 = 0.0f;
     ordered_sums_l2(a.part1, a.part2, a.nblkN, g, r1, r2);
-    row_verdict(a, i, valid, r1, r2, c1, c2, tv);
+    row_verdict<F>(a, i, valid, r1, r2, c1, c2, tv);
 }
 
 // Self-resetting grid barrier for a co-resident (cooperative) grid: the last

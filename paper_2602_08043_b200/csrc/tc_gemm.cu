@@ -97,10 +97,11 @@ __device__ __forceinline__ unsigned int warp_arrive(unsigned int* cnt) {
     return __shfl_sync(0xffffffffu, old, 0);
 }
 
+template <int F>
 __device__ __forceinline__ void final_arrive(const TcParams& p, int64_t g) {
     unsigned int* cnt = p.epi.group_cnt + 2 * g + 1;
     if (warp_arrive(cnt) != unsigned(p.num_n_blk)) return;  // target num_n_blk + 1
-    if (p.epi.debug != 7) final_half_direct(p.epi.tail, g);  // 7: ablation, no verification
+    if (p.epi.debug != 7) final_half_direct<F>(p.epi.tail, g);  // 7: ablation, no verification
     __syncwarp();
     if ((threadIdx.x & 31) == 0) *cnt = 0u;  // ready for the next launch
 }
@@ -112,7 +113,72 @@ __device__ __forceinline__ void stats_arrive(const TcParams& p, int64_t g) {
     if (p.epi.debug != 7) stats_half_direct<F>(p.epi.tail, g);
     __syncwarp();
     if ((threadIdx.x & 31) == 0) *cnt = 0u;
-    final_arrive(p, g);
+    final_arrive<F>(p, g);
+}
+
+// ----------------------------------------------------- operand faults
+// inject (faults.cpp:104-168) on an operand element as the tensor cores see
+// it: one 16-bit pattern in a swizzled shared-memory tile.
+template <int F>
+__device__ __forceinline__ void flip16(uint16_t* e, int bit, int dir, vabft_fault_record* rec) {
+    const uint16_t before = *e;
+    const bool ok = bit_eligible(before, bit, dir);
+    const uint16_t after = ok ? uint16_t(before ^ (1u << bit)) : before;
+    *e = after;
+    if (rec) {
+        vabft_fault_record r;
+        r.value_before = double(bits16_to_float<F>(before));
+        r.value_after = double(bits16_to_float<F>(after));
+        r.applied = ok ? 1 : 0;
+        r.reserved = 0;
+        *rec = r;
+    }
+}
+
+// Apply the planned operand faults that fall into k-stage kb of tile
+// (m_blk, n_blk) to the stage's A / B tiles (called by all lanes of the MMA
+// warp after the stage's full barrier, before the MMAs). SWIZZLE_128B: a
+// 128-byte row r keeps 16-byte chunk c at chunk c ^ (r & 7). A is K-major
+// (row = A row, 64 k per row); B is N-major as 4 boxes of 64 k-rows x 64 n
+// (8 KiB each) or K-major (row = B column). Every tile of the row / column
+// block gets the same flip (the element as seen by all MMAs); the record is
+// written once. The statistics warps read their own A copy and the B-side
+// checksums come from the clean B, so the checksums stay clean.
+template <int F, bool kBKMajor>
+__device__ __forceinline__ void operand_faults_stage(const TcParams& p, uint8_t* sa, uint8_t* sb, int m_blk,
+                                                     int n_blk, int kb) {
+    const int lane = threadIdx.x & 31;
+    const int k0 = kb * 64;
+    bool wrote = false;
+    if (p.epi.fault_target == 1) {
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            const int r = q * 32 + lane;
+            const int row = m_blk * 128 + r;
+            if (row >= p.M) continue;
+            const int k = p.epi.fault_col[row];
+            if (k < k0 || k >= k0 + 64) continue;
+            const int kk = k - k0;
+            uint16_t* e = reinterpret_cast<uint16_t*>(sa + r * 128 + ((((kk >> 3) ^ (r & 7))) << 4) + (kk & 7) * 2);
+            flip16<F>(e, p.epi.fault_bit[row], p.epi.fault_dir[row],
+                      (n_blk == 0 && p.epi.fault_records) ? p.epi.fault_records + row : nullptr);
+            wrote = true;
+        }
+    } else {
+        for (int t = lane; t < p.epi.n_operand_faults; t += 32) {
+            const vabft_fault f = p.epi.operand_faults[t];
+            if (f.i < k0 || f.i >= k0 + 64 || f.j < int64_t(n_blk) * 256 || f.j >= int64_t(n_blk) * 256 + 256) continue;
+            const int kk = int(f.i - k0), jj = int(f.j - int64_t(n_blk) * 256);
+            uint8_t* a = kBKMajor ? sb + jj * 128 + ((((kk >> 3) ^ (jj & 7))) << 4) + (kk & 7) * 2
+                                  : sb + (jj >> 6) * 8192 + kk * 128 + (((((jj & 63) >> 3) ^ (kk & 7))) << 4) +
+                                        (jj & 7) * 2;
+            flip16<F>(reinterpret_cast<uint16_t*>(a), f.bit, f.direction,
+                      (m_blk == 0 && p.epi.operand_fault_records) ? p.epi.operand_fault_records + t : nullptr);
+            wrote = true;
+        }
+    }
+    // generic-proxy writes -> the tensor cores' async-proxy reads
+    if (wrote) asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
 }
 
 // ------------------------------------------------ in-GEMM A statistics
@@ -336,7 +402,7 @@ __device__ __forceinline__ void stats_warps(const TcParams& p, const uint8_t* sm
 template <int kFmt, bool kBKMajor, int kAbft, bool kInject, bool kStats>
 __global__ void __launch_bounds__(kThreadsStats, 1)
     tc_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
-                   const TcParams p) {
+                   const __grid_constant__ TcParams p) {
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                                ~uintptr_t(1023));
@@ -409,7 +475,11 @@ __global__ void __launch_bounds__(kThreadsStats, 1)
             }
         }
     } else if (warp == 1) {
-        if (lane == 0) {
+        // With operand faults (campaign instantiations only) the whole warp
+        // walks the stages: its lanes flip the planned operand bits in the
+        // freshly loaded shared-memory tiles before lane 0 issues the MMAs.
+        const bool opf = kInject && p.epi.fault_target != 0;
+        if (lane == 0 || opf) {
             // --------------------------------------------------- MMA issuer
             constexpr uint32_t idesc =
                 umma_idesc_f16(kFmt == VABFT_BF16 ? 1u : 0u, !kBKMajor, kBM, kBN);
@@ -418,32 +488,44 @@ __global__ void __launch_bounds__(kThreadsStats, 1)
             int acc = 0;
             uint32_t acc_phase = 0;
             for (int tile = blockIdx.x; tile < p.num_tiles; tile += gridDim.x) {
-                mbar_wait(smem_u32(&tempty_bar[acc]), acc_phase ^ 1);
-                tc_fence_after();
+                int m_blk = 0, n_blk = 0;
+                if (opf) tile_coords(p, tile, m_blk, n_blk);
+                if (lane == 0) {
+                    mbar_wait(smem_u32(&tempty_bar[acc]), acc_phase ^ 1);
+                    tc_fence_after();
+                }
                 const uint32_t d_tmem = tmem_base + uint32_t(acc * kBN);
                 for (int kb = 0; kb < p.num_k_blk; ++kb) {
                     mbar_wait(smem_u32(&full_bar[stage]), phase);
-                    tc_fence_after();
-                    const uint64_t adesc = umma_desc_sw128(smem_u32(smA + stage * kABytes), 16, 1024);
-                    const uint64_t bdesc =
-                        kBKMajor ? umma_desc_sw128(smem_u32(smB + stage * kBBytes), 16, 1024)
-                                 : umma_desc_sw128(smem_u32(smB + stage * kBBytes), 8192, 1024);
-#pragma unroll
-                    for (int k = 0; k < kBK / 16; ++k) {
-                        // K-major: +32 bytes per 16 elements inside the 128B swizzle row.
-                        // N-major: +16 k-rows = 2 swizzle atoms = 2048 bytes.
-                        const uint64_t a_off = uint64_t((k * 32) >> 4);
-                        const uint64_t b_off = kBKMajor ? uint64_t((k * 32) >> 4) : uint64_t((k * 2048) >> 4);
-                        umma_f16(d_tmem, adesc + a_off, bdesc + b_off, idesc,
-                                 (kb > 0 || k > 0) ? 1u : 0u);
+                    if constexpr (kInject) {
+                        if (opf) {
+                            operand_faults_stage<kFmt, kBKMajor>(p, smA + stage * kABytes, smB + stage * kBBytes,
+                                                                m_blk, n_blk, kb);
+                            __syncwarp();
+                        }
                     }
-                    umma_commit(smem_u32(&empty_bar[stage]));
+                    if (lane == 0) {
+                        tc_fence_after();
+                        const uint64_t adesc = umma_desc_sw128(smem_u32(smA + stage * kABytes), 16, 1024);
+                        const uint64_t bdesc =
+                            kBKMajor ? umma_desc_sw128(smem_u32(smB + stage * kBBytes), 16, 1024)
+                                     : umma_desc_sw128(smem_u32(smB + stage * kBBytes), 8192, 1024);
+#pragma unroll
+                        for (int k = 0; k < kBK / 16; ++k) {
+                            // K-major: +32 bytes per 16 elements inside the 128B swizzle row.
+                            // N-major: +16 k-rows = 2 swizzle atoms = 2048 bytes.
+                            const uint64_t a_off = uint64_t((k * 32) >> 4);
+                            const uint64_t b_off = kBKMajor ? uint64_t((k * 32) >> 4) : uint64_t((k * 2048) >> 4);
+                            umma_f16(d_tmem, adesc + a_off, bdesc + b_off, idesc, (kb > 0 || k > 0) ? 1u : 0u);
+                        }
+                        umma_commit(smem_u32(&empty_bar[stage]));
+                    }
                     if (++stage == kStages) {
                         stage = 0;
                         phase ^= 1;
                     }
                 }
-                umma_commit(smem_u32(&tfull_bar[acc]));
+                if (lane == 0) umma_commit(smem_u32(&tfull_bar[acc]));
                 if (++acc == 2) {
                     acc = 0;
                     acc_phase ^= 1;
@@ -471,7 +553,7 @@ __global__ void __launch_bounds__(kThreadsStats, 1)
 
             int fcol = -1, fbit = 0, fdir = 0;
             if constexpr (kInject) {
-                if (row_ok) {
+                if (row_ok && p.epi.fault_target == 0) {
                     fcol = p.epi.fault_col[row];
                     if (fcol >= n0 && fcol < n0 + kBN) {
                         fbit = p.epi.fault_bit[row];
@@ -597,7 +679,7 @@ __global__ void __launch_bounds__(kThreadsStats, 1)
             }
             if constexpr (kStats) {
                 if (p.epi.stream_verify && (int64_t(m_blk) * 4 + quad) * 32 < p.M)
-                    final_arrive(p, int64_t(m_blk) * 4 + quad);
+                    final_arrive<kFmt>(p, int64_t(m_blk) * 4 + quad);
             }
         }
     }
@@ -707,7 +789,7 @@ void launch_inst(const CUtensorMap& ta, const CUtensorMap& tb, const TcParams& p
 template <int kFmt, bool kBKMajor>
 void dispatch_epi(const CUtensorMap& ta, const CUtensorMap& tb, const TcParams& p,
                   cudaStream_t stream) {
-    const bool inj = p.epi.fault_col != nullptr;
+    const bool inj = p.epi.fault_col != nullptr || (p.epi.fault_target == 2 && p.epi.n_operand_faults > 0);
     const bool st = p.epi.sp1 != nullptr && p.epi.debug != 3;  // 3: ablation, ABFT epilogue only
     switch (p.epi.abft) {
         case 0: launch_inst<kFmt, kBKMajor, 0, false>(ta, tb, p, stream); break;

@@ -22,6 +22,15 @@ from .device import ptr, stream_ptr
 
 _FMT = {torch.bfloat16: _capi.BF16, torch.float16: _capi.FP16}
 _METHOD = {"vabft": 0, "aabft-fixed-y": 1, "aabft-computed-y": 2}
+_TARGET = {"output": 0, "A": 1, "B": 2}  # FaultTarget (faults.hpp:15)
+
+
+def operand_faults(faults, device="cuda") -> torch.Tensor:
+    """vabft_fault array for B-operand faults: [(k, j, bit, direction), ...]
+    -> an int64 [n, 3] device tensor with the C struct layout
+    {int64 i = k, int64 j, int32 bit, int32 direction}."""
+    rows = [[int(k), int(j), (int(bit) & 0xFFFFFFFF) | (int(d) << 32)] for (k, j, bit, d) in faults]
+    return torch.tensor(rows, dtype=torch.int64, device=device).reshape(-1, 3)
 
 _FMT_NAME = {torch.bfloat16: "bf16", torch.float16: "fp16"}
 
@@ -85,7 +94,13 @@ class FusedAbftGemm:
 
     def __call__(self, A: torch.Tensor, out: Optional[torch.Tensor] = None, *, verdicts: bool = True,
                  thresholds: bool = True, counts: Optional[torch.Tensor] = None,
-                 faults: Optional[dict] = None, stages: int = 0, checksums: bool = False) -> FusedResult:
+                 faults: Optional[dict] = None, stages: int = 0, checksums: bool = False,
+                 correct: bool = False) -> FusedResult:
+        """faults: {"target": "output" | "A" | "B", ...}. output / A: per-row
+        int32 tensors "col" (output column, or the k index of A[i][k]; < 0 =
+        none), "bit", "dir" and optional "records" (M x 24-byte records). B:
+        "operand" = operand_faults(...) and optional "records" (per fault).
+        correct: in-kernel correction of located single errors."""
         if A.dtype != self.B.dtype or A.dim() != 2 or A.shape[1] != self.k:
             raise _capi.InvalidArgument("FusedAbftGemm: A must be M x K with B's dtype")
         m = A.shape[0]
@@ -118,10 +133,21 @@ class FusedAbftGemm:
             opts.stages = stages
         if faults is not None:
             opts = _capi.FusedOpts.from_buffer_copy(opts)
-            opts.fault_col = ptr(faults["col"])
-            opts.fault_bit = ptr(faults["bit"])
-            opts.fault_dir = ptr(faults["dir"])
-            opts.fault_records = ptr(faults.get("records"))
+            target = faults.get("target", "output")
+            opts.fault_target = _TARGET[target]
+            if target == "B":
+                op = faults["operand"]
+                opts.operand_faults = ptr(op)
+                opts.n_operand_faults = int(op.shape[0])
+                opts.operand_fault_records = ptr(faults.get("records"))
+            else:
+                opts.fault_col = ptr(faults["col"])
+                opts.fault_bit = ptr(faults["bit"])
+                opts.fault_dir = ptr(faults["dir"])
+                opts.fault_records = ptr(faults.get("records"))
+        if correct:
+            opts = _capi.FusedOpts.from_buffer_copy(opts)
+            opts.correct = 1
         ws = self.workspace(m)
         check(lib.vabft_fused_gemm(C.byref(opts), self.h, m, ptr(A.contiguous()), ptr(C_), ptr(T), v, ptr(counts),
                                    ptr(ws), ws.numel(), stream_ptr()))
