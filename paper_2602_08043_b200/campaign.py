@@ -127,10 +127,63 @@ class DeviceCampaign:
         totals += torch.stack([torch.tensor(m, device=dev, dtype=torch.int64), applied.sum(), det.sum(),
                                located.sum(), nonfinite.sum()]).to(torch.int64)
 
-    def run(self, bit: int, trials: int, reduce: bool = True) -> CampaignOutcome:
+    def launch_operand_a(self, bit: int, totals: torch.Tensor) -> None:
+        """M trials: one fault per row i in A[i][k_i] (bits of the BF16/FP16
+        operand) as the tensor cores read it; checksums from the clean A.
+        The error spreads over row i, so only detection is tallied (located
+        stays 0)."""
+        if self.launches and self.launches % self.refresh == 0:
+            self._redraw()
+        self.launches += 1
+        m, dev = self.m, self.device
+        k_idx = torch.randint(0, self.k, (m,), generator=self.gen, device=dev, dtype=torch.int32)
+        bits = torch.full((m,), bit, dtype=torch.int32, device=dev)
+        dirs = torch.full((m,), self.direction, dtype=torch.int32, device=dev)
+        r = self.g(self.A, faults={"target": "A", "col": k_idx, "bit": bits, "dir": dirs, "records": self.rec})
+        recs = self.rec.view(m, _REC_BYTES)
+        after = recs[:, 8:16].contiguous().view(torch.float64).view(m)
+        applied = recs[:, 16:20].contiguous().view(torch.int32).view(m) != 0
+        det = (r.detected != 0) & applied
+        nonfinite = applied & ~torch.isfinite(after)
+        z = torch.zeros((), dtype=torch.int64, device=dev)
+        totals += torch.stack([torch.tensor(m, device=dev, dtype=torch.int64), applied.sum(), det.sum(), z,
+                               nonfinite.sum()]).to(torch.int64)
+
+    def launch_operand_b(self, bit: int, totals: torch.Tensor) -> None:
+        """One trial: one fault in B[k][j] (every row's column j is hit).
+        Detected = some row flags it; located = every flagging row points at
+        column j."""
+        from .fused import operand_faults
+        if self.launches and self.launches % self.refresh == 0:
+            self._redraw()
+        self.launches += 1
+        dev = self.device
+        k = int(torch.randint(0, self.k, (1,), generator=self.gen, device=dev).item())
+        j = int(torch.randint(0, self.n, (1,), generator=self.gen, device=dev).item())
+        rec = self.rec[:_REC_BYTES]
+        r = self.g(self.A, faults={"target": "B", "operand": operand_faults([(k, j, bit, self.direction)], dev),
+                                   "records": rec})
+        after = rec[8:16].view(torch.float64)
+        applied = rec[16:20].view(torch.int32)[0] != 0
+        det_rows = r.detected != 0
+        det = applied & det_rows.any()
+        located = det & (r.location[det_rows] == j).all()
+        nonfinite = applied & ~torch.isfinite(after[0])
+        totals += torch.stack([torch.ones((), dtype=torch.int64, device=dev), applied.long(), det.long(),
+                               located.long(), nonfinite.long()])
+
+    def run(self, bit: int, trials: int, reduce: bool = True, target: str = "output") -> CampaignOutcome:
+        """target: "output" (accumulator online / output offline, M trials per
+        launch), "A" (operand A, M trials per launch), "B" (operand B, one
+        trial per launch)."""
         totals = torch.zeros(5, dtype=torch.int64, device=self.device)
-        for _ in range(math.ceil(trials / self.m)):
-            self.launch(bit, totals)
+        if target == "B":
+            for _ in range(trials):
+                self.launch_operand_b(bit, totals)
+        else:
+            step = self.launch if target == "output" else self.launch_operand_a
+            for _ in range(math.ceil(trials / self.m)):
+                step(bit, totals)
         if reduce:
             allreduce_counts(totals)
         t = totals.tolist()

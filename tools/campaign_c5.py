@@ -34,6 +34,7 @@ def main():
     ap.add_argument("--trials-per-bit", type=int, default=8192)
     ap.add_argument("--shapes", default=",".join(SHAPES))
     ap.add_argument("--dist", default="normal:1e-6,1")
+    ap.add_argument("--b-trials-per-bit", type=int, default=256, help="B-operand trials (one per launch)")
     args = ap.parse_args()
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -45,18 +46,24 @@ def main():
     t_all = time.time()
     for name in args.shapes.split(","):
         m, k, n = SHAPES[name]
-        for mode, bits in (("online", range(32)), ("offline", range(16))):
+        # (mode, fault target, bits, trials per bit): FP32-accumulator bits
+        # online, output bits offline, BF16 A / B operand bits (online verify)
+        plan = (("online", "output", range(32), args.trials_per_bit),
+                ("offline", "output", range(16), args.trials_per_bit),
+                ("online", "A", range(16), args.trials_per_bit),
+                ("online", "B", range(16), args.b_trials_per_bit))
+        for mode, target, bits, tpb in plan:
             e_max = default_e_max("bf16", mode, k)
             camp = DeviceCampaign(m, k, n, dist=args.dist, mode=mode, e_max=e_max, seed=1000 * rank + 7)
             for b in bits:
-                per_rank = (args.trials_per_bit + world - 1) // world
+                per_rank = (tpb + world - 1) // world
                 t0 = time.time()
-                o = camp.run(b, per_rank, reduce=world > 1)  # all-reduced counters
+                o = camp.run(b, per_rank, reduce=world > 1, target=target)  # all-reduced counters
                 total += o.trials
                 if rank == 0:
-                    print(json.dumps({"shape": name, "mkn": [m, k, n], "mode": mode, "bit": b, "e_max": e_max,
-                                      "ranks": world, **o.as_dict(), "seconds": round(time.time() - t0, 3)}),
-                          flush=True)
+                    print(json.dumps({"shape": name, "mkn": [m, k, n], "mode": mode, "target": target, "bit": b,
+                                      "e_max": e_max, "ranks": world, **o.as_dict(),
+                                      "seconds": round(time.time() - t0, 3)}), flush=True)
             camp.close()
     if rank == 0:
         print(json.dumps({"summary": True, "trials_total": total if world == 1 else None,
