@@ -44,6 +44,7 @@
 #include <array>
 #include <cmath>
 #include <cstdint>
+#include <cstdio>
 #include <cstring>
 #include <functional>
 #include <limits>
@@ -1089,6 +1090,124 @@ inline CampaignOutcome injection_campaign(const CampaignConfig& config, const Th
         if (!std::isfinite(rec.value_after)) ++out.nonfinite_after;
     }
     return out;
+}
+
+// ------------------------------------------------------------ matrix_io.hpp
+// VABFTMAT binary: magic, u32 version, u8 format id, u64 rows, u64 cols,
+// rows*cols little-endian FP64 (matrix_io.hpp:12-17); CSV one row per line.
+// Loading quantizes finite values (Matrix::set) and keeps non-finite values
+// raw (matrix_io.cpp:34-45). Host file I/O.
+inline constexpr uint32_t kMatrixFileVersion = 1;
+
+namespace detail {
+inline constexpr char kMatrixMagic[8] = {'V', 'A', 'B', 'F', 'T', 'M', 'A', 'T'};
+inline void fill_values(Matrix& m, const std::vector<double>& vals) {
+    for (int64_t i = 0; i < m.rows(); ++i)
+        for (int64_t j = 0; j < m.cols(); ++j) {
+            const double v = vals[size_t(i * m.cols() + j)];
+            if (std::isfinite(v)) m.set(i, j, v);
+            else m.set_raw(i, j, v);
+        }
+}
+}  // namespace detail
+
+inline void save_matrix_binary(const Matrix& m, const std::string& path) {
+    std::FILE* f = std::fopen(path.c_str(), "wb");
+    if (!f) throw std::runtime_error("cannot open for writing: " + path);
+    const uint32_t version = kMatrixFileVersion;
+    const uint8_t fmt = uint8_t(m.format().format);
+    const uint64_t rows = uint64_t(m.rows()), cols = uint64_t(m.cols());
+    bool ok = std::fwrite(detail::kMatrixMagic, 1, 8, f) == 8 && std::fwrite(&version, 4, 1, f) == 1 &&
+              std::fwrite(&fmt, 1, 1, f) == 1 && std::fwrite(&rows, 8, 1, f) == 1 && std::fwrite(&cols, 8, 1, f) == 1 &&
+              std::fwrite(m.values().data(), 8, m.values().size(), f) == m.values().size();
+    ok = (std::fclose(f) == 0) && ok;
+    if (!ok) throw std::runtime_error("write failed: " + path);
+}
+
+inline Matrix load_matrix_binary(const std::string& path) {
+    std::FILE* f = std::fopen(path.c_str(), "rb");
+    if (!f) throw std::runtime_error("cannot open: " + path);
+    struct Closer {
+        std::FILE* f;
+        ~Closer() { std::fclose(f); }
+    } closer{f};
+    char magic[8];
+    if (std::fread(magic, 1, 8, f) != 8 || std::memcmp(magic, detail::kMatrixMagic, 8) != 0)
+        throw std::runtime_error("not a VABFTMAT file: " + path);
+    uint32_t version;
+    uint8_t fmt;
+    uint64_t rows, cols;
+    if (std::fread(&version, 4, 1, f) != 1) throw std::runtime_error("truncated matrix file: " + path);
+    if (version != kMatrixFileVersion) throw std::runtime_error("unsupported matrix file version in " + path);
+    if (std::fread(&fmt, 1, 1, f) != 1) throw std::runtime_error("truncated matrix file: " + path);
+    if (fmt > 3) throw std::runtime_error("bad format id in " + path);
+    if (std::fread(&rows, 8, 1, f) != 1 || std::fread(&cols, 8, 1, f) != 1)
+        throw std::runtime_error("truncated matrix file: " + path);
+    if (rows < 1 || cols < 1 || rows > (uint64_t(1) << 32) || cols > (uint64_t(1) << 32))
+        throw std::runtime_error("implausible dimensions in " + path);
+    std::vector<double> vals(size_t(rows * cols));
+    if (std::fread(vals.data(), 8, vals.size(), f) != vals.size())
+        throw std::runtime_error("truncated matrix file: " + path);
+    Matrix m(int64_t(rows), int64_t(cols), PrecisionSpec::of(Format(fmt)));
+    detail::fill_values(m, vals);
+    return m;
+}
+
+inline void save_matrix_csv(const Matrix& m, const std::string& path) {
+    std::FILE* f = std::fopen(path.c_str(), "w");
+    if (!f) throw std::runtime_error("cannot open for writing: " + path);
+    for (int64_t i = 0; i < m.rows(); ++i) {
+        for (int64_t j = 0; j < m.cols(); ++j) std::fprintf(f, j ? ",%.17g" : "%.17g", m(i, j));
+        std::fputc('\n', f);
+    }
+    std::fclose(f);
+}
+
+inline Matrix load_matrix_csv(const std::string& path, const PrecisionSpec& fmt) {
+    std::FILE* f = std::fopen(path.c_str(), "r");
+    if (!f) throw std::runtime_error("cannot open: " + path);
+    std::vector<double> vals;
+    int64_t rows = 0, cols = -1;
+    std::string line;
+    auto flush_line = [&] {
+        if (line.empty()) return;
+        int64_t c = 0;
+        size_t pos = 0;
+        while (pos <= line.size()) {
+            const size_t comma = line.find(',', pos);
+            const std::string tok = line.substr(pos, comma == std::string::npos ? std::string::npos : comma - pos);
+            if (!tok.empty()) {
+                vals.push_back(std::stod(tok));
+                ++c;
+            }
+            if (comma == std::string::npos) break;
+            pos = comma + 1;
+        }
+        if (cols == -1) cols = c;
+        else if (c != cols) throw std::runtime_error("ragged CSV row in " + path);
+        ++rows;
+        line.clear();
+    };
+    for (int ch; (ch = std::fgetc(f)) != EOF;) {
+        if (ch == '\n') flush_line();
+        else line.push_back(char(ch));
+    }
+    std::fclose(f);
+    flush_line();
+    if (rows == 0) throw std::runtime_error("empty CSV: " + path);
+    Matrix m(rows, cols, fmt);
+    detail::fill_values(m, vals);
+    return m;
+}
+
+inline Matrix load_matrix_auto(const std::string& path, const std::optional<PrecisionSpec>& csv_format = std::nullopt) {
+    std::FILE* f = std::fopen(path.c_str(), "rb");
+    if (!f) throw std::runtime_error("cannot open: " + path);
+    char magic[8] = {};
+    const size_t got = std::fread(magic, 1, 8, f);
+    std::fclose(f);
+    if (got == 8 && std::memcmp(magic, detail::kMatrixMagic, 8) == 0) return load_matrix_binary(path);
+    return load_matrix_csv(path, csv_format.value_or(PrecisionSpec::fp64()));
 }
 
 // =========================================================== B200 extension

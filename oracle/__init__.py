@@ -130,6 +130,10 @@ class Oracle:
             L.ref_correct.restype = cint
             L.ref_correct.argtypes = [cint, i64, i64, _D, i64, i64, dbl, _D]
             L.ref_max_threads.restype = cint
+            L.ref_save_matrix.restype = cint
+            L.ref_save_matrix.argtypes = [cint, cint, i64, i64, _D, C.c_char_p]
+            L.ref_load_matrix.restype = cint
+            L.ref_load_matrix.argtypes = [C.c_char_p, cint, _I64, _D]
         else:
             L.vo_threshold_row.restype = cint
             L.vo_threshold_row.argtypes = [_D, _D, i64, dbl, dbl, _D]
@@ -306,6 +310,19 @@ class Oracle:
         self._call("injection_campaign", m, k, n, FORMATS[fmt], kind, p0, p1, lo, hi, bit, direction, trials, seed,
                    1 if mode == "online" else 0, method, e_max, c_sigma, out.ctypes.data_as(_I64))
         return out
+
+    def save_matrix(self, X, fmt, path, binary=True):
+        """Reference save_matrix_binary / save_matrix_csv (matrix_io.cpp:49-101); reference only."""
+        X = _arr(X)
+        self._call("save_matrix", int(binary), FORMATS[fmt], X.shape[0], X.shape[1], _dp(X), path.encode())
+
+    def load_matrix(self, path, csv_fmt="fp64"):
+        """Reference load_matrix_auto (matrix_io.cpp:127-137) -> (values, format); reference only."""
+        dims = np.zeros(3, dtype=np.int64)
+        self._call("load_matrix", path.encode(), FORMATS[csv_fmt], dims.ctypes.data_as(_I64), None)
+        out = np.zeros((int(dims[0]), int(dims[1])))
+        self._call("load_matrix", path.encode(), FORMATS[csv_fmt], dims.ctypes.data_as(_I64), _dp(out))
+        return out, list(FORMATS)[int(dims[2])]
 
     def campaign_trial(self, m, k, n, fmt, dist, bit, seed, trial, mode="offline", method=0, e_max=8e-3,
                        c_sigma=2.5, direction=1):

@@ -17,6 +17,7 @@
 #include <vector>
 
 #include "vabft/calibration.hpp"
+#include "vabft/matrix_io.hpp"
 #include "vabft/checksum.hpp"
 #include "vabft/detect.hpp"
 #include "vabft/distribution.hpp"
@@ -417,5 +418,24 @@ int ref_calibrate(int fmt, int mode, const int64_t* sizes, int64_t n_sizes, int6
 }
 
 int ref_max_threads() { return max_threads(); }
+
+// matrix_io (matrix_io.cpp:49-137): save a raw matrix / load with the
+// reference's loaders (dims first with out == nullptr, then the values).
+int ref_save_matrix(int binary, int fmt, int64_t m, int64_t n, const double* v, const char* path) {
+    return guard([&] {
+        const Matrix mat = raw_matrix(m, n, v, PrecisionSpec::of(Format(fmt)));
+        if (binary) save_matrix_binary(mat, path);
+        else save_matrix_csv(mat, path);
+    });
+}
+int ref_load_matrix(const char* path, int csv_fmt, int64_t* dims, double* out) {
+    return guard([&] {
+        const Matrix mat = load_matrix_auto(path, PrecisionSpec::of(Format(csv_fmt)));
+        dims[0] = mat.rows();
+        dims[1] = mat.cols();
+        dims[2] = int64_t(mat.format().format);
+        if (out) copy_out(mat, out);
+    });
+}
 
 }  // extern "C"

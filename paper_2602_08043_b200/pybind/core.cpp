@@ -272,4 +272,11 @@ PYBIND11_MODULE(_core, m) {
         .def("detection_rate", &CampaignOutcome::detection_rate)
         .def("localization_accuracy", &CampaignOutcome::localization_accuracy);
     m.def("injection_campaign", &injection_campaign);
+
+    m.attr("kMatrixFileVersion") = kMatrixFileVersion;
+    m.def("save_matrix_binary", &save_matrix_binary);
+    m.def("load_matrix_binary", &load_matrix_binary);
+    m.def("save_matrix_csv", &save_matrix_csv);
+    m.def("load_matrix_csv", &load_matrix_csv);
+    m.def("load_matrix_auto", &load_matrix_auto, py::arg("path"), py::arg("csv_format") = std::nullopt);
 }
