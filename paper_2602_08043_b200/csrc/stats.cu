@@ -38,22 +38,24 @@ __global__ void row_stats_kernel(const typename Elem<F>::T* __restrict__ X, int6
     const int lane = threadIdx.x & 31;
     if (r >= rows) return;
     const typename Elem<F>::T* row = X + r * cols;
-    Neu n;
     double mx = -INFINITY, mn = INFINITY;
     bool bad = false;
     for (int64_t q = lane; q < cols; q += 32) {
         const double x = Elem<F>::d(row[q]);
         bad |= !isfinite(x);
-        n.add(x);
         mx = fmax(mx, x);
         mn = fmin(mn, x);
     }
-    n = warp_merge(n);
     mx = warp_max(mx);
     mn = warp_min(mn);
     const unsigned anybad = __ballot_sync(0xffffffffu, bad);
     if (lane == 0) {
         if (anybad) atomicExch(nonfinite, 1);
+        // the reference's sequential Neumaier loop (stats.cpp:12-24), so the
+        // mean is bit-exact for every input (API path; the fused path uses the
+        // order-free exact sum under its guard)
+        Neu n;
+        for (int64_t q = 0; q < cols; ++q) n.add(Elem<F>::d(row[q]));
         double m, vb;
         stats_finish(n, mx, mn, cols, &m, &vb);
         if (mean) mean[r] = m;
@@ -77,7 +79,6 @@ __global__ void bside_rows_kernel(const typename Elem<F>::T* __restrict__ B, int
     if (k >= K) return;
     const typename Elem<F>::T* row = B + k * N;
     const int64_t nblk = (N + 127) / 128;
-    Neu n;
     double mx = -INFINITY, mn = INFINITY;
     bool bad = false;
     float t1 = 0.0f, t2 = 0.0f;  // every lane accumulates the block partials in block order
@@ -91,7 +92,6 @@ __global__ void bside_rows_kernel(const typename Elem<F>::T* __restrict__ B, int
                 const float xf = Elem<F>::f(e);
                 const double x = Elem<F>::d(e);
                 bad |= !isfinite(x);
-                n.add(x);
                 mx = fmax(mx, x);
                 mn = fmin(mn, x);
                 p1 = __fadd_rn(p1, xf);
@@ -104,12 +104,22 @@ __global__ void bside_rows_kernel(const typename Elem<F>::T* __restrict__ B, int
             t2 = __fadd_rn(t2, __shfl_sync(0xffffffffu, p2, l));
         }
     }
-    n = warp_merge(n);
     mx = warp_max(mx);
     mn = warp_min(mn);
     const unsigned anybad = __ballot_sync(0xffffffffu, bad);
     if (lane == 0) {
         if (anybad) atomicExch(nonfinite, 1);
+        // the reference's sequential loops over the row (FP32 / FP64 weights;
+        // the 16-bit pass is bside_rows16_kernel): Neumaier for the mean
+        // (stats.cpp:12-24), the plain FP64 sum for A-ABFT's computed y
+        // (threshold_aabft.cpp:42-46) — both bit-exact for every input
+        Neu n;
+        double plain = 0.0;
+        for (int64_t j = 0; j < N; ++j) {
+            const double x = Elem<F>::d(row[j]);
+            n.add(x);
+            plain = __dadd_rn(plain, x);
+        }
         double m, v;
         stats_finish(n, mx, mn, N, &m, &v);
         mean[k] = m;
@@ -123,10 +133,7 @@ __global__ void bside_rows_kernel(const typename Elem<F>::T* __restrict__ B, int
         const int64_t idx = k;  // plain layout: A-side reads are warp-uniform broadcasts
         br1[idx] = t1;
         br2[idx] = t2;
-        // aabft_computed_y's FP64 row sum: the compensated sum rounded once
-        // (equal to the reference's sequential sum whenever that is exact,
-        // e.g. for every BF16/FP16 row of realistic range).
-        rowsum_abs[k] = fabs(__dadd_rn(n.s, n.c));
+        rowsum_abs[k] = fabs(plain);
     }
 }
 

@@ -1,0 +1,94 @@
+"""Experiment runners (tightness / FPR, harness.cpp:175-351) and block-wise
+V-ABFT on the device, against the same computations composed from the
+reference (oracle) on the same Philox trials."""
+import math
+
+import numpy as np
+import pytest
+
+from paper_2602_08043_b200 import harness
+
+
+def compensated(row):
+    s = c = 0.0
+    for x in row:
+        t = s + x
+        c += ((s - t) + x) if abs(s) >= abs(x) else ((x - t) + s)
+        s = t
+    return s + c
+
+
+def test_trial_operands_are_the_reference_trials(ref_or_port):
+    pytest.importorskip("paper_2602_08043_b200._core")
+    for fmt, dist in [("fp32", "uniform:-1,1"), ("bf16", "normal:1e-6,1"), ("fp64", "truncnormal:0,1,-1,1")]:
+        cfg = harness.ExperimentConfig(precision=fmt, dist=dist, m=5, k=7, n=3, seed=12)
+        for t in (0, 3):
+            a, b = harness.trial_operands(cfg, t)
+            A, B = ref_or_port.trial_inputs(5, 7, 3, fmt, dist, 12, t)
+            assert np.array_equal(a, A) and np.array_equal(b, B)
+
+
+def test_compensated_sum_rows():
+    rng = np.random.default_rng(0)
+    x = rng.normal(0, 1, (6, 50)) * np.logspace(-8, 8, 50)
+    got = harness.compensated_sum_rows(x)
+    assert all(got[i] == compensated(x[i]) for i in range(6))
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("fmt,mode", [("fp32", "offline"), ("fp64", "offline"), ("bf16", "online")])
+def test_tightness_and_fpr_match_reference_composition(ref_or_port, fmt, mode):
+    O = ref_or_port
+    cfg = harness.ExperimentConfig(precision=fmt, dist="normal:1e-6,1", m=16, k=64, n=24, trials=3, seed=4,
+                                   mode=mode, methods=["vabft", "aabft-fixed-y", "aabft-computed-y"])
+    doc = harness.run_tightness(cfg)
+    fpr = harness.run_fpr(cfg)
+    e_max = doc["config"]["e_max"]["value"]
+    assert e_max == O.resolve_e_max(fmt, 64)
+    means, thr_means, unc = [], {m: [] for m in cfg.methods}, {m: 0 for m in cfg.methods}
+    for t in range(cfg.trials):
+        A, B = O.trial_inputs(16, 64, 24, fmt, "normal:1e-6,1", 4, t)
+        e = O.encode_and_multiply(A, B, fmt, mode)
+        src = e.c_accum if mode == "online" else e.c
+        if fmt == "fp64":
+            actual = np.array([abs(math.fsum([e.row_check1[i]] + [-x for x in src[i]])) for i in range(16)])
+        else:
+            actual = np.array([abs(e.row_check1[i] - compensated(src[i])) for i in range(16)])
+        means.append(harness.seq_mean(actual))
+        for m in cfg.methods:
+            if m == "vabft":
+                T = O.vabft_thresholds(A, B, e_max, 2.5, fmt)[0]
+            else:
+                T = O.aabft_threshold(A, B, fmt, computed=(m == "aabft-computed-y"),
+                                      fixed_y=21.0 if m == "aabft-fixed-y" else None)[0]
+            thr_means[m].append(harness.seq_mean(T))
+            unc[m] += int((actual > T).sum())
+    assert doc["actual"]["per_trial_mean"] == means
+    for m in cfg.methods:
+        assert doc["methods"][m]["per_trial_mean_threshold"] == thr_means[m]
+        assert doc["methods"][m]["rows_not_covered"] == unc[m]
+    assert fpr["methods"]["vabft"]["false_positive_rows"] == 0
+
+
+@pytest.mark.gpu
+def test_blockwise_matches_reference_on_slices(ref_or_port):
+    from paper_2602_08043_b200 import blockwise
+    O = ref_or_port
+    A, B = O.trial_inputs(16, 64, 24, "bf16", "normal:1e-6,1", 8, 0)
+    T = blockwise.blockwise_thresholds(A, B, "bf16", tile_k=32, tile_n=8, e_max=8e-3)
+    assert T.shape == (16, 3)
+    for jb, j0 in enumerate((0, 8, 16)):
+        exp = sum(O.vabft_thresholds(np.ascontiguousarray(A[:, k0:k0 + 32]),
+                                     np.ascontiguousarray(B[k0:k0 + 32, j0:j0 + 8]), 8e-3, 2.5, "bf16")[0]
+                  for k0 in (0, 32))
+        assert np.array_equal(T[:, jb], exp)
+    e = O.encode_and_multiply(A, B, "bf16", "offline")
+    C = e.c.copy()
+    C[5, 13] = 512.0  # a single error, on the BF16 grid
+    v = blockwise.blockwise_verify(A, B, C, "bf16", "offline", tile_k=32, tile_n=8, e_max=8e-3)
+    assert v.detected[5] and v.location[5] == 13 and v.block_detected[5].tolist() == [False, True, False]
+    assert not v.detected[np.arange(16) != 5].any()
+    # block 1 verdicts are the reference's verify on that slice
+    e1 = O.encode_and_multiply(A, np.ascontiguousarray(B[:, 8:16]), "bf16", "offline")
+    r = O.verify(np.ascontiguousarray(C[:, 8:16]), e1.row_check1, e1.row_check2, T[:, 1], "bf16", "offline")
+    assert np.array_equal(v.diff1[:, 1], r["diff1"])
