@@ -275,6 +275,11 @@ typedef struct vabft_fused_opts {
                          counts[VABFT_COUNT_CORRECTED] */
     const vabft_fault* operand_faults;
     vabft_fault_record* operand_fault_records;
+    /* tcgen05 kernel shape: -1 automatic (CTA pairs, cta_group::2 on 256 x 256
+     * tiles over two SMs, when N >= 24 x 256; else one CTA per 128 x 256
+     * tile), 0 one CTA, 1 CTA pairs (N-major B without fault injection). */
+    int32_t cta_mode;
+    int32_t reserved;
 } vabft_fused_opts;
 
 /* Workspace bytes for vabft_fused_gemm at this shape. */
@@ -293,6 +298,13 @@ vabft_status vabft_fused_gemm(const vabft_fused_opts* opts, vabft_bside_t bside,
  * baseline): C = A B in BF16/FP16 with FP32 accumulation. */
 vabft_status vabft_gemm_plain(int32_t format, int32_t b_kmajor, int64_t m, int64_t n, int64_t k,
                               const void* A, const void* B, void* C, void* stream);
+/* Same with an explicit kernel shape (cta_mode as in vabft_fused_opts; the
+ * plain GEMM's automatic choice is CTA pairs whenever eligible). */
+vabft_status vabft_gemm_plain_mode(int32_t format, int32_t b_kmajor, int64_t m, int64_t n, int64_t k,
+                                   const void* A, const void* B, void* C, int32_t cta_mode, void* stream);
+/* 1 if vabft_fused_gemm with these options and shape runs the CTA-pair
+ * kernel, 0 if the one-CTA kernel. */
+int32_t vabft_fused_uses_cta_pairs(const vabft_fused_opts* opts, int64_t m, int64_t n, int64_t k);
 
 #ifdef __cplusplus
 }

@@ -63,7 +63,7 @@ class FusedOpts(C.Structure):
                 ("fault_col", C.c_void_p), ("fault_bit", C.c_void_p), ("fault_dir", C.c_void_p),
                 ("fault_records", C.c_void_p), ("stages", C.c_int32), ("fault_target", C.c_int32),
                 ("n_operand_faults", C.c_int32), ("correct", C.c_int32), ("operand_faults", C.c_void_p),
-                ("operand_fault_records", C.c_void_p)]
+                ("operand_fault_records", C.c_void_p), ("cta_mode", C.c_int32), ("reserved", C.c_int32)]
 
 
 _st = C.c_int
@@ -101,6 +101,8 @@ _SIGS = {
     "vabft_fused_workspace_size": (_st, [_i64, _i64, _i64, C.POINTER(C.c_size_t)]),
     "vabft_fused_gemm": (_st, [C.POINTER(FusedOpts), _vp, _i64, _vp, _vp, _vp, Verdicts, _vp, _vp, C.c_size_t, _vp]),
     "vabft_gemm_plain": (_st, [_i32, _i32, _i64, _i64, _i64, _vp, _vp, _vp, _vp]),
+    "vabft_gemm_plain_mode": (_st, [_i32, _i32, _i64, _i64, _i64, _vp, _vp, _vp, _i32, _vp]),
+    "vabft_fused_uses_cta_pairs": (_i32, [C.POINTER(FusedOpts), _i64, _i64, _i64]),
 }
 
 for _name, (_res, _args) in _SIGS.items():

@@ -266,6 +266,7 @@ extern "C" vabft_status vabft_fused_gemm(const vabft_fused_opts* o, vabft_bside_
             epi.fault_dir = o->fault_dir;
             epi.fault_records = o->fault_records;
             epi.fault_target = o->fault_target;
+            epi.cta_mode = o->cta_mode;
             epi.n_operand_faults = o->n_operand_faults;
             epi.operand_faults = o->operand_faults;
             epi.operand_fault_records = o->operand_fault_records;
@@ -308,3 +309,18 @@ extern "C" vabft_status vabft_fused_gemm(const vabft_fused_opts* o, vabft_bside_
         check_cuda(cudaGetLastError(), "fused tail launch");
     });
 }
+
+extern "C" int32_t vabft_fused_uses_cta_pairs(const vabft_fused_opts* o, int64_t m, int64_t n, int64_t k) {
+    (void)m;
+    (void)k;
+    if (!o) return 0;
+    TcEpilogue epi;
+    epi.sp1 = reinterpret_cast<float*>(1);  // the fused kernel (statistics warps present)
+    epi.fault_col = o->fault_col;
+    epi.fault_target = o->fault_target;
+    epi.n_operand_faults = o->n_operand_faults;
+    epi.tail_phases = o->threshold_method == 2 ? 1 : 0;
+    epi.cta_mode = o->cta_mode;
+    return tc_gemm_uses_pairs(o->b_kmajor != 0, n, epi) ? 1 : 0;
+}
+

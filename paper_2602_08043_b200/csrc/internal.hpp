@@ -82,7 +82,9 @@ struct TcEpilogue {
     uint32_t* rmax = nullptr;
     uint32_t* rmin = nullptr;
     uint32_t* rmnz = nullptr;
+    int cta_mode = -1;  // -1 automatic, 0 one CTA per tile, 1 CTA pairs (vabft_fused_opts.cta_mode)
     int debug = 0;  // profiling ablations (VABFT_DEBUG_STATS): 1 = no stats loads, 2 = no stats math
+    unsigned long long* trace = nullptr;  // developer timeline (VABFT_TRACE): 8 %globaltimer stamps per CTA
     // In-kernel verify tail after a grid barrier (cooperative launch):
     // 0 = none, 3 = single pass, 1|2 = two passes with a second barrier.
     int tail_phases = 0;
@@ -103,5 +105,7 @@ __host__ __device__ inline size_t part_index(int64_t b, int64_t row, int64_t nb)
 void tc_gemm_launch(int fmt, bool b_kmajor, int64_t M, int64_t N, int64_t K, const void* A,
                     const void* B, void* C, const TcEpilogue& epi, cudaStream_t stream);
 bool tc_gemm_supported(int fmt, int64_t M, int64_t N, int64_t K);
+// the kernel-shape decision of tc_gemm_launch (CTA pairs or not)
+bool tc_gemm_uses_pairs(bool b_kmajor, int64_t N, const TcEpilogue& epi);
 
 }  // namespace vabft_dev

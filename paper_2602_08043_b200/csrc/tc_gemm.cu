@@ -33,7 +33,17 @@
 
 namespace vabft_dev {
 
+// developer timeline buffer (VABFT_TRACE): 8 stamps per CTA, read back with
+// vabft_debug_trace
+__device__ unsigned long long g_trace[1024 * 8];
+
 namespace {
+
+__device__ __forceinline__ unsigned long long gtime() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
 
 constexpr int kBM = 128;
 constexpr int kBN = 256;
@@ -53,6 +63,12 @@ static_assert(size_t(kStages) * kStageBytes + 2 * (kABytes + 2 * kBK * 4) + 1024
 // + the statistics warps' private 2-slot A ring (fused path)
 constexpr uint32_t kSlotBytes = kABytes + 2 * kBK * 4;  // A tile + B r1/B r2 segments
 constexpr size_t kSmemBytesStats = kSmemBytes + 2 * size_t(kSlotBytes);
+// CTA-pair kernel: 16 KiB of A + 16 KiB of B per stage per CTA
+constexpr int kStagesPair = 6;
+constexpr size_t kSmemBytesPair = size_t(kStagesPair) * (kABytes + kBBytes / 2) + 1024 + 256;
+constexpr size_t kSmemBytesPairStats = kSmemBytesPair + 2 * size_t(kSlotBytes);
+static_assert(kSmemBytesPairStats <= 232448, "pair smem budget");
+static_assert((2 * kStagesPair + 9 + 9) * 8 <= 256, "pair barrier area");
 // warps running the in-kernel verify tail, each with a 24 KiB slice of the
 // (then idle) pipeline shared memory
 constexpr int kTailWarps = 9;
@@ -63,6 +79,7 @@ struct TcParams {
     int M, N, K;
     int num_m_blk, num_n_blk, num_k_blk, num_tiles;
     int group_m;  // tile raster: groups of group_m row blocks, n-major inside a group
+    int pair;     // 1: CTA-pair kernel (tiles of 256 rows, num_m_blk in 256-row blocks)
     uint16_t* C;
     TcEpilogue epi;
 };
@@ -83,6 +100,21 @@ __device__ __forceinline__ void tile_coords(const TcParams& p, int tile, int& m_
     n_blk = rem / gm;
 }
 
+// This CTA's persistent tile loop. In pair mode (2 x 1 clusters, cta_group::2)
+// both CTAs of a pair walk the same pair tiles (256 x 256 outputs; num_m_blk
+// counts 256-row blocks) and each owns one 128-row half, so everything
+// downstream of the MMA sees 128-row blocks either way.
+__device__ __forceinline__ int tile_first(const TcParams& p) {
+    return p.pair ? int(blockIdx.x >> 1) : int(blockIdx.x);
+}
+__device__ __forceinline__ int tile_stride(const TcParams& p) {
+    return p.pair ? int(gridDim.x >> 1) : int(gridDim.x);
+}
+__device__ __forceinline__ void cta_tile(const TcParams& p, int tile, int& m_blk, int& n_blk) {
+    tile_coords(p, tile, m_blk, n_blk);
+    if (p.pair) m_blk = 2 * m_blk + int(cluster_ctarank());
+}
+
 // Streamed verification (see TcEpilogue::stream_verify). Per 32-row group g
 // two self-resetting counters: group_cnt[2g] counts statistics arrivals (one
 // per N tile), group_cnt[2g+1] final arrivals (one per N tile from the
@@ -101,7 +133,7 @@ template <int F>
 __device__ __forceinline__ void final_arrive(const TcParams& p, int64_t g) {
     unsigned int* cnt = p.epi.group_cnt + 2 * g + 1;
     if (warp_arrive(cnt) != unsigned(p.num_n_blk)) return;  // target num_n_blk + 1
-    if (p.epi.debug != 7) final_half_direct<F>(p.epi.tail, g);  // 7: ablation, no verification
+    if (p.epi.debug != 7 && p.epi.debug != 9) final_half_direct<F>(p.epi.tail, g);  // 7: no verification, 9: no final half
     __syncwarp();
     if ((threadIdx.x & 31) == 0) *cnt = 0u;  // ready for the next launch
 }
@@ -110,7 +142,12 @@ template <int F>
 __device__ __forceinline__ void stats_arrive(const TcParams& p, int64_t g) {
     unsigned int* cnt = p.epi.group_cnt + 2 * g;
     if (warp_arrive(cnt) != unsigned(p.num_n_blk) - 1u) return;
-    if (p.epi.debug != 7) stats_half_direct<F>(p.epi.tail, g);
+    const unsigned long long t0 = p.epi.trace ? gtime() : 0ull;
+    if (p.epi.debug != 7 && p.epi.debug != 8) stats_half_direct<F>(p.epi.tail, g);
+    if (p.epi.trace && (threadIdx.x & 31) == 0) {
+        atomicAdd(p.epi.trace + blockIdx.x * 8 + 6, gtime() - t0);
+        atomicAdd(p.epi.trace + blockIdx.x * 8 + 7, 1ull);
+    }  // 8: no statistics half
     __syncwarp();
     if ((threadIdx.x & 31) == 0) *cnt = 0u;
     final_arrive<F>(p, g);
@@ -180,6 +217,11 @@ __device__ __forceinline__ void operand_faults_stage(const TcParams& p, uint8_t*
     // generic-proxy writes -> the tensor cores' async-proxy reads
     if (wrote) asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
 }
+
+// N tiles of a row block that compute its statistics: K block b belongs to
+// tile b mod stats_tiles (all N tiles: concentrating the blocks on fewer
+// tiles was measured to put the statistics warps on the critical path).
+__device__ __forceinline__ int stats_tiles(const TcParams& p) { return p.num_n_blk; }
 
 // ------------------------------------------------ in-GEMM A statistics
 // Four statistics warps (thread = row of the 128-row A tile). The 128-column
@@ -314,10 +356,10 @@ __device__ __forceinline__ void stats_producer(const TcParams& p, const CUtensor
                                                uint64_t* sfull_bar, uint64_t* sempty_bar) {
     uint32_t cnt = 0;
     const int nblk = (p.K + 127) / 128;
-    for (int tile = blockIdx.x; tile < p.num_tiles; tile += gridDim.x) {
+    for (int tile = tile_first(p); tile < p.num_tiles; tile += tile_stride(p)) {
         int m_blk, n_blk;
-        tile_coords(p, tile, m_blk, n_blk);
-        for (int b = n_blk; b < nblk; b += p.num_n_blk) {
+        cta_tile(p, tile, m_blk, n_blk);
+        for (int b = n_blk; n_blk < stats_tiles(p) && b < nblk; b += stats_tiles(p)) {
             for (int kb = 2 * b; kb < 2 * b + 2 && kb < p.num_k_blk; ++kb, ++cnt) {
                 const int slot = int(cnt & 1u);
                 mbar_wait(smem_u32(&sempty_bar[slot]), ((cnt >> 1) & 1u) ^ 1u);
@@ -347,11 +389,11 @@ __device__ __forceinline__ void stats_warps(const TcParams& p, const uint8_t* sm
     acc.reset();
     uint32_t cnt = 0;  // statistics stages consumed: slot = cnt & 1, phase = (cnt >> 1) & 1
     const int nblk = (p.K + 127) / 128;
-    for (int tile = blockIdx.x; tile < p.num_tiles; tile += gridDim.x) {
+    for (int tile = tile_first(p); tile < p.num_tiles; tile += tile_stride(p)) {
         int m_blk, n_blk;
-        tile_coords(p, tile, m_blk, n_blk);
+        cta_tile(p, tile, m_blk, n_blk);
         const int row = m_blk * kBM + r;
-        for (int b = n_blk; b < nblk; b += p.num_n_blk) {
+        for (int b = n_blk; n_blk < stats_tiles(p) && b < nblk; b += stats_tiles(p)) {
             for (int kb = 2 * b; kb < 2 * b + 2 && kb < p.num_k_blk; ++kb, ++cnt) {
                 const int slot = int(cnt & 1u);
                 mbar_wait(smem_u32(&sfull_bar[slot]), (cnt >> 1) & 1u);
@@ -397,39 +439,49 @@ __device__ __forceinline__ void stats_warps(const TcParams& p, const uint8_t* sm
         if (p.epi.stream_verify && (int64_t(m_blk) * 4 + sw) * 32 < p.M)
             stats_arrive<kFmt>(p, int64_t(m_blk) * 4 + sw);
     }
+    if (p.epi.trace && lane == 0) atomicMax(p.epi.trace + blockIdx.x * 8 + 3, gtime());
 }
 
-template <int kFmt, bool kBKMajor, int kAbft, bool kInject, bool kStats>
+template <int kFmt, bool kBKMajor, int kAbft, bool kInject, bool kStats, bool kPair = false>
 __global__ void __launch_bounds__(kThreadsStats, 1)
     tc_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                    const __grid_constant__ TcParams p) {
+    // Pair mode: the leader's tcgen05.mma.cta_group::2 (M = 256) reads 128 A
+    // rows and 128 B columns from each CTA's ring, so a CTA stages 32 KiB per
+    // k-block instead of 48 and holds kStagesPair stages in the same space.
+    constexpr int kST = kPair ? kStagesPair : kStages;
+    constexpr uint32_t kBB = kPair ? kBBytes / 2 : kBBytes;
+    constexpr uint32_t kSB = kABytes + kBB;
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                                ~uintptr_t(1023));
     uint8_t* smA = smem;
-    uint8_t* smB = smem + kStages * kABytes;
-    uint8_t* smS = smem + kStages * kStageBytes;  // statistics ring (kStats only)
+    uint8_t* smB = smem + kST * kABytes;
+    uint8_t* smS = smem + kST * kSB;  // statistics ring (kStats only)
     uint64_t* bars = reinterpret_cast<uint64_t*>(smS + (kStats ? 2 * kSlotBytes : 0));
     uint64_t* full_bar = bars;
-    uint64_t* empty_bar = bars + kStages;
-    uint64_t* tfull_bar = bars + 2 * kStages;
-    uint64_t* tempty_bar = bars + 2 * kStages + 2;
-    uint64_t* sfull_bar = bars + 2 * kStages + 4;
-    uint64_t* sempty_bar = bars + 2 * kStages + 6;
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * kStages + 8);
-    uint64_t* tail_bar = bars + 2 * kStages + 9;  // kTailWarps verify-tail barriers
+    uint64_t* empty_bar = bars + kST;
+    uint64_t* tfull_bar = bars + 2 * kST;
+    uint64_t* tempty_bar = bars + 2 * kST + 2;
+    uint64_t* sfull_bar = bars + 2 * kST + 4;
+    uint64_t* sempty_bar = bars + 2 * kST + 6;
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * kST + 8);
+    uint64_t* tail_bar = bars + 2 * kST + 9;  // kTailWarps verify-tail barriers
 
     const int warp = threadIdx.x >> 5;
     const int lane = threadIdx.x & 31;
+    const uint32_t rank = kPair ? cluster_ctarank() : 0u;  // 0 = the pair's MMA leader
 
     if (threadIdx.x == 0) {
-        for (int s = 0; s < kStages; ++s) {
-            mbar_init(smem_u32(&full_bar[s]), 1);
-            mbar_init(smem_u32(&empty_bar[s]), 1);  // MMA commit
+        for (int s = 0; s < kST; ++s) {
+            // pair: the leader's full barrier takes an arrival from each CTA's
+            // producer and the transaction bytes of both halves
+            mbar_init(smem_u32(&full_bar[s]), kPair ? 2 : 1);
+            mbar_init(smem_u32(&empty_bar[s]), 1);  // MMA commit (multicast to both CTAs in pair mode)
         }
         for (int a = 0; a < 2; ++a) {
             mbar_init(smem_u32(&tfull_bar[a]), 1);
-            mbar_init(smem_u32(&tempty_bar[a]), 4);
+            mbar_init(smem_u32(&tempty_bar[a]), kPair ? 8 : 4);  // both CTAs' epilogue warps (leader's)
             mbar_init(smem_u32(&sfull_bar[a]), 1);
             mbar_init(smem_u32(&sempty_bar[a]), 4);  // the 4 statistics warps
         }
@@ -440,34 +492,52 @@ __global__ void __launch_bounds__(kThreadsStats, 1)
         tma_prefetch_desc(&tmA);
         tma_prefetch_desc(&tmB);
     }
-    if (warp == 1) tmem_alloc(smem_u32(tmem_slot), kTmemCols);
+    if (warp == 1) {
+        if constexpr (kPair) tmem_alloc_pair(smem_u32(tmem_slot), kTmemCols);
+        else tmem_alloc(smem_u32(tmem_slot), kTmemCols);
+    }
     tc_fence_before();
-    __syncthreads();
+    if constexpr (kPair) cluster_sync_all();  // barriers initialised in both CTAs before any remote arrive
+    else __syncthreads();
     tc_fence_after();
     const uint32_t tmem_base = *tmem_slot;
+    if (p.epi.trace && threadIdx.x == 0) p.epi.trace[blockIdx.x * 8 + 0] = gtime();
 
     if (warp == 0) {
         if (lane == 0) {
             // ------------------------------------------------ TMA producer
             int stage = 0;
             uint32_t phase = 0;
-            for (int tile = blockIdx.x; tile < p.num_tiles; tile += gridDim.x) {
+            for (int tile = tile_first(p); tile < p.num_tiles; tile += tile_stride(p)) {
                 int m_blk, n_blk;
-                tile_coords(p, tile, m_blk, n_blk);
+                cta_tile(p, tile, m_blk, n_blk);
                 for (int kb = 0; kb < p.num_k_blk; ++kb) {
                     mbar_wait(smem_u32(&empty_bar[stage]), phase ^ 1);
                     const uint32_t fb = smem_u32(&full_bar[stage]);
-                    mbar_arrive_expect_tx(fb, kStageBytes);
-                    tma_load_2d(smem_u32(smA + stage * kABytes), &tmA, fb, kb * kBK, m_blk * kBM);
-                    const uint32_t bdst = smem_u32(smB + stage * kBBytes);
-                    if constexpr (kBKMajor) {
-                        tma_load_2d(bdst, &tmB, fb, kb * kBK, n_blk * kBN);
-                    } else {
+                    const uint32_t adst = smem_u32(smA + stage * kABytes);
+                    const uint32_t bdst = smem_u32(smB + stage * kBB);
+                    if constexpr (kPair) {
+                        // this CTA's 128 A rows and 128 of the tile's 256 B columns,
+                        // completion bytes on the leader's full barrier
+                        if (rank == 0) mbar_arrive_expect_tx(fb, 2 * kSB);
+                        else mbar_arrive_cluster_relaxed(mapa_shared(fb, 0));
+                        tma_load_2d_pair(adst, &tmA, fb, kb * kBK, m_blk * kBM);
 #pragma unroll
-                        for (int c = 0; c < kBN / 64; ++c)
-                            tma_load_2d(bdst + c * 8192, &tmB, fb, n_blk * kBN + c * 64, kb * kBK);
+                        for (int c = 0; c < 2; ++c)
+                            tma_load_2d_pair(bdst + c * 8192, &tmB, fb, n_blk * kBN + int(rank) * 128 + c * 64,
+                                             kb * kBK);
+                    } else {
+                        mbar_arrive_expect_tx(fb, kStageBytes);
+                        tma_load_2d(adst, &tmA, fb, kb * kBK, m_blk * kBM);
+                        if constexpr (kBKMajor) {
+                            tma_load_2d(bdst, &tmB, fb, kb * kBK, n_blk * kBN);
+                        } else {
+#pragma unroll
+                            for (int c = 0; c < kBN / 64; ++c)
+                                tma_load_2d(bdst + c * 8192, &tmB, fb, n_blk * kBN + c * 64, kb * kBK);
+                        }
                     }
-                    if (++stage == kStages) {
+                    if (++stage == kST) {
                         stage = 0;
                         phase ^= 1;
                     }
@@ -479,17 +549,18 @@ __global__ void __launch_bounds__(kThreadsStats, 1)
         // walks the stages: its lanes flip the planned operand bits in the
         // freshly loaded shared-memory tiles before lane 0 issues the MMAs.
         const bool opf = kInject && p.epi.fault_target != 0;
-        if (lane == 0 || opf) {
+        // pair mode: only the leader issues (cta_group::2, M = 256)
+        if ((lane == 0 || opf) && rank == 0) {
             // --------------------------------------------------- MMA issuer
             constexpr uint32_t idesc =
-                umma_idesc_f16(kFmt == VABFT_BF16 ? 1u : 0u, !kBKMajor, kBM, kBN);
+                umma_idesc_f16(kFmt == VABFT_BF16 ? 1u : 0u, !kBKMajor, kPair ? 2 * kBM : kBM, kBN);
             int stage = 0;
             uint32_t phase = 0;
             int acc = 0;
             uint32_t acc_phase = 0;
-            for (int tile = blockIdx.x; tile < p.num_tiles; tile += gridDim.x) {
+            for (int tile = tile_first(p); tile < p.num_tiles; tile += tile_stride(p)) {
                 int m_blk = 0, n_blk = 0;
-                if (opf) tile_coords(p, tile, m_blk, n_blk);
+                if (opf) cta_tile(p, tile, m_blk, n_blk);
                 if (lane == 0) {
                     mbar_wait(smem_u32(&tempty_bar[acc]), acc_phase ^ 1);
                     tc_fence_after();
@@ -508,29 +579,38 @@ __global__ void __launch_bounds__(kThreadsStats, 1)
                         tc_fence_after();
                         const uint64_t adesc = umma_desc_sw128(smem_u32(smA + stage * kABytes), 16, 1024);
                         const uint64_t bdesc =
-                            kBKMajor ? umma_desc_sw128(smem_u32(smB + stage * kBBytes), 16, 1024)
-                                     : umma_desc_sw128(smem_u32(smB + stage * kBBytes), 8192, 1024);
+                            kBKMajor ? umma_desc_sw128(smem_u32(smB + stage * kBB), 16, 1024)
+                                     : umma_desc_sw128(smem_u32(smB + stage * kBB), 8192, 1024);
 #pragma unroll
                         for (int k = 0; k < kBK / 16; ++k) {
                             // K-major: +32 bytes per 16 elements inside the 128B swizzle row.
                             // N-major: +16 k-rows = 2 swizzle atoms = 2048 bytes.
                             const uint64_t a_off = uint64_t((k * 32) >> 4);
                             const uint64_t b_off = kBKMajor ? uint64_t((k * 32) >> 4) : uint64_t((k * 2048) >> 4);
-                            umma_f16(d_tmem, adesc + a_off, bdesc + b_off, idesc, (kb > 0 || k > 0) ? 1u : 0u);
+                            if constexpr (kPair)
+                                umma_f16_pair(d_tmem, adesc + a_off, bdesc + b_off, idesc, (kb > 0 || k > 0) ? 1u : 0u);
+                            else
+                                umma_f16(d_tmem, adesc + a_off, bdesc + b_off, idesc, (kb > 0 || k > 0) ? 1u : 0u);
                         }
-                        umma_commit(smem_u32(&empty_bar[stage]));
+                        // frees the stage in both CTAs of a pair
+                        if constexpr (kPair) umma_commit_pair(smem_u32(&empty_bar[stage]), 0x3);
+                        else umma_commit(smem_u32(&empty_bar[stage]));
                     }
-                    if (++stage == kStages) {
+                    if (++stage == kST) {
                         stage = 0;
                         phase ^= 1;
                     }
                 }
-                if (lane == 0) umma_commit(smem_u32(&tfull_bar[acc]));
+                if (lane == 0) {
+                    if constexpr (kPair) umma_commit_pair(smem_u32(&tfull_bar[acc]), 0x3);
+                    else umma_commit(smem_u32(&tfull_bar[acc]));
+                }
                 if (++acc == 2) {
                     acc = 0;
                     acc_phase ^= 1;
                 }
             }
+            if (p.epi.trace && lane == 0) p.epi.trace[blockIdx.x * 8 + 1] = gtime();
         }
     } else if (warp == 10) {
         if constexpr (kStats) {
@@ -544,9 +624,9 @@ __global__ void __launch_bounds__(kThreadsStats, 1)
         const int row_in_tile = quad * 32 + lane;
         int acc = 0;
         uint32_t acc_phase = 0;
-        for (int tile = blockIdx.x; tile < p.num_tiles; tile += gridDim.x) {
+        for (int tile = tile_first(p); tile < p.num_tiles; tile += tile_stride(p)) {
             int m_blk, n_blk;
-            tile_coords(p, tile, m_blk, n_blk);
+            cta_tile(p, tile, m_blk, n_blk);
             const int row = m_blk * kBM + row_in_tile;
             const bool row_ok = row < p.M;
             const int n0 = n_blk * kBN;
@@ -672,7 +752,11 @@ __global__ void __launch_bounds__(kThreadsStats, 1)
             }
             tc_fence_before();
             __syncwarp();
-            if (lane == 0) mbar_arrive(smem_u32(&tempty_bar[acc]));
+            if (lane == 0) {
+                // pair: the leader's MMA waits for both CTAs' epilogues
+                if (kPair && rank != 0) mbar_arrive_cluster(mapa_shared(smem_u32(&tempty_bar[acc]), 0));
+                else mbar_arrive(smem_u32(&tempty_bar[acc]));
+            }
             if (++acc == 2) {
                 acc = 0;
                 acc_phase ^= 1;
@@ -682,15 +766,20 @@ __global__ void __launch_bounds__(kThreadsStats, 1)
                     final_arrive<kFmt>(p, int64_t(m_blk) * 4 + quad);
             }
         }
+        if (p.epi.trace && lane == 0) atomicMax(p.epi.trace + blockIdx.x * 8 + 2, gtime());
     }
 
+    if (p.epi.trace && threadIdx.x == 0) p.epi.trace[blockIdx.x * 8 + 4] = gtime();
     tc_fence_before();
-    __syncthreads();
+    if constexpr (kPair) cluster_sync_all();  // both CTAs done with the pair's TMEM and barriers
+    else __syncthreads();
     if (warp == 1) {
         __syncwarp();
         tc_fence_after();
-        tmem_dealloc(tmem_base, kTmemCols);
+        if constexpr (kPair) tmem_dealloc_pair(tmem_base, kTmemCols);
+        else tmem_dealloc(tmem_base, kTmemCols);
     }
+    if (p.epi.trace && threadIdx.x == 0) p.epi.trace[blockIdx.x * 8 + 5] = gtime();
     if constexpr (kStats) {
         // ---------------------------------------------- in-kernel verify tail
         // every tile's C partials and statistics partials are in global memory
@@ -754,36 +843,78 @@ CUtensorMap make_map_2d(int fmt, const void* base, uint64_t rows, uint64_t cols,
     return m;
 }
 
-template <int kFmt, bool kBKMajor, int kAbft, bool kInject, bool kStats = false>
+template <int kFmt, bool kBKMajor, int kAbft, bool kInject, bool kStats = false, bool kPair = false>
 void launch_inst(const CUtensorMap& ta, const CUtensorMap& tb, const TcParams& p,
                  cudaStream_t stream) {
-    auto kern = tc_gemm_kernel<kFmt, kBKMajor, kAbft, kInject, kStats>;
+    auto kern = tc_gemm_kernel<kFmt, kBKMajor, kAbft, kInject, kStats, kPair>;
+    constexpr size_t smem = kPair ? (kStats ? kSmemBytesPairStats : kSmemBytesPair)
+                                  : (kStats ? kSmemBytesStats : kSmemBytes);
+    constexpr unsigned threads = kStats ? kThreadsStats : kThreads;
     static bool attr_set = false;  // per instantiation
     if (!attr_set) {
-        check_cuda(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                        int(kStats ? kSmemBytesStats : kSmemBytes)),
+        check_cuda(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)),
                    "cudaFuncSetAttribute(tc_gemm)");
         attr_set = true;
     }
-    const int grid = p.num_tiles < sm_count() ? p.num_tiles : sm_count();
-    if (kStats && p.epi.tail_phases) {
-        // the in-kernel verify tail synchronizes the grid: cooperative launch
-        // guarantees every CTA is co-resident (grid <= #SMs, 1 CTA/SM)
+    if constexpr (kPair) {
+        // 2 x 1 clusters: the two CTAs of a pair share one TPC. A persistent
+        // grid must fit in ONE wave: size it by the co-resident cluster count
+        // (not every TPC can host a pair at one 227 KiB CTA per SM).
         cudaLaunchConfig_t cfg{};
-        cfg.gridDim = dim3(unsigned(grid));
-        cfg.blockDim = dim3(kStats ? kThreadsStats : kThreads);
-        cfg.dynamicSmemBytes = kStats ? kSmemBytesStats : kSmemBytes;
+        cfg.blockDim = dim3(threads);
+        cfg.dynamicSmemBytes = smem;
         cfg.stream = stream;
         cudaLaunchAttribute attr[1];
-        attr[0].id = cudaLaunchAttributeCooperative;
-        attr[0].val.cooperative = 1;
+        attr[0].id = cudaLaunchAttributeClusterDimension;
+        attr[0].val.clusterDim.x = 2;
+        attr[0].val.clusterDim.y = 1;
+        attr[0].val.clusterDim.z = 1;
         cfg.attrs = attr;
         cfg.numAttrs = 1;
-        check_cuda(cudaLaunchKernelEx(&cfg, kern, ta, tb, p), "tc_gemm cooperative launch");
+        static int max_clusters = [&] {
+            cudaLaunchConfig_t q = cfg;
+            q.gridDim = dim3(unsigned(sm_count() & ~1));
+            int n = 0;
+            check_cuda(cudaOccupancyMaxActiveClusters(&n, kern, &q), "cudaOccupancyMaxActiveClusters");
+            return n > 0 ? n : 1;
+        }();
+        const int pairs = p.num_tiles < max_clusters ? p.num_tiles : max_clusters;
+        cfg.gridDim = dim3(unsigned(2 * pairs));
+        check_cuda(cudaLaunchKernelEx(&cfg, kern, ta, tb, p), "tc_gemm pair launch");
     } else {
-        kern<<<grid, kStats ? kThreadsStats : kThreads, kStats ? kSmemBytesStats : kSmemBytes, stream>>>(ta, tb, p);
+        const int grid = p.num_tiles < sm_count() ? p.num_tiles : sm_count();
+        if (kStats && p.epi.tail_phases) {
+            // the in-kernel verify tail synchronizes the grid: cooperative launch
+            // guarantees every CTA is co-resident (grid <= #SMs, 1 CTA/SM)
+            cudaLaunchConfig_t cfg{};
+            cfg.gridDim = dim3(unsigned(grid));
+            cfg.blockDim = dim3(threads);
+            cfg.dynamicSmemBytes = smem;
+            cfg.stream = stream;
+            cudaLaunchAttribute attr[1];
+            attr[0].id = cudaLaunchAttributeCooperative;
+            attr[0].val.cooperative = 1;
+            cfg.attrs = attr;
+            cfg.numAttrs = 1;
+            check_cuda(cudaLaunchKernelEx(&cfg, kern, ta, tb, p), "tc_gemm cooperative launch");
+        } else {
+            kern<<<grid, threads, smem, stream>>>(ta, tb, p);
+        }
     }
     check_cuda(cudaGetLastError(), "tc_gemm launch");
+}
+
+// pair-mode kernels exist for N-major B without fault injection
+template <int kFmt, bool kBKMajor, int kAbft, bool kInject, bool kStats = false>
+void launch_sel(const CUtensorMap& ta, const CUtensorMap& tb, const TcParams& p, cudaStream_t stream) {
+    if constexpr (!kBKMajor && !kInject) {
+        if (p.pair) {
+            launch_inst<kFmt, kBKMajor, kAbft, kInject, kStats, true>(ta, tb, p, stream);
+            return;
+        }
+    }
+    if (p.pair) fail(VABFT_LOGIC_ERROR, "tc_gemm: no CTA-pair kernel for this configuration");
+    launch_inst<kFmt, kBKMajor, kAbft, kInject, kStats, false>(ta, tb, p, stream);
 }
 
 template <int kFmt, bool kBKMajor>
@@ -792,29 +923,41 @@ void dispatch_epi(const CUtensorMap& ta, const CUtensorMap& tb, const TcParams& 
     const bool inj = p.epi.fault_col != nullptr || (p.epi.fault_target == 2 && p.epi.n_operand_faults > 0);
     const bool st = p.epi.sp1 != nullptr && p.epi.debug != 3;  // 3: ablation, ABFT epilogue only
     switch (p.epi.abft) {
-        case 0: launch_inst<kFmt, kBKMajor, 0, false>(ta, tb, p, stream); break;
+        case 0: launch_sel<kFmt, kBKMajor, 0, false>(ta, tb, p, stream); break;
         case 1:
             if (st) {
-                if (inj) launch_inst<kFmt, kBKMajor, 1, true, true>(ta, tb, p, stream);
-                else launch_inst<kFmt, kBKMajor, 1, false, true>(ta, tb, p, stream);
+                if (inj) launch_sel<kFmt, kBKMajor, 1, true, true>(ta, tb, p, stream);
+                else launch_sel<kFmt, kBKMajor, 1, false, true>(ta, tb, p, stream);
             } else {
-                if (inj) launch_inst<kFmt, kBKMajor, 1, true>(ta, tb, p, stream);
-                else launch_inst<kFmt, kBKMajor, 1, false>(ta, tb, p, stream);
+                if (inj) launch_sel<kFmt, kBKMajor, 1, true>(ta, tb, p, stream);
+                else launch_sel<kFmt, kBKMajor, 1, false>(ta, tb, p, stream);
             }
             break;
         default:
             if (st) {
-                if (inj) launch_inst<kFmt, kBKMajor, 2, true, true>(ta, tb, p, stream);
-                else launch_inst<kFmt, kBKMajor, 2, false, true>(ta, tb, p, stream);
+                if (inj) launch_sel<kFmt, kBKMajor, 2, true, true>(ta, tb, p, stream);
+                else launch_sel<kFmt, kBKMajor, 2, false, true>(ta, tb, p, stream);
             } else {
-                if (inj) launch_inst<kFmt, kBKMajor, 2, true>(ta, tb, p, stream);
-                else launch_inst<kFmt, kBKMajor, 2, false>(ta, tb, p, stream);
+                if (inj) launch_sel<kFmt, kBKMajor, 2, true>(ta, tb, p, stream);
+                else launch_sel<kFmt, kBKMajor, 2, false>(ta, tb, p, stream);
             }
             break;
     }
 }
 
 }  // namespace
+
+bool tc_gemm_uses_pairs(bool b_kmajor, int64_t N, const TcEpilogue& epi) {
+    static const int pair_env = [] {
+        const char* e = std::getenv("VABFT_PAIR");  // developer override of the automatic choice
+        return e ? std::atoi(e) : -1;
+    }();
+    const bool inj = epi.fault_col != nullptr || (epi.fault_target == 2 && epi.n_operand_faults > 0);
+    const bool eligible = !b_kmajor && !inj && epi.tail_phases == 0 && sm_count() >= 2;
+    const int mode = epi.cta_mode >= 0 ? epi.cta_mode : pair_env;
+    const bool want = mode >= 0 ? mode != 0 : (epi.sp1 == nullptr || (N + kBN - 1) / kBN >= 24);
+    return eligible && want;
+}
 
 bool tc_gemm_supported(int fmt, int64_t M, int64_t N, int64_t K) {
     if (fmt != VABFT_BF16 && fmt != VABFT_FP16) return false;
@@ -843,6 +986,29 @@ void tc_gemm_launch(int fmt, bool b_kmajor, int64_t M, int64_t N, int64_t K, con
     p.group_m = raster <= 0 || raster > p.num_m_blk ? p.num_m_blk : raster;
     p.C = static_cast<uint16_t*>(C);
     p.epi = epi;
+    static unsigned long long* trace_buf = [] {
+        unsigned long long* t = nullptr;
+        if (std::getenv("VABFT_TRACE")) {  // developer timeline, see tools/trace_probe.py
+            void* sym = nullptr;
+            check_cuda(cudaGetSymbolAddress(&sym, g_trace), "trace symbol");
+            t = static_cast<unsigned long long*>(sym);
+        }
+        return t;
+    }();
+    p.epi.trace = trace_buf;
+    // CTA pairs (cta_group::2, 256 x 256 tiles over two SMs): N-major B, no
+    // fault injection, no grid-barrier tail. Policy (measured):
+    // the plain GEMM always; the fused kernel when N >= 24 tiles of 256 — its
+    // A-statistics work per tile scales as 1 / #N-tiles, and with fewer N
+    // tiles the pair's faster MMA exposes the statistics warps.
+    // VABFT_PAIR = 0 / 1 forces the 1-CTA / pair kernels.
+    p.pair = tc_gemm_uses_pairs(b_kmajor, N, epi) ? 1 : 0;
+    if (p.pair) {
+        p.num_m_blk = int((M + 2 * kBM - 1) / (2 * kBM));
+        p.num_tiles = p.num_m_blk * p.num_n_blk;
+        const int g = raster / 2;
+        p.group_m = g <= 0 || g > p.num_m_blk ? p.num_m_blk : g;
+    }
     const CUtensorMap ta = make_map_2d(fmt, A, uint64_t(M), uint64_t(K), kBK, kBM);
     const CUtensorMap tb = b_kmajor ? make_map_2d(fmt, B, uint64_t(N), uint64_t(K), kBK, kBN)
                                     : make_map_2d(fmt, B, uint64_t(K), uint64_t(N), 64, kBK);
@@ -856,3 +1022,13 @@ void tc_gemm_launch(int fmt, bool b_kmajor, int64_t M, int64_t N, int64_t K, con
 }
 
 }  // namespace vabft_dev
+
+// developer timeline read-back (not part of the C-ABI header)
+extern "C" int vabft_debug_trace(unsigned long long* out, int n, int reset) {
+    if (cudaMemcpyFromSymbol(out, vabft_dev::g_trace, sizeof(unsigned long long) * size_t(n)) != cudaSuccess) return 1;
+    if (reset) {
+        static unsigned long long zeros[1024 * 8] = {};
+        if (cudaMemcpyToSymbol(vabft_dev::g_trace, zeros, sizeof(zeros)) != cudaSuccess) return 1;
+    }
+    return 0;
+}

@@ -75,11 +75,16 @@ class FusedAbftGemm:
         self.opts.b_kmajor = 0
         self.opts.aabft_fixed_y = aabft_fixed_y
         self.opts.aabft_confidence = aabft_confidence
+        self.opts.cta_mode = -1
         self.h = C.c_void_p()
         check(lib.vabft_bside_create(self.fmt, self.mode, self.k, self.n, ptr(self.B), C.byref(self.h),
                                      stream_ptr()))
         self._ws = None
         self._bufs = {}
+
+    def uses_cta_pairs(self, m: int) -> bool:
+        """Whether a launch of M rows runs the CTA-pair (cta_group::2) kernel."""
+        return bool(lib.vabft_fused_uses_cta_pairs(C.byref(self.opts), m, self.n, self.k))
 
     def update_weight(self, B: torch.Tensor) -> None:
         self.B = B.contiguous()
@@ -165,10 +170,14 @@ class FusedAbftGemm:
             pass
 
 
-def plain_gemm(A: torch.Tensor, B: torch.Tensor, out: Optional[torch.Tensor] = None, b_kmajor: bool = False):
-    """The same tcgen05 kernel with the ABFT epilogue compiled out (overhead baseline)."""
+def plain_gemm(A: torch.Tensor, B: torch.Tensor, out: Optional[torch.Tensor] = None, b_kmajor: bool = False,
+               cta_mode: int = -1):
+    """The same tcgen05 kernel with the ABFT epilogue compiled out (overhead
+    baseline). cta_mode: -1 automatic (CTA pairs when eligible), 0 one CTA per
+    128 x 256 tile, 1 CTA pairs (cta_group::2, 256 x 256)."""
     m, k = A.shape
     n = B.shape[0] if b_kmajor else B.shape[1]
     C_ = out if out is not None else torch.empty((m, n), dtype=A.dtype, device=A.device)
-    check(lib.vabft_gemm_plain(_FMT[A.dtype], int(b_kmajor), m, n, k, ptr(A), ptr(B), ptr(C_), stream_ptr()))
+    check(lib.vabft_gemm_plain_mode(_FMT[A.dtype], int(b_kmajor), m, n, k, ptr(A), ptr(B), ptr(C_), int(cta_mode),
+                                    stream_ptr()))
     return C_

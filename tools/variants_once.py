@@ -13,7 +13,8 @@ import statistics
 import sys
 
 VARIANTS = [("plain", None, None), ("epi", "3", 2), ("st_nomath", "2", 2), ("st_noload", "1", 2),
-            ("gemm+stats", "0", 2), ("arrive_only", "7", 0), ("full", "0", 0)]
+            ("gemm+stats", "0", 2), ("arrive_only", "7", 0), ("no_stats_half", "8", 0), ("no_final_half", "9", 0),
+            ("full", "0", 0)]
 REPS = 5
 
 
