@@ -210,7 +210,8 @@ def encode_and_multiply(a: np.ndarray, b: np.ndarray, mode="offline", spec="fp64
     """encode_and_multiply (checksum.cpp:150-158) on the GPU.
 
     engine="exact": order-exact kernels, bit-identical to the reference.
-    engine="tensor": tcgen05 GEMM (BF16/FP16), checksums in blocked:128 order.
+    engine="tensor": tcgen05 GEMM (BF16/FP16) or the SIMT DFMA GEMM (FP64),
+    checksums in blocked:128 order.
     """
     s = _spec(spec)
     a = np.asarray(a, dtype=np.float64)
@@ -232,8 +233,9 @@ def encode_and_multiply(a: np.ndarray, b: np.ndarray, mode="offline", spec="fp64
     torch.cuda.synchronize()
     cs = checksum_precision_for(s, mode)
     if engine == "tensor":
-        # FP32 arithmetic, blocked:128 order, in both modes
-        cs = PrecisionSpec.fp32().with_accumulation(AccumStrategy(AccumKind.NATIVE_BLOCKED, 128))
+        # FP32 arithmetic (FP64 for FP64), blocked:128 order, in both modes
+        base = PrecisionSpec.fp64() if s.format == "fp64" else PrecisionSpec.fp32()
+        cs = base.with_accumulation(AccumStrategy(AccumKind.NATIVE_BLOCKED, 128))
     out = EncodedProduct(to_host(dC), to_host(r1), to_host(r2), to_host(c1), to_host(c2), cs,
                          "online" if mc else "offline", to_host(dCa), s.format, engine)
     if mc == _capi.OFFLINE:

@@ -27,7 +27,7 @@ from .fused import FusedAbftGemm
 def calibrate(fmt: str = "bf16", sizes: Sequence[int] = (128, 256, 512, 1024, 2048, 4096), trials: int = 20,
               mode: str = "online", seed: int = 0, dist: str = "absnormal:1,1") -> CalibrationResult:
     """calibrate (calibration.cpp:88-150) on the fused tcgen05 path."""
-    dtype = torch.bfloat16 if fmt == "bf16" else torch.float16
+    dtype = {"bf16": torch.bfloat16, "fp16": torch.float16, "fp32": torch.float32, "fp64": torch.float64}[fmt]
     dev = torch.device("cuda", torch.cuda.current_device())
     gen = torch.Generator(device=dev)
     gen.manual_seed(seed)

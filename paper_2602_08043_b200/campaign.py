@@ -42,21 +42,22 @@ def sample_matrix(shape, dist: str, gen: torch.Generator, device, dtype=torch.bf
     values are quantized to the format by the final cast (RNE)."""
     name, _, rest = dist.partition(":")
     args = [float(t) for t in rest.split(",") if t] if rest else []
+    wd = torch.float64 if dtype == torch.float64 else torch.float32  # draw in FP64 for FP64 operands
     arg = lambda i, d: args[i] if i < len(args) else d  # noqa: E731
     if name == "normal":
-        x = torch.randn(shape, generator=gen, device=device) * arg(1, 1.0) + arg(0, 0.0)
+        x = torch.randn(shape, generator=gen, device=device, dtype=wd) * arg(1, 1.0) + arg(0, 0.0)
     elif name == "uniform":
         a, b = arg(0, -1.0), arg(1, 1.0)
-        x = torch.rand(shape, generator=gen, device=device) * (b - a) + a
+        x = torch.rand(shape, generator=gen, device=device, dtype=wd) * (b - a) + a
     elif name == "truncnormal":
         mu, sd, lo, hi = arg(0, 0.0), arg(1, 1.0), arg(2, -1.0), arg(3, 1.0)
-        x = torch.randn(shape, generator=gen, device=device) * sd + mu
+        x = torch.randn(shape, generator=gen, device=device, dtype=wd) * sd + mu
         bad = (x < lo) | (x > hi)
         while bool(bad.any()):
-            x[bad] = torch.randn(int(bad.sum()), generator=gen, device=device) * sd + mu
+            x[bad] = torch.randn(int(bad.sum()), generator=gen, device=device, dtype=wd) * sd + mu
             bad = (x < lo) | (x > hi)
     elif name == "absnormal":
-        x = (torch.randn(shape, generator=gen, device=device) * arg(1, 1.0) + arg(0, 1.0)).abs()
+        x = (torch.randn(shape, generator=gen, device=device, dtype=wd) * arg(1, 1.0) + arg(0, 1.0)).abs()
     else:
         raise _capi.InvalidArgument(f"unknown distribution: {dist}")
     return x.to(dtype)

@@ -100,8 +100,9 @@ extern "C" vabft_status vabft_encode_and_multiply(const vabft_precision* spec, i
         cs_prec(*spec, mode, &csf, &csa);
         if (engine == VABFT_ENGINE_TENSOR) {
             // TENSOR engine checksum precision: FP32 arithmetic in blocked:128
-            // order for both modes (an FP32 PrecisionSpec with NativeBlocked(128))
-            csf = VABFT_FP32;
+            // order for both modes (an FP32 PrecisionSpec with NativeBlocked(128));
+            // FP64 keeps FP64 arithmetic in the same order
+            csf = f == VABFT_FP64 ? VABFT_FP64 : VABFT_FP32;
             csa = vabft_accum{VABFT_ACCUM_BLOCKED, 0, 128};
         }
         check_weights(n, csf, csa.kind);
@@ -111,9 +112,27 @@ extern "C" vabft_status vabft_encode_and_multiply(const vabft_precision* spec, i
         const bool flt = accumulates_in_float(csf, csa.kind);
         const int qfmt = mode == VABFT_OFFLINE ? f : -1;
 
-        if (engine == VABFT_ENGINE_TENSOR) {
+        if (engine == VABFT_ENGINE_TENSOR && f == VABFT_FP64) {
+            // K5: SIMT DFMA GEMM; C and C_accum are the same FP64 values
+            double* c = static_cast<double*>(C ? C : (C_accum ? C_accum : nullptr));
+            if (c) {
+                dgemm_launch(m, n, k, static_cast<const double*>(A), static_cast<const double*>(B), c,
+                             WideEpilogue{}, s);
+                if (C && C_accum)
+                    check_cuda(cudaMemcpyAsync(C_accum, C, sizeof(double) * size_t(m * n), cudaMemcpyDeviceToDevice, s),
+                               "copy");
+            }
+            if (rc1 || rc2) {
+                double* br1 = tmp.get<double>(k);
+                double* br2 = tmp.get<double>(k);
+                launch_row_reduce(f, false, 0, csa, k, n, B, nullptr, nullptr, qfmt, br1, br2, s);
+                double* o1 = rc1 ? rc1 : tmp.get<double>(m);
+                double* o2 = rc2 ? rc2 : tmp.get<double>(m);
+                launch_row_reduce(f, false, 1, csa, m, k, A, br1, br2, qfmt, o1, o2, s);
+            }
+        } else if (engine == VABFT_ENGINE_TENSOR) {
             if (f != VABFT_BF16 && f != VABFT_FP16)
-                fail(VABFT_UNSUPPORTED, "TENSOR engine supports BF16/FP16 only");
+                fail(VABFT_UNSUPPORTED, "TENSOR engine supports BF16/FP16/FP64");
             void* c = C ? C : tmp.get<uint16_t>(size_t(m * n));
             TcEpilogue epi;
             epi.accum_out = static_cast<float*>(C_accum);

@@ -20,10 +20,12 @@
 //                           partial sets, D1/D2, strict compare, NaN rule,
 //                           localization (detect.cpp:9-55), counters.
 // No host synchronization anywhere on this path.
+#include <algorithm>
 #include <cstdlib>
 #include <cstring>
 
 #include "devcommon.cuh"
+#include "exact.hpp"
 #include "guard.hpp"
 #include "internal.hpp"
 #include "numerics.cuh"
@@ -41,6 +43,11 @@ struct vabft_bside {
     unsigned int* gbar;  // grid-barrier state of the fused kernel (inside storage)
     const void* ws_ready = nullptr;  // workspace whose per-row atomics hold their identities
     size_t ws_ready_bytes = 0;
+    // wide formats (FP32 / FP64): B r1 / B r2 in the working type (held as
+    // doubles), and the side stream the A-side pass runs on, overlapping the GEMM
+    double* brd = nullptr;  // [2][K]
+    cudaStream_t side = nullptr;
+    cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
 };
 
 namespace vabft_dev {
@@ -105,6 +112,120 @@ FusedWs carve(void* base, int64_t M, int64_t N, int64_t K) {
     return w;
 }
 
+// Workspace of the wide-format (FP32 / FP64) path, carved from the same buffer.
+struct WideWs {
+    void *part1, *part2;  // [ceil(N/128)][ld] working type
+    int64_t ld;
+    double *mean, *mx, *mn, *vb, *cr1, *cr2, *max_abs_a;
+    int* nonfinite;
+    size_t bytes;
+};
+
+WideWs carve_wide(void* base, int64_t M, int64_t N) {
+    const size_t nN = size_t((N + 127) / 128), m = size_t(M);
+    const size_t ld = (m + 31) / 32 * 32;
+    WideWs w{};
+    size_t off = 0;
+    char* b = static_cast<char*>(base);
+    auto take = [&](size_t sz) {
+        char* p = b ? b + off : nullptr;
+        off += align_up(sz);
+        return p;
+    };
+    w.ld = int64_t(ld);
+    w.part1 = take(8 * nN * ld);
+    w.part2 = take(8 * nN * ld);
+    w.mean = reinterpret_cast<double*>(take(8 * m));
+    w.mx = reinterpret_cast<double*>(take(8 * m));
+    w.mn = reinterpret_cast<double*>(take(8 * m));
+    w.vb = reinterpret_cast<double*>(take(8 * m));
+    w.cr1 = reinterpret_cast<double*>(take(8 * m));
+    w.cr2 = reinterpret_cast<double*>(take(8 * m));
+    w.max_abs_a = reinterpret_cast<double*>(take(8));
+    w.nonfinite = reinterpret_cast<int*>(take(4));
+    w.bytes = off;
+    return w;
+}
+
+bool is_wide(int fmt) { return fmt == VABFT_FP32 || fmt == VABFT_FP64; }
+
+// TENSOR-engine checksum precision of the wide formats: the working type in
+// NativeBlocked(128) order.
+const vabft_accum kBlocked128{VABFT_ACCUM_BLOCKED, 0, 128};
+
+// B r1 / B r2 (checksum.cpp:110-115) of a wide-format weight.
+void wide_bside(vabft_bside* h, cudaStream_t s) {
+    launch_row_reduce(h->fmt, h->fmt == VABFT_FP32, 0, kBlocked128, h->k, h->n, h->B, nullptr, nullptr,
+                      h->mode == VABFT_OFFLINE ? h->fmt : -1, h->brd, h->brd + h->k, s);
+}
+
+// vabft_fused_gemm for FP32 / FP64: the A-side pass (row statistics and
+// A (B r), on the handle's side stream) overlaps the GEMM; the verify tail
+// joins both.
+void wide_fused(const vabft_fused_opts* o, vabft_bside* h, int64_t m, const void* A, void* C, double* T,
+                const vabft_verdicts& verdicts, int64_t* counts, void* workspace, cudaStream_t s) {
+    if (h->fmt != VABFT_FP64) fail(VABFT_UNSUPPORTED, "vabft_fused_gemm: FP32 fused path not built");
+    if (o->fault_target != 0) fail(VABFT_UNSUPPORTED, "vabft_fused_gemm: operand faults need a 16-bit format");
+    const int64_t n = h->n, k = h->k;
+    const WideWs ws = carve_wide(workspace, m, n);
+    const int stages = o->stages == 0 ? 7 : o->stages;
+    const bool tail = (stages & 4) != 0;
+    if (tail) {
+        check_cuda(cudaEventRecord(h->ev_fork, s), "event");
+        check_cuda(cudaStreamWaitEvent(h->side, h->ev_fork, 0), "wait");
+        launch_wide_aside(h->fmt, m, k, A, h->brd, h->brd + k, o->mode == VABFT_OFFLINE ? h->fmt : -1, ws.mean,
+                          ws.vb, ws.mx, ws.mn, ws.cr1, ws.cr2, h->side);
+        if (o->threshold_method == 2) {
+            check_cuda(cudaMemsetAsync(ws.max_abs_a, 0, sizeof(double), h->side), "memset");
+            launch_max_abs_rows(m, ws.mx, ws.mn, ws.max_abs_a, h->side);
+        }
+        check_cuda(cudaEventRecord(h->ev_join, h->side), "event");
+    }
+    if (stages & 2) {
+        WideEpilogue epi;
+        epi.abft = 1;
+        epi.part1 = ws.part1;
+        epi.part2 = ws.part2;
+        epi.ld = ws.ld;
+        epi.fault_col = o->fault_col;
+        epi.fault_bit = o->fault_bit;
+        epi.fault_dir = o->fault_dir;
+        epi.fault_records = o->fault_records;
+        dgemm_launch(m, n, k, static_cast<const double*>(A), static_cast<const double*>(h->B), static_cast<double*>(C),
+                     epi, s);
+    }
+    if (!tail) return;
+    check_cuda(cudaStreamWaitEvent(s, h->ev_join, 0), "wait");
+    WideTail t{};
+    t.M = m;
+    t.N = n;
+    t.K = k;
+    t.nblk = (n + 127) / 128;
+    t.ld = ws.ld;
+    t.fmt = h->fmt;
+    t.part1 = ws.part1;
+    t.part2 = ws.part2;
+    t.mean = ws.mean;
+    t.vb = ws.vb;
+    t.cr1 = ws.cr1;
+    t.cr2 = ws.cr2;
+    t.bsum = h->buf.summary;
+    t.max_abs_a = ws.max_abs_a;
+    t.method = o->threshold_method;
+    t.aabft_t = o->aabft_mantissa_bits > 0 ? o->aabft_mantissa_bits : (h->fmt == VABFT_FP64 ? 53 : 23);
+    t.e_max = o->e_max;
+    t.c_sigma = o->c_sigma;
+    t.aabft_fixed_y = o->aabft_fixed_y;
+    t.aabft_conf = o->aabft_confidence > 0 ? o->aabft_confidence : 3.0;
+    t.floor_scale = o->floor_scale;
+    t.T_out = T;
+    t.v = verdicts;
+    t.counts = counts;
+    t.C = C;
+    t.correct = o->correct;
+    launch_wide_tail(t, s);
+}
+
 }  // namespace
 }  // namespace vabft_dev
 
@@ -147,10 +268,17 @@ extern "C" vabft_status vabft_bside_create(int32_t format, int32_t mode, int64_t
         h->buf.done = reinterpret_cast<unsigned int*>(p);
         check_cuda(cudaMemset(h->gbar, 0, 2 * sizeof(unsigned int)), "memset(grid barrier)");
         check_cuda(cudaMemset(h->buf.done, 0, sizeof(unsigned int)), "memset(bside counter)");
+        if (is_wide(format)) {
+            check_cuda(cudaMalloc(&h->brd, 2 * sizeof(double) * K), "cudaMalloc(bside B r)");
+            check_cuda(cudaStreamCreateWithFlags(&h->side, cudaStreamNonBlocking), "stream");
+            check_cuda(cudaEventCreateWithFlags(&h->ev_fork, cudaEventDisableTiming), "event");
+            check_cuda(cudaEventCreateWithFlags(&h->ev_join, cudaEventDisableTiming), "event");
+        }
         *out = h;
         if (B) {
             check_cuda(cudaMemsetAsync(h->buf.nonfinite, 0, sizeof(int), as_stream(stream)), "memset");
             launch_bside(format, k, n, B, mode == VABFT_OFFLINE ? 1 : 0, h->buf, as_stream(stream));
+            if (is_wide(format)) wide_bside(h, as_stream(stream));
         }
     });
 }
@@ -161,6 +289,7 @@ extern "C" vabft_status vabft_bside_update(vabft_bside_t h, const void* B, void*
         h->B = B;
         check_cuda(cudaMemsetAsync(h->buf.nonfinite, 0, sizeof(int), as_stream(stream)), "memset");
         launch_bside(h->fmt, h->k, h->n, B, h->mode == VABFT_OFFLINE ? 1 : 0, h->buf, as_stream(stream));
+        if (is_wide(h->fmt)) wide_bside(h, as_stream(stream));
     });
 }
 
@@ -168,6 +297,10 @@ extern "C" vabft_status vabft_bside_destroy(vabft_bside_t h) {
     return guarded([&] {
         if (!h) return;
         cudaFree(h->storage);
+        if (h->brd) cudaFree(h->brd);
+        if (h->ev_fork) cudaEventDestroy(h->ev_fork);
+        if (h->ev_join) cudaEventDestroy(h->ev_join);
+        if (h->side) cudaStreamDestroy(h->side);
         delete h;
     });
 }
@@ -176,7 +309,7 @@ extern "C" vabft_status vabft_fused_workspace_size(int64_t m, int64_t n, int64_t
     return guarded([&] {
         if (!bytes) fail(VABFT_INVALID_ARGUMENT, "null bytes");
         if (m < 1 || n < 1 || k < 1) fail(VABFT_INVALID_ARGUMENT, "dims must be >= 1");
-        *bytes = carve(nullptr, m, n, k).bytes;
+        *bytes = std::max(carve(nullptr, m, n, k).bytes, carve_wide(nullptr, m, n).bytes);
     });
 }
 
@@ -187,8 +320,6 @@ extern "C" vabft_status vabft_fused_gemm(const vabft_fused_opts* o, vabft_bside_
                                          void* stream) {
     return guarded([&] {
         if (!o || !h || !A || !C || !h->B) fail(VABFT_INVALID_ARGUMENT, "vabft_fused_gemm: null argument");
-        if (h->fmt != VABFT_BF16 && h->fmt != VABFT_FP16)
-            fail(VABFT_UNSUPPORTED, "vabft_fused_gemm: TENSOR engine needs BF16/FP16 (use the EXACT engine)");
         if (o->mode != h->mode) fail(VABFT_INVALID_ARGUMENT, "vabft_fused_gemm: mode differs from the B-side handle");
         if (o->threshold_method < 0 || o->threshold_method > 2) fail(VABFT_INVALID_ARGUMENT, "bad threshold method");
         if (o->b_kmajor != h->b_kmajor)
@@ -197,9 +328,15 @@ extern "C" vabft_status vabft_fused_gemm(const vabft_fused_opts* o, vabft_bside_
         if (m > (int64_t(1) << 24)) fail(VABFT_INVALID_ARGUMENT, "ChecksumVectors: weights exceed exact range");
         const int64_t n = h->n, k = h->k;
         if (k % 8 != 0 || n % 8 != 0) fail(VABFT_UNSUPPORTED, "vabft_fused_gemm: K and N must be multiples of 8");
-        const FusedWs ws = carve(workspace, m, n, k);
-        if (!workspace || ws_bytes < ws.bytes) fail(VABFT_INVALID_ARGUMENT, "vabft_fused_gemm: workspace too small");
+        const size_t need = std::max(carve(nullptr, m, n, k).bytes, carve_wide(nullptr, m, n).bytes);
+        if (!workspace || ws_bytes < need) fail(VABFT_INVALID_ARGUMENT, "vabft_fused_gemm: workspace too small");
         cudaStream_t s = as_stream(stream);
+        if (o->fault_target < 0 || o->fault_target > 2) fail(VABFT_INVALID_ARGUMENT, "bad fault target");
+        if (is_wide(h->fmt)) {
+            wide_fused(o, h, m, A, C, T, verdicts, counts, workspace, s);
+            return;
+        }
+        const FusedWs ws = carve(workspace, m, n, k);
         const bool offline = o->mode == VABFT_OFFLINE;
         const int stages = o->stages == 0 ? 7 : o->stages;
 

@@ -108,4 +108,43 @@ bool tc_gemm_supported(int fmt, int64_t M, int64_t N, int64_t K);
 // the kernel-shape decision of tc_gemm_launch (CTA pairs or not)
 bool tc_gemm_uses_pairs(bool b_kmajor, int64_t N, const TcEpilogue& epi);
 
+// ---- wide formats (wide.cu): FP64 SIMT DFMA GEMM and the verify pipeline
+// shared by the FP32 / FP64 fused paths. Checksum precision of these paths:
+// the format's own working type (FP32 / FP64) in NativeBlocked(128) order.
+struct WideEpilogue {
+    int abft = 0;            // 1: per-(128-column block, row) partials of C r1 / C r2
+    void* part1 = nullptr;   // [ceil(N/128)][ld] working type (double for FP64, float for FP32)
+    void* part2 = nullptr;
+    int64_t ld = 0;          // row stride of the partial arrays (M padded)
+    const int32_t* fault_col = nullptr;  // per-row output fault (< 0: none), as TcEpilogue
+    const int32_t* fault_bit = nullptr;
+    const int32_t* fault_dir = nullptr;
+    vabft_fault_record* fault_records = nullptr;
+};
+void dgemm_launch(int64_t M, int64_t N, int64_t K, const double* A, const double* B, double* C,
+                  const WideEpilogue& epi, cudaStream_t stream);
+
+struct WideTail {
+    int64_t M, N, K, nblk, ld;
+    int fmt;                               // VABFT_FP32 / VABFT_FP64 (C element type)
+    const void *part1, *part2;             // as WideEpilogue
+    const double *mean, *vb;               // A row statistics (stats.cpp:9-32)
+    const double *cr1, *cr2;               // row checksums A (B r)
+    const double* bsum;                    // B summary (4)
+    const double* max_abs_a;               // A-ABFT computed y
+    int method, aabft_t;
+    double e_max, c_sigma, aabft_fixed_y, aabft_conf, floor_scale;
+    double* T_out;
+    vabft_verdicts v;
+    int64_t* counts;
+    void* C;
+    int correct;
+};
+void launch_wide_tail(const WideTail& t, cudaStream_t stream);
+// one pass over A: row statistics and the blocked:128 row checksums A (B r)
+void launch_wide_aside(int fmt, int64_t M, int64_t K, const void* A, const double* br1, const double* br2, int qfmt,
+                       double* mean, double* vb, double* mx, double* mn, double* cr1, double* cr2,
+                       cudaStream_t stream);
+void launch_max_abs_rows(int64_t m, const double* mx, const double* mn, double* out, cudaStream_t stream);
+
 }  // namespace vabft_dev

@@ -1,0 +1,448 @@
+// K5 — the FP64 fused V-ABFT GEMM (SIMT DFMA) and the verify tail shared by
+// the wide formats (FP32 / FP64) of vabft_fused_gemm.
+//
+//   dgemm_kernel      C = A B in FP64 with DFMA, k in increasing order per
+//                     output (sequential FMA accumulation); the ABFT epilogue
+//                     stages the 128 x 128 tile in shared memory, applies the
+//                     non-finite saturation of run_gemm (precision.cpp:303-310)
+//                     and the optional per-row bit flip (faults.cpp:104-168,
+//                     bits 0-63 of the FP64 accumulator), and writes the
+//                     per-(128-column block, row) partials of C r1 / C r2
+//                     summed in column order (checksum.cpp:160-187 with a
+//                     NativeBlocked(128) FP64 precision).
+//   wide_tail_kernel  per row: blocked:128 combination of the partials, the
+//                     V-ABFT / A-ABFT threshold (threshold_vabft.cpp:28-61,
+//                     threshold_aabft.cpp:31-60), D1 / D2, strict compare, NaN
+//                     rule, localization and optional correction
+//                     (detect.cpp:9-64), counters.
+//
+// DGEMM mapping: 128 x 128 x 16 CTA tiles, 256 threads (8 warps as 4 x 2),
+// an 8 x 8 register tile per thread (rows wm*32 + 8j + 2ty + {0,1}, columns
+// wn*64 + 16j + 2tx + {0,1}) so that every shared-memory fragment read is a
+// conflict-free 16-byte access; a 4-stage cp.async ring (A rows padded to 18
+// doubles). Per k pair: 16 LDS.128 for 128 DFMA — the FP64 pipe (64 DFMA /
+// clk / SM) is the bound, not shared memory.
+#include "devcommon.cuh"
+#include "internal.hpp"
+#include "numerics.cuh"
+#include "ptx.cuh"
+#include "reducers.cuh"
+
+namespace vabft_dev {
+
+namespace {
+
+constexpr int kDBM = 128, kDBN = 128, kDBK = 16, kDStages = 4, kDThreads = 256;
+constexpr int kALd = kDBK + 2;          // doubles per staged A row (16-byte aligned, conflict-free)
+constexpr int kAStage = kDBM * kALd;    // doubles
+constexpr int kBStage = kDBK * kDBN;
+constexpr int kStage = kAStage + kBStage;
+constexpr int kCLd = kDBN + 1;          // epilogue staging stride: row walks are conflict-free
+constexpr size_t kDSmem = sizeof(double) * size_t(kDStages) * kStage;
+static_assert(sizeof(double) * kDBM * kCLd <= kDSmem, "epilogue staging reuses the operand ring");
+
+__device__ __forceinline__ void cp_async16(uint32_t dst, const void* src, bool valid) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(dst), "l"(src), "r"(valid ? 16 : 0)
+                 : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+    asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory");
+}
+
+struct DgemmParams {
+    int64_t M, N, K;
+    const double* A;
+    const double* B;
+    double* C;
+    WideEpilogue epi;
+};
+
+__device__ __forceinline__ double saturate_f64(double x) {
+    return isfinite(x) ? x : copysign(1.7976931348623157e308, x);
+}
+
+template <bool kAbft, bool kInject>
+__global__ void __launch_bounds__(kDThreads, 1) dgemm_kernel(const __grid_constant__ DgemmParams p) {
+    extern __shared__ __align__(16) double sm[];
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int64_t m0 = int64_t(blockIdx.y) * kDBM, n0 = int64_t(blockIdx.x) * kDBN;
+    const int wm = warp & 3, wn = warp >> 2, ty = lane >> 3, tx = lane & 7;
+    const int64_t ktiles = (p.K + kDBK - 1) / kDBK;
+
+    auto load_stage = [&](int64_t kt, int slot) {
+        double* As = sm + size_t(slot) * kStage;
+        double* Bs = As + kAStage;
+        const int64_t k0 = kt * kDBK;
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {  // A: 128 rows x 8 chunks of 2 doubles
+            const int c = tid + q * kDThreads;
+            const int r = c >> 3, part = c & 7;
+            const int64_t gr = m0 + r, gk = k0 + part * 2;
+            const bool ok = gr < p.M && gk < p.K;
+            cp_async16(smem_u32(As + r * kALd + part * 2), ok ? p.A + gr * p.K + gk : p.A, ok);
+        }
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {  // B: 16 rows x 64 chunks
+            const int c = tid + q * kDThreads;
+            const int r = c >> 6, part = c & 63;
+            const int64_t gk = k0 + r, gc = n0 + part * 2;
+            const bool ok = gk < p.K && gc < p.N;
+            cp_async16(smem_u32(Bs + r * kDBN + part * 2), ok ? p.B + gk * p.N + gc : p.B, ok);
+        }
+    };
+
+    double acc[8][8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i)
+#pragma unroll
+        for (int j = 0; j < 8; ++j) acc[i][j] = 0.0;
+
+#pragma unroll
+    for (int s = 0; s < kDStages - 1; ++s) {
+        if (s < ktiles) load_stage(s, s);
+        cp_async_commit();
+    }
+#pragma unroll 1
+    for (int64_t kt = 0; kt < ktiles; ++kt) {
+        cp_async_wait<kDStages - 2>();
+        __syncthreads();
+        const int64_t nk = kt + kDStages - 1;
+        if (nk < ktiles) load_stage(nk, int(nk % kDStages));
+        cp_async_commit();
+        const double* As = sm + size_t(kt % kDStages) * kStage;
+        const double* Bs = As + kAStage;
+#pragma unroll
+        for (int kk = 0; kk < kDBK; kk += 2) {
+            double2 a[8], b0[4], b1[4];
+#pragma unroll
+            for (int ri = 0; ri < 8; ++ri) {
+                const int r = wm * 32 + (ri >> 1) * 8 + ty * 2 + (ri & 1);
+                a[ri] = *reinterpret_cast<const double2*>(As + r * kALd + kk);
+            }
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+                const int c = wn * 64 + j * 16 + tx * 2;
+                b0[j] = *reinterpret_cast<const double2*>(Bs + kk * kDBN + c);
+                b1[j] = *reinterpret_cast<const double2*>(Bs + (kk + 1) * kDBN + c);
+            }
+#pragma unroll
+            for (int ri = 0; ri < 8; ++ri)
+#pragma unroll
+                for (int j = 0; j < 4; ++j) {
+                    acc[ri][2 * j] = fma(a[ri].x, b0[j].x, acc[ri][2 * j]);
+                    acc[ri][2 * j + 1] = fma(a[ri].x, b0[j].y, acc[ri][2 * j + 1]);
+                }
+#pragma unroll
+            for (int ri = 0; ri < 8; ++ri)
+#pragma unroll
+                for (int j = 0; j < 4; ++j) {
+                    acc[ri][2 * j] = fma(a[ri].y, b1[j].x, acc[ri][2 * j]);
+                    acc[ri][2 * j + 1] = fma(a[ri].y, b1[j].y, acc[ri][2 * j + 1]);
+                }
+        }
+    }
+    cp_async_wait<0>();
+    __syncthreads();
+
+    // ---- epilogue: stage the tile, ABFT row pass, coalesced store
+    double* Cs = sm;
+#pragma unroll
+    for (int ri = 0; ri < 8; ++ri) {
+        const int r = wm * 32 + (ri >> 1) * 8 + ty * 2 + (ri & 1);
+#pragma unroll
+        for (int ci = 0; ci < 8; ++ci) {
+            const int c = wn * 64 + (ci >> 1) * 16 + tx * 2 + (ci & 1);
+            Cs[r * kCLd + c] = saturate_f64(acc[ri][ci]);
+        }
+    }
+    __syncthreads();
+    if constexpr (kAbft) {
+        if (tid < kDBM && m0 + tid < p.M) {
+            const int64_t row = m0 + tid;
+            double* cr = Cs + tid * kCLd;
+            const int nc = int(p.N - n0 < kDBN ? p.N - n0 : kDBN);
+            if constexpr (kInject) {
+                const int64_t fc = p.epi.fault_col[row];
+                if (fc >= n0 && fc < n0 + nc) {
+                    const int fbit = p.epi.fault_bit[row], fdir = p.epi.fault_dir[row];
+                    const double x = cr[fc - n0];
+                    const uint64_t bb = uint64_t(__double_as_longlong(x));
+                    const bool ok = bit_eligible(bb, fbit, fdir);
+                    const double x2 = ok ? __longlong_as_double(int64_t(bb ^ (uint64_t(1) << fbit))) : x;
+                    if (p.epi.fault_records) {
+                        vabft_fault_record rr;
+                        rr.value_before = x;
+                        rr.value_after = x2;
+                        rr.applied = ok ? 1 : 0;
+                        rr.reserved = 0;
+                        p.epi.fault_records[row] = rr;
+                    }
+                    cr[fc - n0] = x2;
+                }
+            }
+            double s1 = 0.0, s2 = 0.0;
+#pragma unroll 4
+            for (int c = 0; c < nc; ++c) {
+                const double x = cr[c];
+                s1 = __dadd_rn(s1, x);
+                s2 = __dadd_rn(s2, __dmul_rn(double(n0 + c + 1), x));
+            }
+            const size_t o = size_t(blockIdx.x) * size_t(p.epi.ld) + size_t(row);
+            static_cast<double*>(p.epi.part1)[o] = s1;
+            static_cast<double*>(p.epi.part2)[o] = s2;
+        }
+        __syncthreads();
+    }
+#pragma unroll 4
+    for (int q = 0; q < (kDBM * kDBN / 2) / kDThreads; ++q) {
+        const int idx = tid + q * kDThreads;
+        const int r = idx >> 6, cp = idx & 63;
+        const int64_t gr = m0 + r, gc = n0 + cp * 2;
+        if (gr < p.M && gc < p.N)
+            __stcs(reinterpret_cast<double2*>(p.C + gr * p.N + gc),
+                   make_double2(Cs[r * kCLd + cp * 2], Cs[r * kCLd + cp * 2 + 1]));
+    }
+}
+
+template <class W>
+__device__ __forceinline__ W load_part(const void* p, size_t o) {
+    return static_cast<const W*>(p)[o];
+}
+
+// One thread per row.
+template <class W>
+__global__ void __launch_bounds__(256) wide_tail_kernel(const WideTail a) {
+    const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    const int lane = threadIdx.x & 31;
+    const bool valid = i < a.M;
+    bool det = false, located = false, isnan_row = false, corrected = false;
+    if (valid) {
+        W r1 = W(0), r2 = W(0);
+        for (int64_t b = 0; b < a.nblk; ++b) {
+            const size_t o = size_t(b) * size_t(a.ld) + size_t(i);
+            r1 = radd(r1, load_part<W>(a.part1, o));
+            r2 = radd(r2, load_part<W>(a.part2, o));
+        }
+        double t;
+        if (a.method == 0) {
+            t = vabft_threshold_total(a.mean[i], a.vb[i], a.bsum[0], a.bsum[1], a.bsum[2], a.N, a.e_max, a.c_sigma);
+        } else {
+            const double y = a.method == 1 ? a.aabft_fixed_y : __dmul_rn(*a.max_abs_a, a.bsum[3]);
+            t = aabft_total(a.K, a.aabft_t, y, a.aabft_conf);
+        }
+        if (a.T_out) a.T_out[i] = t;
+        const double c1 = a.cr1[i], c2 = a.cr2[i];
+        const double d1 = __dsub_rn(double(r1), c1);
+        const double d2 = __dsub_rn(double(r2), c2);
+        int64_t loc = -1;
+        double res = 0.0;
+        if (isnan(d1) || isnan(d2)) {
+            det = true;
+            isnan_row = true;
+        } else {
+            det = fabs(d1) > t;
+            if (det && fabs(d1) > __dmul_rn(a.floor_scale, t)) {
+                int64_t j;
+                double rr;
+                if (localize_dev(d1, d2, a.N, &j, &rr)) {
+                    loc = j;
+                    res = rr;
+                    located = true;
+                    // correct (detect.cpp:57-64): C[i][j] = quantize(C[i][j] - diff1)
+                    if (a.correct && a.C != nullptr && rr < 0.4) {
+                        if (a.fmt == VABFT_FP64) {
+                            double* cij = static_cast<double*>(a.C) + i * a.N + j;
+                            *cij = __dsub_rn(*cij, d1);
+                        } else {
+                            float* cij = static_cast<float*>(a.C) + i * a.N + j;
+                            const float q = __double2float_rn(__dsub_rn(double(*cij), d1));
+                            *cij = isinf(q) ? copysignf(3.40282346638528859812e+38f, q) : q;
+                        }
+                        corrected = true;
+                    }
+                }
+            }
+        }
+        if (a.v.diff1) a.v.diff1[i] = d1;
+        if (a.v.diff2) a.v.diff2[i] = d2;
+        if (a.v.detected) a.v.detected[i] = det ? 1 : 0;
+        if (a.v.location) a.v.location[i] = loc;
+        if (a.v.residual) a.v.residual[i] = res;
+        if (a.v.row_check1) a.v.row_check1[i] = c1;
+        if (a.v.row_check2) a.v.row_check2[i] = c2;
+    }
+    if (a.counts) {
+        const unsigned mv = __ballot_sync(0xffffffffu, valid);
+        const unsigned md = __ballot_sync(0xffffffffu, det);
+        const unsigned ml = __ballot_sync(0xffffffffu, located);
+        const unsigned mn = __ballot_sync(0xffffffffu, isnan_row);
+        const unsigned mc = __ballot_sync(0xffffffffu, corrected);
+        if (lane == 0) {
+            auto add = [&](int slot, unsigned mask) {
+                if (mask) atomicAdd(reinterpret_cast<unsigned long long*>(a.counts + slot), __popc(mask));
+            };
+            add(VABFT_COUNT_ROWS, mv);
+            add(VABFT_COUNT_DETECTED, md);
+            add(VABFT_COUNT_LOCATED, ml);
+            add(VABFT_COUNT_NAN, mn);
+            add(VABFT_COUNT_CORRECTED, mc);
+        }
+    }
+}
+
+// A side of the wide fused path in one pass over A: per row the reference's
+// sequential Neumaier mean, max, min and var_bound (stats.cpp:9-32) and the
+// row checksums A (B r1), A (B r2) in the working type W, NativeBlocked(128)
+// (checksum.cpp:103-146, encode's second stage). A warp owns 32 rows (lane =
+// row); 32 x 32 tiles are double-buffered in shared memory by cp.async so
+// every lane's sequential chain runs at add latency while the next tile is in
+// flight. Two warps per CTA and few registers, so the CTAs co-reside with the
+// DGEMM's (the pass runs on a side stream, overlapping the GEMM).
+constexpr int kAsWarps = 2;
+
+template <int F, class W>
+__global__ void __launch_bounds__(32 * kAsWarps) wide_aside_kernel(const typename Elem<F>::T* __restrict__ A,
+                                                                  int64_t M, int64_t K, const double* __restrict__ br1,
+                                                                  const double* __restrict__ br2, int qfmt,
+                                                                  double* mean, double* vb, double* mx_out,
+                                                                  double* mn_out, double* cr1, double* cr2) {
+    using T = typename Elem<F>::T;
+    __shared__ T tile[kAsWarps][2][32][33];
+    const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int64_t r0 = (int64_t(blockIdx.x) * kAsWarps + w) * 32;
+    if (r0 >= M) return;
+    const int64_t row = r0 + lane;
+    auto fetch = [&](int64_t c0, int buf) {
+        const int64_t c = c0 + lane;
+#pragma unroll 8
+        for (int rr = 0; rr < 32; ++rr) {
+            const int64_t r = r0 + rr;
+            const bool ok = r < M && c < K;
+            const uint32_t dst = smem_u32(&tile[w][buf][rr][lane]);
+            const T* src = ok ? A + r * K + c : A;
+            if constexpr (sizeof(T) == 8)
+                asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(dst), "l"(src), "r"(ok ? 8 : 0)
+                             : "memory");
+            else
+                asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;\n" ::"r"(dst), "l"(src), "r"(ok ? 4 : 0)
+                             : "memory");
+        }
+        asm volatile("cp.async.commit_group;\n" ::: "memory");
+    };
+    Neu ns;
+    double mx = -INFINITY, mn = INFINITY;
+    W p1 = W(0), p2 = W(0), t1 = W(0), t2 = W(0);
+    fetch(0, 0);
+    int buf = 0;
+    for (int64_t c0 = 0; c0 < K; c0 += 32, buf ^= 1) {
+        if (c0 + 32 < K) {
+            fetch(c0 + 32, buf ^ 1);
+            asm volatile("cp.async.wait_group 1;\n" ::: "memory");
+        } else {
+            asm volatile("cp.async.wait_group 0;\n" ::: "memory");
+        }
+        __syncwarp();
+        const W w1l = c0 + lane < K ? W(br1[c0 + lane]) : W(0);
+        const W w2l = c0 + lane < K ? W(br2[c0 + lane]) : W(0);
+        const int cmax = int(K - c0 < 32 ? K - c0 : 32);
+        for (int jj = 0; jj < cmax; ++jj) {
+            const double x = Elem<F>::d(tile[w][buf][lane][jj]);
+            const W w1 = __shfl_sync(0xffffffffu, w1l, jj), w2 = __shfl_sync(0xffffffffu, w2l, jj);
+            ns.add(x);
+            mx = fmax(mx, x);
+            mn = fmin(mn, x);
+            const W xw = W(x);
+            p1 = radd(p1, rmul(w1, xw));
+            p2 = radd(p2, rmul(w2, xw));
+            const int64_t q = c0 + jj + 1;
+            if (q % 128 == 0 || q == K) {
+                t1 = radd(t1, p1);
+                t2 = radd(t2, p2);
+                p1 = W(0);
+                p2 = W(0);
+            }
+        }
+        __syncwarp();
+    }
+    if (row < M) {
+        double m, v;
+        stats_finish(ns, mx, mn, K, &m, &v);
+        mean[row] = m;
+        vb[row] = v;
+        mx_out[row] = mx;
+        mn_out[row] = mn;
+        double c1 = double(t1), c2 = double(t2);
+        if (qfmt == VABFT_FP32) {  // offline FP32: the checksum rounded to the input format (a no-op for W = float)
+            c1 = double(float(c1));
+            c2 = double(float(c2));
+        }
+        cr1[row] = c1;
+        cr2[row] = c2;
+    }
+}
+
+__global__ void max_abs_rows_kernel(int64_t m, const double* mx, const double* mn, double* out) {
+    const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    double v = i < m ? fmax(fabs(mx[i]), fabs(mn[i])) : 0.0;
+#pragma unroll
+    for (int s = 16; s >= 1; s >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, s));
+    if ((threadIdx.x & 31) == 0 && v > 0.0) atomic_max_nonneg(out, v);
+}
+
+}  // namespace
+
+void dgemm_launch(int64_t M, int64_t N, int64_t K, const double* A, const double* B, double* C,
+                  const WideEpilogue& epi, cudaStream_t stream) {
+    if (M < 1 || N < 1 || K < 1) fail(VABFT_INVALID_ARGUMENT, "dims must be >= 1");
+    if (K % 2 != 0 || N % 2 != 0) fail(VABFT_UNSUPPORTED, "FP64 GEMM: K and N must be even");
+    if ((reinterpret_cast<uintptr_t>(A) | reinterpret_cast<uintptr_t>(B) | reinterpret_cast<uintptr_t>(C)) & 15)
+        fail(VABFT_INVALID_ARGUMENT, "FP64 GEMM: operands must be 16-byte aligned");
+    if ((N + kDBN - 1) / kDBN > 0x7FFFFFFF || (M + kDBM - 1) / kDBM > 65535)
+        fail(VABFT_UNSUPPORTED, "FP64 GEMM: grid too large");
+    DgemmParams p{M, N, K, A, B, C, epi};
+    const dim3 grid(unsigned((N + kDBN - 1) / kDBN), unsigned((M + kDBM - 1) / kDBM));
+    static bool attr_set[3] = {false, false, false};  // per variant (one pointer type for all)
+    auto run = [&](void (*kern)(DgemmParams), int variant) {
+        if (!attr_set[variant]) {
+            check_cuda(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kDSmem)),
+                       "attr(dgemm)");
+            attr_set[variant] = true;
+        }
+        kern<<<grid, kDThreads, kDSmem, stream>>>(p);
+    };
+    if (!epi.abft) run(dgemm_kernel<false, false>, 0);
+    else if (epi.fault_col) run(dgemm_kernel<true, true>, 1);
+    else run(dgemm_kernel<true, false>, 2);
+    check_cuda(cudaGetLastError(), "dgemm launch");
+}
+
+void launch_wide_tail(const WideTail& t, cudaStream_t stream) {
+    const unsigned grid = unsigned((t.M + 255) / 256);
+    if (t.fmt == VABFT_FP64) wide_tail_kernel<double><<<grid, 256, 0, stream>>>(t);
+    else wide_tail_kernel<float><<<grid, 256, 0, stream>>>(t);
+    check_cuda(cudaGetLastError(), "wide tail launch");
+}
+
+void launch_wide_aside(int fmt, int64_t M, int64_t K, const void* A, const double* br1, const double* br2, int qfmt,
+                       double* mean, double* vb, double* mx, double* mn, double* cr1, double* cr2,
+                       cudaStream_t stream) {
+    const unsigned grid = unsigned((M + 32 * kAsWarps - 1) / (32 * kAsWarps));
+    if (fmt == VABFT_FP64)
+        wide_aside_kernel<VABFT_FP64, double><<<grid, 32 * kAsWarps, 0, stream>>>(
+            static_cast<const double*>(A), M, K, br1, br2, qfmt, mean, vb, mx, mn, cr1, cr2);
+    else if (fmt == VABFT_FP32)
+        wide_aside_kernel<VABFT_FP32, float><<<grid, 32 * kAsWarps, 0, stream>>>(
+            static_cast<const float*>(A), M, K, br1, br2, qfmt, mean, vb, mx, mn, cr1, cr2);
+    else
+        fail(VABFT_INVALID_ARGUMENT, "wide A side: FP32 / FP64 only");
+    check_cuda(cudaGetLastError(), "wide A-side launch");
+}
+
+void launch_max_abs_rows(int64_t m, const double* mx, const double* mn, double* out, cudaStream_t stream) {
+    max_abs_rows_kernel<<<unsigned((m + 255) / 256), 256, 0, stream>>>(m, mx, mn, out);
+    check_cuda(cudaGetLastError(), "max|A| launch");
+}
+
+}  // namespace vabft_dev

@@ -102,7 +102,7 @@ def unit_roundoff_for(precision: str, mode: str) -> float:
     """u of the verification precision: the FP32 accumulator online, the
     format itself offline (checksum_precision_for, checksum.cpp:18-24)."""
     if mode == "online":
-        return 2.0 ** -24
+        return 2.0 ** -53 if precision == "fp64" else 2.0 ** -24
     return {"bf16": 2.0 ** -8, "fp16": 2.0 ** -11, "fp32": 2.0 ** -24, "fp64": 2.0 ** -53}[precision]
 
 
@@ -118,10 +118,17 @@ DEVICE_CALIBRATION: Dict[Tuple[str, str], Tuple[List[int], List[float]]] = {
     # format constant stays.)
     ("fp16", "online"): ([128, 256, 512, 1024, 2048, 4096, 8192, 16384],
                          [1.48e-06, 1.88e-06, 3.39e-06, 6.62e-06, 1.35e-05, 2.73e-05, 5.45e-05, 1.10e-04]),
+    # FP64 SIMT DFMA path (sequential FMA accumulation, FP64 blocked:128
+    # checksums; online == offline), 4 trials per size
+    # (profiles/r01_calibration_fp64_device.json)
+    ("fp64", "online"): ([128, 256, 512, 1024, 2048, 4096, 8192, 16384],
+                         [1.72e-15, 1.25e-15, 1.01e-15, 8.18e-16, 8.21e-16, 9.85e-16, 1.47e-15, 2.28e-15]),
 }
 
 # reference format defaults (PrecisionSpec::bf16/fp16, precision.cpp:44-62)
 FORMAT_DEFAULT = {"bf16": 8e-3, "fp16": 1e-3}
+# sqrt-scaled format models a*sqrt(dim) + b (PrecisionSpec::fp32/fp64, precision.cpp:64-82)
+FORMAT_MODEL = {"fp32": (5e-9, 1.2e-7), "fp64": (1e-17, 2.5e-16)}
 
 
 def device_calibration(precision: str, mode: str) -> CalibrationResult:
@@ -172,8 +179,15 @@ def default_e_max(precision: str, mode: str, k: int) -> float:
     its table when it has none of its own; offline without a table, the
     format constant."""
     key = (precision, mode) if (precision, mode) in DEVICE_CALIBRATION else None
-    if key is None and mode == "online":
+    if key is None and mode == "online" and precision == "fp16":
         key = ("bf16", "online")
+    if key is None and precision in ("fp32", "fp64"):
+        # the wide formats verify in their own precision: online == offline
+        other = (precision, "offline" if mode == "online" else "online")
+        key = other if other in DEVICE_CALIBRATION else None
     if key is None:
+        if precision in FORMAT_MODEL:
+            a, b = FORMAT_MODEL[precision]
+            return a * math.sqrt(k) + b
         return FORMAT_DEFAULT[precision]
     return max(1.2 * measured_max(key[0], key[1], k), 2.0 * unit_roundoff_for(precision, mode))

@@ -20,7 +20,8 @@ from ._capi import check, lib
 from .emax import default_e_max
 from .device import ptr, stream_ptr
 
-_FMT = {torch.bfloat16: _capi.BF16, torch.float16: _capi.FP16}
+_FMT = {torch.bfloat16: _capi.BF16, torch.float16: _capi.FP16, torch.float32: _capi.FP32,
+        torch.float64: _capi.FP64}
 _METHOD = {"vabft": 0, "aabft-fixed-y": 1, "aabft-computed-y": 2}
 _TARGET = {"output": 0, "A": 1, "B": 2}  # FaultTarget (faults.hpp:15)
 
@@ -32,7 +33,7 @@ def operand_faults(faults, device="cuda") -> torch.Tensor:
     rows = [[int(k), int(j), (int(bit) & 0xFFFFFFFF) | (int(d) << 32)] for (k, j, bit, d) in faults]
     return torch.tensor(rows, dtype=torch.int64, device=device).reshape(-1, 3)
 
-_FMT_NAME = {torch.bfloat16: "bf16", torch.float16: "fp16"}
+_FMT_NAME = {torch.bfloat16: "bf16", torch.float16: "fp16", torch.float32: "fp32", torch.float64: "fp64"}
 
 
 @dataclass
@@ -50,13 +51,14 @@ class FusedResult:
 
 
 class FusedAbftGemm:
-    """Fault-tolerant C = A B for a fixed BF16/FP16 weight B (K x N, row-major)."""
+    """Fault-tolerant C = A B for a fixed weight B (K x N, row-major): BF16 /
+    FP16 on the tcgen05 kernel, FP64 on the SIMT DFMA kernel (K5)."""
 
     def __init__(self, B: torch.Tensor, mode: str = "online", threshold: str = "vabft",
                  e_max: Optional[float] = None, c_sigma: float = 2.5, floor_scale: float = 1e-3,
                  aabft_mantissa_bits: int = 0, aabft_fixed_y: float = 21.0, aabft_confidence: float = 3.0):
         if B.dtype not in _FMT or not B.is_cuda or B.dim() != 2:
-            raise _capi.InvalidArgument("FusedAbftGemm: B must be a 2-D BF16/FP16 CUDA tensor")
+            raise _capi.InvalidArgument("FusedAbftGemm: B must be a 2-D BF16/FP16/FP32/FP64 CUDA tensor")
         self.B = B.contiguous()
         self.fmt = _FMT[B.dtype]
         self.k, self.n = self.B.shape

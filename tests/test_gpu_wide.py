@@ -1,0 +1,148 @@
+"""GPU parity of the wide-format fused path (K5: FP64 SIMT DFMA GEMM + the
+shared verify tail) against the oracle.
+
+Bars: C within the FP64 accumulation bound (test_precision.cpp:181-206 with
+u = 2^-53); checksums, row sums, thresholds, verdicts, locations and counts
+bit-exact against the oracle run on the device's own C with an FP64
+NativeBlocked(128) checksum precision (the TENSOR engine's).
+"""
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+BLK = (2, 128)  # AccumKind::NativeBlocked, block 128
+
+
+def bits(x):
+    return np.asarray(x, dtype=np.float64).view(np.uint64)
+
+
+def same(a, b):
+    a, b = np.asarray(a, dtype=np.float64), np.asarray(b, dtype=np.float64)
+    na, nb = np.isnan(a), np.isnan(b)
+    return a.shape == b.shape and np.array_equal(na, nb) and np.array_equal(bits(a[~na]), bits(b[~nb]))
+
+
+@pytest.fixture(scope="module")
+def torch_cuda():
+    import torch
+    assert torch.cuda.is_available(), "GPU tests need a CUDA device"
+    return torch
+
+
+@pytest.mark.parametrize("mode", ["offline", "online"])
+@pytest.mark.parametrize("shape", [(64, 128, 96), (200, 264, 72), (256, 520, 384)])
+def test_fp64_tensor_engine_parity(torch_cuda, port, mode, shape):
+    from paper_2602_08043_b200 import api
+    m, k, n = shape
+    A, B = port.trial_inputs(m, k, n, "fp64", "normal:0,1", 5, 1)
+    e = api.encode_and_multiply(A, B, mode, "fp64", engine="tensor")
+    o = port.encode_and_multiply(A, B, "fp64", mode, accum=BLK)
+    bound = 2 * (k + 1) * 2.0**-53 * (np.abs(A) @ np.abs(B))
+    assert np.all(np.abs(e.c - o.c) <= bound)
+    assert same(e.c, e.c_accum)
+    assert same(e.row_check1, o.row_check1) and same(e.row_check2, o.row_check2)
+    r1, r2 = api.row_sums(e.c, e.checksum_precision, "fp64")
+    p1, p2 = port.row_sums(e.c, "fp64", "offline", accum=BLK)
+    assert same(r1, p1) and same(r2, p2)
+
+
+def _fused(torch, A, B, mode, **kw):
+    from paper_2602_08043_b200.fused import FusedAbftGemm
+    dA = torch.from_numpy(A).cuda()
+    dB = torch.from_numpy(B).cuda()
+    return FusedAbftGemm(dB, mode=mode, **kw), dA
+
+
+@pytest.mark.parametrize("mode", ["online", "offline"])
+@pytest.mark.parametrize("bit", [2, 30, 51, 62])
+def test_fp64_fused_injection_matches_oracle(torch_cuda, port, mode, bit):
+    torch = torch_cuda
+    from paper_2602_08043_b200 import api
+    m, k, n = 160, 256, 392
+    A, B = port.trial_inputs(m, k, n, "fp64", "normal:1e-6,1", 17, bit)
+    cols = np.random.default_rng(bit).integers(0, n, m)
+    e_max = 4e-15
+    g, dA = _fused(torch, A, B, mode, e_max=e_max)
+    rec = torch.zeros(m * 24, dtype=torch.uint8, device="cuda")
+    f = {"col": torch.from_numpy(cols.astype(np.int32)).cuda(),
+         "bit": torch.full((m,), bit, dtype=torch.int32, device="cuda"),
+         "dir": torch.full((m,), 0, dtype=torch.int32, device="cuda"), "records": rec}
+    counts = torch.zeros(6, dtype=torch.int64, device="cuda")
+    r = g(dA, faults=f, checksums=True, counts=counts)
+    torch.cuda.synchronize()
+    Cf = r.C.cpu().numpy()
+    # the clean product from the same kernel (TENSOR engine) and the flips
+    e = api.encode_and_multiply(A, B, mode, "fp64", engine="tensor")
+    flipped = e.c.copy()
+    for i, j in enumerate(cols):
+        flipped[i, j] = (np.array([e.c[i, j]]).view(np.uint64) ^ np.uint64(1 << bit)).view(np.float64)[0]
+    assert same(Cf, flipped)
+    applied = rec.view(m, 24)[:, 16:20].contiguous().view(torch.int32).view(m).cpu().numpy()
+    assert np.all(applied == 1)  # Flip direction: always applicable
+    # checksums and thresholds: bit-exact against the oracle
+    o = port.encode_and_multiply(A, B, "fp64", mode, accum=BLK)
+    assert same(r.row_check1.cpu().numpy(), o.row_check1) and same(r.row_check2.cpu().numpy(), o.row_check2)
+    T_ref, _ = port.vabft_thresholds(A, B, e_max, fmt="fp64")
+    assert same(r.T.cpu().numpy(), T_ref)
+    # verdicts of the device's faulty C under the oracle's verify
+    v = port.verify(Cf, o.row_check1, o.row_check2, T_ref, "fp64", mode, accum=BLK)
+    assert np.array_equal(v["detected"], r.detected.cpu().numpy().astype(bool))
+    assert np.array_equal(v["location"], r.location.cpu().numpy())
+    assert same(v["diff1"], r.diff1.cpu().numpy()) and same(v["diff2"], r.diff2.cpu().numpy())
+    c = counts.cpu().numpy()
+    assert c[0] == m and c[1] == int(v["detected"].sum())
+    if bit >= 51:  # high mantissa / exponent bits: every row caught
+        assert v["detected"].all()
+    if bit == 51:  # ... and located (at bit 62 the weighted sum overflows: no location, as in the reference)
+        assert np.array_equal(v["location"], cols)
+
+
+def test_fp64_fused_correction(torch_cuda, port):
+    torch = torch_cuda
+    m, k, n = 128, 192, 256
+    A, B = port.trial_inputs(m, k, n, "fp64", "normal:0,1", 3, 0)
+    g, dA = _fused(torch, A, B, "online", e_max=4e-15)
+    clean = g(dA).C.clone()
+    cols = (np.arange(m) * 7) % n
+    f = {"col": torch.from_numpy(cols.astype(np.int32)).cuda(),
+         "bit": torch.full((m,), 55, dtype=torch.int32, device="cuda"),
+         "dir": torch.full((m,), 0, dtype=torch.int32, device="cuda")}
+    counts = torch.zeros(6, dtype=torch.int64, device="cuda")
+    r = g(dA, faults=f, counts=counts, correct=True)
+    torch.cuda.synchronize()
+    c = counts.cpu().numpy()
+    assert c[1] == m and c[2] == m and c[5] == m
+    err = (r.C - clean).abs().max().item() / clean.abs().max().item()
+    assert err < 1e-12
+
+
+@pytest.mark.parametrize("dist", ["normal:0,1", "uniform:-1,1", "truncnormal:0,1,-1,1"])
+def test_fp64_fused_no_false_positives(torch_cuda, dist):
+    torch = torch_cuda
+    from paper_2602_08043_b200.campaign import sample_matrix
+    from paper_2602_08043_b200.fused import FusedAbftGemm
+    gen = torch.Generator(device="cuda")
+    gen.manual_seed(1)
+    for (m, k, n) in [(256, 1024, 512), (512, 4096, 256)]:
+        A = sample_matrix((m, k), dist, gen, "cuda", torch.float64)
+        B = sample_matrix((k, n), dist, gen, "cuda", torch.float64)
+        counts = torch.zeros(6, dtype=torch.int64, device="cuda")
+        for mode in ("online", "offline"):
+            counts.zero_()
+            FusedAbftGemm(B, mode=mode)(A, counts=counts)
+            assert int(counts[1].item()) == 0, (dist, m, k, n, mode)
+
+
+def test_fp64_plain_gemm_matches_torch(torch_cuda):
+    torch = torch_cuda
+    from paper_2602_08043_b200.fused import plain_gemm
+    torch.manual_seed(0)
+    for (m, n, k) in [(128, 128, 16), (200, 264, 72), (1000, 770, 514)]:
+        a = torch.randn(m, k, device="cuda", dtype=torch.float64)
+        b = torch.randn(k, n, device="cuda", dtype=torch.float64)
+        c = plain_gemm(a, b)
+        ref = a @ b
+        bound = 2 * (k + 1) * 2.0**-53 * (a.abs() @ b.abs())
+        assert bool(((c - ref).abs() <= bound).all())
