@@ -279,23 +279,29 @@ typedef struct vabft_fused_opts {
      * tiles over two SMs, when N >= 24 x 256; else one CTA per 128 x 256
      * tile), 0 one CTA, 1 CTA pairs (N-major B without fault injection). */
     int32_t cta_mode;
-    int32_t reserved;
+    /* FP32 handles (tcgen05 kind::tf32): 0 or 3 = 3xTF32 error compensation
+     * (FP32-level products), 1 = a single TF32 pass. Ignored otherwise. */
+    int32_t tf32_passes;
 } vabft_fused_opts;
 
 /* Workspace bytes for vabft_fused_gemm at this shape. */
 vabft_status vabft_fused_workspace_size(int64_t m, int64_t n, int64_t k, size_t* bytes);
 
 /* The hot path: stats of A (row stats + A (B r) checksums + thresholds),
- * tcgen05 GEMM with the ABFT epilogue (row partials of the FP32 accumulator
- * or the quantized output), and the verify tail. Writes C (M x N, format of
- * the B-side handle), thresholds T (M doubles, may be NULL), verdicts and
- * accumulates counts. No host synchronization. */
+ * the GEMM with the ABFT epilogue (row partials of the FP32 accumulator or
+ * the quantized output), and the verify tail. BF16/FP16: one persistent
+ * tcgen05 kernel; FP32: tcgen05 kind::tf32 (3xTF32) + side-stream A pass +
+ * tail kernel; FP64: SIMT DFMA + side-stream A pass + tail kernel. Writes C
+ * (M x N, format of the B-side handle), thresholds T (M doubles, may be
+ * NULL), verdicts and accumulates counts. No host synchronization. */
 vabft_status vabft_fused_gemm(const vabft_fused_opts* opts, vabft_bside_t bside, int64_t m,
                               const void* A, void* C, double* T, vabft_verdicts verdicts,
                               int64_t* counts, void* workspace, size_t ws_bytes, void* stream);
 
-/* Plain tcgen05 GEMM with the ABFT epilogue compiled out (the overhead
- * baseline): C = A B in BF16/FP16 with FP32 accumulation. */
+/* Plain GEMM with the ABFT epilogue compiled out (the overhead baseline):
+ * C = A B — BF16/FP16 on tcgen05 with FP32 accumulation, FP32 on tcgen05
+ * with 3xTF32 compensation (operands split into temporaries), FP64 on the
+ * SIMT DFMA kernel. */
 vabft_status vabft_gemm_plain(int32_t format, int32_t b_kmajor, int64_t m, int64_t n, int64_t k,
                               const void* A, const void* B, void* C, void* stream);
 /* Same with an explicit kernel shape (cta_mode as in vabft_fused_opts; the

@@ -26,8 +26,11 @@ from .fused import FusedAbftGemm
 
 def calibrate(fmt: str = "bf16", sizes: Sequence[int] = (128, 256, 512, 1024, 2048, 4096), trials: int = 20,
               mode: str = "online", seed: int = 0, dist: str = "absnormal:1,1") -> CalibrationResult:
-    """calibrate (calibration.cpp:88-150) on the fused tcgen05 path."""
-    dtype = {"bf16": torch.bfloat16, "fp16": torch.float16, "fp32": torch.float32, "fp64": torch.float64}[fmt]
+    """calibrate (calibration.cpp:88-150) on the fused device path. fmt
+    "tf32" calibrates FP32 operands on the single-pass TF32 kernel."""
+    passes = 1 if fmt == "tf32" else 3
+    dtype = {"bf16": torch.bfloat16, "fp16": torch.float16, "fp32": torch.float32, "tf32": torch.float32,
+             "fp64": torch.float64}[fmt]
     dev = torch.device("cuda", torch.cuda.current_device())
     gen = torch.Generator(device=dev)
     gen.manual_seed(seed)
@@ -37,7 +40,7 @@ def calibrate(fmt: str = "bf16", sizes: Sequence[int] = (128, 256, 512, 1024, 20
         for _ in range(trials):
             A = sample_matrix((s, s), dist, gen, dev, dtype)
             B = sample_matrix((s, s), dist, gen, dev, dtype)
-            g = FusedAbftGemm(B, mode=mode, e_max=1.0)
+            g = FusedAbftGemm(B, mode=mode, e_max=1.0, tf32_passes=passes)
             r = g(A, checksums=True)
             rel = (r.diff1.abs() / r.row_check1.abs())
             if not bool(torch.isfinite(rel).all()):

@@ -112,27 +112,33 @@ extern "C" vabft_status vabft_encode_and_multiply(const vabft_precision* spec, i
         const bool flt = accumulates_in_float(csf, csa.kind);
         const int qfmt = mode == VABFT_OFFLINE ? f : -1;
 
-        if (engine == VABFT_ENGINE_TENSOR && f == VABFT_FP64) {
-            // K5: SIMT DFMA GEMM; C and C_accum are the same FP64 values
-            double* c = static_cast<double*>(C ? C : (C_accum ? C_accum : nullptr));
+        if (engine == VABFT_ENGINE_TENSOR && (f == VABFT_FP64 || f == VABFT_FP32)) {
+            // FP64: SIMT DFMA GEMM; FP32: tcgen05 3xTF32. C and C_accum hold
+            // the same values (the accumulator is in the output format).
+            const size_t es = f == VABFT_FP64 ? 8 : 4;
+            void* c = C ? C : C_accum;
             if (c) {
-                dgemm_launch(m, n, k, static_cast<const double*>(A), static_cast<const double*>(B), c,
-                             WideEpilogue{}, s);
+                if (f == VABFT_FP64)
+                    dgemm_launch(m, n, k, static_cast<const double*>(A), static_cast<const double*>(B),
+                                 static_cast<double*>(c), WideEpilogue{}, s);
+                else
+                    tf32_gemm_run(m, n, k, static_cast<const float*>(A), static_cast<const float*>(B),
+                                  static_cast<float*>(c), WideEpilogue{}, 3, s);
                 if (C && C_accum)
-                    check_cuda(cudaMemcpyAsync(C_accum, C, sizeof(double) * size_t(m * n), cudaMemcpyDeviceToDevice, s),
-                               "copy");
+                    check_cuda(cudaMemcpyAsync(C_accum, C, es * size_t(m * n), cudaMemcpyDeviceToDevice, s), "copy");
             }
             if (rc1 || rc2) {
+                const bool fl = f == VABFT_FP32;
                 double* br1 = tmp.get<double>(k);
                 double* br2 = tmp.get<double>(k);
-                launch_row_reduce(f, false, 0, csa, k, n, B, nullptr, nullptr, qfmt, br1, br2, s);
+                launch_row_reduce(f, fl, 0, csa, k, n, B, nullptr, nullptr, qfmt, br1, br2, s);
                 double* o1 = rc1 ? rc1 : tmp.get<double>(m);
                 double* o2 = rc2 ? rc2 : tmp.get<double>(m);
-                launch_row_reduce(f, false, 1, csa, m, k, A, br1, br2, qfmt, o1, o2, s);
+                launch_row_reduce(f, fl, 1, csa, m, k, A, br1, br2, qfmt, o1, o2, s);
             }
         } else if (engine == VABFT_ENGINE_TENSOR) {
             if (f != VABFT_BF16 && f != VABFT_FP16)
-                fail(VABFT_UNSUPPORTED, "TENSOR engine supports BF16/FP16/FP64");
+                fail(VABFT_UNSUPPORTED, "TENSOR engine: unsupported format");
             void* c = C ? C : tmp.get<uint16_t>(size_t(m * n));
             TcEpilogue epi;
             epi.accum_out = static_cast<float*>(C_accum);

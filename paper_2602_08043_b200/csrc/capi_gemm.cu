@@ -1,5 +1,5 @@
 // C-ABI entry points of the plain GEMMs (overhead baselines): tcgen05 for the
-// 16-bit formats, the SIMT DFMA kernel (wide.cu) for FP64.
+// 16-bit formats and FP32 (3xTF32), the SIMT DFMA kernel (wide.cu) for FP64.
 #include "guard.hpp"
 #include "internal.hpp"
 
@@ -14,6 +14,12 @@ extern "C" vabft_status vabft_gemm_plain(int32_t format, int32_t b_kmajor, int64
             if (b_kmajor) fail(VABFT_UNSUPPORTED, "vabft_gemm_plain: FP64 needs a row-major B");
             dgemm_launch(m, n, k, static_cast<const double*>(A), static_cast<const double*>(B),
                          static_cast<double*>(C), WideEpilogue{}, as_stream(stream));
+            return;
+        }
+        if (format == VABFT_FP32) {
+            if (b_kmajor) fail(VABFT_UNSUPPORTED, "vabft_gemm_plain: FP32 needs a row-major B");
+            tf32_gemm_run(m, n, k, static_cast<const float*>(A), static_cast<const float*>(B), static_cast<float*>(C),
+                          WideEpilogue{}, 3, as_stream(stream));
             return;
         }
         TcEpilogue epi;
@@ -31,6 +37,12 @@ extern "C" vabft_status vabft_gemm_plain_mode(int32_t format, int32_t b_kmajor, 
             if (b_kmajor) fail(VABFT_UNSUPPORTED, "vabft_gemm_plain: FP64 needs a row-major B");
             dgemm_launch(m, n, k, static_cast<const double*>(A), static_cast<const double*>(B),
                          static_cast<double*>(C), WideEpilogue{}, as_stream(stream));
+            return;
+        }
+        if (format == VABFT_FP32) {
+            if (b_kmajor) fail(VABFT_UNSUPPORTED, "vabft_gemm_plain: FP32 needs a row-major B");
+            tf32_gemm_run(m, n, k, static_cast<const float*>(A), static_cast<const float*>(B), static_cast<float*>(C),
+                          WideEpilogue{}, 3, as_stream(stream));
             return;
         }
         TcEpilogue epi;

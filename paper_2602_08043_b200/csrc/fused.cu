@@ -48,6 +48,12 @@ struct vabft_bside {
     double* brd = nullptr;  // [2][K]
     cudaStream_t side = nullptr;
     cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+    // FP32 (3xTF32): the weight split once into hi / lo parts, transposed
+    // ([2][N][K], K-major for kind::tf32), and
+    // the activation's split buffers [2][M][K], grown on demand
+    float* b_split = nullptr;
+    float* a_split = nullptr;
+    size_t a_split_elems = 0;
 };
 
 namespace vabft_dev {
@@ -115,14 +121,15 @@ FusedWs carve(void* base, int64_t M, int64_t N, int64_t K) {
 // Workspace of the wide-format (FP32 / FP64) path, carved from the same buffer.
 struct WideWs {
     void *part1, *part2;  // [ceil(N/128)][ld] working type
+    void* cpart;          // [2][ceil(K/128)][ld] checksum block partials
     int64_t ld;
     double *mean, *mx, *mn, *vb, *cr1, *cr2, *max_abs_a;
     int* nonfinite;
     size_t bytes;
 };
 
-WideWs carve_wide(void* base, int64_t M, int64_t N) {
-    const size_t nN = size_t((N + 127) / 128), m = size_t(M);
+WideWs carve_wide(void* base, int64_t M, int64_t N, int64_t K) {
+    const size_t nN = size_t((N + 127) / 128), nK = size_t((K + 127) / 128), m = size_t(M);
     const size_t ld = (m + 31) / 32 * 32;
     WideWs w{};
     size_t off = 0;
@@ -135,6 +142,7 @@ WideWs carve_wide(void* base, int64_t M, int64_t N) {
     w.ld = int64_t(ld);
     w.part1 = take(8 * nN * ld);
     w.part2 = take(8 * nN * ld);
+    w.cpart = take(2 * 8 * nK * ld);
     w.mean = reinterpret_cast<double*>(take(8 * m));
     w.mx = reinterpret_cast<double*>(take(8 * m));
     w.mn = reinterpret_cast<double*>(take(8 * m));
@@ -157,6 +165,9 @@ const vabft_accum kBlocked128{VABFT_ACCUM_BLOCKED, 0, 128};
 void wide_bside(vabft_bside* h, cudaStream_t s) {
     launch_row_reduce(h->fmt, h->fmt == VABFT_FP32, 0, kBlocked128, h->k, h->n, h->B, nullptr, nullptr,
                       h->mode == VABFT_OFFLINE ? h->fmt : -1, h->brd, h->brd + h->k, s);
+    if (h->fmt == VABFT_FP32)
+        split_tf32_t(static_cast<const float*>(h->B), h->b_split, h->b_split + size_t(h->k) * size_t(h->n), h->k,
+                     h->n, s);
 }
 
 // vabft_fused_gemm for FP32 / FP64: the A-side pass (row statistics and
@@ -164,17 +175,18 @@ void wide_bside(vabft_bside* h, cudaStream_t s) {
 // joins both.
 void wide_fused(const vabft_fused_opts* o, vabft_bside* h, int64_t m, const void* A, void* C, double* T,
                 const vabft_verdicts& verdicts, int64_t* counts, void* workspace, cudaStream_t s) {
-    if (h->fmt != VABFT_FP64) fail(VABFT_UNSUPPORTED, "vabft_fused_gemm: FP32 fused path not built");
+    if (o->tf32_passes != 0 && o->tf32_passes != 1 && o->tf32_passes != 3)
+        fail(VABFT_INVALID_ARGUMENT, "vabft_fused_gemm: tf32_passes must be 0, 1 or 3");
     if (o->fault_target != 0) fail(VABFT_UNSUPPORTED, "vabft_fused_gemm: operand faults need a 16-bit format");
     const int64_t n = h->n, k = h->k;
-    const WideWs ws = carve_wide(workspace, m, n);
+    const WideWs ws = carve_wide(workspace, m, n, k);
     const int stages = o->stages == 0 ? 7 : o->stages;
     const bool tail = (stages & 4) != 0;
     if (tail) {
         check_cuda(cudaEventRecord(h->ev_fork, s), "event");
         check_cuda(cudaStreamWaitEvent(h->side, h->ev_fork, 0), "wait");
         launch_wide_aside(h->fmt, m, k, A, h->brd, h->brd + k, o->mode == VABFT_OFFLINE ? h->fmt : -1, ws.mean,
-                          ws.vb, ws.mx, ws.mn, ws.cr1, ws.cr2, h->side);
+                          ws.vb, ws.mx, ws.mn, ws.cr1, ws.cr2, ws.cpart, ws.ld, h->side);
         if (o->threshold_method == 2) {
             check_cuda(cudaMemsetAsync(ws.max_abs_a, 0, sizeof(double), h->side), "memset");
             launch_max_abs_rows(m, ws.mx, ws.mn, ws.max_abs_a, h->side);
@@ -191,8 +203,28 @@ void wide_fused(const vabft_fused_opts* o, vabft_bside* h, int64_t m, const void
         epi.fault_bit = o->fault_bit;
         epi.fault_dir = o->fault_dir;
         epi.fault_records = o->fault_records;
-        dgemm_launch(m, n, k, static_cast<const double*>(A), static_cast<const double*>(h->B), static_cast<double*>(C),
-                     epi, s);
+        if (h->fmt == VABFT_FP64) {
+            dgemm_launch(m, n, k, static_cast<const double*>(A), static_cast<const double*>(h->B),
+                         static_cast<double*>(C), epi, s);
+        } else if (o->tf32_passes == 1) {
+            tf32_gemm_launch(m, n, k, static_cast<const float*>(A), nullptr, h->b_split, nullptr,
+                             static_cast<float*>(C), epi, s);
+        } else {
+            const size_t need = 2 * size_t(m) * size_t(k);
+            if (h->a_split_elems < need) {
+                if (h->a_split) check_cuda(cudaFreeAsync(h->a_split, s), "cudaFreeAsync");
+                h->a_split = nullptr;
+                h->a_split_elems = 0;
+                check_cuda(cudaMallocAsync(reinterpret_cast<void**>(&h->a_split), need * sizeof(float), s),
+                           "cudaMallocAsync(A split)");
+                h->a_split_elems = need;
+            }
+            float* ahi = h->a_split;
+            float* alo = h->a_split + size_t(m) * size_t(k);
+            split_tf32(static_cast<const float*>(A), ahi, alo, m * k, s);
+            const float* bhi = h->b_split;
+            tf32_gemm_launch(m, n, k, ahi, alo, bhi, bhi + size_t(k) * size_t(n), static_cast<float*>(C), epi, s);
+        }
     }
     if (!tail) return;
     check_cuda(cudaStreamWaitEvent(s, h->ev_join, 0), "wait");
@@ -273,6 +305,10 @@ extern "C" vabft_status vabft_bside_create(int32_t format, int32_t mode, int64_t
             check_cuda(cudaStreamCreateWithFlags(&h->side, cudaStreamNonBlocking), "stream");
             check_cuda(cudaEventCreateWithFlags(&h->ev_fork, cudaEventDisableTiming), "event");
             check_cuda(cudaEventCreateWithFlags(&h->ev_join, cudaEventDisableTiming), "event");
+            if (format == VABFT_FP32) {
+                if ((k * n) % 4 != 0) fail(VABFT_UNSUPPORTED, "FP32 weights: K x N must be a multiple of 4");
+                check_cuda(cudaMalloc(&h->b_split, 2 * sizeof(float) * K * size_t(n)), "cudaMalloc(B split)");
+            }
         }
         *out = h;
         if (B) {
@@ -298,6 +334,8 @@ extern "C" vabft_status vabft_bside_destroy(vabft_bside_t h) {
         if (!h) return;
         cudaFree(h->storage);
         if (h->brd) cudaFree(h->brd);
+        if (h->b_split) cudaFree(h->b_split);
+        if (h->a_split) cudaFree(h->a_split);
         if (h->ev_fork) cudaEventDestroy(h->ev_fork);
         if (h->ev_join) cudaEventDestroy(h->ev_join);
         if (h->side) cudaStreamDestroy(h->side);
@@ -309,7 +347,7 @@ extern "C" vabft_status vabft_fused_workspace_size(int64_t m, int64_t n, int64_t
     return guarded([&] {
         if (!bytes) fail(VABFT_INVALID_ARGUMENT, "null bytes");
         if (m < 1 || n < 1 || k < 1) fail(VABFT_INVALID_ARGUMENT, "dims must be >= 1");
-        *bytes = std::max(carve(nullptr, m, n, k).bytes, carve_wide(nullptr, m, n).bytes);
+        *bytes = std::max(carve(nullptr, m, n, k).bytes, carve_wide(nullptr, m, n, k).bytes);
     });
 }
 
@@ -328,7 +366,7 @@ extern "C" vabft_status vabft_fused_gemm(const vabft_fused_opts* o, vabft_bside_
         if (m > (int64_t(1) << 24)) fail(VABFT_INVALID_ARGUMENT, "ChecksumVectors: weights exceed exact range");
         const int64_t n = h->n, k = h->k;
         if (k % 8 != 0 || n % 8 != 0) fail(VABFT_UNSUPPORTED, "vabft_fused_gemm: K and N must be multiples of 8");
-        const size_t need = std::max(carve(nullptr, m, n, k).bytes, carve_wide(nullptr, m, n).bytes);
+        const size_t need = std::max(carve(nullptr, m, n, k).bytes, carve_wide(nullptr, m, n, k).bytes);
         if (!workspace || ws_bytes < need) fail(VABFT_INVALID_ARGUMENT, "vabft_fused_gemm: workspace too small");
         cudaStream_t s = as_stream(stream);
         if (o->fault_target < 0 || o->fault_target > 2) fail(VABFT_INVALID_ARGUMENT, "bad fault target");

@@ -123,6 +123,16 @@ struct WideEpilogue {
 };
 void dgemm_launch(int64_t M, int64_t N, int64_t K, const double* A, const double* B, double* C,
                   const WideEpilogue& epi, cudaStream_t stream);
+// FP32 on tcgen05 kind::tf32 (tf32_gemm.cu): 3xTF32 when the lo parts are
+// given, else one TF32 pass over a_hi / b_hi. B parts are N x K (K-major).
+void split_tf32(const float* x, float* hi, float* lo, int64_t n, cudaStream_t stream);
+// the split of a K x N weight written transposed (N x K): B operands are K-major
+void split_tf32_t(const float* x, float* hi_t, float* lo_t, int64_t K, int64_t N, cudaStream_t stream);
+void tf32_gemm_launch(int64_t M, int64_t N, int64_t K, const float* a_hi, const float* a_lo, const float* b_hi,
+                      const float* b_lo, float* C, const WideEpilogue& epi, cudaStream_t stream);
+// the same on raw FP32 operands, splitting both into stream-ordered temporaries
+void tf32_gemm_run(int64_t M, int64_t N, int64_t K, const float* A, const float* B, float* C, const WideEpilogue& epi,
+                   int passes, cudaStream_t stream);
 
 struct WideTail {
     int64_t M, N, K, nblk, ld;
@@ -141,10 +151,12 @@ struct WideTail {
     int correct;
 };
 void launch_wide_tail(const WideTail& t, cudaStream_t stream);
-// one pass over A: row statistics and the blocked:128 row checksums A (B r)
+// A side: row statistics and the blocked:128 row checksums A (B r); cpart is
+// scratch for the checksum block partials, 2 x ceil(K/128) x ld elements of
+// the working type
 void launch_wide_aside(int fmt, int64_t M, int64_t K, const void* A, const double* br1, const double* br2, int qfmt,
-                       double* mean, double* vb, double* mx, double* mn, double* cr1, double* cr2,
-                       cudaStream_t stream);
+                       double* mean, double* vb, double* mx, double* mn, double* cr1, double* cr2, void* cpart,
+                       int64_t ld, cudaStream_t stream);
 void launch_max_abs_rows(int64_t m, const double* mx, const double* mn, double* out, cudaStream_t stream);
 
 }  // namespace vabft_dev

@@ -292,95 +292,168 @@ __global__ void __launch_bounds__(256) wide_tail_kernel(const WideTail a) {
     }
 }
 
-// A side of the wide fused path in one pass over A: per row the reference's
-// sequential Neumaier mean, max, min and var_bound (stats.cpp:9-32) and the
-// row checksums A (B r1), A (B r2) in the working type W, NativeBlocked(128)
-// (checksum.cpp:103-146, encode's second stage). A warp owns 32 rows (lane =
-// row); 32 x 32 tiles are double-buffered in shared memory by cp.async so
-// every lane's sequential chain runs at add latency while the next tile is in
-// flight. Two warps per CTA and few registers, so the CTAs co-reside with the
-// DGEMM's (the pass runs on a side stream, overlapping the GEMM).
-constexpr int kAsWarps = 2;
+// A side of the wide fused path, on the side stream:
+//
+// wide_rowstats_kernel: per row the reference's sequential Neumaier mean,
+// max, min and var_bound (stats.cpp:9-32). The sum must follow the row order
+// to be bit-exact, so one lane owns one row (a warp per 32 rows); 32 x 32
+// tiles stream through a deep cp.async ring in shared memory (16-byte copies,
+// rows padded to 16-byte multiples, read back with 16-byte loads) and the
+// loop carries only the Neumaier chain and the max/min trackers.
+//
+// wide_cpart_kernel + wide_ccombine_kernel: the row checksums A (B r1),
+// A (B r2) in the working type W, NativeBlocked(128) (checksum.cpp:103-146).
+// A warp takes 32 rows x one 128-column block (coalesced tile loads through
+// shared memory, lane = row walks the block in order) and writes the block
+// partial; the combine adds the partials in block order.
+//
+// Small CTAs that co-reside with the GEMM's.
+template <class T>
+struct AsideCfg {
+    static constexpr int kVec = 16 / int(sizeof(T));        // elements per 16-byte copy
+    static constexpr int kRS = 32 + kVec;                    // padded row stride (elements)
+    static constexpr int kPieces = 32 / kVec;                // 16-byte pieces per tile row
+    static constexpr int kStages = sizeof(T) == 8 ? 6 : 5;   // FP32: fits beside the 198 KiB TF32 GEMM CTA
+    static constexpr size_t kSmem = size_t(kStages) * 32 * kRS * sizeof(T);
+};
+
+template <int F>
+__global__ void __launch_bounds__(32) wide_rowstats_kernel(const typename Elem<F>::T* __restrict__ A, int64_t M,
+                                                           int64_t K, double* mean, double* vb, double* mx_out,
+                                                           double* mn_out) {
+    using T = typename Elem<F>::T;
+    using Cfg = AsideCfg<T>;
+    constexpr int S = Cfg::kStages, RS = Cfg::kRS, V = Cfg::kVec, P = Cfg::kPieces;
+    extern __shared__ __align__(16) uint8_t as_raw[];
+    T* tiles = reinterpret_cast<T*>(as_raw);
+    const int lane = threadIdx.x & 31;
+    const int64_t r0 = int64_t(blockIdx.x) * 32;
+    const int64_t row = r0 + lane;
+    const int64_t nchunks = (K + 31) / 32;
+    auto fetch = [&](int64_t ch) {
+        if (ch < nchunks) {
+            T* tile = tiles + size_t(ch % S) * 32 * RS;
+#pragma unroll
+            for (int t = 0; t < P; ++t) {
+                const int q = lane + 32 * t, rr = q / P, pc = q % P;
+                const int64_t r = r0 + rr, c = ch * 32 + int64_t(pc) * V;
+                const bool ok = r < M && c < K;
+                asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(smem_u32(tile + rr * RS + pc * V)),
+                             "l"(ok ? A + r * K + c : A), "r"(ok ? 16 : 0)
+                             : "memory");
+            }
+        }
+        asm volatile("cp.async.commit_group;\n" ::: "memory");  // (possibly empty) group per chunk
+    };
+    double s = 0.0, comp = 0.0;
+    T mx = T(-INFINITY), mn = T(INFINITY);
+    auto step = [&](T e) {
+        const double x = double(e);
+        // Neumaier (stats.cpp:12-24), branch-free
+        const double t = __dadd_rn(s, x);
+        const bool big = fabs(s) >= fabs(x);
+        const double hi = big ? s : x, lo = big ? x : s;
+        comp = __dadd_rn(comp, __dadd_rn(__dsub_rn(hi, t), lo));
+        s = t;
+        mx = mx < e ? e : mx;  // NaN-free rows: identical to fmax / fmin
+        mn = e < mn ? e : mn;
+    };
+#pragma unroll
+    for (int q = 0; q < S - 1; ++q) fetch(q);
+    for (int64_t ch = 0; ch < nchunks; ++ch) {
+        asm volatile("cp.async.wait_group %0;\n" ::"n"(S - 2) : "memory");
+        __syncwarp();
+        const T* trow = tiles + size_t(ch % S) * 32 * RS + lane * RS;
+        const int cmax = int(K - ch * 32 < 32 ? K - ch * 32 : 32);
+        if (cmax == 32) {
+#pragma unroll
+            for (int v = 0; v < P; ++v) {
+                if constexpr (sizeof(T) == 4) {
+                    const float4 q = *reinterpret_cast<const float4*>(trow + v * 4);
+                    step(q.x);
+                    step(q.y);
+                    step(q.z);
+                    step(q.w);
+                } else {
+                    const double2 q = *reinterpret_cast<const double2*>(trow + v * 2);
+                    step(q.x);
+                    step(q.y);
+                }
+            }
+        } else {
+            for (int jj = 0; jj < cmax; ++jj) step(trow[jj]);
+        }
+        __syncwarp();
+        fetch(ch + S - 1);  // refills the slot consumed one iteration ago
+    }
+    asm volatile("cp.async.wait_group 0;\n" ::: "memory");
+    if (row < M) {
+        Neu ns;
+        ns.s = s;
+        ns.c = comp;
+        double m, v;
+        stats_finish(ns, double(mx), double(mn), K, &m, &v);
+        mean[row] = m;
+        vb[row] = v;
+        mx_out[row] = double(mx);
+        mn_out[row] = double(mn);
+    }
+}
 
 template <int F, class W>
-__global__ void __launch_bounds__(32 * kAsWarps) wide_aside_kernel(const typename Elem<F>::T* __restrict__ A,
-                                                                  int64_t M, int64_t K, const double* __restrict__ br1,
-                                                                  const double* __restrict__ br2, int qfmt,
-                                                                  double* mean, double* vb, double* mx_out,
-                                                                  double* mn_out, double* cr1, double* cr2) {
+__global__ void __launch_bounds__(128) wide_cpart_kernel(const typename Elem<F>::T* __restrict__ A, int64_t M,
+                                                         int64_t K, const double* __restrict__ br1,
+                                                         const double* __restrict__ br2, W* cp1, W* cp2,
+                                                         int64_t ld) {
     using T = typename Elem<F>::T;
-    __shared__ T tile[kAsWarps][2][32][33];
+    __shared__ T tile[4][32][33];
     const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int64_t r0 = (int64_t(blockIdx.x) * kAsWarps + w) * 32;
+    const int64_t r0 = (int64_t(blockIdx.x) * 4 + w) * 32, b = blockIdx.y;
     if (r0 >= M) return;
-    const int64_t row = r0 + lane;
-    auto fetch = [&](int64_t c0, int buf) {
-        const int64_t c = c0 + lane;
+    W p1 = W(0), p2 = W(0);
+    for (int c = 0; c < 4; ++c) {
+        const int64_t col0 = b * 128 + c * 32;
+        if (col0 >= K) break;
+        const int64_t col = col0 + lane;
 #pragma unroll 8
         for (int rr = 0; rr < 32; ++rr) {
             const int64_t r = r0 + rr;
-            const bool ok = r < M && c < K;
-            const uint32_t dst = smem_u32(&tile[w][buf][rr][lane]);
-            const T* src = ok ? A + r * K + c : A;
-            if constexpr (sizeof(T) == 8)
-                asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(dst), "l"(src), "r"(ok ? 8 : 0)
-                             : "memory");
-            else
-                asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;\n" ::"r"(dst), "l"(src), "r"(ok ? 4 : 0)
-                             : "memory");
+            tile[w][rr][lane] = (r < M && col < K) ? A[r * K + col] : T(0);
         }
-        asm volatile("cp.async.commit_group;\n" ::: "memory");
-    };
-    Neu ns;
-    double mx = -INFINITY, mn = INFINITY;
-    W p1 = W(0), p2 = W(0), t1 = W(0), t2 = W(0);
-    fetch(0, 0);
-    int buf = 0;
-    for (int64_t c0 = 0; c0 < K; c0 += 32, buf ^= 1) {
-        if (c0 + 32 < K) {
-            fetch(c0 + 32, buf ^ 1);
-            asm volatile("cp.async.wait_group 1;\n" ::: "memory");
-        } else {
-            asm volatile("cp.async.wait_group 0;\n" ::: "memory");
-        }
+        const W w1l = col < K ? W(br1[col]) : W(0), w2l = col < K ? W(br2[col]) : W(0);
         __syncwarp();
-        const W w1l = c0 + lane < K ? W(br1[c0 + lane]) : W(0);
-        const W w2l = c0 + lane < K ? W(br2[c0 + lane]) : W(0);
-        const int cmax = int(K - c0 < 32 ? K - c0 : 32);
+        const int cmax = int(K - col0 < 32 ? K - col0 : 32);
         for (int jj = 0; jj < cmax; ++jj) {
-            const double x = Elem<F>::d(tile[w][buf][lane][jj]);
-            const W w1 = __shfl_sync(0xffffffffu, w1l, jj), w2 = __shfl_sync(0xffffffffu, w2l, jj);
-            ns.add(x);
-            mx = fmax(mx, x);
-            mn = fmin(mn, x);
-            const W xw = W(x);
-            p1 = radd(p1, rmul(w1, xw));
-            p2 = radd(p2, rmul(w2, xw));
-            const int64_t q = c0 + jj + 1;
-            if (q % 128 == 0 || q == K) {
-                t1 = radd(t1, p1);
-                t2 = radd(t2, p2);
-                p1 = W(0);
-                p2 = W(0);
-            }
+            const W x = W(tile[w][lane][jj]);
+            p1 = radd(p1, rmul(__shfl_sync(0xffffffffu, w1l, jj), x));
+            p2 = radd(p2, rmul(__shfl_sync(0xffffffffu, w2l, jj), x));
         }
         __syncwarp();
     }
+    const int64_t row = r0 + lane;
     if (row < M) {
-        double m, v;
-        stats_finish(ns, mx, mn, K, &m, &v);
-        mean[row] = m;
-        vb[row] = v;
-        mx_out[row] = mx;
-        mn_out[row] = mn;
-        double c1 = double(t1), c2 = double(t2);
-        if (qfmt == VABFT_FP32) {  // offline FP32: the checksum rounded to the input format (a no-op for W = float)
-            c1 = double(float(c1));
-            c2 = double(float(c2));
-        }
-        cr1[row] = c1;
-        cr2[row] = c2;
+        cp1[size_t(b) * size_t(ld) + size_t(row)] = p1;
+        cp2[size_t(b) * size_t(ld) + size_t(row)] = p2;
     }
+}
+
+template <class W>
+__global__ void wide_ccombine_kernel(int64_t M, int64_t nb, const W* cp1, const W* cp2, int64_t ld, int qfmt,
+                                     double* cr1, double* cr2) {
+    const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i >= M) return;
+    W t1 = W(0), t2 = W(0);
+    for (int64_t b = 0; b < nb; ++b) {
+        t1 = radd(t1, cp1[size_t(b) * size_t(ld) + size_t(i)]);
+        t2 = radd(t2, cp2[size_t(b) * size_t(ld) + size_t(i)]);
+    }
+    double c1 = double(t1), c2 = double(t2);
+    if (qfmt == VABFT_FP32) {  // offline FP32: the checksum rounded to the input format (a no-op for W = float)
+        c1 = double(float(c1));
+        c2 = double(float(c2));
+    }
+    cr1[i] = c1;
+    cr2[i] = c2;
 }
 
 __global__ void max_abs_rows_kernel(int64_t m, const double* mx, const double* mn, double* out) {
@@ -426,17 +499,37 @@ void launch_wide_tail(const WideTail& t, cudaStream_t stream) {
 }
 
 void launch_wide_aside(int fmt, int64_t M, int64_t K, const void* A, const double* br1, const double* br2, int qfmt,
-                       double* mean, double* vb, double* mx, double* mn, double* cr1, double* cr2,
-                       cudaStream_t stream) {
-    const unsigned grid = unsigned((M + 32 * kAsWarps - 1) / (32 * kAsWarps));
-    if (fmt == VABFT_FP64)
-        wide_aside_kernel<VABFT_FP64, double><<<grid, 32 * kAsWarps, 0, stream>>>(
-            static_cast<const double*>(A), M, K, br1, br2, qfmt, mean, vb, mx, mn, cr1, cr2);
-    else if (fmt == VABFT_FP32)
-        wide_aside_kernel<VABFT_FP32, float><<<grid, 32 * kAsWarps, 0, stream>>>(
-            static_cast<const float*>(A), M, K, br1, br2, qfmt, mean, vb, mx, mn, cr1, cr2);
-    else
-        fail(VABFT_INVALID_ARGUMENT, "wide A side: FP32 / FP64 only");
+                       double* mean, double* vb, double* mx, double* mn, double* cr1, double* cr2, void* cpart,
+                       int64_t ld, cudaStream_t stream) {
+    const unsigned grid_rows = unsigned((M + 31) / 32);
+    const int64_t nb = (K + 127) / 128;
+    const dim3 grid_cp(unsigned((M + 127) / 128), unsigned(nb));
+    const unsigned grid_cc = unsigned((M + 255) / 256);
+    // SMs running these small CTAs must keep the maximum shared-memory
+    // carveout, or the GEMM's CTAs cannot co-reside and the overlap is lost
+    auto prep = [](const void* kern, size_t smem) {
+        check_cuda(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)),
+                   "attr(wide aside)");
+        check_cuda(cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, 100),
+                   "carveout(wide aside)");
+    };
+    auto run = [&](auto tag, auto wtag) {
+        using T = decltype(tag);
+        using W = decltype(wtag);
+        constexpr int F = sizeof(T) == 8 ? VABFT_FP64 : VABFT_FP32;
+        static const bool once = (prep(reinterpret_cast<const void*>(wide_rowstats_kernel<F>), AsideCfg<T>::kSmem),
+                                  prep(reinterpret_cast<const void*>(wide_cpart_kernel<F, W>), 0), true);
+        (void)once;
+        const T* a = static_cast<const T*>(A);
+        W* cp1 = static_cast<W*>(cpart);
+        W* cp2 = cp1 + size_t(nb) * size_t(ld);
+        wide_rowstats_kernel<F><<<grid_rows, 32, AsideCfg<T>::kSmem, stream>>>(a, M, K, mean, vb, mx, mn);
+        wide_cpart_kernel<F, W><<<grid_cp, 128, 0, stream>>>(a, M, K, br1, br2, cp1, cp2, ld);
+        wide_ccombine_kernel<W><<<grid_cc, 256, 0, stream>>>(M, nb, cp1, cp2, ld, qfmt, cr1, cr2);
+    };
+    if (fmt == VABFT_FP64) run(double{}, double{});
+    else if (fmt == VABFT_FP32) run(float{}, float{});
+    else fail(VABFT_INVALID_ARGUMENT, "wide A side: FP32 / FP64 only");
     check_cuda(cudaGetLastError(), "wide A-side launch");
 }
 

@@ -101,6 +101,8 @@ class CalibrationResult:
 def unit_roundoff_for(precision: str, mode: str) -> float:
     """u of the verification precision: the FP32 accumulator online, the
     format itself offline (checksum_precision_for, checksum.cpp:18-24)."""
+    if precision == "tf32":  # FP32 operands on one TF32 pass: the products carry TF32 rounding
+        return 2.0 ** -11
     if mode == "online":
         return 2.0 ** -53 if precision == "fp64" else 2.0 ** -24
     return {"bf16": 2.0 ** -8, "fp16": 2.0 ** -11, "fp32": 2.0 ** -24, "fp64": 2.0 ** -53}[precision]
@@ -123,12 +125,23 @@ DEVICE_CALIBRATION: Dict[Tuple[str, str], Tuple[List[int], List[float]]] = {
     # (profiles/r01_calibration_fp64_device.json)
     ("fp64", "online"): ([128, 256, 512, 1024, 2048, 4096, 8192, 16384],
                          [1.72e-15, 1.25e-15, 1.01e-15, 8.18e-16, 8.21e-16, 9.85e-16, 1.47e-15, 2.28e-15]),
+    # FP32 on tcgen05 with 3xTF32 (profiles/r01_calibration_fp32_3xtf32_device.json):
+    # the products are FP32-accurate but the tensor core's FP32 accumulation
+    # truncates, so |D1|/|r| grows linearly in n (as for BF16 online)
+    ("fp32", "online"): ([128, 256, 512, 1024, 2048, 4096, 8192, 16384],
+                         [1.90e-06, 3.29e-06, 6.38e-06, 1.24e-05, 2.52e-05, 4.96e-05, 9.86e-05, 1.89e-04]),
+    # one TF32 pass (profiles/r01_calibration_tf32_device.json): TF32 operand
+    # rounding dominates, flat in n; the 2u floor (u = 2^-11) applies
+    ("tf32", "online"): ([128, 256, 512, 1024, 2048, 4096, 8192, 16384],
+                         [4.18e-04, 4.17e-04, 3.93e-04, 3.90e-04, 3.91e-04, 3.99e-04, 4.26e-04, 4.86e-04]),
 }
 
 # reference format defaults (PrecisionSpec::bf16/fp16, precision.cpp:44-62)
 FORMAT_DEFAULT = {"bf16": 8e-3, "fp16": 1e-3}
 # sqrt-scaled format models a*sqrt(dim) + b (PrecisionSpec::fp32/fp64, precision.cpp:64-82)
-FORMAT_MODEL = {"fp32": (5e-9, 1.2e-7), "fp64": (1e-17, 2.5e-16)}
+FORMAT_MODEL = {"fp32": (5e-9, 1.2e-7), "fp64": (1e-17, 2.5e-16),
+                # single-pass TF32 (no reference format): 4 u of TF32 until calibrated
+                "tf32": (0.0, 4 * 2.0 ** -11)}
 
 
 def device_calibration(precision: str, mode: str) -> CalibrationResult:
@@ -181,7 +194,7 @@ def default_e_max(precision: str, mode: str, k: int) -> float:
     key = (precision, mode) if (precision, mode) in DEVICE_CALIBRATION else None
     if key is None and mode == "online" and precision == "fp16":
         key = ("bf16", "online")
-    if key is None and precision in ("fp32", "fp64"):
+    if key is None and precision in ("fp32", "tf32", "fp64"):
         # the wide formats verify in their own precision: online == offline
         other = (precision, "offline" if mode == "online" else "online")
         key = other if other in DEVICE_CALIBRATION else None

@@ -52,11 +52,13 @@ class FusedResult:
 
 class FusedAbftGemm:
     """Fault-tolerant C = A B for a fixed weight B (K x N, row-major): BF16 /
-    FP16 on the tcgen05 kernel, FP64 on the SIMT DFMA kernel (K5)."""
+    FP16 on the tcgen05 kernel, FP32 on tcgen05 kind::tf32 (3xTF32, or one
+    TF32 pass with tf32_passes=1), FP64 on the SIMT DFMA kernel (K5)."""
 
     def __init__(self, B: torch.Tensor, mode: str = "online", threshold: str = "vabft",
                  e_max: Optional[float] = None, c_sigma: float = 2.5, floor_scale: float = 1e-3,
-                 aabft_mantissa_bits: int = 0, aabft_fixed_y: float = 21.0, aabft_confidence: float = 3.0):
+                 aabft_mantissa_bits: int = 0, aabft_fixed_y: float = 21.0, aabft_confidence: float = 3.0,
+                 tf32_passes: int = 3):
         if B.dtype not in _FMT or not B.is_cuda or B.dim() != 2:
             raise _capi.InvalidArgument("FusedAbftGemm: B must be a 2-D BF16/FP16/FP32/FP64 CUDA tensor")
         self.B = B.contiguous()
@@ -65,8 +67,8 @@ class FusedAbftGemm:
         self.mode = _capi.ONLINE if mode == "online" else _capi.OFFLINE
         if e_max is None:
             # resolve_run_e_max (harness.cpp): the calibrated model at dim = K
-            e_max = default_e_max(_FMT_NAME[B.dtype], "online" if self.mode == _capi.ONLINE else "offline",
-                                  self.k)
+            name = "tf32" if (B.dtype == torch.float32 and tf32_passes == 1) else _FMT_NAME[B.dtype]
+            e_max = default_e_max(name, "online" if self.mode == _capi.ONLINE else "offline", self.k)
         self.opts = _capi.FusedOpts()
         self.opts.mode = self.mode
         self.opts.threshold_method = _METHOD[threshold]
@@ -78,6 +80,7 @@ class FusedAbftGemm:
         self.opts.aabft_fixed_y = aabft_fixed_y
         self.opts.aabft_confidence = aabft_confidence
         self.opts.cta_mode = -1
+        self.opts.tf32_passes = tf32_passes  # FP32 weights: 3xTF32 (default) or one TF32 pass
         self.h = C.c_void_p()
         check(lib.vabft_bside_create(self.fmt, self.mode, self.k, self.n, ptr(self.B), C.byref(self.h),
                                      stream_ptr()))

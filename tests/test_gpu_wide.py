@@ -146,3 +146,115 @@ def test_fp64_plain_gemm_matches_torch(torch_cuda):
         ref = a @ b
         bound = 2 * (k + 1) * 2.0**-53 * (a.abs() @ b.abs())
         assert bool(((c - ref).abs() <= bound).all())
+
+
+# ---------------------------------------------------------------- FP32 (3xTF32)
+def _prod_bound(A, B, k):
+    """3xTF32 products (< 2^-21 relative each) accumulated in FP32 over k
+    terms, against the oracle's FP32 pairwise product."""
+    return (2 * (k + 1) * 2.0**-23 + 2.0**-20) * (np.abs(A) @ np.abs(B))
+
+
+@pytest.mark.parametrize("mode", ["offline", "online"])
+@pytest.mark.parametrize("shape", [(64, 128, 96), (200, 264, 72), (256, 520, 384)])
+def test_fp32_tensor_engine_parity(torch_cuda, port, mode, shape):
+    from paper_2602_08043_b200 import api
+    m, k, n = shape
+    A, B = port.trial_inputs(m, k, n, "fp32", "normal:0,1", 6, 1)
+    e = api.encode_and_multiply(A, B, mode, "fp32", engine="tensor")
+    o = port.encode_and_multiply(A, B, "fp32", mode, accum=BLK)
+    assert np.all(np.abs(e.c - o.c) <= _prod_bound(A, B, k))
+    assert same(e.c, e.c_accum)
+    assert same(e.row_check1, o.row_check1) and same(e.row_check2, o.row_check2)
+    r1, r2 = api.row_sums(e.c, e.checksum_precision, "fp32")
+    p1, p2 = port.row_sums(e.c, "fp32", "offline", accum=BLK)
+    assert same(r1, p1) and same(r2, p2)
+
+
+@pytest.mark.parametrize("mode", ["online", "offline"])
+@pytest.mark.parametrize("bit", [2, 15, 22, 30])
+def test_fp32_fused_injection_matches_oracle(torch_cuda, port, mode, bit):
+    torch = torch_cuda
+    from paper_2602_08043_b200 import api
+    m, k, n = 160, 256, 392
+    A, B = port.trial_inputs(m, k, n, "fp32", "normal:1e-6,1", 23, bit)
+    cols = np.random.default_rng(bit).integers(0, n, m)
+    e_max = 2e-6
+    from paper_2602_08043_b200.fused import FusedAbftGemm
+    dA = torch.from_numpy(A).float().cuda()
+    g = FusedAbftGemm(torch.from_numpy(B).float().cuda(), mode=mode, e_max=e_max)
+    rec = torch.zeros(m * 24, dtype=torch.uint8, device="cuda")
+    f = {"col": torch.from_numpy(cols.astype(np.int32)).cuda(),
+         "bit": torch.full((m,), bit, dtype=torch.int32, device="cuda"),
+         "dir": torch.full((m,), 0, dtype=torch.int32, device="cuda"), "records": rec}
+    counts = torch.zeros(6, dtype=torch.int64, device="cuda")
+    r = g(dA, faults=f, checksums=True, counts=counts)
+    torch.cuda.synchronize()
+    Cf = r.C.double().cpu().numpy()
+    e = api.encode_and_multiply(A, B, mode, "fp32", engine="tensor")
+    flipped = e.c.astype(np.float32)
+    for i, j in enumerate(cols):
+        flipped[i, j] = (np.array([flipped[i, j]], dtype=np.float32).view(np.uint32) ^ np.uint32(1 << bit)).view(
+            np.float32)[0]
+    assert same(Cf, flipped.astype(np.float64))
+    o = port.encode_and_multiply(A, B, "fp32", mode, accum=BLK)
+    assert same(r.row_check1.cpu().numpy(), o.row_check1) and same(r.row_check2.cpu().numpy(), o.row_check2)
+    T_ref, _ = port.vabft_thresholds(A, B, e_max, fmt="fp32")
+    assert same(r.T.cpu().numpy(), T_ref)
+    v = port.verify(Cf, o.row_check1, o.row_check2, T_ref, "fp32", mode, accum=BLK)
+    assert np.array_equal(v["detected"], r.detected.cpu().numpy().astype(bool))
+    assert np.array_equal(v["location"], r.location.cpu().numpy())
+    assert same(v["diff1"], r.diff1.cpu().numpy()) and same(v["diff2"], r.diff2.cpu().numpy())
+    assert counts.cpu().numpy()[1] == int(v["detected"].sum())
+    if bit in (22, 30):  # top mantissa / exponent bits: every row caught
+        assert v["detected"].all()
+
+
+def test_fp32_single_pass_tf32(torch_cuda):
+    torch = torch_cuda
+    from paper_2602_08043_b200.fused import FusedAbftGemm
+    torch.manual_seed(3)
+    m, k, n = 512, 1024, 768
+    A = torch.randn(m, k, device="cuda")
+    B = torch.randn(k, n, device="cuda")
+    ref = A.double() @ B.double()
+    g1 = FusedAbftGemm(B, tf32_passes=1, e_max=2e-3)
+    g3 = FusedAbftGemm(B)
+    c1 = torch.zeros(6, dtype=torch.int64, device="cuda")
+    c3 = torch.zeros(6, dtype=torch.int64, device="cuda")
+    r1 = g1(A, counts=c1)
+    e1 = ((r1.C.double() - ref).abs().max() / ref.abs().max()).item()
+    r3 = g3(A, counts=c3)
+    e3 = ((r3.C.double() - ref).abs().max() / ref.abs().max()).item()
+    assert e1 < 2e-3 and e3 < 1e-5 and e3 < e1 / 20, (e1, e3)
+    assert int(c1[1]) == 0 and int(c3[1]) == 0
+
+
+@pytest.mark.parametrize("dist", ["normal:0,1", "uniform:-1,1", "truncnormal:0,1,-1,1"])
+def test_fp32_fused_no_false_positives(torch_cuda, dist):
+    torch = torch_cuda
+    from paper_2602_08043_b200.campaign import sample_matrix
+    from paper_2602_08043_b200.fused import FusedAbftGemm
+    gen = torch.Generator(device="cuda")
+    gen.manual_seed(2)
+    for (m, k, n) in [(256, 1024, 512), (512, 4096, 256)]:
+        A = sample_matrix((m, k), dist, gen, "cuda", torch.float32)
+        B = sample_matrix((k, n), dist, gen, "cuda", torch.float32)
+        counts = torch.zeros(6, dtype=torch.int64, device="cuda")
+        for mode in ("online", "offline"):
+            counts.zero_()
+            FusedAbftGemm(B, mode=mode)(A, counts=counts)
+            assert int(counts[1].item()) == 0, (dist, m, k, n, mode)
+
+
+def test_fp32_plain_gemm_matches_fp64(torch_cuda):
+    torch = torch_cuda
+    from paper_2602_08043_b200.fused import plain_gemm
+    torch.manual_seed(0)
+    for (m, n, k) in [(128, 256, 16), (200, 264, 72), (1000, 772, 516)]:
+        a = torch.randn(m, k, device="cuda")
+        b = torch.randn(k, n, device="cuda")
+        c = plain_gemm(a, b)
+        ref = a.double() @ b.double()
+        bound = (2 * (k + 1) * 2.0**-23 + 2.0**-20) * (a.double().abs() @ b.double().abs())
+        assert bool(((c.double() - ref).abs() <= bound).all())
