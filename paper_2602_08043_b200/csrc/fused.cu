@@ -121,7 +121,7 @@ FusedWs carve(void* base, int64_t M, int64_t N, int64_t K) {
 // Workspace of the wide-format (FP32 / FP64) path, carved from the same buffer.
 struct WideWs {
     void *part1, *part2;  // [ceil(N/128)][ld] working type
-    void* cpart;          // [2][ceil(K/128)][ld] checksum block partials
+    void* cpart;          // [7][ceil(K/128)][ld] A-side block partials (wide.cu)
     int64_t ld;
     double *mean, *mx, *mn, *vb, *cr1, *cr2, *max_abs_a;
     int* nonfinite;
@@ -142,7 +142,7 @@ WideWs carve_wide(void* base, int64_t M, int64_t N, int64_t K) {
     w.ld = int64_t(ld);
     w.part1 = take(8 * nN * ld);
     w.part2 = take(8 * nN * ld);
-    w.cpart = take(2 * 8 * nK * ld);
+    w.cpart = take(7 * 8 * nK * ld);
     w.mean = reinterpret_cast<double*>(take(8 * m));
     w.mx = reinterpret_cast<double*>(take(8 * m));
     w.mn = reinterpret_cast<double*>(take(8 * m));
@@ -186,7 +186,7 @@ void wide_fused(const vabft_fused_opts* o, vabft_bside* h, int64_t m, const void
         check_cuda(cudaEventRecord(h->ev_fork, s), "event");
         check_cuda(cudaStreamWaitEvent(h->side, h->ev_fork, 0), "wait");
         launch_wide_aside(h->fmt, m, k, A, h->brd, h->brd + k, o->mode == VABFT_OFFLINE ? h->fmt : -1, ws.mean,
-                          ws.vb, ws.mx, ws.mn, ws.cr1, ws.cr2, ws.cpart, ws.ld, h->side);
+                          ws.vb, ws.mx, ws.mn, ws.cr1, ws.cr2, ws.cpart, ws.ld, counts, h->side);
         if (o->threshold_method == 2) {
             check_cuda(cudaMemsetAsync(ws.max_abs_a, 0, sizeof(double), h->side), "memset");
             launch_max_abs_rows(m, ws.mx, ws.mn, ws.max_abs_a, h->side);

@@ -151,12 +151,12 @@ struct WideTail {
     int correct;
 };
 void launch_wide_tail(const WideTail& t, cudaStream_t stream);
-// A side: row statistics and the blocked:128 row checksums A (B r); cpart is
-// scratch for the checksum block partials, 2 x ceil(K/128) x ld elements of
-// the working type
+// A side: row statistics and the blocked:128 row checksums A (B r); apart is
+// scratch for the per-(128-column block, row) partials, 7 x ceil(K/128) x ld
+// doubles
 void launch_wide_aside(int fmt, int64_t M, int64_t K, const void* A, const double* br1, const double* br2, int qfmt,
-                       double* mean, double* vb, double* mx, double* mn, double* cr1, double* cr2, void* cpart,
-                       int64_t ld, cudaStream_t stream);
+                       double* mean, double* vb, double* mx, double* mn, double* cr1, double* cr2, void* apart,
+                       int64_t ld, int64_t* counts, cudaStream_t stream);
 void launch_max_abs_rows(int64_t m, const double* mx, const double* mn, double* out, cudaStream_t stream);
 
 }  // namespace vabft_dev

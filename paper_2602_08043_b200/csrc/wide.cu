@@ -292,127 +292,64 @@ __global__ void __launch_bounds__(256) wide_tail_kernel(const WideTail a) {
     }
 }
 
-// A side of the wide fused path, on the side stream:
+// A side of the wide fused path: ONE pass over A on the side stream, then a
+// per-row combine.
 //
-// wide_rowstats_kernel: per row the reference's sequential Neumaier mean,
-// max, min and var_bound (stats.cpp:9-32). The sum must follow the row order
-// to be bit-exact, so one lane owns one row (a warp per 32 rows); 32 x 32
-// tiles stream through a deep cp.async ring in shared memory (16-byte copies,
-// rows padded to 16-byte multiples, read back with 16-byte loads) and the
-// loop carries only the Neumaier chain and the max/min trackers.
-//
-// wide_cpart_kernel + wide_ccombine_kernel: the row checksums A (B r1),
-// A (B r2) in the working type W, NativeBlocked(128) (checksum.cpp:103-146).
-// A warp takes 32 rows x one 128-column block (coalesced tile loads through
-// shared memory, lane = row walks the block in order) and writes the block
-// partial; the combine adds the partials in block order.
-//
-// Small CTAs that co-reside with the GEMM's.
-template <class T>
-struct AsideCfg {
-    static constexpr int kVec = 16 / int(sizeof(T));        // elements per 16-byte copy
-    static constexpr int kRS = 32 + kVec;                    // padded row stride (elements)
-    static constexpr int kPieces = 32 / kVec;                // 16-byte pieces per tile row
-    static constexpr int kStages = sizeof(T) == 8 ? 6 : 5;   // FP32: fits beside the 198 KiB TF32 GEMM CTA
-    static constexpr size_t kSmem = size_t(kStages) * 32 * kRS * sizeof(T);
+// wide_apart_kernel: a warp takes 32 rows x one 128-column block (coalesced
+// tile loads through shared memory; lane = row walks the block in order) and
+// writes, per (block, row):
+//  - the NativeBlocked(128) checksum partials sum_j T(br_j) T(a_j) in the
+//    working type W (checksum.cpp:103-146);
+//  - an error-free cascaded sum (TwoSum: s, c) of the row segment in FP64,
+//    sum |a|, and max / min (stats.cpp:9-32).
+// wide_acombine_kernel (thread per row): checksum partials in block order;
+// the (s, c) pairs merged with TwoSum. With hi = fl(s + c), |s + c - S| <=
+// (K u)^2 sum|x| for the exact row sum S, and the reference's sequential
+// Neumaier sum + comp obeys the same bound — both round to fl(S) unless S lies
+// within 8 (K u)^2 sum|x| of a rounding midpoint. That is checked per row;
+// such rows (and non-finite ones) rerun the reference's loop (counted as
+// slow-stats rows), so the mean is bit-identical in every case.
+__device__ __forceinline__ void two_sum(double a, double b, double& s, double& e) {
+    s = __dadd_rn(a, b);
+    const double bb = __dsub_rn(s, a);
+    e = __dadd_rn(__dsub_rn(a, __dsub_rn(s, bb)), __dsub_rn(b, bb));
+}
+
+template <class W>
+struct APart {  // per (block, row) partial arrays, each [nb][ld]
+    W *p1, *p2;
+    double *s, *c, *sabs, *mx, *mn;
 };
 
-template <int F>
-__global__ void __launch_bounds__(32) wide_rowstats_kernel(const typename Elem<F>::T* __restrict__ A, int64_t M,
-                                                           int64_t K, double* mean, double* vb, double* mx_out,
-                                                           double* mn_out) {
-    using T = typename Elem<F>::T;
-    using Cfg = AsideCfg<T>;
-    constexpr int S = Cfg::kStages, RS = Cfg::kRS, V = Cfg::kVec, P = Cfg::kPieces;
-    extern __shared__ __align__(16) uint8_t as_raw[];
-    T* tiles = reinterpret_cast<T*>(as_raw);
-    const int lane = threadIdx.x & 31;
-    const int64_t r0 = int64_t(blockIdx.x) * 32;
-    const int64_t row = r0 + lane;
-    const int64_t nchunks = (K + 31) / 32;
-    auto fetch = [&](int64_t ch) {
-        if (ch < nchunks) {
-            T* tile = tiles + size_t(ch % S) * 32 * RS;
-#pragma unroll
-            for (int t = 0; t < P; ++t) {
-                const int q = lane + 32 * t, rr = q / P, pc = q % P;
-                const int64_t r = r0 + rr, c = ch * 32 + int64_t(pc) * V;
-                const bool ok = r < M && c < K;
-                asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(smem_u32(tile + rr * RS + pc * V)),
-                             "l"(ok ? A + r * K + c : A), "r"(ok ? 16 : 0)
-                             : "memory");
-            }
-        }
-        asm volatile("cp.async.commit_group;\n" ::: "memory");  // (possibly empty) group per chunk
-    };
-    double s = 0.0, comp = 0.0;
-    T mx = T(-INFINITY), mn = T(INFINITY);
-    auto step = [&](T e) {
-        const double x = double(e);
-        // Neumaier (stats.cpp:12-24), branch-free
-        const double t = __dadd_rn(s, x);
-        const bool big = fabs(s) >= fabs(x);
-        const double hi = big ? s : x, lo = big ? x : s;
-        comp = __dadd_rn(comp, __dadd_rn(__dsub_rn(hi, t), lo));
-        s = t;
-        mx = mx < e ? e : mx;  // NaN-free rows: identical to fmax / fmin
-        mn = e < mn ? e : mn;
-    };
-#pragma unroll
-    for (int q = 0; q < S - 1; ++q) fetch(q);
-    for (int64_t ch = 0; ch < nchunks; ++ch) {
-        asm volatile("cp.async.wait_group %0;\n" ::"n"(S - 2) : "memory");
-        __syncwarp();
-        const T* trow = tiles + size_t(ch % S) * 32 * RS + lane * RS;
-        const int cmax = int(K - ch * 32 < 32 ? K - ch * 32 : 32);
-        if (cmax == 32) {
-#pragma unroll
-            for (int v = 0; v < P; ++v) {
-                if constexpr (sizeof(T) == 4) {
-                    const float4 q = *reinterpret_cast<const float4*>(trow + v * 4);
-                    step(q.x);
-                    step(q.y);
-                    step(q.z);
-                    step(q.w);
-                } else {
-                    const double2 q = *reinterpret_cast<const double2*>(trow + v * 2);
-                    step(q.x);
-                    step(q.y);
-                }
-            }
-        } else {
-            for (int jj = 0; jj < cmax; ++jj) step(trow[jj]);
-        }
-        __syncwarp();
-        fetch(ch + S - 1);  // refills the slot consumed one iteration ago
-    }
-    asm volatile("cp.async.wait_group 0;\n" ::: "memory");
-    if (row < M) {
-        Neu ns;
-        ns.s = s;
-        ns.c = comp;
-        double m, v;
-        stats_finish(ns, double(mx), double(mn), K, &m, &v);
-        mean[row] = m;
-        vb[row] = v;
-        mx_out[row] = double(mx);
-        mn_out[row] = double(mn);
-    }
+template <class W>
+__host__ __device__ inline APart<W> apart_view(void* base, int64_t nb, int64_t ld) {
+    const size_t n = size_t(nb) * size_t(ld);
+    double* d = static_cast<double*>(base);
+    APart<W> a;
+    a.p1 = reinterpret_cast<W*>(d);
+    a.p2 = reinterpret_cast<W*>(d + n);
+    a.s = d + 2 * n;
+    a.c = d + 3 * n;
+    a.sabs = d + 4 * n;
+    a.mx = d + 5 * n;
+    a.mn = d + 6 * n;
+    return a;
 }
 
 template <int F, class W>
-__global__ void __launch_bounds__(128) wide_cpart_kernel(const typename Elem<F>::T* __restrict__ A, int64_t M,
+__global__ void __launch_bounds__(128) wide_apart_kernel(const typename Elem<F>::T* __restrict__ A, int64_t M,
                                                          int64_t K, const double* __restrict__ br1,
-                                                         const double* __restrict__ br2, W* cp1, W* cp2,
-                                                         int64_t ld) {
+                                                         const double* __restrict__ br2, APart<W> out, int64_t ld) {
     using T = typename Elem<F>::T;
     __shared__ T tile[4][32][33];
     const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int64_t r0 = (int64_t(blockIdx.x) * 4 + w) * 32, b = blockIdx.y;
     if (r0 >= M) return;
     W p1 = W(0), p2 = W(0);
-    for (int c = 0; c < 4; ++c) {
-        const int64_t col0 = b * 128 + c * 32;
+    double s = 0.0, c = 0.0, sabs = 0.0;
+    T mx = T(-INFINITY), mn = T(INFINITY);
+    for (int q = 0; q < 4; ++q) {
+        const int64_t col0 = b * 128 + q * 32;
         if (col0 >= K) break;
         const int64_t col = col0 + lane;
 #pragma unroll 8
@@ -424,29 +361,80 @@ __global__ void __launch_bounds__(128) wide_cpart_kernel(const typename Elem<F>:
         __syncwarp();
         const int cmax = int(K - col0 < 32 ? K - col0 : 32);
         for (int jj = 0; jj < cmax; ++jj) {
-            const W x = W(tile[w][lane][jj]);
+            const T e = tile[w][lane][jj];
+            const W x = W(e);
             p1 = radd(p1, rmul(__shfl_sync(0xffffffffu, w1l, jj), x));
             p2 = radd(p2, rmul(__shfl_sync(0xffffffffu, w2l, jj), x));
+            const double xd = double(e);
+            double t, err;
+            two_sum(s, xd, t, err);
+            s = t;
+            c = __dadd_rn(c, err);
+            sabs = __dadd_rn(sabs, fabs(xd));
+            mx = mx < e ? e : mx;  // NaN-free rows: identical to fmax / fmin
+            mn = e < mn ? e : mn;
         }
         __syncwarp();
     }
     const int64_t row = r0 + lane;
     if (row < M) {
-        cp1[size_t(b) * size_t(ld) + size_t(row)] = p1;
-        cp2[size_t(b) * size_t(ld) + size_t(row)] = p2;
+        const size_t o = size_t(b) * size_t(ld) + size_t(row);
+        out.p1[o] = p1;
+        out.p2[o] = p2;
+        out.s[o] = s;
+        out.c[o] = c;
+        out.sabs[o] = sabs;
+        out.mx[o] = double(mx);
+        out.mn[o] = double(mn);
     }
 }
 
-template <class W>
-__global__ void wide_ccombine_kernel(int64_t M, int64_t nb, const W* cp1, const W* cp2, int64_t ld, int qfmt,
-                                     double* cr1, double* cr2) {
+template <int F, class W>
+__global__ void __launch_bounds__(256) wide_acombine_kernel(const typename Elem<F>::T* __restrict__ A, int64_t M,
+                                                            int64_t K, APart<W> in, int64_t ld, int qfmt, double* mean,
+                                                            double* vb, double* mx_out, double* mn_out, double* cr1,
+                                                            double* cr2, int64_t* counts) {
     const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
     if (i >= M) return;
+    const int64_t nb = (K + 127) / 128;
     W t1 = W(0), t2 = W(0);
+    double s = 0.0, c = 0.0, sabs = 0.0, mx = -INFINITY, mn = INFINITY;
     for (int64_t b = 0; b < nb; ++b) {
-        t1 = radd(t1, cp1[size_t(b) * size_t(ld) + size_t(i)]);
-        t2 = radd(t2, cp2[size_t(b) * size_t(ld) + size_t(i)]);
+        const size_t o = size_t(b) * size_t(ld) + size_t(i);
+        t1 = radd(t1, in.p1[o]);
+        t2 = radd(t2, in.p2[o]);
+        double t, err;
+        two_sum(s, in.s[o], t, err);
+        s = t;
+        c = __dadd_rn(__dadd_rn(c, in.c[o]), err);
+        sabs = __dadd_rn(sabs, in.sabs[o]);
+        mx = mx < in.mx[o] ? in.mx[o] : mx;
+        mn = in.mn[o] < mn ? in.mn[o] : mn;
     }
+    double hi, lo;
+    two_sum(s, c, hi, lo);
+    const double ku = double(K) * 1.1102230246251565e-16;  // K u, u = 2^-53
+    const double margin = 8.0 * ku * ku * sabs * 1.0000001;
+    bool safe = isfinite(hi) && isfinite(lo) && isfinite(margin);
+    if (safe) {
+        // the rounding midpoint on lo's side of hi
+        const double nb2 = nextafter(hi, (lo > 0.0) ? INFINITY : -INFINITY);
+        safe = fabs(lo) + margin < fabs(__dsub_rn(nb2, hi)) * 0.5;
+    }
+    Neu ns;
+    if (safe) {
+        ns.s = hi;  // = fl(sum + comp) of the reference
+    } else {
+        if (counts) atomicAdd(reinterpret_cast<unsigned long long*>(counts + VABFT_COUNT_SLOW_STATS), 1ull);
+        const typename Elem<F>::T* arow = A + i * K;
+        for (int64_t j = 0; j < K; ++j) ns.add(double(arow[j]));  // the reference's loop (stats.cpp:12-24)
+    }
+    double m, v;
+    stats_finish(ns, mx, mn, K, &m, &v);
+    mean[i] = m;
+    vb[i] = v;
+    mx_out[i] = mx;
+    mn_out[i] = mn;
     double c1 = double(t1), c2 = double(t2);
     if (qfmt == VABFT_FP32) {  // offline FP32: the checksum rounded to the input format (a no-op for W = float)
         c1 = double(float(c1));
@@ -499,33 +487,28 @@ void launch_wide_tail(const WideTail& t, cudaStream_t stream) {
 }
 
 void launch_wide_aside(int fmt, int64_t M, int64_t K, const void* A, const double* br1, const double* br2, int qfmt,
-                       double* mean, double* vb, double* mx, double* mn, double* cr1, double* cr2, void* cpart,
-                       int64_t ld, cudaStream_t stream) {
-    const unsigned grid_rows = unsigned((M + 31) / 32);
+                       double* mean, double* vb, double* mx, double* mn, double* cr1, double* cr2, void* apart,
+                       int64_t ld, int64_t* counts, cudaStream_t stream) {
     const int64_t nb = (K + 127) / 128;
-    const dim3 grid_cp(unsigned((M + 127) / 128), unsigned(nb));
-    const unsigned grid_cc = unsigned((M + 255) / 256);
+    const dim3 grid_p(unsigned((M + 127) / 128), unsigned(nb));
+    const unsigned grid_c = unsigned((M + 255) / 256);
     // SMs running these small CTAs must keep the maximum shared-memory
     // carveout, or the GEMM's CTAs cannot co-reside and the overlap is lost
-    auto prep = [](const void* kern, size_t smem) {
-        check_cuda(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)),
-                   "attr(wide aside)");
-        check_cuda(cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, 100),
-                   "carveout(wide aside)");
-    };
     auto run = [&](auto tag, auto wtag) {
         using T = decltype(tag);
         using W = decltype(wtag);
         constexpr int F = sizeof(T) == 8 ? VABFT_FP64 : VABFT_FP32;
-        static const bool once = (prep(reinterpret_cast<const void*>(wide_rowstats_kernel<F>), AsideCfg<T>::kSmem),
-                                  prep(reinterpret_cast<const void*>(wide_cpart_kernel<F, W>), 0), true);
+        static const bool once = [] {
+            check_cuda(cudaFuncSetAttribute(wide_apart_kernel<F, W>, cudaFuncAttributePreferredSharedMemoryCarveout,
+                                            100),
+                       "carveout(wide aside)");
+            return true;
+        }();
         (void)once;
-        const T* a = static_cast<const T*>(A);
-        W* cp1 = static_cast<W*>(cpart);
-        W* cp2 = cp1 + size_t(nb) * size_t(ld);
-        wide_rowstats_kernel<F><<<grid_rows, 32, AsideCfg<T>::kSmem, stream>>>(a, M, K, mean, vb, mx, mn);
-        wide_cpart_kernel<F, W><<<grid_cp, 128, 0, stream>>>(a, M, K, br1, br2, cp1, cp2, ld);
-        wide_ccombine_kernel<W><<<grid_cc, 256, 0, stream>>>(M, nb, cp1, cp2, ld, qfmt, cr1, cr2);
+        const APart<W> part = apart_view<W>(apart, nb, ld);
+        wide_apart_kernel<F, W><<<grid_p, 128, 0, stream>>>(static_cast<const T*>(A), M, K, br1, br2, part, ld);
+        wide_acombine_kernel<F, W><<<grid_c, 256, 0, stream>>>(static_cast<const T*>(A), M, K, part, ld, qfmt, mean,
+                                                               vb, mx, mn, cr1, cr2, counts);
     };
     if (fmt == VABFT_FP64) run(double{}, double{});
     else if (fmt == VABFT_FP32) run(float{}, float{});

@@ -258,3 +258,26 @@ def test_fp32_plain_gemm_matches_fp64(torch_cuda):
         ref = a.double() @ b.double()
         bound = (2 * (k + 1) * 2.0**-23 + 2.0**-20) * (a.double().abs() @ b.double().abs())
         assert bool(((c.double() - ref).abs() <= bound).all())
+
+
+def test_wide_rowstats_midpoint_fallback(torch_cuda, port):
+    """Rows whose exact sum sits on a rounding midpoint take the reference's
+    sequential Neumaier loop; every mean (hence T) stays bit-identical."""
+    torch = torch_cuda
+    from paper_2602_08043_b200.fused import FusedAbftGemm
+    m, k, n = 32, 64, 64
+    rng = np.random.default_rng(7)
+    A = rng.standard_normal((m, k))
+    A[0, :] = 0.0
+    A[0, 0], A[0, 1] = 1.0, 2.0**-53          # 1 + 2^-53: exactly between 1 and 1 + 2^-52
+    A[1, :] = 0.0
+    A[1, 0], A[1, 5], A[1, 9] = 3.0, 2.0**-52, 2.0**-52 * 0.5
+    A[2, :3] = [1e16, 1.0, -1e16]              # cancellation
+    B = rng.standard_normal((k, n))
+    counts = torch.zeros(6, dtype=torch.int64, device="cuda")
+    g = FusedAbftGemm(torch.from_numpy(B).cuda(), e_max=4e-15)
+    r = g(torch.from_numpy(A).cuda(), counts=counts)
+    torch.cuda.synchronize()
+    T_ref, _ = port.vabft_thresholds(A, B, 4e-15, fmt="fp64")
+    assert same(r.T.cpu().numpy(), T_ref)
+    assert int(counts[4].item()) >= 1  # the midpoint row went the sequential way

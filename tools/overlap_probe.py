@@ -1,0 +1,22 @@
+"""Kernel timeline (CUPTI via torch.profiler) of one wide-format fused call:
+shows whether the side-stream A pass overlaps the GEMM."""
+import os, sys
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import torch
+from torch.profiler import profile, ProfilerActivity
+from paper_2602_08043_b200.fused import FusedAbftGemm
+n = int(sys.argv[1]) if len(sys.argv) > 1 else 4096
+dt = {"fp32": torch.float32, "fp64": torch.float64}[sys.argv[2] if len(sys.argv) > 2 else "fp32"]
+passes = int(sys.argv[3]) if len(sys.argv) > 3 else 1
+a = torch.randn(n, n, device="cuda", dtype=dt); b = torch.randn(n, n, device="cuda", dtype=dt)
+g = FusedAbftGemm(b, tf32_passes=passes, e_max=1e-2)
+for _ in range(3):
+    g(a)
+torch.cuda.synchronize()
+with profile(activities=[ProfilerActivity.CUDA]) as prof:
+    g(a)
+    torch.cuda.synchronize()
+evs = [e for e in prof.events() if e.device_type == torch.autograd.DeviceType.CUDA]
+t0 = min(e.time_range.start for e in evs)
+for e in sorted(evs, key=lambda e: e.time_range.start):
+    print(f"{e.time_range.start - t0:9.1f} {e.time_range.end - t0:9.1f}  {e.name[:70]}")
