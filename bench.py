@@ -161,6 +161,57 @@ def run_reference_arm(args, cfg):
     print(json.dumps(line), flush=True)
 
 
+# ------------------------------------------------ wide formats (secondary)
+def measure_formats(dev, flush, torch, n=4096, steps=20, warmup=3):
+    """The other precisions of the fused path at n^3, N(0,1) operands, L2
+    flushed between steps, CUDA events on the launching stream: FP32 on
+    tcgen05 (3xTF32), FP32 with one TF32 pass, FP64 on the SIMT DFMA kernel.
+    Plain = the same GEMM kernel with the ABFT epilogue off (stage mask 2|8;
+    the 3xTF32 plain step includes the activation split, as the fused one)."""
+    from paper_2602_08043_b200.fused import FusedAbftGemm
+    out = {}
+    stream = torch.cuda.current_stream()
+    for name, dt, passes in (("fp32_3xtf32", torch.float32, 3), ("fp32_1xtf32", torch.float32, 1),
+                             ("fp64_dfma", torch.float64, 3)):
+        nn = n if dt == torch.float32 else n // 2  # FP64: 2048^3 keeps the run short
+        A = torch.randn(nn, nn, device=dev, dtype=dt)
+        B = torch.randn(nn, nn, device=dev, dtype=dt)
+        g = FusedAbftGemm(B, tf32_passes=passes)
+        Cc = torch.empty(nn, nn, device=dev, dtype=dt)
+        counts = torch.zeros(6, dtype=torch.int64, device=dev)
+
+        def run(stages):
+            # one call = one CUDA graph (the side-stream fork/join is captured
+            # with it), as for the BF16 step: device time, not host launch time
+            for _ in range(warmup):
+                flush.zero_()
+                g(A, out=Cc, counts=counts, stages=stages)
+            torch.cuda.synchronize()
+            gr = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(gr):
+                g(A, out=Cc, counts=counts, stages=stages)
+            ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(steps)]
+            torch.cuda.synchronize()
+            for s, e in ev:
+                flush.zero_()
+                s.record(stream)
+                gr.replay()
+                e.record(stream)
+            torch.cuda.synchronize()
+            return sum(s.elapsed_time(e) for s, e in ev) / steps
+        ms_f = min(run(0), run(0))
+        ms_p = min(run(2 | 8), run(2 | 8))
+        counts.zero_()
+        g(A, out=Cc, counts=counts)
+        torch.cuda.synchronize()
+        fl = 2.0 * nn ** 3
+        out[name] = {"shape": [nn, nn, nn], "fused_tflops": fl / ms_f / 1e9, "plain_tflops": fl / ms_p / 1e9,
+                     "abft_overhead_pct": 100.0 * (ms_f / ms_p - 1.0), "e_max": g.opts.e_max,
+                     "fpr": {"false_positive_rows": int(counts[1].item()), "rows_checked": int(counts[0].item())}}
+        g.close()
+    return out
+
+
 # ---------------------------------------------------------------- GPU arm
 def run_ours(args, cfg):
     import torch
@@ -319,6 +370,10 @@ def run_ours(args, cfg):
     h2d = sum(A.numel() * 2 + B.numel() * 2 for A, B in zip(As, Bs))
     d2h = sum(Cc.numel() * 2 for Cc in Cs) + hcounts.numel() * 8
 
+    formats = None
+    if world == 1 and not args.no_formats:
+        formats = measure_formats(dev, flush, torch)
+
     value = flops_rank * world / (ms_fused / args.steps / 1e3) / 1e12
     plain_tf = flops_rank * world / (ms_plain / args.steps / 1e3) / 1e12
     kernel_tf = flops_rank / (ms_kernel / args.steps / 1e3) / 1e12
@@ -371,6 +426,7 @@ def run_ours(args, cfg):
                 "path": "pinned host A,B -> H2D -> B-side update + fused GEMM -> D2H C + counts"},
         "gpu_launches": args.steps * len(gemms),  # one fused kernel per GEMM
         "clocks": clocks,
+        "formats": formats,
     }
     print(json.dumps(line), flush=True)
     if world > 1:
@@ -387,6 +443,7 @@ def main():
     ap.add_argument("--mode", default="online", choices=["online", "offline"])
     ap.add_argument("--ref-rows", type=int, default=8, help="rows per reference call (CPU sample)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-formats", action="store_true", help="skip the FP32 / TF32 / FP64 fused-path lines")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3

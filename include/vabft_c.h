@@ -253,8 +253,9 @@ typedef struct vabft_fused_opts {
     const int32_t* fault_bit;
     const int32_t* fault_dir;
     vabft_fault_record* fault_records; /* device, length M, may be NULL */
-    /* Stage mask for profiling (0 = all): 1 statistics pass, 2 tcgen05 GEMM
-     * with the ABFT epilogue, 4 verify tail. */
+    /* Stage mask for profiling (0 = all): 1 statistics pass, 2 GEMM with the
+     * ABFT epilogue, 4 verify tail; FP32 / FP64 handles: 8 with 2 runs the
+     * same GEMM kernel with the ABFT epilogue off (overhead baseline). */
     int32_t stages;
     /* Where the planned faults land (FaultTarget, faults.hpp:15):
      *  0 OutputC: fault_col/bit/dir per row as above (accumulator online,

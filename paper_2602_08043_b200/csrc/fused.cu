@@ -43,11 +43,8 @@ struct vabft_bside {
     unsigned int* gbar;  // grid-barrier state of the fused kernel (inside storage)
     const void* ws_ready = nullptr;  // workspace whose per-row atomics hold their identities
     size_t ws_ready_bytes = 0;
-    // wide formats (FP32 / FP64): B r1 / B r2 in the working type (held as
-    // doubles), and the side stream the A-side pass runs on, overlapping the GEMM
+    // wide formats (FP32 / FP64): B r1 / B r2 in the working type (held as doubles)
     double* brd = nullptr;  // [2][K]
-    cudaStream_t side = nullptr;
-    cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
     // FP32 (3xTF32): the weight split once into hi / lo parts, transposed
     // ([2][N][K], K-major for kind::tf32), and
     // the activation's split buffers [2][M][K], grown on demand
@@ -170,9 +167,9 @@ void wide_bside(vabft_bside* h, cudaStream_t s) {
                      h->n, s);
 }
 
-// vabft_fused_gemm for FP32 / FP64: the A-side pass (row statistics and
-// A (B r), on the handle's side stream) overlaps the GEMM; the verify tail
-// joins both.
+// vabft_fused_gemm for FP32 / FP64: the GEMM with the ABFT epilogue, the
+// A-side pass (row statistics and A (B r) block partials, one read of A) and
+// the verify tail, stream-ordered.
 void wide_fused(const vabft_fused_opts* o, vabft_bside* h, int64_t m, const void* A, void* C, double* T,
                 const vabft_verdicts& verdicts, int64_t* counts, void* workspace, cudaStream_t s) {
     if (o->tf32_passes != 0 && o->tf32_passes != 1 && o->tf32_passes != 3)
@@ -182,20 +179,9 @@ void wide_fused(const vabft_fused_opts* o, vabft_bside* h, int64_t m, const void
     const WideWs ws = carve_wide(workspace, m, n, k);
     const int stages = o->stages == 0 ? 7 : o->stages;
     const bool tail = (stages & 4) != 0;
-    if (tail) {
-        check_cuda(cudaEventRecord(h->ev_fork, s), "event");
-        check_cuda(cudaStreamWaitEvent(h->side, h->ev_fork, 0), "wait");
-        launch_wide_aside(h->fmt, m, k, A, h->brd, h->brd + k, o->mode == VABFT_OFFLINE ? h->fmt : -1, ws.mean,
-                          ws.vb, ws.mx, ws.mn, ws.cr1, ws.cr2, ws.cpart, ws.ld, counts, h->side);
-        if (o->threshold_method == 2) {
-            check_cuda(cudaMemsetAsync(ws.max_abs_a, 0, sizeof(double), h->side), "memset");
-            launch_max_abs_rows(m, ws.mx, ws.mn, ws.max_abs_a, h->side);
-        }
-        check_cuda(cudaEventRecord(h->ev_join, h->side), "event");
-    }
     if (stages & 2) {
         WideEpilogue epi;
-        epi.abft = 1;
+        epi.abft = (stages & 8) ? 0 : 1;  // bit 8: the same GEMM with the ABFT epilogue off (overhead baseline)
         epi.part1 = ws.part1;
         epi.part2 = ws.part2;
         epi.ld = ws.ld;
@@ -227,7 +213,15 @@ void wide_fused(const vabft_fused_opts* o, vabft_bside* h, int64_t m, const void
         }
     }
     if (!tail) return;
-    check_cuda(cudaStreamWaitEvent(s, h->ev_join, 0), "wait");
+    // A-ABFT computed y needs the global max|A| first: combine in a separate
+    // pass; otherwise the tail combines the A partials itself
+    const bool global_y = o->threshold_method == 2;
+    launch_wide_aside(h->fmt, m, k, A, h->brd, h->brd + k, o->mode == VABFT_OFFLINE ? h->fmt : -1, ws.mean, ws.vb,
+                      ws.mx, ws.mn, ws.cr1, ws.cr2, ws.cpart, ws.ld, counts, global_y, s);
+    if (global_y) {
+        check_cuda(cudaMemsetAsync(ws.max_abs_a, 0, sizeof(double), s), "memset");
+        launch_max_abs_rows(m, ws.mx, ws.mn, ws.max_abs_a, s);
+    }
     WideTail t{};
     t.M = m;
     t.N = n;
@@ -255,6 +249,11 @@ void wide_fused(const vabft_fused_opts* o, vabft_bside* h, int64_t m, const void
     t.counts = counts;
     t.C = C;
     t.correct = o->correct;
+    if (!global_y) {
+        t.apart = ws.cpart;
+        t.A = A;
+        t.qfmt = o->mode == VABFT_OFFLINE ? h->fmt : -1;
+    }
     launch_wide_tail(t, s);
 }
 
@@ -302,9 +301,6 @@ extern "C" vabft_status vabft_bside_create(int32_t format, int32_t mode, int64_t
         check_cuda(cudaMemset(h->buf.done, 0, sizeof(unsigned int)), "memset(bside counter)");
         if (is_wide(format)) {
             check_cuda(cudaMalloc(&h->brd, 2 * sizeof(double) * K), "cudaMalloc(bside B r)");
-            check_cuda(cudaStreamCreateWithFlags(&h->side, cudaStreamNonBlocking), "stream");
-            check_cuda(cudaEventCreateWithFlags(&h->ev_fork, cudaEventDisableTiming), "event");
-            check_cuda(cudaEventCreateWithFlags(&h->ev_join, cudaEventDisableTiming), "event");
             if (format == VABFT_FP32) {
                 if ((k * n) % 4 != 0) fail(VABFT_UNSUPPORTED, "FP32 weights: K x N must be a multiple of 4");
                 check_cuda(cudaMalloc(&h->b_split, 2 * sizeof(float) * K * size_t(n)), "cudaMalloc(B split)");
@@ -336,9 +332,6 @@ extern "C" vabft_status vabft_bside_destroy(vabft_bside_t h) {
         if (h->brd) cudaFree(h->brd);
         if (h->b_split) cudaFree(h->b_split);
         if (h->a_split) cudaFree(h->a_split);
-        if (h->ev_fork) cudaEventDestroy(h->ev_fork);
-        if (h->ev_join) cudaEventDestroy(h->ev_join);
-        if (h->side) cudaStreamDestroy(h->side);
         delete h;
     });
 }

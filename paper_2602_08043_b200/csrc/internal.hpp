@@ -149,6 +149,10 @@ struct WideTail {
     int64_t* counts;
     void* C;
     int correct;
+    // A-side partials to combine in the tail (nullptr: mean/vb/cr1/cr2 given)
+    const void* apart = nullptr;
+    const void* A = nullptr;
+    int qfmt = -1;
 };
 void launch_wide_tail(const WideTail& t, cudaStream_t stream);
 // A side: row statistics and the blocked:128 row checksums A (B r); apart is
@@ -156,7 +160,7 @@ void launch_wide_tail(const WideTail& t, cudaStream_t stream);
 // doubles
 void launch_wide_aside(int fmt, int64_t M, int64_t K, const void* A, const double* br1, const double* br2, int qfmt,
                        double* mean, double* vb, double* mx, double* mn, double* cr1, double* cr2, void* apart,
-                       int64_t ld, int64_t* counts, cudaStream_t stream);
+                       int64_t ld, int64_t* counts, bool combine, cudaStream_t stream);
 void launch_max_abs_rows(int64_t m, const double* mx, const double* mn, double* out, cudaStream_t stream);
 
 }  // namespace vabft_dev

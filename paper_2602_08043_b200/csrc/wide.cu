@@ -22,6 +22,9 @@
 // conflict-free 16-byte access; a 4-stage cp.async ring (A rows padded to 18
 // doubles). Per k pair: 16 LDS.128 for 128 DFMA — the FP64 pipe (64 DFMA /
 // clk / SM) is the bound, not shared memory.
+#include <algorithm>
+#include <type_traits>
+
 #include "devcommon.cuh"
 #include "internal.hpp"
 #include "numerics.cuh"
@@ -206,94 +209,10 @@ __global__ void __launch_bounds__(kDThreads, 1) dgemm_kernel(const __grid_consta
     }
 }
 
-template <class W>
-__device__ __forceinline__ W load_part(const void* p, size_t o) {
-    return static_cast<const W*>(p)[o];
-}
-
-// One thread per row.
-template <class W>
-__global__ void __launch_bounds__(256) wide_tail_kernel(const WideTail a) {
-    const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
-    const int lane = threadIdx.x & 31;
-    const bool valid = i < a.M;
-    bool det = false, located = false, isnan_row = false, corrected = false;
-    if (valid) {
-        W r1 = W(0), r2 = W(0);
-        for (int64_t b = 0; b < a.nblk; ++b) {
-            const size_t o = size_t(b) * size_t(a.ld) + size_t(i);
-            r1 = radd(r1, load_part<W>(a.part1, o));
-            r2 = radd(r2, load_part<W>(a.part2, o));
-        }
-        double t;
-        if (a.method == 0) {
-            t = vabft_threshold_total(a.mean[i], a.vb[i], a.bsum[0], a.bsum[1], a.bsum[2], a.N, a.e_max, a.c_sigma);
-        } else {
-            const double y = a.method == 1 ? a.aabft_fixed_y : __dmul_rn(*a.max_abs_a, a.bsum[3]);
-            t = aabft_total(a.K, a.aabft_t, y, a.aabft_conf);
-        }
-        if (a.T_out) a.T_out[i] = t;
-        const double c1 = a.cr1[i], c2 = a.cr2[i];
-        const double d1 = __dsub_rn(double(r1), c1);
-        const double d2 = __dsub_rn(double(r2), c2);
-        int64_t loc = -1;
-        double res = 0.0;
-        if (isnan(d1) || isnan(d2)) {
-            det = true;
-            isnan_row = true;
-        } else {
-            det = fabs(d1) > t;
-            if (det && fabs(d1) > __dmul_rn(a.floor_scale, t)) {
-                int64_t j;
-                double rr;
-                if (localize_dev(d1, d2, a.N, &j, &rr)) {
-                    loc = j;
-                    res = rr;
-                    located = true;
-                    // correct (detect.cpp:57-64): C[i][j] = quantize(C[i][j] - diff1)
-                    if (a.correct && a.C != nullptr && rr < 0.4) {
-                        if (a.fmt == VABFT_FP64) {
-                            double* cij = static_cast<double*>(a.C) + i * a.N + j;
-                            *cij = __dsub_rn(*cij, d1);
-                        } else {
-                            float* cij = static_cast<float*>(a.C) + i * a.N + j;
-                            const float q = __double2float_rn(__dsub_rn(double(*cij), d1));
-                            *cij = isinf(q) ? copysignf(3.40282346638528859812e+38f, q) : q;
-                        }
-                        corrected = true;
-                    }
-                }
-            }
-        }
-        if (a.v.diff1) a.v.diff1[i] = d1;
-        if (a.v.diff2) a.v.diff2[i] = d2;
-        if (a.v.detected) a.v.detected[i] = det ? 1 : 0;
-        if (a.v.location) a.v.location[i] = loc;
-        if (a.v.residual) a.v.residual[i] = res;
-        if (a.v.row_check1) a.v.row_check1[i] = c1;
-        if (a.v.row_check2) a.v.row_check2[i] = c2;
-    }
-    if (a.counts) {
-        const unsigned mv = __ballot_sync(0xffffffffu, valid);
-        const unsigned md = __ballot_sync(0xffffffffu, det);
-        const unsigned ml = __ballot_sync(0xffffffffu, located);
-        const unsigned mn = __ballot_sync(0xffffffffu, isnan_row);
-        const unsigned mc = __ballot_sync(0xffffffffu, corrected);
-        if (lane == 0) {
-            auto add = [&](int slot, unsigned mask) {
-                if (mask) atomicAdd(reinterpret_cast<unsigned long long*>(a.counts + slot), __popc(mask));
-            };
-            add(VABFT_COUNT_ROWS, mv);
-            add(VABFT_COUNT_DETECTED, md);
-            add(VABFT_COUNT_LOCATED, ml);
-            add(VABFT_COUNT_NAN, mn);
-            add(VABFT_COUNT_CORRECTED, mc);
-        }
-    }
-}
-
-// A side of the wide fused path: ONE pass over A on the side stream, then a
-// per-row combine.
+// A side of the wide fused path: ONE pass over A, then a per-row combine
+// (inside the verify tail). It runs after the GEMM on the same stream: run
+// beside the GEMM on a second stream it was starved of memory bandwidth and
+// finished late (measured), so the serial order is the faster one.
 //
 // wide_apart_kernel: a warp takes 32 rows x one 128-column block (coalesced
 // tile loads through shared memory; lane = row walks the block in order) and
@@ -313,6 +232,20 @@ __device__ __forceinline__ void two_sum(double a, double b, double& s, double& e
     s = __dadd_rn(a, b);
     const double bb = __dsub_rn(s, a);
     e = __dadd_rn(__dsub_rn(a, __dsub_rn(s, bb)), __dsub_rn(b, bb));
+}
+
+// hi = fl(s + c) equals the reference's fl(sum + comp) unless the exact sum
+// lies within 8 (K u)^2 sum|x| of a rounding midpoint (see above).
+__device__ __forceinline__ bool exact_sum_safe(double s, double c, double sabs, int64_t K, double* hi_out) {
+    double hi, lo;
+    two_sum(s, c, hi, lo);
+    const double ku = double(K) * 1.1102230246251565e-16;  // K u, u = 2^-53
+    const double margin = 8.0 * ku * ku * sabs * 1.0000001;
+    if (!(isfinite(hi) && isfinite(lo) && isfinite(margin))) return false;
+    const double nb = nextafter(hi, (lo > 0.0) ? INFINITY : -INFINITY);  // the midpoint on lo's side
+    if (!(fabs(lo) + margin < fabs(__dsub_rn(nb, hi)) * 0.5)) return false;
+    *hi_out = hi;
+    return true;
 }
 
 template <class W>
@@ -352,12 +285,15 @@ __global__ void __launch_bounds__(128) wide_apart_kernel(const typename Elem<F>:
         const int64_t col0 = b * 128 + q * 32;
         if (col0 >= K) break;
         const int64_t col = col0 + lane;
-#pragma unroll 8
+        T v[32];  // all 32 row loads in flight before the first smem store
+#pragma unroll
         for (int rr = 0; rr < 32; ++rr) {
             const int64_t r = r0 + rr;
-            tile[w][rr][lane] = (r < M && col < K) ? A[r * K + col] : T(0);
+            v[rr] = (r < M && col < K) ? __ldcs(A + r * K + col) : T(0);
         }
         const W w1l = col < K ? W(br1[col]) : W(0), w2l = col < K ? W(br2[col]) : W(0);
+#pragma unroll
+        for (int rr = 0; rr < 32; ++rr) tile[w][rr][lane] = v[rr];
         __syncwarp();
         const int cmax = int(K - col0 < 32 ? K - col0 : 32);
         for (int jj = 0; jj < cmax; ++jj) {
@@ -389,16 +325,18 @@ __global__ void __launch_bounds__(128) wide_apart_kernel(const typename Elem<F>:
     }
 }
 
+// Per-row combine of the A-side partials: stats (mean, var_bound, max, min)
+// and the row checksums; see the comment above.
 template <int F, class W>
-__global__ void __launch_bounds__(256) wide_acombine_kernel(const typename Elem<F>::T* __restrict__ A, int64_t M,
-                                                            int64_t K, APart<W> in, int64_t ld, int qfmt, double* mean,
-                                                            double* vb, double* mx_out, double* mn_out, double* cr1,
-                                                            double* cr2, int64_t* counts) {
-    const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
-    if (i >= M) return;
+__device__ __forceinline__ void acombine_row(const typename Elem<F>::T* __restrict__ A, int64_t K, const APart<W>& in,
+                                             int64_t ld, int qfmt, int64_t i, int64_t* counts, double& mean,
+                                             double& vb, double& mx, double& mn, double& c1, double& c2) {
     const int64_t nb = (K + 127) / 128;
     W t1 = W(0), t2 = W(0);
-    double s = 0.0, c = 0.0, sabs = 0.0, mx = -INFINITY, mn = INFINITY;
+    double s = 0.0, c = 0.0, sabs = 0.0;
+    mx = -INFINITY;
+    mn = INFINITY;
+#pragma unroll 4
     for (int64_t b = 0; b < nb; ++b) {
         const size_t o = size_t(b) * size_t(ld) + size_t(i);
         t1 = radd(t1, in.p1[o]);
@@ -411,37 +349,200 @@ __global__ void __launch_bounds__(256) wide_acombine_kernel(const typename Elem<
         mx = mx < in.mx[o] ? in.mx[o] : mx;
         mn = in.mn[o] < mn ? in.mn[o] : mn;
     }
-    double hi, lo;
-    two_sum(s, c, hi, lo);
-    const double ku = double(K) * 1.1102230246251565e-16;  // K u, u = 2^-53
-    const double margin = 8.0 * ku * ku * sabs * 1.0000001;
-    bool safe = isfinite(hi) && isfinite(lo) && isfinite(margin);
-    if (safe) {
-        // the rounding midpoint on lo's side of hi
-        const double nb2 = nextafter(hi, (lo > 0.0) ? INFINITY : -INFINITY);
-        safe = fabs(lo) + margin < fabs(__dsub_rn(nb2, hi)) * 0.5;
-    }
     Neu ns;
-    if (safe) {
-        ns.s = hi;  // = fl(sum + comp) of the reference
+    if (exact_sum_safe(s, c, sabs, K, &ns.s)) {
+        // ns.s = fl(sum + comp) of the reference
     } else {
         if (counts) atomicAdd(reinterpret_cast<unsigned long long*>(counts + VABFT_COUNT_SLOW_STATS), 1ull);
         const typename Elem<F>::T* arow = A + i * K;
         for (int64_t j = 0; j < K; ++j) ns.add(double(arow[j]));  // the reference's loop (stats.cpp:12-24)
     }
-    double m, v;
-    stats_finish(ns, mx, mn, K, &m, &v);
-    mean[i] = m;
-    vb[i] = v;
-    mx_out[i] = mx;
-    mn_out[i] = mn;
-    double c1 = double(t1), c2 = double(t2);
+    stats_finish(ns, mx, mn, K, &mean, &vb);
+    c1 = double(t1);
+    c2 = double(t2);
     if (qfmt == VABFT_FP32) {  // offline FP32: the checksum rounded to the input format (a no-op for W = float)
         c1 = double(float(c1));
         c2 = double(float(c2));
     }
+}
+
+template <int F, class W>
+__global__ void __launch_bounds__(256) wide_acombine_kernel(const typename Elem<F>::T* __restrict__ A, int64_t M,
+                                                            int64_t K, APart<W> in, int64_t ld, int qfmt, double* mean,
+                                                            double* vb, double* mx_out, double* mn_out, double* cr1,
+                                                            double* cr2, int64_t* counts) {
+    const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i >= M) return;
+    double m, v, mx, mn, c1, c2;
+    acombine_row<F, W>(A, K, in, ld, qfmt, i, counts, m, v, mx, mn, c1, c2);
+    mean[i] = m;
+    vb[i] = v;
+    mx_out[i] = mx;
+    mn_out[i] = mn;
     cr1[i] = c1;
     cr2[i] = c2;
+}
+
+template <class W>
+__device__ __forceinline__ W load_part(const void* p, size_t o) {
+    return static_cast<const W*>(p)[o];
+}
+
+// Verify tail, a warp per row: the C-row partials (blocked:128 order) and,
+// with a.apart set (threshold methods without a global dependency), the
+// A-side partials are combined across the lanes (lane = 128-column block,
+// ordered sums through shuffles, TwoSum merges in a butterfly); lane 0 then
+// evaluates the threshold, D1 / D2, the strict compare, NaN rule,
+// localization and the optional correction. Counters are aggregated per CTA.
+template <int F>
+__global__ void __launch_bounds__(256) wide_tail_kernel(const WideTail a) {
+    using W = std::conditional_t<F == VABFT_FP64, double, float>;
+    using T = typename Elem<F>::T;
+    __shared__ unsigned long long cnt[6];
+    const int lane = threadIdx.x & 31;
+    if (threadIdx.x < 6) cnt[threadIdx.x] = 0;
+    __syncthreads();
+    const int64_t i = int64_t(blockIdx.x) * 8 + (threadIdx.x >> 5);
+    if (i < a.M) {
+        // C r1 / C r2: block partials in order
+        W r1 = W(0), r2 = W(0);
+        for (int64_t g = 0; g < a.nblk; g += 32) {
+            const int64_t b = g + lane;
+            W q1 = W(0), q2 = W(0);
+            if (b < a.nblk) {
+                const size_t o = size_t(b) * size_t(a.ld) + size_t(i);
+                q1 = load_part<W>(a.part1, o);
+                q2 = load_part<W>(a.part2, o);
+            }
+            const int n = a.nblk - g < 32 ? int(a.nblk - g) : 32;
+            for (int l = 0; l < n; ++l) {
+                r1 = radd(r1, __shfl_sync(0xffffffffu, q1, l));
+                r2 = radd(r2, __shfl_sync(0xffffffffu, q2, l));
+            }
+        }
+        double mean_i = 0.0, vb_i = 0.0, c1 = 0.0, c2 = 0.0;
+        if (a.apart) {
+            const int64_t nbk = (a.K + 127) / 128;
+            const APart<W> in = apart_view<W>(const_cast<void*>(a.apart), nbk, a.ld);
+            W t1 = W(0), t2 = W(0);
+            double s = 0.0, c = 0.0, sabs = 0.0, mx = -INFINITY, mn = INFINITY;
+            for (int64_t g = 0; g < nbk; g += 32) {
+                const int64_t b = g + lane;
+                W q1 = W(0), q2 = W(0);
+                if (b < nbk) {
+                    const size_t o = size_t(b) * size_t(a.ld) + size_t(i);
+                    q1 = in.p1[o];
+                    q2 = in.p2[o];
+                    double t, err;
+                    two_sum(s, in.s[o], t, err);
+                    s = t;
+                    c = __dadd_rn(__dadd_rn(c, in.c[o]), err);
+                    sabs = __dadd_rn(sabs, in.sabs[o]);
+                    mx = mx < in.mx[o] ? in.mx[o] : mx;
+                    mn = in.mn[o] < mn ? in.mn[o] : mn;
+                }
+                const int n = nbk - g < 32 ? int(nbk - g) : 32;
+                for (int l = 0; l < n; ++l) {
+                    t1 = radd(t1, __shfl_sync(0xffffffffu, q1, l));
+                    t2 = radd(t2, __shfl_sync(0xffffffffu, q2, l));
+                }
+            }
+#pragma unroll
+            for (int o = 16; o >= 1; o >>= 1) {
+                const double so = __shfl_xor_sync(0xffffffffu, s, o), co = __shfl_xor_sync(0xffffffffu, c, o);
+                double t, err;
+                two_sum(s, so, t, err);
+                s = t;
+                c = __dadd_rn(__dadd_rn(c, co), err);
+                sabs = __dadd_rn(sabs, __shfl_xor_sync(0xffffffffu, sabs, o));
+                const double mxo = __shfl_xor_sync(0xffffffffu, mx, o), mno = __shfl_xor_sync(0xffffffffu, mn, o);
+                mx = mx < mxo ? mxo : mx;
+                mn = mno < mn ? mno : mn;
+            }
+            if (lane == 0) {
+                Neu ns;
+                if (exact_sum_safe(s, c, sabs, a.K, &ns.s)) {
+                    // ns.s = fl(sum + comp) of the reference
+                } else {
+                    if (a.counts) atomicAdd(&cnt[VABFT_COUNT_SLOW_STATS], 1ull);
+                    const T* arow = static_cast<const T*>(a.A) + i * a.K;
+                    ns = Neu{};
+                    for (int64_t j = 0; j < a.K; ++j) ns.add(double(arow[j]));  // the reference's loop
+                }
+                stats_finish(ns, mx, mn, a.K, &mean_i, &vb_i);
+                c1 = double(t1);
+                c2 = double(t2);
+                if (a.qfmt == VABFT_FP32) {  // offline FP32: rounded to the input format (no-op for W = float)
+                    c1 = double(float(c1));
+                    c2 = double(float(c2));
+                }
+            }
+        } else if (lane == 0) {
+            mean_i = a.mean[i];
+            vb_i = a.vb[i];
+            c1 = a.cr1[i];
+            c2 = a.cr2[i];
+        }
+        if (lane == 0) {
+            bool det = false, located = false, isnan_row = false, corrected = false;
+            double t;
+            if (a.method == 0) {
+                t = vabft_threshold_total(mean_i, vb_i, a.bsum[0], a.bsum[1], a.bsum[2], a.N, a.e_max, a.c_sigma);
+            } else {
+                const double y = a.method == 1 ? a.aabft_fixed_y : __dmul_rn(*a.max_abs_a, a.bsum[3]);
+                t = aabft_total(a.K, a.aabft_t, y, a.aabft_conf);
+            }
+            if (a.T_out) a.T_out[i] = t;
+            const double d1 = __dsub_rn(double(r1), c1);
+            const double d2 = __dsub_rn(double(r2), c2);
+            int64_t loc = -1;
+            double res = 0.0;
+            if (isnan(d1) || isnan(d2)) {
+                det = true;
+                isnan_row = true;
+            } else {
+                det = fabs(d1) > t;
+                if (det && fabs(d1) > __dmul_rn(a.floor_scale, t)) {
+                    int64_t j;
+                    double rr;
+                    if (localize_dev(d1, d2, a.N, &j, &rr)) {
+                        loc = j;
+                        res = rr;
+                        located = true;
+                        // correct (detect.cpp:57-64): C[i][j] = quantize(C[i][j] - diff1)
+                        if (a.correct && a.C != nullptr && rr < 0.4) {
+                            if (a.fmt == VABFT_FP64) {
+                                double* cij = static_cast<double*>(a.C) + i * a.N + j;
+                                *cij = __dsub_rn(*cij, d1);
+                            } else {
+                                float* cij = static_cast<float*>(a.C) + i * a.N + j;
+                                const float q = __double2float_rn(__dsub_rn(double(*cij), d1));
+                                *cij = isinf(q) ? copysignf(3.40282346638528859812e+38f, q) : q;
+                            }
+                            corrected = true;
+                        }
+                    }
+                }
+            }
+            if (a.v.diff1) a.v.diff1[i] = d1;
+            if (a.v.diff2) a.v.diff2[i] = d2;
+            if (a.v.detected) a.v.detected[i] = det ? 1 : 0;
+            if (a.v.location) a.v.location[i] = loc;
+            if (a.v.residual) a.v.residual[i] = res;
+            if (a.v.row_check1) a.v.row_check1[i] = c1;
+            if (a.v.row_check2) a.v.row_check2[i] = c2;
+            if (a.counts) {
+                atomicAdd(&cnt[VABFT_COUNT_ROWS], 1ull);
+                if (det) atomicAdd(&cnt[VABFT_COUNT_DETECTED], 1ull);
+                if (located) atomicAdd(&cnt[VABFT_COUNT_LOCATED], 1ull);
+                if (isnan_row) atomicAdd(&cnt[VABFT_COUNT_NAN], 1ull);
+                if (corrected) atomicAdd(&cnt[VABFT_COUNT_CORRECTED], 1ull);
+            }
+        }
+    }
+    __syncthreads();
+    if (a.counts && threadIdx.x < 6 && cnt[threadIdx.x])
+        atomicAdd(reinterpret_cast<unsigned long long*>(a.counts + threadIdx.x), cnt[threadIdx.x]);
 }
 
 __global__ void max_abs_rows_kernel(int64_t m, const double* mx, const double* mn, double* out) {
@@ -480,35 +581,27 @@ void dgemm_launch(int64_t M, int64_t N, int64_t K, const double* A, const double
 }
 
 void launch_wide_tail(const WideTail& t, cudaStream_t stream) {
-    const unsigned grid = unsigned((t.M + 255) / 256);
-    if (t.fmt == VABFT_FP64) wide_tail_kernel<double><<<grid, 256, 0, stream>>>(t);
-    else wide_tail_kernel<float><<<grid, 256, 0, stream>>>(t);
+    const unsigned grid = unsigned((t.M + 7) / 8);
+    if (t.fmt == VABFT_FP64) wide_tail_kernel<VABFT_FP64><<<grid, 256, 0, stream>>>(t);
+    else wide_tail_kernel<VABFT_FP32><<<grid, 256, 0, stream>>>(t);  // 8 rows (warps) per CTA
     check_cuda(cudaGetLastError(), "wide tail launch");
 }
 
 void launch_wide_aside(int fmt, int64_t M, int64_t K, const void* A, const double* br1, const double* br2, int qfmt,
                        double* mean, double* vb, double* mx, double* mn, double* cr1, double* cr2, void* apart,
-                       int64_t ld, int64_t* counts, cudaStream_t stream) {
+                       int64_t ld, int64_t* counts, bool combine, cudaStream_t stream) {
     const int64_t nb = (K + 127) / 128;
     const dim3 grid_p(unsigned((M + 127) / 128), unsigned(nb));
     const unsigned grid_c = unsigned((M + 255) / 256);
-    // SMs running these small CTAs must keep the maximum shared-memory
-    // carveout, or the GEMM's CTAs cannot co-reside and the overlap is lost
     auto run = [&](auto tag, auto wtag) {
         using T = decltype(tag);
         using W = decltype(wtag);
         constexpr int F = sizeof(T) == 8 ? VABFT_FP64 : VABFT_FP32;
-        static const bool once = [] {
-            check_cuda(cudaFuncSetAttribute(wide_apart_kernel<F, W>, cudaFuncAttributePreferredSharedMemoryCarveout,
-                                            100),
-                       "carveout(wide aside)");
-            return true;
-        }();
-        (void)once;
         const APart<W> part = apart_view<W>(apart, nb, ld);
         wide_apart_kernel<F, W><<<grid_p, 128, 0, stream>>>(static_cast<const T*>(A), M, K, br1, br2, part, ld);
-        wide_acombine_kernel<F, W><<<grid_c, 256, 0, stream>>>(static_cast<const T*>(A), M, K, part, ld, qfmt, mean,
-                                                               vb, mx, mn, cr1, cr2, counts);
+        if (combine)
+            wide_acombine_kernel<F, W><<<grid_c, 256, 0, stream>>>(static_cast<const T*>(A), M, K, part, ld, qfmt,
+                                                                   mean, vb, mx, mn, cr1, cr2, counts);
     };
     if (fmt == VABFT_FP64) run(double{}, double{});
     else if (fmt == VABFT_FP32) run(float{}, float{});

@@ -10,13 +10,20 @@ dt = {"fp32": torch.float32, "fp64": torch.float64}[sys.argv[2] if len(sys.argv)
 passes = int(sys.argv[3]) if len(sys.argv) > 3 else 1
 a = torch.randn(n, n, device="cuda", dtype=dt); b = torch.randn(n, n, device="cuda", dtype=dt)
 g = FusedAbftGemm(b, tf32_passes=passes, e_max=1e-2)
+flush = torch.empty(512 * 1024 * 1024, dtype=torch.uint8, device="cuda") if "flush" in sys.argv else None
+counts = torch.zeros(6, dtype=torch.int64, device="cuda") if "counts" in sys.argv else None
 for _ in range(3):
-    g(a)
+    g(a, counts=counts)
 torch.cuda.synchronize()
 with profile(activities=[ProfilerActivity.CUDA]) as prof:
-    g(a)
+    for _ in range(2):
+        if flush is not None:
+            flush.zero_()
+        g(a, counts=counts)
     torch.cuda.synchronize()
 evs = [e for e in prof.events() if e.device_type == torch.autograd.DeviceType.CUDA]
 t0 = min(e.time_range.start for e in evs)
+if counts is not None:
+    print("counts", counts.tolist())
 for e in sorted(evs, key=lambda e: e.time_range.start):
     print(f"{e.time_range.start - t0:9.1f} {e.time_range.end - t0:9.1f}  {e.name[:70]}")
