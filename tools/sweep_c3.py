@@ -9,7 +9,8 @@ A-ABFT thresholds, tightness and false positives, on the device paths
 BF16/FP16: the fused tcgen05 path (FusedAbftGemm: T_V with the device
 e_max defaults, T_A = A-ABFT computed y), operands drawn on the device; the
 actual difference is |D1| of the fused verification (FP32 blocked:128 row
-sums of the accumulator vs the checksums). FP32/FP64: the EXACT engine
+sums of the accumulator vs the checksums); FP32 / FP64 also on their fused
+device paths up to n = 16384 / 8192. FP32/FP64 "exact" lines: the EXACT engine
 (api.py), sizes capped like the reference (FP64 at 512); the actual
 difference is |row_check1 - exactly rounded row sum of the source|
 (math.fsum, the role MPFR plays in oracle_row_diffs), T_V with
@@ -36,17 +37,21 @@ DISTS = ["normal:0,1", "normal:1e-6,1", "normal:1,1", "uniform:-1,1", "truncnorm
 
 
 def sweep16(fmt, dist, n, trials, mode, gen):
-    dtype = torch.bfloat16 if fmt == "bf16" else torch.float16
+    """The fused device path (any format): T_V with the device e_max defaults,
+    T_A per AabftParams::for_format (computed y for 16-bit, y = 21 for
+    FP32 / FP64, threshold_aabft.cpp:8-29)."""
+    dtype = {"bf16": torch.bfloat16, "fp16": torch.float16, "fp32": torch.float32, "fp64": torch.float64}[fmt]
+    aab = "aabft-computed-y" if fmt in ("bf16", "fp16") else "aabft-fixed-y"
     dev = torch.device("cuda")
     acc = {"tv": 0.0, "ta": 0.0, "act": 0.0, "max_act": 0.0, "fp_v": 0, "fp_a": 0, "rows": 0, "e_max": None}
     for _ in range(trials):
         A = sample_matrix((n, n), dist, gen, dev, dtype)
         B = sample_matrix((n, n), dist, gen, dev, dtype)
-        cv = torch.zeros(5, dtype=torch.int64, device=dev)
-        ca = torch.zeros(5, dtype=torch.int64, device=dev)
+        cv = torch.zeros(6, dtype=torch.int64, device=dev)
+        ca = torch.zeros(6, dtype=torch.int64, device=dev)
         gv = FusedAbftGemm(B, mode=mode)
         rv = gv(A, counts=cv)
-        ga = FusedAbftGemm(B, mode=mode, threshold="aabft-computed-y")
+        ga = FusedAbftGemm(B, mode=mode, threshold=aab)
         ra = ga(A, counts=ca)
         d1 = rv.diff1.abs()
         acc["tv"] += rv.T.mean().item()
@@ -123,17 +128,26 @@ def main():
     for fmt, sz in wide.items():
         for dist in DISTS:
             for n, t in sz:
-                plan.append((fmt, "offline", dist, n, t))
+                plan.append((fmt + ":exact", "offline", dist, n, t))
+    # the fused device paths for FP32 (3xTF32 on tcgen05) and FP64 (DFMA), up to 16384
+    sizesw = {"fp32": [(256, 3), (1024, 2), (4096, 2), (16384, 1)], "fp64": [(256, 3), (1024, 2), (4096, 1), (8192, 1)]}
+    if args.quick:
+        sizesw = {"fp32": [(256, 1)], "fp64": [(256, 1)]}
+    for fmt, sz in sizesw.items():
+        for dist in DISTS:
+            for n, t in sz:
+                plan.append((fmt, "online", dist, n, t))
     for fmt, mode, dist, n, trials in plan:
         t0 = time.time()
-        if fmt in ("bf16", "fp16"):
+        if fmt.endswith(":exact"):
+            fmt = fmt.split(":")[0]
+            a = sweep_wide(fmt, dist, n, trials, mode, rng)
+            engine = "exact (order-exact SIMT)"
+        else:
             if fmt == "fp16" and dist == "normal:1,1" and n >= 4096 and mode == "offline":
                 continue  # FP16 output overflows (|C| ~ n): saturated, not a rounding experiment
             a = sweep16(fmt, dist, n, trials, mode, gen)
-            engine = "tensor (fused tcgen05)"
-        else:
-            a = sweep_wide(fmt, dist, n, trials, mode, rng)
-            engine = "exact (order-exact SIMT)"
+            engine = {"fp32": "tensor (fused tcgen05 3xTF32)", "fp64": "fused SIMT DFMA"}.get(fmt, "tensor (fused tcgen05)")
         mt_v, mt_a, ma = a["tv"] / trials, a["ta"] / trials, a["act"] / trials
         line = {"precision": fmt, "mode": mode, "dist": dist, "n": n, "trials": trials, "engine": engine,
                 "e_max": a["e_max"], "mean_T_vabft": mt_v, "mean_T_aabft": mt_a,
