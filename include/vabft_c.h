@@ -266,8 +266,10 @@ typedef struct vabft_fused_opts {
      *  2 InputB: operand_faults[t] = {i = k, j = column, bit, direction} —
      *    B[k][j] flipped in the operand tiles of every M tile; the checksums
      *    come from the clean B of the B-side handle.
-     * Operand bits are the BF16/FP16 patterns (0..15). Records: fault_records
-     * per row for InputA, operand_fault_records per fault for InputB. */
+     * Operand bits are the BF16/FP16 patterns (0..15); FP32 / FP64 handles
+     * flip IEEE bits (0..31 / 0..63) in a copy of the operand the GEMM reads
+     * (FP32: before its TF32 split). Records: fault_records per row for
+     * InputA, operand_fault_records per fault for InputB. */
     int32_t fault_target;
     int32_t n_operand_faults;
     int32_t correct;  /* 1: rows with a located single error (residual < 0.5 - 0.1,

@@ -366,10 +366,12 @@ __global__ void inject_kernel(int fmt, int64_t n, void* X, const vabft_fault* fa
             static_cast<double*>(X)[idx] = __longlong_as_double(int64_t(nb));
             after = __longlong_as_double(int64_t(nb));
         }
-        rec[f].value_before = before;
-        rec[f].value_after = after;
-        rec[f].applied = ok ? 1 : 0;
-        rec[f].reserved = 0;
+        if (rec) {  // records are optional for campaign callers
+            rec[f].value_before = before;
+            rec[f].value_after = after;
+            rec[f].applied = ok ? 1 : 0;
+            rec[f].reserved = 0;
+        }
     }
 }
 

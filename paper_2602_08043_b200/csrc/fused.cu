@@ -174,26 +174,60 @@ void wide_fused(const vabft_fused_opts* o, vabft_bside* h, int64_t m, const void
                 const vabft_verdicts& verdicts, int64_t* counts, void* workspace, cudaStream_t s) {
     if (o->tf32_passes != 0 && o->tf32_passes != 1 && o->tf32_passes != 3)
         fail(VABFT_INVALID_ARGUMENT, "vabft_fused_gemm: tf32_passes must be 0, 1 or 3");
-    if (o->fault_target != 0) fail(VABFT_UNSUPPORTED, "vabft_fused_gemm: operand faults need a 16-bit format");
     const int64_t n = h->n, k = h->k;
     const WideWs ws = carve_wide(workspace, m, n, k);
     const int stages = o->stages == 0 ? 7 : o->stages;
     const bool tail = (stages & 4) != 0;
+    if (o->fault_target == 1 && (!o->fault_col || !o->fault_bit || !o->fault_dir))
+        fail(VABFT_INVALID_ARGUMENT, "InputA faults need fault_col / fault_bit / fault_dir");
+    if (o->fault_target == 2 && o->n_operand_faults > 0 && !o->operand_faults)
+        fail(VABFT_INVALID_ARGUMENT, "InputB faults need operand_faults");
     if (stages & 2) {
         WideEpilogue epi;
         epi.abft = (stages & 8) ? 0 : 1;  // bit 8: the same GEMM with the ABFT epilogue off (overhead baseline)
         epi.part1 = ws.part1;
         epi.part2 = ws.part2;
         epi.ld = ws.ld;
-        epi.fault_col = o->fault_col;
-        epi.fault_bit = o->fault_bit;
-        epi.fault_dir = o->fault_dir;
-        epi.fault_records = o->fault_records;
+        if (o->fault_target == 0) {
+            epi.fault_col = o->fault_col;
+            epi.fault_bit = o->fault_bit;
+            epi.fault_dir = o->fault_dir;
+            epi.fault_records = o->fault_records;
+        }
+        // Operand faults (FaultTarget InputA / InputB, faults.hpp:15): the GEMM
+        // multiplies a copy of the operand with the planned bits flipped (what
+        // the FP64 pipe / tensor cores see), while the A side and the checksums
+        // read the clean operands. Campaign path: the copies come from the
+        // stream-ordered allocator.
+        const size_t es = h->fmt == VABFT_FP64 ? 8 : 4;
+        const void* Ag = A;
+        const void* Bg = h->B;
+        void* scratch = nullptr;
+        if (o->fault_target == 1) {
+            check_cuda(cudaMallocAsync(&scratch, es * size_t(m) * size_t(k), s), "cudaMallocAsync(A')");
+            check_cuda(cudaMemcpyAsync(scratch, A, es * size_t(m) * size_t(k), cudaMemcpyDeviceToDevice, s), "copy");
+            launch_flip_rows(h->fmt, scratch, m, k, o->fault_col, o->fault_bit, o->fault_dir, o->fault_records, s);
+            Ag = scratch;
+        } else if (o->fault_target == 2 && o->n_operand_faults > 0) {
+            // B' plus, for FP32, its transposed TF32 split
+            const size_t nb = size_t(k) * size_t(n), extra = h->fmt == VABFT_FP32 ? 2 * nb : 0;
+            check_cuda(cudaMallocAsync(&scratch, es * (nb + extra), s), "cudaMallocAsync(B')");
+            check_cuda(cudaMemcpyAsync(scratch, h->B, es * nb, cudaMemcpyDeviceToDevice, s), "copy");
+            launch_inject(h->fmt, n, scratch, o->operand_faults, o->n_operand_faults, o->operand_fault_records, s);
+            Bg = scratch;
+            if (h->fmt == VABFT_FP32) {
+                float* t = static_cast<float*>(scratch) + nb;
+                split_tf32_t(static_cast<const float*>(scratch), t, t + nb, k, n, s);
+            }
+        }
+        const float* bsplit = (o->fault_target == 2 && o->n_operand_faults > 0 && h->fmt == VABFT_FP32)
+                                  ? static_cast<const float*>(Bg) + size_t(k) * size_t(n)
+                                  : h->b_split;
         if (h->fmt == VABFT_FP64) {
-            dgemm_launch(m, n, k, static_cast<const double*>(A), static_cast<const double*>(h->B),
+            dgemm_launch(m, n, k, static_cast<const double*>(Ag), static_cast<const double*>(Bg),
                          static_cast<double*>(C), epi, s);
         } else if (o->tf32_passes == 1) {
-            tf32_gemm_launch(m, n, k, static_cast<const float*>(A), nullptr, h->b_split, nullptr,
+            tf32_gemm_launch(m, n, k, static_cast<const float*>(Ag), nullptr, bsplit, nullptr,
                              static_cast<float*>(C), epi, s);
         } else {
             const size_t need = 2 * size_t(m) * size_t(k);
@@ -207,10 +241,10 @@ void wide_fused(const vabft_fused_opts* o, vabft_bside* h, int64_t m, const void
             }
             float* ahi = h->a_split;
             float* alo = h->a_split + size_t(m) * size_t(k);
-            split_tf32(static_cast<const float*>(A), ahi, alo, m * k, s);
-            const float* bhi = h->b_split;
-            tf32_gemm_launch(m, n, k, ahi, alo, bhi, bhi + size_t(k) * size_t(n), static_cast<float*>(C), epi, s);
+            split_tf32(static_cast<const float*>(Ag), ahi, alo, m * k, s);
+            tf32_gemm_launch(m, n, k, ahi, alo, bsplit, bsplit + size_t(k) * size_t(n), static_cast<float*>(C), epi, s);
         }
+        if (scratch) check_cuda(cudaFreeAsync(scratch, s), "cudaFreeAsync");
     }
     if (!tail) return;
     // A-ABFT computed y needs the global max|A| first: combine in a separate

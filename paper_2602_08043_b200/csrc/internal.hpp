@@ -162,5 +162,9 @@ void launch_wide_aside(int fmt, int64_t M, int64_t K, const void* A, const doubl
                        double* mean, double* vb, double* mx, double* mn, double* cr1, double* cr2, void* apart,
                        int64_t ld, int64_t* counts, bool combine, cudaStream_t stream);
 void launch_max_abs_rows(int64_t m, const double* mx, const double* mn, double* out, cudaStream_t stream);
+// InputA operand faults of the wide path: per row i, flip bit[i] of
+// X[i][col[i]] (col < 0: none), per-row records
+void launch_flip_rows(int fmt, void* X, int64_t rows, int64_t cols, const int32_t* col, const int32_t* bit,
+                      const int32_t* dir, vabft_fault_record* rec, cudaStream_t stream);
 
 }  // namespace vabft_dev

@@ -615,3 +615,53 @@ void launch_max_abs_rows(int64_t m, const double* mx, const double* mn, double* 
 }
 
 }  // namespace vabft_dev
+
+namespace vabft_dev {
+
+namespace {
+
+// InputA faults of the wide path: per row i, bit fault_bit[i] of
+// X[i][fault_col[i]] (inject's eligibility rule, faults.cpp:91-102), with a
+// per-row record.
+template <class T, class U>
+__global__ void flip_rows_kernel(T* X, int64_t rows, int64_t cols, const int32_t* col, const int32_t* bit,
+                                 const int32_t* dir, vabft_fault_record* rec) {
+    const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i >= rows) return;
+    const int64_t k = col[i];
+    if (k < 0 || k >= cols) return;
+    U* p = reinterpret_cast<U*>(X + i * cols + k);
+    const U b = *p;
+    const bool ok = bit_eligible(uint64_t(b), bit[i], dir[i]);
+    const U nb = ok ? U(b ^ (U(1) << bit[i])) : b;
+    *p = nb;
+    if (rec) {
+        vabft_fault_record r;
+        T before, after;
+        memcpy(&before, &b, sizeof(T));
+        memcpy(&after, &nb, sizeof(T));
+        r.value_before = double(before);
+        r.value_after = double(after);
+        r.applied = ok ? 1 : 0;
+        r.reserved = 0;
+        rec[i] = r;
+    }
+}
+
+}  // namespace
+
+void launch_flip_rows(int fmt, void* X, int64_t rows, int64_t cols, const int32_t* col, const int32_t* bit,
+                      const int32_t* dir, vabft_fault_record* rec, cudaStream_t s) {
+    const unsigned grid = unsigned((rows + 255) / 256);
+    if (fmt == VABFT_FP64)
+        flip_rows_kernel<double, unsigned long long><<<grid, 256, 0, s>>>(static_cast<double*>(X), rows, cols, col,
+                                                                          bit, dir, rec);
+    else if (fmt == VABFT_FP32)
+        flip_rows_kernel<float, unsigned int><<<grid, 256, 0, s>>>(static_cast<float*>(X), rows, cols, col, bit, dir,
+                                                                   rec);
+    else
+        fail(VABFT_INVALID_ARGUMENT, "flip rows: FP32 / FP64 only");
+    check_cuda(cudaGetLastError(), "flip rows launch");
+}
+
+}  // namespace vabft_dev

@@ -281,3 +281,54 @@ def test_wide_rowstats_midpoint_fallback(torch_cuda, port):
     T_ref, _ = port.vabft_thresholds(A, B, 4e-15, fmt="fp64")
     assert same(r.T.cpu().numpy(), T_ref)
     assert int(counts[4].item()) >= 1  # the midpoint row went the sequential way
+
+
+@pytest.mark.parametrize("fmt,target,bit", [("fp64", "A", 52), ("fp64", "B", 40), ("fp32", "A", 23),
+                                            ("fp32", "B", 20)])
+def test_wide_operand_faults_match_oracle(torch_cuda, port, fmt, target, bit):
+    """Operand faults on the wide path: the GEMM multiplies the flipped operand,
+    the checksums / thresholds come from the clean ones; verdicts bit-exact
+    against the oracle's verify of the same product."""
+    torch = torch_cuda
+    from paper_2602_08043_b200 import api
+    from paper_2602_08043_b200.fused import FusedAbftGemm, operand_faults
+    m, k, n = 128, 256, 264
+    A, B = port.trial_inputs(m, k, n, fmt, "normal:0,1", 29, bit)
+    dt = torch.float64 if fmt == "fp64" else torch.float32
+    npdt = np.float64 if fmt == "fp64" else np.float32
+    udt = np.uint64 if fmt == "fp64" else np.uint32
+    e_max = 4e-15 if fmt == "fp64" else 2e-6
+    g = FusedAbftGemm(torch.from_numpy(B).to(dt).cuda(), e_max=e_max)
+    dA = torch.from_numpy(A).to(dt).cuda()
+    rng = np.random.default_rng(bit)
+    Af, Bf = A.astype(npdt), B.astype(npdt)
+
+    def flip(x, bitpos):
+        return (np.array([x], dtype=npdt).view(udt) ^ udt(1 << bitpos)).view(npdt)[0]
+    if target == "A":
+        ks = rng.integers(0, k, m)
+        for i, kk in enumerate(ks):
+            Af[i, kk] = flip(Af[i, kk], bit)
+        rec = torch.zeros(m * 24, dtype=torch.uint8, device="cuda")
+        f = {"target": "A", "col": torch.from_numpy(ks.astype(np.int32)).cuda(),
+             "bit": torch.full((m,), bit, dtype=torch.int32, device="cuda"),
+             "dir": torch.zeros(m, dtype=torch.int32, device="cuda"), "records": rec}
+    else:
+        pos = [(int(rng.integers(0, k)), int(rng.integers(0, n))) for _ in range(3)]
+        for (kk, j) in pos:
+            Bf[kk, j] = flip(Bf[kk, j], bit)
+        f = {"target": "B", "operand": operand_faults([(kk, j, bit, 0) for (kk, j) in pos])}
+    counts = torch.zeros(6, dtype=torch.int64, device="cuda")
+    r = g(dA, faults=f, checksums=True, counts=counts)
+    torch.cuda.synchronize()
+    Cf = r.C.double().cpu().numpy()
+    e = api.encode_and_multiply(Af.astype(np.float64), Bf.astype(np.float64), "online", fmt, engine="tensor")
+    assert same(Cf, e.c)  # the same kernel on the flipped operand
+    o = port.encode_and_multiply(A, B, fmt, "online", accum=BLK)  # clean checksums
+    assert same(r.row_check1.cpu().numpy(), o.row_check1)
+    T_ref, _ = port.vabft_thresholds(A, B, e_max, fmt=fmt)
+    assert same(r.T.cpu().numpy(), T_ref)
+    v = port.verify(Cf, o.row_check1, o.row_check2, T_ref, fmt, "online", accum=BLK)
+    assert np.array_equal(v["detected"], r.detected.cpu().numpy().astype(bool))
+    assert np.array_equal(v["location"], r.location.cpu().numpy())
+    assert int(counts[1].item()) == int(v["detected"].sum()) and v["detected"].any()
