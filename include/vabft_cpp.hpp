@@ -1211,17 +1211,18 @@ inline Matrix load_matrix_auto(const std::string& path, const std::optional<Prec
 }
 
 // =========================================================== B200 extension
-// The hot path on caller-owned device memory: the tcgen05 fused V-ABFT GEMM
+// The hot path on caller-owned device memory: the fused V-ABFT GEMM
 // (vabft_bside_* / vabft_fused_gemm), RAII over the B-side handle and the
 // workspace. Not part of the reference API.
 namespace b200 {
 
 class FusedGemm {
 public:
-    // B: K x N device matrix (BF16 / FP16 bits), fixed weight.
+    // B: K x N device matrix in the format's native storage (BF16 / FP16 bits
+    // on tcgen05, FP32 on tcgen05 kind::tf32 with 3xTF32, FP64 on the SIMT
+    // DFMA kernel), fixed weight.
     FusedGemm(Format fmt, VerifyMode mode, int64_t k, int64_t n, const void* B, double e_max, void* stream = nullptr)
         : k_(k), n_(n) {
-        if (fmt != Format::BF16 && fmt != Format::FP16) throw std::invalid_argument("FusedGemm: BF16/FP16 only");
         opts_.mode = mode == VerifyMode::Online ? VABFT_ONLINE : VABFT_OFFLINE;
         opts_.threshold_method = 0;
         opts_.e_max = e_max;
@@ -1229,6 +1230,8 @@ public:
         opts_.floor_scale = 1e-3;
         opts_.aabft_fixed_y = 21.0;
         opts_.aabft_confidence = 3.0;
+        opts_.cta_mode = -1;    // the measured kernel-shape policy
+        opts_.tf32_passes = 3;  // FP32: 3xTF32
         detail::check(vabft_bside_create(int32_t(fmt), opts_.mode, k, n, B, &h_, stream));
     }
     ~FusedGemm() {

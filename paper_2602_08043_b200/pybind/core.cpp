@@ -279,4 +279,26 @@ PYBIND11_MODULE(_core, m) {
     m.def("save_matrix_csv", &save_matrix_csv);
     m.def("load_matrix_csv", &load_matrix_csv);
     m.def("load_matrix_auto", &load_matrix_auto, py::arg("path"), py::arg("csv_format") = std::nullopt);
+
+    // B200 extension: the fused path on device pointers (integers, e.g.
+    // torch's data_ptr()); verdict arrays optional (0 = not written)
+    py::class_<b200::FusedGemm>(m, "FusedGemm")
+        .def(py::init([](Format fmt, VerifyMode mode, int64_t k, int64_t n, uintptr_t B, double e_max,
+                         uintptr_t stream) {
+                 return std::make_unique<b200::FusedGemm>(fmt, mode, k, n, reinterpret_cast<const void*>(B), e_max,
+                                                          reinterpret_cast<void*>(stream));
+             }),
+             py::arg("format"), py::arg("mode"), py::arg("k"), py::arg("n"), py::arg("B"), py::arg("e_max"),
+             py::arg("stream") = 0)
+        .def("__call__",
+             [](b200::FusedGemm& g, int64_t m, uintptr_t A, uintptr_t C, uintptr_t T, uintptr_t detected,
+                uintptr_t location, uintptr_t counts, uintptr_t stream) {
+                 vabft_verdicts v{};
+                 v.detected = reinterpret_cast<uint8_t*>(detected);
+                 v.location = reinterpret_cast<int64_t*>(location);
+                 g(m, reinterpret_cast<const void*>(A), reinterpret_cast<void*>(C), reinterpret_cast<double*>(T), v,
+                   reinterpret_cast<int64_t*>(counts), reinterpret_cast<void*>(stream));
+             },
+             py::arg("m"), py::arg("A"), py::arg("C"), py::arg("T") = 0, py::arg("detected") = 0,
+             py::arg("location") = 0, py::arg("counts") = 0, py::arg("stream") = 0);
 }

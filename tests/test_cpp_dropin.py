@@ -247,3 +247,34 @@ def test_injection_campaign_counts_equal_reference(ref_or_port, mode, bit):
                                        e_max=e_max)
         tot += o[:4]
     assert (out.applicable, out.detected, out.located_correctly, out.nonfinite_after) == tuple(int(x) for x in tot)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("fmt", ["bf16", "fp32", "fp64"])
+def test_cpp_fused_gemm_matches_python_path(fmt):
+    """vabft::b200::FusedGemm (the C++ drop-in's hot path) == FusedAbftGemm
+    on the same device inputs: C, thresholds, verdicts bit-identical."""
+    import torch
+    from paper_2602_08043_b200 import _core
+    from paper_2602_08043_b200.fused import FusedAbftGemm
+    dt = {"bf16": torch.bfloat16, "fp32": torch.float32, "fp64": torch.float64}[fmt]
+    torch.manual_seed(5)
+    m, k, n = 256, 512, 384
+    A = torch.randn(m, k, device="cuda").to(dt)
+    B = torch.randn(k, n, device="cuda").to(dt)
+    py = FusedAbftGemm(B, mode="online")
+    r = py(A)
+    F = {"bf16": _core.Format.BF16, "fp32": _core.Format.FP32, "fp64": _core.Format.FP64}[fmt]
+    g = _core.FusedGemm(F, _core.VerifyMode.Online, k, n, B.data_ptr(), py.opts.e_max,
+                        torch.cuda.current_stream().cuda_stream)
+    C = torch.empty(m, n, device="cuda", dtype=dt)
+    T = torch.empty(m, device="cuda", dtype=torch.float64)
+    det = torch.empty(m, device="cuda", dtype=torch.uint8)
+    loc = torch.empty(m, device="cuda", dtype=torch.int64)
+    counts = torch.zeros(6, device="cuda", dtype=torch.int64)
+    g(m, A.data_ptr(), C.data_ptr(), T.data_ptr(), det.data_ptr(), loc.data_ptr(), counts.data_ptr(),
+      torch.cuda.current_stream().cuda_stream)
+    torch.cuda.synchronize()
+    assert torch.equal(C.view(torch.uint8), r.C.view(torch.uint8))
+    assert torch.equal(T, r.T) and torch.equal(det, r.detected) and torch.equal(loc, r.location)
+    assert int(counts[0]) == m and int(counts[1]) == 0
