@@ -955,7 +955,11 @@ bool tc_gemm_uses_pairs(bool b_kmajor, int64_t N, const TcEpilogue& epi) {
     const bool inj = epi.fault_col != nullptr || (epi.fault_target == 2 && epi.n_operand_faults > 0);
     const bool eligible = !b_kmajor && !inj && epi.tail_phases == 0 && sm_count() >= 2;
     const int mode = epi.cta_mode >= 0 ? epi.cta_mode : pair_env;
-    const bool want = mode >= 0 ? mode != 0 : (epi.sp1 == nullptr || (N + kBN - 1) / kBN >= 24);
+    (void)N;
+    // automatic: CTA pairs whenever eligible — measured faster for the plain
+    // and (with the fused kernel's raster of 32-row-block groups) the fused
+    // kernel at every bench shape
+    const bool want = mode >= 0 ? mode != 0 : true;
     return eligible && want;
 }
 
@@ -1002,9 +1006,9 @@ void tc_gemm_launch(int fmt, bool b_kmajor, int64_t M, int64_t N, int64_t K, con
     p.epi.trace = trace_buf;
     // CTA pairs (cta_group::2, 256 x 256 tiles over two SMs): N-major B, no
     // fault injection, no grid-barrier tail. Policy (measured):
-    // the plain GEMM always; the fused kernel when N >= 24 tiles of 256 — its
-    // A-statistics work per tile scales as 1 / #N-tiles, and with fewer N
-    // tiles the pair's faster MMA exposes the statistics warps.
+    // pairs whenever eligible, plain and fused (the fused kernel lost to the
+    // one-CTA kernel at N = 4096 only with groups of 4 pair-row blocks; with
+    // its 16-pair-block groups it wins at every bench shape).
     // VABFT_PAIR = 0 / 1 forces the 1-CTA / pair kernels.
     p.pair = tc_gemm_uses_pairs(b_kmajor, N, epi) ? 1 : 0;
     if (p.pair) {
