@@ -13,7 +13,7 @@ torch.manual_seed(0)
 A = torch.randn(m, k, device="cuda").bfloat16()
 B = torch.randn(k, n, device="cuda").bfloat16()
 g = FusedAbftGemm(B, mode=mode)
-counts = torch.zeros(5, dtype=torch.int64, device="cuda")
+counts = torch.zeros(6, dtype=torch.int64, device="cuda")
 for _ in range(3):
     r = g(A, counts=counts)
     plain_gemm(A, B, out=r.C)
