@@ -28,7 +28,7 @@ def run(shape):
     B = torch.randn(k, n, device="cuda").bfloat16()
     C = torch.empty(m, n, device="cuda", dtype=torch.bfloat16)
     g = FusedAbftGemm(B)
-    counts = torch.zeros(5, dtype=torch.int64, device="cuda")
+    counts = torch.zeros(6, dtype=torch.int64, device="cuda")
     g(A, out=C, counts=counts)  # first use: workspace identities (not counted: parse skips it)
     for name, dbg, stages in VARIANTS:
         for _ in range(REPS):
