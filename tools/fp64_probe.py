@@ -1,3 +1,5 @@
+"""FP64 fused V-ABFT GEMM (SIMT DFMA) throughput vs the plain kernel and cuBLAS
+(DMMA) at 2048-8192^3; the overhead of the A-side pass + verify tail."""
 import torch, time, json, sys
 sys.path.insert(0, '.')
 from paper_2602_08043_b200.fused import plain_gemm, FusedAbftGemm

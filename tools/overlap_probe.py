@@ -1,5 +1,5 @@
-"""Kernel timeline (CUPTI via torch.profiler) of one wide-format fused call:
-shows whether the side-stream A pass overlaps the GEMM."""
+"""Kernel timeline (CUPTI via torch.profiler) of one wide-format fused call
+(GEMM, A-side pass, verify tail); args: n fp32|fp64 passes [flush] [counts]."""
 import os, sys
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch
