@@ -279,8 +279,9 @@ typedef struct vabft_fused_opts {
     const vabft_fault* operand_faults;
     vabft_fault_record* operand_fault_records;
     /* tcgen05 kernel shape: -1 automatic (CTA pairs, cta_group::2 on 256 x 256
-     * tiles over two SMs, when N >= 24 x 256; else one CTA per 128 x 256
-     * tile), 0 one CTA, 1 CTA pairs (N-major B without fault injection). */
+     * tiles over two SMs, whenever eligible: N-major B, no fault injection, no
+     * grid-barrier tail; else one CTA per 128 x 256 tile), 0 one CTA, 1 CTA
+     * pairs. */
     int32_t cta_mode;
     /* FP32 handles (tcgen05 kind::tf32): 0 or 3 = 3xTF32 error compensation
      * (FP32-level products), 1 = a single TF32 pass. Ignored otherwise. */
