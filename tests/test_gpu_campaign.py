@@ -78,3 +78,28 @@ def test_campaign_rates(torch_cuda):
     assert hi.applicable > 200 and hi.detection_rate() == 1.0 and hi.localization_accuracy() > 0.99
     assert lo.applicable > 100 and lo.detection_rate() == 0.0
     assert mid.detection_rate() > 0.99 and mid.localization_accuracy() > 0.99
+
+
+@pytest.mark.parametrize("mode", ["online", "offline"])
+@pytest.mark.parametrize("shape", [(512, 1024, 1024), (384, 512, 768)])
+def test_cta_pair_and_one_cta_kernels_agree(torch_cuda, mode, shape):
+    """The CTA-pair (cta_group::2) and one-CTA fused kernels run the same MMA
+    order per output, statistics and verification: C, thresholds, differences
+    and verdicts are bit-identical."""
+    torch = torch_cuda
+    from paper_2602_08043_b200.fused import FusedAbftGemm
+    m, k, n = shape
+    torch.manual_seed(3)
+    A = torch.randn(m, k, device="cuda").bfloat16()
+    B = torch.randn(k, n, device="cuda").bfloat16()
+    g = FusedAbftGemm(B, mode=mode)
+    out = {}
+    for cm in (0, 1):
+        g.opts.cta_mode = cm
+        r = g(A, out=torch.empty(m, n, device="cuda", dtype=torch.bfloat16))
+        torch.cuda.synchronize()
+        out[cm] = (r.C.clone(), r.T.clone(), r.diff1.clone(), r.detected.clone())
+    assert g.uses_cta_pairs(m)
+    c0, c1 = out[0], out[1]
+    assert torch.equal(c0[0].view(torch.int16), c1[0].view(torch.int16))
+    assert torch.equal(c0[1], c1[1]) and torch.equal(c0[2], c1[2]) and torch.equal(c0[3], c1[3])
