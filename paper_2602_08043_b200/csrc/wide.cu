@@ -459,16 +459,38 @@ __global__ void __launch_bounds__(256) wide_tail_kernel(const WideTail a) {
                 mx = mx < mxo ? mxo : mx;
                 mn = mno < mn ? mno : mn;
             }
-            if (lane == 0) {
-                Neu ns;
-                if (exact_sum_safe(s, c, sabs, a.K, &ns.s)) {
-                    // ns.s = fl(sum + comp) of the reference
-                } else {
-                    if (a.counts) atomicAdd(&cnt[VABFT_COUNT_SLOW_STATS], 1ull);
-                    const T* arow = static_cast<const T*>(a.A) + i * a.K;
-                    ns = Neu{};
-                    for (int64_t j = 0; j < a.K; ++j) ns.add(double(arow[j]));  // the reference's loop
+            Neu ns;
+            const bool safe = __shfl_sync(0xffffffffu, exact_sum_safe(s, c, sabs, a.K, &ns.s) ? 1 : 0, 0) != 0;
+            if (!safe) {
+                // the reference's sequential loop (stats.cpp:12-24) — rows whose exact
+                // sum sits on a rounding midpoint (measured ~1 in 4096 for FP64 N(0,1)
+                // rows at K = 4096). The warp streams the row in coalesced 32-element
+                // chunks (next chunk in flight) and lane 0 walks them in order.
+                if (lane == 0 && a.counts) atomicAdd(&cnt[VABFT_COUNT_SLOW_STATS], 1ull);
+                const T* arow = static_cast<const T*>(a.A) + i * a.K;
+                ns = Neu{};
+                T nxt = lane < a.K ? arow[lane] : T(0);
+                for (int64_t j0 = 0; j0 < a.K; j0 += 32) {
+                    const T cur = nxt;
+                    nxt = j0 + 32 + lane < a.K ? arow[j0 + 32 + lane] : T(0);
+                    const int n = a.K - j0 < 32 ? int(a.K - j0) : 32;
+                    if (n == 32) {
+                        double xs[32];  // all 32 shuffles issued ahead of the sequential chain
+#pragma unroll
+                        for (int l = 0; l < 32; ++l) xs[l] = double(__shfl_sync(0xffffffffu, cur, l));
+                        if (lane == 0) {
+#pragma unroll
+                            for (int l = 0; l < 32; ++l) ns.add(xs[l]);
+                        }
+                    } else {
+                        for (int l = 0; l < n; ++l) {
+                            const double x = double(__shfl_sync(0xffffffffu, cur, l));
+                            if (lane == 0) ns.add(x);
+                        }
+                    }
                 }
+            }
+            if (lane == 0) {
                 stats_finish(ns, mx, mn, a.K, &mean_i, &vb_i);
                 c1 = double(t1);
                 c2 = double(t2);
