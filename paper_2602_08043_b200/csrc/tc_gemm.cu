@@ -330,12 +330,26 @@ struct StatsAcc {
         const float b1[8] = {u0.x, u0.y, u0.z, u0.w, u1.x, u1.y, u1.z, u1.w};
         const float b2[8] = {v0.x, v0.y, v0.z, v0.w, v1.x, v1.y, v1.z, v1.w};
         const uint32_t ws[4] = {w.x, w.y, w.z, w.w};
+        // the element's integer image m * 2^(e - ebase) = x * 2^(kBias - ebase):
+        // one exact power-of-two FMUL and one float -> int64 conversion (exact
+        // for every element at or above the anchor, truncated below it like the
+        // shift path — such rows fail the guard) instead of ~12 integer
+        // instructions; the shift path remains for stages too small for the
+        // float scale (stage maximum below 2^-72)
+        const int se = kBias - ebase + 127;
+        const bool fast = se >= 1 && se <= 254;
+        const float S = __int_as_float((fast ? se : 127) << 23);
 #pragma unroll
         for (int h = 0; h < 4; ++h) {
-            isum(ws[h] & 0xFFFFu, ebase, pos, neg);
-            isum(ws[h] >> 16, ebase, pos, neg);
             const float xa = bits16_to_float<F>(uint16_t(ws[h] & 0xFFFFu));
             const float xb = bits16_to_float<F>(uint16_t(ws[h] >> 16));
+            if (fast) {
+                pos += static_cast<uint64_t>(__float2ll_rz(__fmul_rn(xa, S)));
+                pos += static_cast<uint64_t>(__float2ll_rz(__fmul_rn(xb, S)));
+            } else {
+                isum(ws[h] & 0xFFFFu, ebase, pos, neg);
+                isum(ws[h] >> 16, ebase, pos, neg);
+            }
             p1 = __fadd_rn(p1, __fmul_rn(b1[2 * h], xa));
             p2 = __fadd_rn(p2, __fmul_rn(b2[2 * h], xa));
             p1 = __fadd_rn(p1, __fmul_rn(b1[2 * h + 1], xb));
