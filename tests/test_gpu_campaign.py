@@ -103,3 +103,31 @@ def test_cta_pair_and_one_cta_kernels_agree(torch_cuda, mode, shape):
     c0, c1 = out[0], out[1]
     assert torch.equal(c0[0].view(torch.int16), c1[0].view(torch.int16))
     assert torch.equal(c0[1], c1[1]) and torch.equal(c0[2], c1[2]) and torch.equal(c0[3], c1[3])
+
+
+@pytest.mark.parametrize("cta_mode", [0, 1])
+def test_statistics_across_magnitudes_bit_exact(torch_cuda, port, cta_mode):
+    """Row statistics inside the GEMM (integer images of the elements, the
+    exactness guard and its sequential fallback) across row magnitudes from
+    BF16 subnormals to 2^60, zero rows and mixed-scale rows: thresholds
+    bit-identical to the oracle's vabft_thresholds."""
+    torch = torch_cuda
+    from paper_2602_08043_b200.fused import FusedAbftGemm
+    m, k, n = 256, 512, 512
+    rng = np.random.default_rng(11)
+    A = rng.standard_normal((m, k))
+    scales = [2.0**-130, 2.0**-100, 2.0**-75, 2.0**-70, 1e-30, 1e-6, 1.0, 2.0**20, 2.0**60]
+    for i in range(m):
+        A[i] *= scales[i % len(scales)]
+    A[5] = 0.0                                   # zero row
+    A[6, ::2] *= 2.0**-40                        # mixed scales inside a row
+    A[7, :64] *= 2.0**-60                        # one tiny stage
+    A = np.array([port.quantize(x, "bf16") for x in A.ravel()]).reshape(m, k)
+    B = np.array([port.quantize(x, "bf16") for x in rng.standard_normal((k, n)).ravel()]).reshape(k, n)
+    g = FusedAbftGemm(torch.from_numpy(B).to(torch.bfloat16).cuda(), e_max=1e-5)
+    g.opts.cta_mode = cta_mode
+    r = g(torch.from_numpy(A).to(torch.bfloat16).cuda())
+    torch.cuda.synchronize()
+    T_ref, _ = port.vabft_thresholds(A, B, 1e-5, fmt="bf16")
+    T = r.T.cpu().numpy()
+    assert np.array_equal(T.view(np.uint64), T_ref.view(np.uint64)), np.where(T != T_ref)[0][:8]
