@@ -417,17 +417,29 @@ __device__ __forceinline__ void stats_warps(const TcParams& p, const uint8_t* sm
                 const int kbase = kb * kBK;
                 const int ng = (p.K - kbase) >= kBK ? 8 : (p.K - kbase) / 8;  // K % 8 == 0: whole granules
                 if (p.epi.debug != 2) {  // 2: ablation, no math
-                    uint32_t amx = 0;
-#pragma unroll 4
-                    for (int c = 0; c < ng; ++c)
-                        acc.track(*reinterpret_cast<const uint4*>(trow + ((c ^ (r & 7)) << 4)), amx);
-                    const int ebase = StatsAcc<kFmt>::anchor(amx);
-                    uint64_t pos = 0, neg = 0;
-#pragma unroll 2
-                    for (int c = 0; c < ng; ++c)
-                        acc.sums(*reinterpret_cast<const uint4*>(trow + ((c ^ (r & 7)) << 4)), sbr1, sbr2, c * 8,
-                                 ebase, pos, neg);
-                    acc.close_stage(pos, neg, ebase);
+                    if (ng == 8) {  // whole stage: one shared-memory pass into registers
+                        uint4 v[8];
+#pragma unroll
+                        for (int c = 0; c < 8; ++c) v[c] = *reinterpret_cast<const uint4*>(trow + ((c ^ (r & 7)) << 4));
+                        uint32_t amx = 0;
+#pragma unroll
+                        for (int c = 0; c < 8; ++c) acc.track(v[c], amx);
+                        const int ebase = StatsAcc<kFmt>::anchor(amx);
+                        uint64_t pos = 0, neg = 0;
+#pragma unroll
+                        for (int c = 0; c < 8; ++c) acc.sums(v[c], sbr1, sbr2, c * 8, ebase, pos, neg);
+                        acc.close_stage(pos, neg, ebase);
+                    } else {
+                        uint32_t amx = 0;
+                        for (int c = 0; c < ng; ++c)
+                            acc.track(*reinterpret_cast<const uint4*>(trow + ((c ^ (r & 7)) << 4)), amx);
+                        const int ebase = StatsAcc<kFmt>::anchor(amx);
+                        uint64_t pos = 0, neg = 0;
+                        for (int c = 0; c < ng; ++c)
+                            acc.sums(*reinterpret_cast<const uint4*>(trow + ((c ^ (r & 7)) << 4)), sbr1, sbr2,
+                                     c * 8, ebase, pos, neg);
+                        acc.close_stage(pos, neg, ebase);
+                    }
                 }
                 __syncwarp();
                 if (lane == 0) mbar_arrive(smem_u32(&sempty_bar[slot]));
