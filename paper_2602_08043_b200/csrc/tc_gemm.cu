@@ -376,7 +376,7 @@ __device__ __forceinline__ void stats_producer(const TcParams& p, const CUtensor
         for (int b = n_blk; n_blk < stats_tiles(p) && b < nblk; b += stats_tiles(p)) {
             for (int kb = 2 * b; kb < 2 * b + 2 && kb < p.num_k_blk; ++kb, ++cnt) {
                 const int slot = int(cnt & 1u);
-                mbar_wait(smem_u32(&sempty_bar[slot]), ((cnt >> 1) & 1u) ^ 1u);
+                mbar_wait_sleep(smem_u32(&sempty_bar[slot]), ((cnt >> 1) & 1u) ^ 1u, 1000000u);
                 const uint32_t sb = smem_u32(&sfull_bar[slot]);
                 // slot layout: [A tile 0][A tile 1] (1024-aligned for SW128), then the
                 // [B r1 | B r2] segments; the br arrays are padded to 128 entries
@@ -410,7 +410,7 @@ __device__ __forceinline__ void stats_warps(const TcParams& p, const uint8_t* sm
         for (int b = n_blk; n_blk < stats_tiles(p) && b < nblk; b += stats_tiles(p)) {
             for (int kb = 2 * b; kb < 2 * b + 2 && kb < p.num_k_blk; ++kb, ++cnt) {
                 const int slot = int(cnt & 1u);
-                mbar_wait(smem_u32(&sfull_bar[slot]), (cnt >> 1) & 1u);
+                mbar_wait_sleep(smem_u32(&sfull_bar[slot]), (cnt >> 1) & 1u, 1000000u);
                 const uint8_t* trow = smS + slot * kABytes + r * 128;
                 const float* sbr1 = reinterpret_cast<const float*>(smS + 2 * kABytes + slot * (2 * kBK * 4));
                 const float* sbr2 = sbr1 + kBK;
@@ -670,7 +670,7 @@ __global__ void __launch_bounds__(kThreadsStats, 1)
                 }
             }
 
-            mbar_wait(smem_u32(&tfull_bar[acc]), acc_phase);
+            mbar_wait_sleep(smem_u32(&tfull_bar[acc]), acc_phase, 1000000u);
             tc_fence_after();
 
             float s1 = 0.0f, s2 = 0.0f;
