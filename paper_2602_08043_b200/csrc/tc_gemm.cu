@@ -350,10 +350,14 @@ struct StatsAcc {
                 isum(ws[h] & 0xFFFFu, ebase, pos, neg);
                 isum(ws[h] >> 16, ebase, pos, neg);
             }
-            p1 = __fadd_rn(p1, __fmul_rn(b1[2 * h], xa));
-            p2 = __fadd_rn(p2, __fmul_rn(b2[2 * h], xa));
-            p1 = __fadd_rn(p1, __fmul_rn(b1[2 * h + 1], xb));
-            p2 = __fadd_rn(p2, __fmul_rn(b2[2 * h + 1], xb));
+            // the two checksum chains' sums as one packed FADD2 per element.
+            // Products stay scalar FMUL: ptxas (12.9) contracts mul.rn.f32x2 +
+            // add.rn.f32x2 into FFMA2, which would change the rounding.
+            float2 pp = make_float2(p1, p2);
+            pp = __fadd2_rn(pp, make_float2(__fmul_rn(b1[2 * h], xa), __fmul_rn(b2[2 * h], xa)));
+            pp = __fadd2_rn(pp, make_float2(__fmul_rn(b1[2 * h + 1], xb), __fmul_rn(b2[2 * h + 1], xb)));
+            p1 = pp.x;
+            p2 = pp.y;
         }
     }
     // close a stage: s += (pos - neg) * 2^(ebase - kBias), exact under the guard
@@ -704,8 +708,11 @@ __global__ void __launch_bounds__(kThreadsStats, 1)
                         }
                         const float f = bits16_to_float<kFmt>(q);
                         if (col < p.N) {
-                            s1 = __fadd_rn(s1, f);
-                            s2 = __fadd_rn(s2, __fmul_rn(float(col + 1), f));
+                            // (s1, s2) += (f, (col + 1) f) as one FADD2 (scalar product, see sums)
+                            const float2 sp =
+                                __fadd2_rn(make_float2(s1, s2), make_float2(f, __fmul_rn(float(col + 1), f)));
+                            s1 = sp.x;
+                            s2 = sp.y;
                         }
                     } else {
                         if constexpr (kAbft == 1 && kInject) {
@@ -726,8 +733,10 @@ __global__ void __launch_bounds__(kThreadsStats, 1)
                         }
                         if constexpr (kAbft == 1) {
                             if (col < p.N) {
-                                s1 = __fadd_rn(s1, x);
-                                s2 = __fadd_rn(s2, __fmul_rn(float(col + 1), x));
+                                const float2 sp =
+                                    __fadd2_rn(make_float2(s1, s2), make_float2(x, __fmul_rn(float(col + 1), x)));
+                                s1 = sp.x;
+                                s2 = sp.y;
                             }
                         }
                         q = quantize16_bits<kFmt>(x);
