@@ -78,6 +78,9 @@ static_assert((2 * kStages + 9 + kTailWarps) * 8 <= 256, "barrier area");
 struct TcParams {
     int M, N, K;
     int num_m_blk, num_n_blk, num_k_blk, num_tiles;
+    // work units of the persistent loop: tiles [0, split_from) whole, each
+    // later tile as two 128-column halves (pair mode's under-filled last wave)
+    int split_from, num_units;
     int group_m;  // tile raster: groups of group_m row blocks, n-major inside a group
     int pair;     // 1: CTA-pair kernel (tiles of 256 rows, num_m_blk in 256-row blocks)
     uint16_t* C;
@@ -114,6 +117,23 @@ __device__ __forceinline__ void cta_tile(const TcParams& p, int tile, int& m_blk
     tile_coords(p, tile, m_blk, n_blk);
     if (p.pair) m_blk = 2 * m_blk + int(cluster_ctarank());
 }
+// Work unit u: its tile, and half = -1 (whole 256-column tile) or 0 / 1 (the
+// tile's left / right 128 columns). Splitting the last wave's tiles when it
+// would leave more than half the pairs idle: 4096^3 is 256 pair tiles = 3
+// waves of 74 + 34, and the 34 become 68 half tiles (each CTA then streams
+// 8 KiB of B per k-block; the whole tile would stream 16).
+__device__ __forceinline__ void cta_unit(const TcParams& p, int u, int& m_blk, int& n_blk, int& half) {
+    int tile = u;
+    half = -1;
+    if (u >= p.split_from) {
+        tile = p.split_from + ((u - p.split_from) >> 1);
+        half = (u - p.split_from) & 1;
+    }
+    cta_tile(p, tile, m_blk, n_blk);
+}
+// arrival weight of a unit on the streamed-verification counters: a whole
+// tile counts 2, a half 1 (targets are 2 per N tile)
+__device__ __forceinline__ unsigned int unit_weight(int half) { return half < 0 ? 2u : 1u; }
 
 // Streamed verification (see TcEpilogue::stream_verify). Per 32-row group g
 // two self-resetting counters: group_cnt[2g] counts statistics arrivals (one
@@ -122,26 +142,27 @@ __device__ __forceinline__ void cta_tile(const TcParams& p, int tile, int& m_blk
 // partial / atomic writes before lane 0's acq_rel RMW at GPU scope (release
 // is cumulative); the acquire side orders the verifier's L2 reads after all
 // earlier arrivals. (A __threadfence per lane is fence.sc + L1 invalidate.)
-__device__ __forceinline__ unsigned int warp_arrive(unsigned int* cnt) {
+__device__ __forceinline__ unsigned int warp_arrive(unsigned int* cnt, unsigned int w) {
     __syncwarp();
     unsigned int old = 0;
-    if ((threadIdx.x & 31) == 0) old = atom_add_acq_rel_gpu(cnt, 1u);
+    if ((threadIdx.x & 31) == 0) old = atom_add_acq_rel_gpu(cnt, w);
     return __shfl_sync(0xffffffffu, old, 0);
 }
 
 template <int F>
-__device__ __forceinline__ void final_arrive(const TcParams& p, int64_t g) {
+__device__ __forceinline__ void final_arrive(const TcParams& p, int64_t g, unsigned int w) {
     unsigned int* cnt = p.epi.group_cnt + 2 * g + 1;
-    if (warp_arrive(cnt) != unsigned(p.num_n_blk)) return;  // target num_n_blk + 1
+    // target 2 num_n_blk (epilogue units) + 2 (the statistics half)
+    if (warp_arrive(cnt, w) + w != 2u * unsigned(p.num_n_blk) + 2u) return;
     if (p.epi.debug != 7 && p.epi.debug != 9) final_half_direct<F>(p.epi.tail, g);  // 7: no verification, 9: no final half
     __syncwarp();
     if ((threadIdx.x & 31) == 0) *cnt = 0u;  // ready for the next launch
 }
 
 template <int F>
-__device__ __forceinline__ void stats_arrive(const TcParams& p, int64_t g) {
+__device__ __forceinline__ void stats_arrive(const TcParams& p, int64_t g, unsigned int w) {
     unsigned int* cnt = p.epi.group_cnt + 2 * g;
-    if (warp_arrive(cnt) != unsigned(p.num_n_blk) - 1u) return;
+    if (warp_arrive(cnt, w) + w != 2u * unsigned(p.num_n_blk)) return;
     const unsigned long long t0 = p.epi.trace ? gtime() : 0ull;
     if (p.epi.debug != 7 && p.epi.debug != 8) stats_half_direct<F>(p.epi.tail, g);
     if (p.epi.trace && (threadIdx.x & 31) == 0) {
@@ -150,7 +171,7 @@ __device__ __forceinline__ void stats_arrive(const TcParams& p, int64_t g) {
     }  // 8: no statistics half
     __syncwarp();
     if ((threadIdx.x & 31) == 0) *cnt = 0u;
-    final_arrive<F>(p, g);
+    final_arrive<F>(p, g, 2u);
 }
 
 // ----------------------------------------------------- operand faults
@@ -374,10 +395,12 @@ __device__ __forceinline__ void stats_producer(const TcParams& p, const CUtensor
                                                uint64_t* sfull_bar, uint64_t* sempty_bar) {
     uint32_t cnt = 0;
     const int nblk = (p.K + 127) / 128;
-    for (int tile = tile_first(p); tile < p.num_tiles; tile += tile_stride(p)) {
-        int m_blk, n_blk;
-        cta_tile(p, tile, m_blk, n_blk);
-        for (int b = n_blk; n_blk < stats_tiles(p) && b < nblk; b += stats_tiles(p)) {
+    for (int u = tile_first(p); u < p.num_units; u += tile_stride(p)) {
+        int m_blk, n_blk, half;
+        cta_unit(p, u, m_blk, n_blk, half);
+        // a half tile takes every other one of its tile's blocks
+        const int st = stats_tiles(p) * (half < 0 ? 1 : 2);
+        for (int b = n_blk + (half > 0 ? stats_tiles(p) : 0); n_blk < stats_tiles(p) && b < nblk; b += st) {
             for (int kb = 2 * b; kb < 2 * b + 2 && kb < p.num_k_blk; ++kb, ++cnt) {
                 const int slot = int(cnt & 1u);
                 mbar_wait_sleep(smem_u32(&sempty_bar[slot]), ((cnt >> 1) & 1u) ^ 1u, 1000000u);
@@ -407,11 +430,12 @@ __device__ __forceinline__ void stats_warps(const TcParams& p, const uint8_t* sm
     acc.reset();
     uint32_t cnt = 0;  // statistics stages consumed: slot = cnt & 1, phase = (cnt >> 1) & 1
     const int nblk = (p.K + 127) / 128;
-    for (int tile = tile_first(p); tile < p.num_tiles; tile += tile_stride(p)) {
-        int m_blk, n_blk;
-        cta_tile(p, tile, m_blk, n_blk);
+    for (int u = tile_first(p); u < p.num_units; u += tile_stride(p)) {
+        int m_blk, n_blk, half;
+        cta_unit(p, u, m_blk, n_blk, half);
         const int row = m_blk * kBM + r;
-        for (int b = n_blk; n_blk < stats_tiles(p) && b < nblk; b += stats_tiles(p)) {
+        const int st = stats_tiles(p) * (half < 0 ? 1 : 2);  // as stats_producer
+        for (int b = n_blk + (half > 0 ? stats_tiles(p) : 0); n_blk < stats_tiles(p) && b < nblk; b += st) {
             for (int kb = 2 * b; kb < 2 * b + 2 && kb < p.num_k_blk; ++kb, ++cnt) {
                 const int slot = int(cnt & 1u);
                 mbar_wait_sleep(smem_u32(&sfull_bar[slot]), (cnt >> 1) & 1u, 1000000u);
@@ -467,7 +491,7 @@ __device__ __forceinline__ void stats_warps(const TcParams& p, const uint8_t* sm
             acc.reset();
         }
         if (p.epi.stream_verify && (int64_t(m_blk) * 4 + sw) * 32 < p.M)
-            stats_arrive<kFmt>(p, int64_t(m_blk) * 4 + sw);
+            stats_arrive<kFmt>(p, int64_t(m_blk) * 4 + sw, unit_weight(half));
     }
     if (p.epi.trace && lane == 0) atomicMax(p.epi.trace + blockIdx.x * 8 + 3, gtime());
 }
@@ -538,24 +562,24 @@ __global__ void __launch_bounds__(kThreadsStats, 1)
             // ------------------------------------------------ TMA producer
             int stage = 0;
             uint32_t phase = 0;
-            for (int tile = tile_first(p); tile < p.num_tiles; tile += tile_stride(p)) {
-                int m_blk, n_blk;
-                cta_tile(p, tile, m_blk, n_blk);
+            for (int u = tile_first(p); u < p.num_units; u += tile_stride(p)) {
+                int m_blk, n_blk, half;
+                cta_unit(p, u, m_blk, n_blk, half);
+                const int nw = half < 0 ? kBN : kBN / 2;              // unit width
+                const int n0 = n_blk * kBN + (half > 0 ? kBN / 2 : 0);  // first column
                 for (int kb = 0; kb < p.num_k_blk; ++kb) {
                     mbar_wait(smem_u32(&empty_bar[stage]), phase ^ 1);
                     const uint32_t fb = smem_u32(&full_bar[stage]);
                     const uint32_t adst = smem_u32(smA + stage * kABytes);
                     const uint32_t bdst = smem_u32(smB + stage * kBB);
                     if constexpr (kPair) {
-                        // this CTA's 128 A rows and 128 of the tile's 256 B columns,
+                        // this CTA's 128 A rows and nw / 2 of the unit's nw B columns,
                         // completion bytes on the leader's full barrier
-                        if (rank == 0) mbar_arrive_expect_tx(fb, 2 * kSB);
+                        if (rank == 0) mbar_arrive_expect_tx(fb, 2 * (kABytes + uint32_t(nw) * kBK));
                         else mbar_arrive_cluster_relaxed(mapa_shared(fb, 0));
                         tma_load_2d_pair(adst, &tmA, fb, kb * kBK, m_blk * kBM);
-#pragma unroll
-                        for (int c = 0; c < 2; ++c)
-                            tma_load_2d_pair(bdst + c * 8192, &tmB, fb, n_blk * kBN + int(rank) * 128 + c * 64,
-                                             kb * kBK);
+                        for (int c = 0; c < nw / 128; ++c)
+                            tma_load_2d_pair(bdst + c * 8192, &tmB, fb, n0 + int(rank) * (nw / 2) + c * 64, kb * kBK);
                     } else {
                         mbar_arrive_expect_tx(fb, kStageBytes);
                         tma_load_2d(adst, &tmA, fb, kb * kBK, m_blk * kBM);
@@ -584,13 +608,16 @@ __global__ void __launch_bounds__(kThreadsStats, 1)
             // --------------------------------------------------- MMA issuer
             constexpr uint32_t idesc =
                 umma_idesc_f16(kFmt == VABFT_BF16 ? 1u : 0u, !kBKMajor, kPair ? 2 * kBM : kBM, kBN);
+            constexpr uint32_t idesc_half =
+                umma_idesc_f16(kFmt == VABFT_BF16 ? 1u : 0u, !kBKMajor, kPair ? 2 * kBM : kBM, kBN / 2);
             int stage = 0;
             uint32_t phase = 0;
             int acc = 0;
             uint32_t acc_phase = 0;
-            for (int tile = tile_first(p); tile < p.num_tiles; tile += tile_stride(p)) {
-                int m_blk = 0, n_blk = 0;
-                if (opf) cta_tile(p, tile, m_blk, n_blk);
+            for (int u = tile_first(p); u < p.num_units; u += tile_stride(p)) {
+                int m_blk = 0, n_blk = 0, half = -1;
+                cta_unit(p, u, m_blk, n_blk, half);
+                const uint32_t id = half < 0 ? idesc : idesc_half;
                 if (lane == 0) {
                     mbar_wait(smem_u32(&tempty_bar[acc]), acc_phase ^ 1);
                     tc_fence_after();
@@ -618,9 +645,9 @@ __global__ void __launch_bounds__(kThreadsStats, 1)
                             const uint64_t a_off = uint64_t((k * 32) >> 4);
                             const uint64_t b_off = kBKMajor ? uint64_t((k * 32) >> 4) : uint64_t((k * 2048) >> 4);
                             if constexpr (kPair)
-                                umma_f16_pair(d_tmem, adesc + a_off, bdesc + b_off, idesc, (kb > 0 || k > 0) ? 1u : 0u);
+                                umma_f16_pair(d_tmem, adesc + a_off, bdesc + b_off, id, (kb > 0 || k > 0) ? 1u : 0u);
                             else
-                                umma_f16(d_tmem, adesc + a_off, bdesc + b_off, idesc, (kb > 0 || k > 0) ? 1u : 0u);
+                                umma_f16(d_tmem, adesc + a_off, bdesc + b_off, id, (kb > 0 || k > 0) ? 1u : 0u);
                         }
                         // frees the stage in both CTAs of a pair
                         if constexpr (kPair) umma_commit_pair(smem_u32(&empty_bar[stage]), 0x3);
@@ -654,18 +681,19 @@ __global__ void __launch_bounds__(kThreadsStats, 1)
         const int row_in_tile = quad * 32 + lane;
         int acc = 0;
         uint32_t acc_phase = 0;
-        for (int tile = tile_first(p); tile < p.num_tiles; tile += tile_stride(p)) {
-            int m_blk, n_blk;
-            cta_tile(p, tile, m_blk, n_blk);
+        for (int u = tile_first(p); u < p.num_units; u += tile_stride(p)) {
+            int m_blk, n_blk, half;
+            cta_unit(p, u, m_blk, n_blk, half);
             const int row = m_blk * kBM + row_in_tile;
             const bool row_ok = row < p.M;
-            const int n0 = n_blk * kBN;
+            const int nw = half < 0 ? kBN : kBN / 2;
+            const int n0 = n_blk * kBN + (half > 0 ? kBN / 2 : 0);
 
             int fcol = -1, fbit = 0, fdir = 0;
             if constexpr (kInject) {
                 if (row_ok && p.epi.fault_target == 0) {
                     fcol = p.epi.fault_col[row];
-                    if (fcol >= n0 && fcol < n0 + kBN) {
+                    if (fcol >= n0 && fcol < n0 + nw) {
                         fbit = p.epi.fault_bit[row];
                         fdir = p.epi.fault_dir[row];
                     } else {
@@ -679,7 +707,7 @@ __global__ void __launch_bounds__(kThreadsStats, 1)
 
             float s1 = 0.0f, s2 = 0.0f;
 #pragma unroll 1
-            for (int c = 0; c < kBN; c += 32) {
+            for (int c = 0; c < nw; c += 32) {
                 uint32_t v[32];
                 tmem_ld32(tmem_base + (uint32_t(quad * 32) << 16) + uint32_t(acc * kBN + c), v);
                 tmem_wait_ld();
@@ -798,7 +826,7 @@ __global__ void __launch_bounds__(kThreadsStats, 1)
             }
             if constexpr (kStats) {
                 if (p.epi.stream_verify && (int64_t(m_blk) * 4 + quad) * 32 < p.M)
-                    final_arrive<kFmt>(p, int64_t(m_blk) * 4 + quad);
+                    final_arrive<kFmt>(p, int64_t(m_blk) * 4 + quad, unit_weight(half));
             }
         }
         if (p.epi.trace && lane == 0) atomicMax(p.epi.trace + blockIdx.x * 8 + 2, gtime());
@@ -913,11 +941,11 @@ void launch_inst(const CUtensorMap& ta, const CUtensorMap& tb, const TcParams& p
             check_cuda(cudaOccupancyMaxActiveClusters(&n, kern, &q), "cudaOccupancyMaxActiveClusters");
             return n > 0 ? n : 1;
         }();
-        const int pairs = p.num_tiles < max_clusters ? p.num_tiles : max_clusters;
+        const int pairs = p.num_units < max_clusters ? p.num_units : max_clusters;
         cfg.gridDim = dim3(unsigned(2 * pairs));
         check_cuda(cudaLaunchKernelEx(&cfg, kern, ta, tb, p), "tc_gemm pair launch");
     } else {
-        const int grid = p.num_tiles < sm_count() ? p.num_tiles : sm_count();
+        const int grid = p.num_units < sm_count() ? p.num_units : sm_count();
         if (kStats && p.epi.tail_phases) {
             // the in-kernel verify tail synchronizes the grid: cooperative launch
             // guarantees every CTA is co-resident (grid <= #SMs, 1 CTA/SM)
@@ -1018,6 +1046,8 @@ void tc_gemm_launch(int fmt, bool b_kmajor, int64_t M, int64_t N, int64_t K, con
     p.num_n_blk = int((N + kBN - 1) / kBN);
     p.num_k_blk = int((K + kBK - 1) / kBK);
     p.num_tiles = p.num_m_blk * p.num_n_blk;
+    p.split_from = p.num_tiles;
+    p.num_units = p.num_tiles;
     static const int raster_env = [] {
         const char* e = std::getenv("VABFT_RASTER_GROUP");  // developer override
         return e ? std::atoi(e) : 0;
@@ -1051,6 +1081,17 @@ void tc_gemm_launch(int fmt, bool b_kmajor, int64_t M, int64_t N, int64_t K, con
         p.num_tiles = p.num_m_blk * p.num_n_blk;
         const int g = raster / 2;
         p.group_m = g <= 0 || g > p.num_m_blk ? p.num_m_blk : g;
+        // split the last wave's tiles into halves when it would leave more
+        // than half the pairs idle (VABFT_SPLIT_LAST = 0 disables)
+        static const bool split_env = [] {
+            const char* e = std::getenv("VABFT_SPLIT_LAST");
+            return !(e && std::atoi(e) == 0);
+        }();
+        const int pairs = sm_count() / 2;
+        const int rem = p.num_tiles % pairs;
+        p.split_from = p.num_tiles;
+        if (split_env && p.num_tiles > pairs && rem > 0 && 2 * rem <= pairs && N > kBN / 2) p.split_from = p.num_tiles - rem;
+        p.num_units = p.split_from + 2 * (p.num_tiles - p.split_from);
     }
     const CUtensorMap ta = make_map_2d(fmt, A, uint64_t(M), uint64_t(K), kBK, kBM);
     const CUtensorMap tb = b_kmajor ? make_map_2d(fmt, B, uint64_t(N), uint64_t(K), kBK, kBN)

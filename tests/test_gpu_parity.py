@@ -235,3 +235,23 @@ def test_plain_gemm_matches_torch(api):
             ref = a.float() @ b.float()
             bound = (k + 1) * 2.0**-24 * (a.float().abs() @ b.float().abs()) + ref.abs() * 2.0**-8
             assert bool(((c.float() - ref).abs() <= bound).all())
+
+
+def test_plain_gemm_pair_split_last_wave_matches_one_cta(api):
+    """Plain GEMM at shapes whose last pair wave runs as 128-column half tiles
+    (4096 x 4096: 256 pair tiles over 74 pairs; 2560 x 4000 ragged): C is
+    bit-identical to the one-CTA kernel's."""
+    import torch
+    from paper_2602_08043_b200 import _capi
+    from paper_2602_08043_b200.device import ptr, stream_ptr
+    torch.manual_seed(1)
+    for (m, n, k) in [(4096, 4096, 256), (2560, 4000, 128)]:
+        a = torch.randn(m, k, device="cuda").bfloat16()
+        b = torch.randn(k, n, device="cuda").bfloat16()
+        out = []
+        for mode in (0, 1):
+            c = torch.full((m, n), float("nan"), device="cuda", dtype=torch.bfloat16)
+            _capi.check(_capi.lib.vabft_gemm_plain_mode(0, 0, m, n, k, ptr(a), ptr(b), ptr(c), mode, stream_ptr()))
+            out.append(c)
+        torch.cuda.synchronize()
+        assert torch.equal(out[0].view(torch.int16), out[1].view(torch.int16))
