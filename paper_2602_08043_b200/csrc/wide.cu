@@ -464,28 +464,38 @@ __global__ void __launch_bounds__(256) wide_tail_kernel(const WideTail a) {
             if (!safe) {
                 // the reference's sequential loop (stats.cpp:12-24) — rows whose exact
                 // sum sits on a rounding midpoint (measured ~1 in 4096 for FP64 N(0,1)
-                // rows at K = 4096). The warp streams the row in coalesced 32-element
-                // chunks (next chunk in flight) and lane 0 walks them in order.
+                // rows at K = 4096). The warp loads the row 512 elements at a time
+                // (16 coalesced loads per lane in flight: one HBM round trip per 512
+                // elements, where a 32-element chunk per trip made the fallback
+                // latency-bound at ~73 us for K = 4096) and lane 0 walks them in order.
                 if (lane == 0 && a.counts) atomicAdd(&cnt[VABFT_COUNT_SLOW_STATS], 1ull);
                 const T* arow = static_cast<const T*>(a.A) + i * a.K;
                 ns = Neu{};
-                T nxt = lane < a.K ? arow[lane] : T(0);
-                for (int64_t j0 = 0; j0 < a.K; j0 += 32) {
-                    const T cur = nxt;
-                    nxt = j0 + 32 + lane < a.K ? arow[j0 + 32 + lane] : T(0);
-                    const int n = a.K - j0 < 32 ? int(a.K - j0) : 32;
-                    if (n == 32) {
-                        double xs[32];  // all 32 shuffles issued ahead of the sequential chain
+                constexpr int kR = 16;
+                for (int64_t j0 = 0; j0 < a.K; j0 += 32 * kR) {
+                    T v[kR];
 #pragma unroll
-                        for (int l = 0; l < 32; ++l) xs[l] = double(__shfl_sync(0xffffffffu, cur, l));
-                        if (lane == 0) {
+                    for (int r = 0; r < kR; ++r) {
+                        const int64_t j = j0 + r * 32 + lane;
+                        v[r] = j < a.K ? arow[j] : T(0);
+                    }
 #pragma unroll
-                            for (int l = 0; l < 32; ++l) ns.add(xs[l]);
-                        }
-                    } else {
-                        for (int l = 0; l < n; ++l) {
-                            const double x = double(__shfl_sync(0xffffffffu, cur, l));
-                            if (lane == 0) ns.add(x);
+                    for (int r = 0; r < kR; ++r) {
+                        const int64_t n = a.K - j0 - r * 32;  // warp-uniform
+                        if (n <= 0) break;
+                        if (n >= 32) {
+                            double xs[32];  // all 32 shuffles issued ahead of the sequential chain
+#pragma unroll
+                            for (int l = 0; l < 32; ++l) xs[l] = double(__shfl_sync(0xffffffffu, v[r], l));
+                            if (lane == 0) {
+#pragma unroll
+                                for (int l = 0; l < 32; ++l) ns.add(xs[l]);
+                            }
+                        } else {
+                            for (int l = 0; l < int(n); ++l) {
+                                const double x = double(__shfl_sync(0xffffffffu, v[r], l));
+                                if (lane == 0) ns.add(x);
+                            }
                         }
                     }
                 }

@@ -8,7 +8,8 @@ from paper_2602_08043_b200 import _capi  # noqa: E402
 from paper_2602_08043_b200.fused import FusedAbftGemm  # noqa: E402
 lib = _capi.lib
 lib.vabft_debug_trace.argtypes = [ctypes.POINTER(ctypes.c_ulonglong), ctypes.c_int, ctypes.c_int]
-m = k = n = int(sys.argv[1]) if len(sys.argv) > 1 else 4096
+arg = sys.argv[1] if len(sys.argv) > 1 else "4096"
+m, k, n = (int(x) for x in arg.split("x")) if "x" in arg else (int(arg),) * 3
 A = torch.randn(m, k, device="cuda").bfloat16(); B = torch.randn(k, n, device="cuda").bfloat16()
 g = FusedAbftGemm(B)
 flush = torch.empty(512 * 1024 * 1024, dtype=torch.uint8, device="cuda") if os.environ.get("FLUSH") else None
@@ -19,7 +20,7 @@ for it in range(4):
     if flush is not None:
         flush.zero_()
     torch.cuda.synchronize()
-    g(A); torch.cuda.synchronize()
+    res = g(A); torch.cuda.synchronize()
     lib.vabft_debug_trace(buf, 148 * 8, 0)
 t = np.array(buf, dtype=np.int64).reshape(148, 8).astype(np.float64)
 t0 = t[:, 0].min()
@@ -33,6 +34,8 @@ for c, nm in enumerate(names):
 sh_ns, sh_n = t[:, 6], t[:, 7]
 print(f"  stats-half calls: total {int(sh_n.sum())}, max per CTA {int(sh_n.max())}, "
       f"mean duration {sh_ns.sum() / max(sh_n.sum(), 1) / 1000:.2f} us, max CTA total {sh_ns.max() / 1000:.1f} us")
+if res.counts is not None:
+    print("  counts [rows, detected, located, nan, slow_stats, corrected]:", res.counts.tolist())
 late = np.argsort(-r[:, 5])[:6]
 print("  latest-ending CTAs (cta: mma_end epi_end stats_end pre_teardown end):")
 for i in late:
