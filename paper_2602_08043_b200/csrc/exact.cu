@@ -250,6 +250,46 @@ __global__ void exact_row_reduce_kernel(const ET<F>* __restrict__ X, int64_t row
     }
 }
 
+// Warp per row for term 0 in NativeBlocked(128) order with the storage type
+// as working type (FP32 / FP64 B r1 / B r2 of the fused path's weights):
+// lane l sums blocks l, l + 32, ... in order (radd / rmul exactly as
+// Reducer's BLOCKED path), then the block partials are added in block order.
+// exact_row_reduce_kernel's thread-per-row walk took 1.9 ms for a 4096 x 4096
+// FP32 weight (32 CTAs); this is one read of the matrix.
+template <class T>
+__global__ void __launch_bounds__(256) blocked128_row_reduce_kernel(const T* __restrict__ X, int64_t rows,
+                                                                   int64_t cols, int qfmt, double* out1,
+                                                                   double* out2) {
+    const int lane = threadIdx.x & 31;
+    const int64_t r = int64_t(blockIdx.x) * 8 + (threadIdx.x >> 5);
+    if (r >= rows) return;
+    const T* row = X + r * cols;
+    const int64_t nblk = (cols + 127) / 128;
+    T acc1 = T(0), acc2 = T(0);
+    for (int64_t b0 = 0; b0 < nblk; b0 += 32) {
+        T p1 = T(0), p2 = T(0);
+        const int64_t b = b0 + lane;
+        if (b < nblk) {
+            const int64_t j0 = b * 128, j1 = cols < j0 + 128 ? cols : j0 + 128;
+#pragma unroll 8
+            for (int64_t j = j0; j < j1; ++j) {
+                const T x = __ldg(row + j);
+                p1 = radd(p1, x);
+                p2 = radd(p2, rmul(T(j + 1), x));
+            }
+        }
+        const int cnt = int(nblk - b0 < 32 ? nblk - b0 : 32);
+        for (int l = 0; l < cnt; ++l) {
+            acc1 = radd(acc1, __shfl_sync(0xffffffffu, p1, l));
+            acc2 = radd(acc2, __shfl_sync(0xffffffffu, p2, l));
+        }
+    }
+    if (lane == 0) {
+        out1[r] = quantize_checksum(double(acc1), qfmt);
+        out2[r] = quantize_checksum(double(acc2), qfmt);
+    }
+}
+
 // ---------------------------------------------------- column reductions
 // One thread per column j of an R x L matrix (coalesced across threads),
 // reducing over rows in order:
@@ -469,6 +509,17 @@ static void col_reduce_t(int term, const vabft_accum& acc, int64_t rows, int64_t
 void launch_row_reduce(int src_fmt, bool flt, int term, const vabft_accum& acc, int64_t rows,
                        int64_t cols, const void* X, const double* w1, const double* w2, int qfmt,
                        double* o1, double* o2, cudaStream_t s) {
+    const bool blocked128 = acc.kind == VABFT_ACCUM_BLOCKED && (acc.block_len <= 0 || acc.block_len == 128);
+    if (term == 0 && blocked128 && rows > 0 && cols > 0 &&
+        ((src_fmt == VABFT_FP32 && flt) || (src_fmt == VABFT_FP64 && !flt))) {
+        const unsigned grid = unsigned((rows + 7) / 8);
+        if (src_fmt == VABFT_FP32)
+            blocked128_row_reduce_kernel<float><<<grid, 256, 0, s>>>(static_cast<const float*>(X), rows, cols, qfmt, o1, o2);
+        else
+            blocked128_row_reduce_kernel<double><<<grid, 256, 0, s>>>(static_cast<const double*>(X), rows, cols, qfmt, o1, o2);
+        check_cuda(cudaGetLastError(), "blocked row reduce launch");
+        return;
+    }
     VABFT_DISPATCH_RED(row_reduce_t, src_fmt, flt, term, acc, rows, cols, X, w1, w2, qfmt, o1, o2, s);
 }
 
