@@ -332,3 +332,34 @@ def test_wide_operand_faults_match_oracle(torch_cuda, port, fmt, target, bit):
     assert np.array_equal(v["detected"], r.detected.cpu().numpy().astype(bool))
     assert np.array_equal(v["location"], r.location.cpu().numpy())
     assert int(counts[1].item()) == int(v["detected"].sum()) and v["detected"].any()
+
+
+@pytest.mark.parametrize("fmt", ["fp32", "fp64"])
+def test_wide_bside_row_sums_guard_and_fallback(torch_cuda, port, fmt):
+    """B-side row statistics of a wide-format weight: rows whose order-free
+    warp sum is exact under the guard, rows with tiny elements that take the
+    sequential (batched-load) loops, a zero row and a row with a lone
+    subnormal-scale element: thresholds and checksums bit-exact vs the oracle."""
+    torch = torch_cuda
+    from paper_2602_08043_b200.fused import FusedAbftGemm
+    rng = np.random.default_rng(11)
+    m, k, n = 64, 96, 1096  # ragged last 128-column block
+    dt = np.float32 if fmt == "fp32" else np.float64
+    B = rng.standard_normal((k, n)).astype(dt)
+    B[3, ::7] *= dt(1e-12)
+    B[5] = 0.0
+    B[9] = 0.0
+    B[9, 17] = dt(3e-30)
+    B[11] = (rng.standard_normal(n) * 1e6).astype(dt)
+    B[11, 1] = dt(1e-20)
+    A = rng.standard_normal((m, k)).astype(dt)
+    A64, B64 = A.astype(np.float64), B.astype(np.float64)
+    e_max = 1e-5
+    g = FusedAbftGemm(torch.from_numpy(B).cuda(), mode="online", e_max=e_max)
+    r = g(torch.from_numpy(A).cuda(), checksums=True)
+    torch.cuda.synchronize()
+    T_ref, _ = port.vabft_thresholds(A64, B64, e_max, fmt=fmt)
+    assert same(r.T.cpu().numpy(), T_ref)
+    o = port.encode_and_multiply(A64, B64, fmt, "online", accum=BLK)
+    assert same(r.row_check1.cpu().numpy(), o.row_check1) and same(r.row_check2.cpu().numpy(), o.row_check2)
+    assert int(r.detected.sum().item()) == 0
