@@ -42,12 +42,15 @@ struct Elem<VABFT_FP64> {
 // --------------------------------------------------- Neumaier (stats.cpp)
 struct Neu {
     double s = 0.0, c = 0.0;
+    // Branch-free (selects, same operations and order as stats.cpp:16-21):
+    // in an unrolled run of adds the scheduler can issue the next element's
+    // s + x while this element's compensation is still in flight (the
+    // sequential-fallback rows of wide_tail_kernel; DESIGN "tie rows").
     __device__ __forceinline__ void add(double x) {
         const double t = __dadd_rn(s, x);
-        if (fabs(s) >= fabs(x))
-            c = __dadd_rn(c, __dadd_rn(__dsub_rn(s, t), x));
-        else
-            c = __dadd_rn(c, __dadd_rn(__dsub_rn(x, t), s));
+        const bool ge = fabs(s) >= fabs(x);
+        const double hi = ge ? s : x, lo = ge ? x : s;
+        c = __dadd_rn(c, __dadd_rn(__dsub_rn(hi, t), lo));
         s = t;
     }
     // Merge two compensated partials (TwoSum of the heads, sum of tails).

@@ -464,39 +464,51 @@ __global__ void __launch_bounds__(256) wide_tail_kernel(const WideTail a) {
             if (!safe) {
                 // the reference's sequential loop (stats.cpp:12-24) — rows whose exact
                 // sum sits on a rounding midpoint (measured ~1 in 4096 for FP64 N(0,1)
-                // rows at K = 4096). The warp loads the row 512 elements at a time
-                // (16 coalesced loads per lane in flight: one HBM round trip per 512
-                // elements, where a 32-element chunk per trip made the fallback
-                // latency-bound at ~73 us for K = 4096) and lane 0 walks them in order.
+                // rows at K = 4096, ~1 in 10^5 FP32 rows). The warp stages the row
+                // 256 elements at a time in its own shared-memory slice (8 coalesced
+                // loads per lane in flight), then lane 0 reads 32 elements per batch
+                // with 16-byte LDS ahead of the chain and runs the adds back to back.
+                // (Broadcasting each element by a shuffle put a SHFL, a branch and
+                // the conversion on the chain: 63 cycles per element, 131 us for
+                // one K = 4096 row.)
                 if (lane == 0 && a.counts) atomicAdd(&cnt[VABFT_COUNT_SLOW_STATS], 1ull);
+                constexpr int kChunk = 256;
+                __shared__ __align__(16) T stage[8][kChunk];
+                T* st = stage[threadIdx.x >> 5];
                 const T* arow = static_cast<const T*>(a.A) + i * a.K;
                 ns = Neu{};
-                constexpr int kR = 16;
-                for (int64_t j0 = 0; j0 < a.K; j0 += 32 * kR) {
-                    T v[kR];
+                for (int64_t j0 = 0; j0 < a.K; j0 += kChunk) {
+                    const int n = a.K - j0 < kChunk ? int(a.K - j0) : kChunk;  // warp-uniform
+                    __syncwarp();
 #pragma unroll
-                    for (int r = 0; r < kR; ++r) {
-                        const int64_t j = j0 + r * 32 + lane;
-                        v[r] = j < a.K ? arow[j] : T(0);
+                    for (int r = 0; r < kChunk / 32; ++r) {
+                        const int q = r * 32 + lane;
+                        if (q < n) st[q] = arow[j0 + q];
                     }
+                    __syncwarp();
+                    if (lane == 0) {
+                        int q = 0;
+                        for (; q + 32 <= n; q += 32) {
+                            using V = std::conditional_t<sizeof(T) == 8, double2, float4>;
+                            constexpr int kPer = 16 / sizeof(T);
+                            T xs[32];
 #pragma unroll
-                    for (int r = 0; r < kR; ++r) {
-                        const int64_t n = a.K - j0 - r * 32;  // warp-uniform
-                        if (n <= 0) break;
-                        if (n >= 32) {
-                            double xs[32];  // all 32 shuffles issued ahead of the sequential chain
-#pragma unroll
-                            for (int l = 0; l < 32; ++l) xs[l] = double(__shfl_sync(0xffffffffu, v[r], l));
-                            if (lane == 0) {
-#pragma unroll
-                                for (int l = 0; l < 32; ++l) ns.add(xs[l]);
+                            for (int u = 0; u < 32 / kPer; ++u) {
+                                const V w = reinterpret_cast<const V*>(st + q)[u];
+                                if constexpr (sizeof(T) == 8) {
+                                    xs[2 * u] = w.x;
+                                    xs[2 * u + 1] = w.y;
+                                } else {
+                                    xs[4 * u] = w.x;
+                                    xs[4 * u + 1] = w.y;
+                                    xs[4 * u + 2] = w.z;
+                                    xs[4 * u + 3] = w.w;
+                                }
                             }
-                        } else {
-                            for (int l = 0; l < int(n); ++l) {
-                                const double x = double(__shfl_sync(0xffffffffu, v[r], l));
-                                if (lane == 0) ns.add(x);
-                            }
+#pragma unroll
+                            for (int l = 0; l < 32; ++l) ns.add(double(xs[l]));
                         }
+                        for (; q < n; ++q) ns.add(double(st[q]));
                     }
                 }
             }
