@@ -133,39 +133,39 @@ __global__ void bside_rows_kernel(const typename Elem<F>::T* __restrict__ B, int
         n.s = ps;
         plain = ps;
     } else {
-        // the reference's loops, warp-cooperative: 512 elements per HBM round
-        // trip (16 loads per lane in flight), lane 0 runs the two chains
-        constexpr int kR = 16;
-        for (int64_t j0 = 0; j0 < N; j0 += 32 * kR) {
-            double v[kR];
+        // the reference's loops, warp-cooperative: the warp stages 256
+        // elements at a time in its shared-memory slice (coalesced loads),
+        // lane 0 reads 32 per batch ahead of the two chains (as the wide
+        // verify tail's fallback: no shuffle or branch on the chains)
+        constexpr int kChunk = 256;
+        using T = typename Elem<F>::T;
+        __shared__ __align__(16) T stage[kWarpsPerBlock][kChunk];
+        T* st = stage[threadIdx.x >> 5];
+        for (int64_t j0 = 0; j0 < N; j0 += kChunk) {
+            const int cnt = N - j0 < kChunk ? int(N - j0) : kChunk;  // warp-uniform
+            __syncwarp();
 #pragma unroll
-            for (int r = 0; r < kR; ++r) {
-                const int64_t j = j0 + r * 32 + lane;
-                v[r] = j < N ? Elem<F>::d(row[j]) : 0.0;
+            for (int r = 0; r < kChunk / 32; ++r) {
+                const int q = r * 32 + lane;
+                if (q < cnt) st[q] = row[j0 + q];
             }
+            __syncwarp();
+            if (lane == 0) {
+                int q = 0;
+                for (; q + 32 <= cnt; q += 32) {
+                    double xs[32];
 #pragma unroll
-            for (int r = 0; r < kR; ++r) {
-                const int64_t left = N - j0 - r * 32;  // warp-uniform
-                if (left <= 0) break;
-                if (left >= 32) {
-                    double xs[32];  // all 32 shuffles issued ahead of the chains
+                    for (int l = 0; l < 32; ++l) xs[l] = Elem<F>::d(st[q + l]);
 #pragma unroll
-                    for (int l = 0; l < 32; ++l) xs[l] = __shfl_sync(0xffffffffu, v[r], l);
-                    if (lane == 0) {
-#pragma unroll
-                        for (int l = 0; l < 32; ++l) {
-                            n.add(xs[l]);
-                            plain = __dadd_rn(plain, xs[l]);
-                        }
+                    for (int l = 0; l < 32; ++l) {
+                        n.add(xs[l]);
+                        plain = __dadd_rn(plain, xs[l]);
                     }
-                } else {
-                    for (int l = 0; l < int(left); ++l) {
-                        const double x = __shfl_sync(0xffffffffu, v[r], l);
-                        if (lane == 0) {
-                            n.add(x);
-                            plain = __dadd_rn(plain, x);
-                        }
-                    }
+                }
+                for (; q < cnt; ++q) {
+                    const double x = Elem<F>::d(st[q]);
+                    n.add(x);
+                    plain = __dadd_rn(plain, x);
                 }
             }
         }
