@@ -25,7 +25,7 @@
 extern "C" {
 #endif
 
-#define VABFT_C_API_VERSION 1
+#define VABFT_C_API_VERSION 2
 
 /* Status codes <-> reference exception types (proj/src/*.cpp throw sites). */
 typedef enum vabft_status {
@@ -197,8 +197,10 @@ vabft_status vabft_vabft_thresholds(int32_t format, int64_t m, int64_t n, int64_
                                     double* b_summary_out, void* stream);
 
 /* aabft_threshold (threshold_aabft.cpp:50-60): fills M doubles with the
- * row-independent bound; *y_used / *degenerate are host outputs.
- * fixed_y <= 0 (or NaN) selects computed y = max|A| * max_k |sum_j B[k][j]|. */
+ * row-independent bound confidence_multiplier * aabft_sigma(K, t, y);
+ * *y_used / *degenerate (y == 0) are host outputs. fixed_y = NaN selects
+ * computed y = max|A| * max_k |sum_j B[k][j]| (AabftParams::fixed_y empty);
+ * any other value, zero and negative included, is used as the fixed y. */
 vabft_status vabft_aabft_threshold(int32_t format, int64_t m, int64_t n, int64_t k, const void* A,
                                    const void* B, int32_t mantissa_bits, double fixed_y,
                                    double confidence_multiplier, double* T, double* y_used,
@@ -279,13 +281,26 @@ typedef struct vabft_fused_opts {
     const vabft_fault* operand_faults;
     vabft_fault_record* operand_fault_records;
     /* tcgen05 kernel shape: -1 automatic (CTA pairs, cta_group::2 on 256 x 256
-     * tiles over two SMs, whenever eligible: N-major B, no fault injection, no
+     * tiles over two SMs, whenever eligible: N-major B, no operand faults, no
      * grid-barrier tail; else one CTA per 128 x 256 tile), 0 one CTA, 1 CTA
      * pairs. */
     int32_t cta_mode;
     /* FP32 handles (tcgen05 kind::tf32): 0 or 3 = 3xTF32 error compensation
      * (FP32-level products), 1 = a single TF32 pass. Ignored otherwise. */
     int32_t tf32_passes;
+    /* [v2] Parity dump (BF16/FP16 handles): an M x N FP32 device buffer that
+     * receives the saturated, post-injection FP32 accumulator — the matrix
+     * online verification reads (EncodedProduct::c_accum, checksum.hpp:45).
+     * NULL = none. FP32 / FP64 handles: C itself is the accumulator. */
+    float* accum_out;
+    /* [v2] Workspace contract: the workspace passed to vabft_fused_gemm
+     * carries per-row counters between launches. The library resets them when
+     * the workspace was last used by another handle, another shape, a wide
+     * (FP32 / FP64) launch or a stage-masked launch; a caller whose workspace
+     * bytes were written by anything else since (pooled or freshly allocated
+     * memory at a reused address) sets workspace_fresh = 1. */
+    int32_t workspace_fresh;
+    int32_t reserved_v2;
 } vabft_fused_opts;
 
 /* Workspace bytes for vabft_fused_gemm at this shape. */

@@ -192,6 +192,33 @@ class Oracle:
         self._call("row_sums", FORMATS[fmt], 1 if mode == "online" else 0, kind, bl, m, n, _dp(src), _dp(r1), _dp(r2))
         return r1, r2
 
+    def blocked_row_checksums(self, A, B, fmt, mode="online", block=128):
+        """Row checksums A (B r1), A (B r2) of encode_impl (checksum.cpp:103-115,
+        129-134) in the fused path's checksum precision — the accumulator's
+        working type (FP32 for BF16/FP16/FP32, FP64 for FP64) in
+        NativeBlocked(block) order — composed from this backend's own row_sums
+        (checksum.cpp:160-187) without the emulated GEMM:
+          B r1, B r2      = row_sums(B)                       (over j, weights j+1)
+          offline         : quantize both to the input format (checksum.cpp:112-115)
+          A (B r)[i]      = row_sums(P)[i], P[i][k] = fl_T(br[k] * A[i][k])
+                            (the contract's products, rounded in T, checksum.cpp:74-79)
+          offline         : quantize to the input format (checksum.cpp:129-134)."""
+        wt = np.float64 if fmt == "fp64" else np.float32
+        wf = "fp64" if fmt == "fp64" else "fp32"
+        br1, br2 = self.row_sums(B, wf, "offline", accum=(2, block))
+        if mode == "offline":
+            br1 = np.array([self.quantize(x, fmt) for x in br1])
+            br2 = np.array([self.quantize(x, fmt) for x in br2])
+        Aw = _arr(A).astype(wt)
+        out = []
+        for br in (br1, br2):
+            P = (br.astype(wt)[None, :] * Aw).astype(np.float64)
+            c, _ = self.row_sums(P, wf, "offline", accum=(2, block))
+            if mode == "offline":
+                c = np.array([self.quantize(x, fmt) for x in c])
+            out.append(c)
+        return out[0], out[1]
+
     def row_stats(self, v):
         v = _arr(v)
         out = np.zeros(5)

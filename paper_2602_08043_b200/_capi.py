@@ -63,7 +63,8 @@ class FusedOpts(C.Structure):
                 ("fault_col", C.c_void_p), ("fault_bit", C.c_void_p), ("fault_dir", C.c_void_p),
                 ("fault_records", C.c_void_p), ("stages", C.c_int32), ("fault_target", C.c_int32),
                 ("n_operand_faults", C.c_int32), ("correct", C.c_int32), ("operand_faults", C.c_void_p),
-                ("operand_fault_records", C.c_void_p), ("cta_mode", C.c_int32), ("tf32_passes", C.c_int32)]
+                ("operand_fault_records", C.c_void_p), ("cta_mode", C.c_int32), ("tf32_passes", C.c_int32),
+                ("accum_out", C.c_void_p), ("workspace_fresh", C.c_int32), ("reserved_v2", C.c_int32)]
 
 
 _st = C.c_int

@@ -424,10 +424,9 @@ def aabft_threshold(a: np.ndarray, b: np.ndarray, params: AabftParams, spec="fp6
     T = torch.empty(m, dtype=torch.float64, device="cuda")
     y = C.c_double()
     dg = C.c_int32()
-    fixed = -1.0 if params.fixed_y is None else float(params.fixed_y)
-    if params.fixed_y is not None and params.fixed_y <= 0:
-        # a fixed y of zero is still "fixed" in the reference; route through computed=False
-        fixed = float(params.fixed_y)
+    # NaN = computed y (AabftParams::fixed_y empty); any other value, zero
+    # included, is a fixed y as in the reference
+    fixed = math.nan if params.fixed_y is None else float(params.fixed_y)
     check(lib.vabft_aabft_threshold(s.code, m, n, k, ptr(dA), ptr(dB), params.mantissa_bits, fixed,
                                     params.confidence_multiplier, ptr(T), C.byref(y), C.byref(dg), stream_ptr()))
     torch.cuda.synchronize()

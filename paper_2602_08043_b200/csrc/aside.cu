@@ -197,18 +197,10 @@ void launch_aside(int fmt, int64_t M, int64_t K, int64_t N, const void* A, const
     const dim3 grid(unsigned((M + kRowsPerCta - 1) / kRowsPerCta)), block(32 * W);
     const uint16_t* a = static_cast<const uint16_t*>(A);
     if (fmt == VABFT_BF16) {
-        static bool set = false;
-        if (!set) {
-            check_cuda(cudaFuncSetAttribute(aside_kernel<VABFT_BF16>, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024), "attr");
-            set = true;
-        }
+        ensure_smem_attr(reinterpret_cast<const void*>(aside_kernel<VABFT_BF16>), 96 * 1024);
         aside_kernel<VABFT_BF16><<<grid, block, smem, s>>>(a, M, K, N, buf.br1, buf.br2, buf.summary, quantize_cr, e_max, c_sigma, T, cr1, cr2, max_abs_a);
     } else if (fmt == VABFT_FP16) {
-        static bool set = false;
-        if (!set) {
-            check_cuda(cudaFuncSetAttribute(aside_kernel<VABFT_FP16>, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024), "attr");
-            set = true;
-        }
+        ensure_smem_attr(reinterpret_cast<const void*>(aside_kernel<VABFT_FP16>), 96 * 1024);
         aside_kernel<VABFT_FP16><<<grid, block, smem, s>>>(a, M, K, N, buf.br1, buf.br2, buf.summary, quantize_cr, e_max, c_sigma, T, cr1, cr2, max_abs_a);
     } else {
         fail(VABFT_UNSUPPORTED, "A-side stats: BF16/FP16 only");

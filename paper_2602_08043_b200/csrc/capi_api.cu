@@ -262,7 +262,7 @@ extern "C" vabft_status vabft_aabft_threshold(int32_t format, int64_t m, int64_t
         if (m < 1 || n < 1 || k < 1) fail(VABFT_INVALID_ARGUMENT, "dims must be >= 1");
         cudaStream_t s = as_stream(stream);
         double y = fixed_y;
-        if (!(fixed_y > 0.0)) {
+        if (std::isnan(fixed_y)) {
             // computed y = max|A| * max_k |sum_j B[k][j]| (threshold_aabft.cpp:38-48)
             Tmp tmp(s);
             BsideBuffers buf;
@@ -290,7 +290,7 @@ extern "C" vabft_status vabft_aabft_threshold(int32_t format, int64_t m, int64_t
         const double nn = double(k);
         const double poly = nn * (nn + 1.0) * (nn + 0.5) + 2.0 * nn;
         const double sig = std::sqrt(poly / 24.0) * std::ldexp(1.0, -t) * y;
-        const double thr = (conf > 0 ? conf : 3.0) * sig;
+        const double thr = conf * sig;  // the caller's multiplier as given (threshold_aabft.cpp:56)
         fill_kernel<<<unsigned((m + 255) / 256), 256, 0, s>>>(T, m, thr);
         check_cuda(cudaGetLastError(), "fill launch");
         if (y_used) *y_used = y;

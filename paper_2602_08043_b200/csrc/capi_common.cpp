@@ -1,6 +1,11 @@
 // C-ABI plumbing: thread-local last error, status mapping, device info.
+#include <atomic>
 #include <cstring>
+#include <map>
+#include <mutex>
+#include <set>
 #include <string>
+#include <tuple>
 
 #include <cuda_runtime.h>
 
@@ -10,19 +15,56 @@ namespace vabft_dev {
 
 thread_local std::string g_last_error;
 
-int sm_count() {
-    static int cached = -1;
+namespace {
+constexpr int kMaxDevices = 64;
+std::atomic<int> g_sm_count[kMaxDevices];  // 0 = not yet queried
+std::mutex g_attr_mu;
+std::set<std::tuple<const void*, int, int>> g_attr_done;   // (kernel, device, smem bytes)
+std::map<std::pair<const void*, int>, int> g_clusters;      // (kernel, device) -> co-resident clusters
+}  // namespace
+
+int current_device() {
     int dev = 0;
-    if (cudaGetDevice(&dev) != cudaSuccess) return 148;
-    static int cached_dev = -1;
-    if (cached < 0 || cached_dev != dev) {
+    if (cudaGetDevice(&dev) != cudaSuccess) return 0;
+    return dev;
+}
+
+// Per device (a process may drive several GPUs), lock-free after the first query.
+int sm_count() {
+    const int dev = current_device();
+    if (dev < 0 || dev >= kMaxDevices) {
         int n = 0;
-        if (cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || n <= 0)
-            n = 148;
-        cached = n;
-        cached_dev = dev;
+        return cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev) == cudaSuccess && n > 0 ? n : 148;
     }
-    return cached;
+    int n = g_sm_count[dev].load(std::memory_order_relaxed);
+    if (n > 0) return n;
+    if (cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || n <= 0) n = 148;
+    g_sm_count[dev].store(n, std::memory_order_relaxed);
+    return n;
+}
+
+// cudaFuncSetAttribute is per (function, device): apply it once for each
+// device the calling thread's launches target, thread-safely.
+void ensure_smem_attr(const void* fn, int bytes) {
+    const auto key = std::make_tuple(fn, current_device(), bytes);
+    std::lock_guard<std::mutex> lk(g_attr_mu);
+    if (g_attr_done.count(key)) return;
+    check_cuda(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes),
+               "cudaFuncSetAttribute(max dynamic shared memory)");
+    g_attr_done.insert(key);
+}
+
+int cached_cluster_count(const void* fn, int (*compute)(const void*, void*), void* ctx) {
+    const auto key = std::make_pair(fn, current_device());
+    {
+        std::lock_guard<std::mutex> lk(g_attr_mu);
+        auto it = g_clusters.find(key);
+        if (it != g_clusters.end()) return it->second;
+    }
+    const int n = compute(fn, ctx);
+    std::lock_guard<std::mutex> lk(g_attr_mu);
+    g_clusters[key] = n;
+    return n;
 }
 
 size_t elem_size(int fmt) {

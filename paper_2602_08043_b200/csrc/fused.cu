@@ -23,6 +23,9 @@
 #include <algorithm>
 #include <cstdlib>
 #include <cstring>
+#include <map>
+#include <memory>
+#include <mutex>
 
 #include "devcommon.cuh"
 #include "exact.hpp"
@@ -41,8 +44,6 @@ struct vabft_bside {
     vabft_dev::BsideBuffers buf;
     void* storage;  // one cudaMalloc holding every buffer
     unsigned int* gbar;  // grid-barrier state of the fused kernel (inside storage)
-    const void* ws_ready = nullptr;  // workspace whose per-row atomics hold their identities
-    size_t ws_ready_bytes = 0;
     // wide formats (FP32 / FP64): B r1 / B r2 in the working type (held as doubles)
     double* brd = nullptr;  // [2][K]
     // FP32 (3xTF32): the weight split once into hi / lo parts, transposed
@@ -56,6 +57,43 @@ struct vabft_bside {
 namespace vabft_dev {
 
 namespace {
+
+void destroy_bside(vabft_bside* h) {
+    if (h->storage) cudaFree(h->storage);
+    if (h->brd) cudaFree(h->brd);
+    if (h->b_split) cudaFree(h->b_split);
+    if (h->a_split) cudaFree(h->a_split);
+    delete h;
+}
+
+// Workspace state across launches. The per-row statistics atomics and the
+// streamed-verification counters of a 16-bit fused workspace hold their
+// identities after every complete launch (the verify tail restores them), so
+// a workspace the same handle used last at the same shape is launched without
+// resetting anything. Any other history — first use, another handle, an
+// FP32 / FP64 launch (whose carve overlays the same bytes), a stage-masked
+// launch that ran the statistics warps without the tail, or
+// vabft_fused_opts.workspace_fresh — resets them first (~20 B per row).
+std::mutex g_ws_mu;
+std::map<const void*, std::pair<const vabft_bside*, size_t>> g_ws_owner;  // workspace -> (handle, bytes)
+
+// true when the workspace needs its identities written before this launch
+bool claim_workspace(const void* ws, const vabft_bside* h, size_t bytes, bool fresh) {
+    std::lock_guard<std::mutex> lk(g_ws_mu);
+    auto it = g_ws_owner.find(ws);
+    const bool ready = !fresh && it != g_ws_owner.end() && it->second.first == h && it->second.second == bytes;
+    g_ws_owner[ws] = {h, bytes};
+    return !ready;
+}
+void release_workspace(const void* ws) {
+    std::lock_guard<std::mutex> lk(g_ws_mu);
+    g_ws_owner.erase(ws);
+}
+void forget_workspaces(const vabft_bside* h) {
+    std::lock_guard<std::mutex> lk(g_ws_mu);
+    for (auto it = g_ws_owner.begin(); it != g_ws_owner.end();)
+        it = it->second.first == h ? g_ws_owner.erase(it) : std::next(it);
+}
 
 // Standalone tail (profiling stage mask 4 without 2): 4 warps per CTA, one
 // 32-row group per warp, each with its own 24 KiB shared-memory slice.
@@ -305,7 +343,11 @@ extern "C" vabft_status vabft_bside_create(int32_t format, int32_t mode, int64_t
         if (k < 1 || n < 1) fail(VABFT_INVALID_ARGUMENT, "dims must be >= 1");
         // ChecksumVectors::make: weights exact in FP32 (checksum.cpp:26-34)
         if (n > (int64_t(1) << 24)) fail(VABFT_INVALID_ARGUMENT, "ChecksumVectors: weights exceed exact range");
-        auto* h = new vabft_bside();
+        if (format == VABFT_FP32 && (k * n) % 4 != 0)
+            fail(VABFT_UNSUPPORTED, "FP32 weights: K x N must be a multiple of 4");
+        // owned until handed out: every early exit below frees what was allocated
+        std::unique_ptr<vabft_bside, void (*)(vabft_bside*)> hp(new vabft_bside(), destroy_bside);
+        vabft_bside* h = hp.get();
         h->fmt = format;
         h->mode = mode;
         h->b_kmajor = 0;
@@ -316,11 +358,7 @@ extern "C" vabft_status vabft_bside_create(int32_t format, int32_t mode, int64_t
         const size_t KB = size_t(br_storage_floats(k));
         const size_t bytes = align_up(8 * K) * 3 + align_up(4 * KB) * 2 + align_up(8 * 4) + align_up(4) + align_up(8) +
                              align_up(4);
-        cudaError_t e = cudaMalloc(&h->storage, bytes);
-        if (e != cudaSuccess) {
-            delete h;
-            fail(VABFT_CUDA_ERROR, std::string("cudaMalloc(bside): ") + cudaGetErrorString(e));
-        }
+        check_cuda(cudaMalloc(&h->storage, bytes), "cudaMalloc(bside)");
         char* p = static_cast<char*>(h->storage);
         h->buf.mean = reinterpret_cast<double*>(p); p += align_up(8 * K);
         h->buf.vb = reinterpret_cast<double*>(p); p += align_up(8 * K);
@@ -336,16 +374,15 @@ extern "C" vabft_status vabft_bside_create(int32_t format, int32_t mode, int64_t
         if (is_wide(format)) {
             check_cuda(cudaMalloc(&h->brd, 2 * sizeof(double) * K), "cudaMalloc(bside B r)");
             if (format == VABFT_FP32) {
-                if ((k * n) % 4 != 0) fail(VABFT_UNSUPPORTED, "FP32 weights: K x N must be a multiple of 4");
                 check_cuda(cudaMalloc(&h->b_split, 2 * sizeof(float) * K * size_t(n)), "cudaMalloc(B split)");
             }
         }
-        *out = h;
         if (B) {
             check_cuda(cudaMemsetAsync(h->buf.nonfinite, 0, sizeof(int), as_stream(stream)), "memset");
             launch_bside(format, k, n, B, mode == VABFT_OFFLINE ? 1 : 0, h->buf, as_stream(stream));
             if (is_wide(format)) wide_bside(h, as_stream(stream));
         }
+        *out = hp.release();
     });
 }
 
@@ -362,11 +399,8 @@ extern "C" vabft_status vabft_bside_update(vabft_bside_t h, const void* B, void*
 extern "C" vabft_status vabft_bside_destroy(vabft_bside_t h) {
     return guarded([&] {
         if (!h) return;
-        cudaFree(h->storage);
-        if (h->brd) cudaFree(h->brd);
-        if (h->b_split) cudaFree(h->b_split);
-        if (h->a_split) cudaFree(h->a_split);
-        delete h;
+        forget_workspaces(h);
+        destroy_bside(h);
     });
 }
 
@@ -398,6 +432,7 @@ extern "C" vabft_status vabft_fused_gemm(const vabft_fused_opts* o, vabft_bside_
         cudaStream_t s = as_stream(stream);
         if (o->fault_target < 0 || o->fault_target > 2) fail(VABFT_INVALID_ARGUMENT, "bad fault target");
         if (is_wide(h->fmt)) {
+            release_workspace(workspace);  // its carve overlays the 16-bit counters
             wide_fused(o, h, m, A, C, T, verdicts, counts, workspace, s);
             return;
         }
@@ -420,17 +455,17 @@ extern "C" vabft_status vabft_fused_gemm(const vabft_fused_opts* o, vabft_bside_
         a.rmax = ws.rmax;
         a.rmin = ws.rmin;
         a.rmnz = ws.rmnz;
-        if (h->ws_ready != workspace || h->ws_ready_bytes != ws.bytes) {
-            // first use of this workspace: per-row atomics to their identities
-            // (the verify tail restores them after every launch)
+        if (claim_workspace(workspace, h, ws.bytes, o->workspace_fresh != 0)) {
+            // per-row atomics and group counters to their identities (the
+            // verify tail restores them after every complete launch)
             check_cuda(cudaMemsetAsync(ws.rsum, 0, sizeof(double) * size_t(m), s), "memset");
             check_cuda(cudaMemsetAsync(ws.rmax, 0, sizeof(uint32_t) * size_t(m), s), "memset");
             check_cuda(cudaMemsetAsync(ws.rmin, 0xFF, size_t(reinterpret_cast<char*>(ws.rmnz + m) -
                                                              reinterpret_cast<char*>(ws.rmin)), s), "memset");
             check_cuda(cudaMemsetAsync(ws.group_cnt, 0, sizeof(unsigned int) * 2 * size_t((m + 31) / 32), s), "memset");
-            h->ws_ready = workspace;
-            h->ws_ready_bytes = ws.bytes;
         }
+        // a launch without the tail leaves the statistics atomics dirty
+        if (!(stages & 4)) release_workspace(workspace);
         a.bsum = h->buf.summary;
         a.cr1 = ws.cr1;
         a.cr2 = ws.cr2;
@@ -472,6 +507,7 @@ extern "C" vabft_status vabft_fused_gemm(const vabft_fused_opts* o, vabft_bside_
             epi.n_operand_faults = o->n_operand_faults;
             epi.operand_faults = o->operand_faults;
             epi.operand_fault_records = o->operand_fault_records;
+            epi.accum_out = o->accum_out;
             epi.br1 = h->buf.br1;
             epi.br2 = h->buf.br2;
             epi.sp1 = ws.sp1;
@@ -498,7 +534,7 @@ extern "C" vabft_status vabft_fused_gemm(const vabft_fused_opts* o, vabft_bside_
         const unsigned grid = unsigned(((m + 31) / 32 + 3) / 4);
         const size_t smem = 4 * size_t(kTailWarpSmem);
         auto run = [&](auto kern) {
-            check_cuda(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)), "attr");
+            ensure_smem_attr(reinterpret_cast<const void*>(kern), int(smem));
             if (two_phase) {
                 kern<<<grid, 128, smem, s>>>(a, 1);
                 kern<<<grid, 128, smem, s>>>(a, 2);

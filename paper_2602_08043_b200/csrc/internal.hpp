@@ -25,7 +25,12 @@ inline void check_cuda(cudaError_t e, const char* what) {
         fail(VABFT_CUDA_ERROR, std::string(what) + ": " + cudaGetErrorString(e));
 }
 
-int sm_count();
+int current_device();
+int sm_count();  // of the current device
+// cudaFuncSetAttribute(MaxDynamicSharedMemorySize) once per (kernel, device)
+void ensure_smem_attr(const void* fn, int bytes);
+// per-(kernel, device) cache of an occupancy query: compute(fn, ctx) on a miss
+int cached_cluster_count(const void* fn, int (*compute)(const void*, void*), void* ctx);
 size_t elem_size(int fmt);
 
 // ---- verify tail (tail.cuh): inputs of one fused launch

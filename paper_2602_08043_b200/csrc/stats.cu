@@ -474,14 +474,8 @@ void launch_bside(int fmt, int64_t K, int64_t N, const void* B, int quantize_br,
     if ((fmt == VABFT_BF16 || fmt == VABFT_FP16) && N % 8 == 0 && N <= (int64_t(1) << 24)) {
         const unsigned grid16 = unsigned((K + kB16Warps - 1) / kB16Warps);
         const size_t smem = size_t(kB16Warps) * kB16StageGranules * sizeof(uint4);  // 64 KiB
-        static bool attr_set[2] = {false, false};  // per format (both kernels share one pointer type)
         auto run = [&](auto kern) {
-            bool& attr = attr_set[fmt == VABFT_BF16 ? 0 : 1];
-            if (!attr) {
-                check_cuda(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)),
-                           "attr(bside_rows16)");
-                attr = true;
-            }
+            ensure_smem_attr(reinterpret_cast<const void*>(kern), int(smem));
             static const bool split = std::getenv("VABFT_BSIDE_SPLIT") != nullptr;  // developer: time the parts
             kern<<<grid16, 32 * kB16Warps, smem, s>>>(static_cast<const uint16_t*>(B), K, N, quantize_br, buf,
                                                        split ? nullptr : buf.done);
@@ -491,12 +485,7 @@ void launch_bside(int fmt, int64_t K, int64_t N, const void* B, int quantize_br,
         else run(bside_rows16_kernel<VABFT_FP16>);
         check_cuda(cudaGetLastError(), "bside16 launch");
         if (buf.done == nullptr) {
-            static bool sattr = false;
-            if (!sattr) {
-                check_cuda(cudaFuncSetAttribute(bside_summary_cta_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                                int(smem)), "attr(bside_summary)");
-                sattr = true;
-            }
+            ensure_smem_attr(reinterpret_cast<const void*>(bside_summary_cta_kernel), int(smem));
             bside_summary_cta_kernel<<<1, 32 * kB16Warps, smem, s>>>(buf.mean, buf.vb, buf.rowsum_abs, K,
                                                                      buf.summary);
             check_cuda(cudaGetLastError(), "bside summary launch");

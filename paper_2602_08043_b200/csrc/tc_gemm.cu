@@ -602,7 +602,7 @@ __global__ void __launch_bounds__(kThreadsStats, 1)
         // With operand faults (campaign instantiations only) the whole warp
         // walks the stages: its lanes flip the planned operand bits in the
         // freshly loaded shared-memory tiles before lane 0 issues the MMAs.
-        const bool opf = kInject && p.epi.fault_target != 0;
+        const bool opf = kInject && !kPair && p.epi.fault_target != 0;  // operand faults: one-CTA kernel only
         // pair mode: only the leader issues (cta_group::2, M = 256)
         if ((lane == 0 || opf) && rank == 0) {
             // --------------------------------------------------- MMA issuer
@@ -913,12 +913,7 @@ void launch_inst(const CUtensorMap& ta, const CUtensorMap& tb, const TcParams& p
     constexpr size_t smem = kPair ? (kStats ? kSmemBytesPairStats : kSmemBytesPair)
                                   : (kStats ? kSmemBytesStats : kSmemBytes);
     constexpr unsigned threads = kStats ? kThreadsStats : kThreads;
-    static bool attr_set = false;  // per instantiation
-    if (!attr_set) {
-        check_cuda(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)),
-                   "cudaFuncSetAttribute(tc_gemm)");
-        attr_set = true;
-    }
+    ensure_smem_attr(reinterpret_cast<const void*>(kern), int(smem));
     if constexpr (kPair) {
         // 2 x 1 clusters: the two CTAs of a pair share one TPC. A persistent
         // grid must fit in ONE wave: size it by the co-resident cluster count
@@ -934,13 +929,17 @@ void launch_inst(const CUtensorMap& ta, const CUtensorMap& tb, const TcParams& p
         attr[0].val.clusterDim.z = 1;
         cfg.attrs = attr;
         cfg.numAttrs = 1;
-        static int max_clusters = [&] {
-            cudaLaunchConfig_t q = cfg;
-            q.gridDim = dim3(unsigned(sm_count() & ~1));
-            int n = 0;
-            check_cuda(cudaOccupancyMaxActiveClusters(&n, kern, &q), "cudaOccupancyMaxActiveClusters");
-            return n > 0 ? n : 1;
-        }();
+        // per (kernel, device): a process may drive several GPUs
+        const int max_clusters = cached_cluster_count(
+            reinterpret_cast<const void*>(kern),
+            [](const void* fn, void* ctx) {
+                cudaLaunchConfig_t q = *static_cast<cudaLaunchConfig_t*>(ctx);
+                q.gridDim = dim3(unsigned(sm_count() & ~1));
+                int n = 0;
+                check_cuda(cudaOccupancyMaxActiveClusters(&n, fn, &q), "cudaOccupancyMaxActiveClusters");
+                return n > 0 ? n : 1;
+            },
+            &cfg);
         const int pairs = p.num_units < max_clusters ? p.num_units : max_clusters;
         cfg.gridDim = dim3(unsigned(2 * pairs));
         check_cuda(cudaLaunchKernelEx(&cfg, kern, ta, tb, p), "tc_gemm pair launch");
@@ -967,10 +966,11 @@ void launch_inst(const CUtensorMap& ta, const CUtensorMap& tb, const TcParams& p
     check_cuda(cudaGetLastError(), "tc_gemm launch");
 }
 
-// pair-mode kernels exist for N-major B without fault injection
+// pair-mode kernels exist for N-major B (with accumulator / output faults,
+// not operand faults: tc_gemm_uses_pairs)
 template <int kFmt, bool kBKMajor, int kAbft, bool kInject, bool kStats = false>
 void launch_sel(const CUtensorMap& ta, const CUtensorMap& tb, const TcParams& p, cudaStream_t stream) {
-    if constexpr (!kBKMajor && !kInject) {
+    if constexpr (!kBKMajor) {
         if (p.pair) {
             launch_inst<kFmt, kBKMajor, kAbft, kInject, kStats, true>(ta, tb, p, stream);
             return;
@@ -1015,8 +1015,9 @@ bool tc_gemm_uses_pairs(bool b_kmajor, int64_t N, const TcEpilogue& epi) {
         const char* e = std::getenv("VABFT_PAIR");  // developer override of the automatic choice
         return e ? std::atoi(e) : -1;
     }();
-    const bool inj = epi.fault_col != nullptr || (epi.fault_target == 2 && epi.n_operand_faults > 0);
-    const bool eligible = !b_kmajor && !inj && epi.tail_phases == 0 && sm_count() >= 2;
+    // operand faults flip bits in one CTA's shared-memory tiles: one-CTA kernel
+    const bool operand_inj = epi.fault_target != 0 && (epi.fault_col != nullptr || epi.n_operand_faults > 0);
+    const bool eligible = !b_kmajor && !operand_inj && epi.tail_phases == 0 && sm_count() >= 2;
     const int mode = epi.cta_mode >= 0 ? epi.cta_mode : pair_env;
     (void)N;
     // automatic: CTA pairs whenever eligible — measured faster for the plain
@@ -1070,7 +1071,7 @@ void tc_gemm_launch(int fmt, bool b_kmajor, int64_t M, int64_t N, int64_t K, con
     }();
     p.epi.trace = trace_buf;
     // CTA pairs (cta_group::2, 256 x 256 tiles over two SMs): N-major B, no
-    // fault injection, no grid-barrier tail. Policy (measured):
+    // no operand faults, no grid-barrier tail. Policy (measured):
     // pairs whenever eligible, plain and fused (the fused kernel lost to the
     // one-CTA kernel at N = 4096 only with groups of 4 pair-row blocks; with
     // its 16-pair-block groups it wins at every bench shape).

@@ -384,12 +384,7 @@ template <bool kSplit, bool kAbft, bool kInject>
 void launch_tf32(const CUtensorMap& ah, const CUtensorMap& al, const CUtensorMap& bh, const CUtensorMap& bl,
                  const Tf32Params& p, cudaStream_t s) {
     auto kern = tf32_gemm_kernel<kSplit, kAbft, kInject>;
-    static bool attr = false;  // per instantiation (distinct function templates)
-    if (!attr) {
-        check_cuda(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kSmem)),
-                   "attr(tf32_gemm)");
-        attr = true;
-    }
+    ensure_smem_attr(reinterpret_cast<const void*>(kern), int(kSmem));
     const int grid = p.num_tiles < sm_count() ? p.num_tiles : sm_count();
     kern<<<grid, kThreads, kSmem, s>>>(ah, al, bh, bl, p);
     check_cuda(cudaGetLastError(), "tf32 gemm launch");

@@ -609,18 +609,13 @@ void dgemm_launch(int64_t M, int64_t N, int64_t K, const double* A, const double
         fail(VABFT_UNSUPPORTED, "FP64 GEMM: grid too large");
     DgemmParams p{M, N, K, A, B, C, epi};
     const dim3 grid(unsigned((N + kDBN - 1) / kDBN), unsigned((M + kDBM - 1) / kDBM));
-    static bool attr_set[3] = {false, false, false};  // per variant (one pointer type for all)
-    auto run = [&](void (*kern)(DgemmParams), int variant) {
-        if (!attr_set[variant]) {
-            check_cuda(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kDSmem)),
-                       "attr(dgemm)");
-            attr_set[variant] = true;
-        }
+    auto run = [&](void (*kern)(DgemmParams)) {
+        ensure_smem_attr(reinterpret_cast<const void*>(kern), int(kDSmem));
         kern<<<grid, kDThreads, kDSmem, stream>>>(p);
     };
-    if (!epi.abft) run(dgemm_kernel<false, false>, 0);
-    else if (epi.fault_col) run(dgemm_kernel<true, true>, 1);
-    else run(dgemm_kernel<true, false>, 2);
+    if (!epi.abft) run(dgemm_kernel<false, false>);
+    else if (epi.fault_col) run(dgemm_kernel<true, true>);
+    else run(dgemm_kernel<true, false>);
     check_cuda(cudaGetLastError(), "dgemm launch");
 }
 

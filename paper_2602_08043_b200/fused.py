@@ -105,12 +105,14 @@ class FusedAbftGemm:
     def __call__(self, A: torch.Tensor, out: Optional[torch.Tensor] = None, *, verdicts: bool = True,
                  thresholds: bool = True, counts: Optional[torch.Tensor] = None,
                  faults: Optional[dict] = None, stages: int = 0, checksums: bool = False,
-                 correct: bool = False) -> FusedResult:
+                 correct: bool = False, accum_out: Optional[torch.Tensor] = None) -> FusedResult:
         """faults: {"target": "output" | "A" | "B", ...}. output / A: per-row
         int32 tensors "col" (output column, or the k index of A[i][k]; < 0 =
         none), "bit", "dir" and optional "records" (M x 24-byte records). B:
         "operand" = operand_faults(...) and optional "records" (per fault).
-        correct: in-kernel correction of located single errors."""
+        correct: in-kernel correction of located single errors.
+        accum_out: M x N FP32 tensor receiving the (post-injection) FP32
+        accumulator that online verification reads (BF16 / FP16 weights)."""
         if A.dtype != self.B.dtype or A.dim() != 2 or A.shape[1] != self.k:
             raise _capi.InvalidArgument("FusedAbftGemm: A must be M x K with B's dtype")
         m = A.shape[0]
@@ -119,8 +121,7 @@ class FusedAbftGemm:
         bufs = self._bufs.get(m)
         if bufs is None:
             dev = A.device
-            bufs = {"C": torch.empty((m, self.n), dtype=A.dtype, device=dev),
-                    "T": torch.empty(m, dtype=torch.float64, device=dev),
+            bufs = {"T": torch.empty(m, dtype=torch.float64, device=dev),
                     "d1": torch.empty(m, dtype=torch.float64, device=dev),
                     "d2": torch.empty(m, dtype=torch.float64, device=dev),
                     "res": torch.empty(m, dtype=torch.float64, device=dev),
@@ -129,6 +130,8 @@ class FusedAbftGemm:
                     "rc1": torch.empty(m, dtype=torch.float64, device=dev),
                     "rc2": torch.empty(m, dtype=torch.float64, device=dev)}
             self._bufs[m] = bufs
+        if out is None and "C" not in bufs:  # only when the caller brings no output
+            bufs["C"] = torch.empty((m, self.n), dtype=A.dtype, device=A.device)
         C_ = out if out is not None else bufs["C"]
         T = bufs["T"] if thresholds else None
         if verdicts:
@@ -158,6 +161,11 @@ class FusedAbftGemm:
         if correct:
             opts = _capi.FusedOpts.from_buffer_copy(opts)
             opts.correct = 1
+        if accum_out is not None:
+            if accum_out.dtype != torch.float32 or tuple(accum_out.shape) != (m, self.n) or not accum_out.is_contiguous():
+                raise _capi.InvalidArgument("accum_out must be a contiguous M x N float32 tensor")
+            opts = _capi.FusedOpts.from_buffer_copy(opts)
+            opts.accum_out = ptr(accum_out)
         ws = self.workspace(m)
         check(lib.vabft_fused_gemm(C.byref(opts), self.h, m, ptr(A.contiguous()), ptr(C_), ptr(T), v, ptr(counts),
                                    ptr(ws), ws.numel(), stream_ptr()))

@@ -1,0 +1,207 @@
+"""Oracle parity of the default fused kernel at the BASELINE.json configs.
+
+The production launch (CTA pairs, cta_group::2 on 256 x 256 tiles, the
+under-filled last wave as 128-column half tiles, statistics warps, streamed
+verification inside the GEMM) runs the full shapes of
+
+  C1  FP32 1024^3 (3xTF32 on tcgen05) with single bit flips, bits 0..31
+  C2  BF16 4096^3, online (FP32 accumulator) and offline (BF16 output)
+  C4  LLaMA-7B layer GEMMs, tokens M = 8192: (K, N) = (4096, 11008), (11008, 4096)
+  C5  ViT-B/16 (M = 32 * 197 = 6304, ragged) and GPT-2 (M = 1024) layer shapes
+      (+ FP16 / FP64 at 2048^3 from the C3 sweep)
+
+and is compared with the reference compiled from its own sources
+(oracle/_ref; the C restatement where it is not built) on a row sample S.
+Rows of a GEMM are independent sub-problems of every reference function on
+the path, so the reference runs on A[S] with the full B:
+
+  T          = vabft_thresholds(A[S], B)             (threshold_vabft.cpp:54-61)   bit-exact
+  row checks = A[S] (B r) in the fused path's FP32 NativeBlocked(128) checksum
+               precision, composed from the reference's row_sums
+               (checksum.cpp:103-187)                                              bit-exact
+  verdicts   = verify(device accumulator / output [S], row checks, T)
+               (detect.cpp:9-55): diff1, diff2, residual, detected, location   bit-exact
+  C          = within the FP32-accumulate bound of test_precision.cpp:181-206
+               against the exact product; C == RNE(accumulator) bit for bit.
+
+Planted faults (one per faulted row, accumulator bits online, output bits
+offline) land in sampled rows, so their verdicts and located columns are
+compared too; every other row of the full matrix is clean and must not be
+flagged (FPR = 0 over all M rows).
+"""
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+BITS_ONLINE = [0, 7, 12, 14, 15, 16, 18, 20, 22, 23, 24, 26, 28, 29, 30, 31]
+BITS_OFFLINE = [0, 3, 6, 7, 8, 9, 10, 11, 12, 13, 14, 15]
+
+
+@pytest.fixture(scope="module")
+def env():
+    import torch
+    assert torch.cuda.is_available()
+    import oracle
+    return torch, oracle.best()
+
+
+def _same(a, b):
+    a, b = np.asarray(a, dtype=np.float64), np.asarray(b, dtype=np.float64)
+    na, nb = np.isnan(a), np.isnan(b)
+    return np.array_equal(na, nb) and np.array_equal(a[~na].view(np.uint64), b[~nb].view(np.uint64))
+
+
+def _sample_rows(m, rng, count=48):
+    """Random rows + the first rows + the last 256-row (pair) block, which
+    holds the ragged M tail and, at split shapes, rows of the half tiles."""
+    if m <= 1024:
+        return np.arange(m)  # C1 and the GPT-2 shapes: every row
+    rows = set(rng.choice(m, size=min(count, m), replace=False).tolist())
+    rows.update(range(min(4, m)))
+    last = max(0, (m - 1) // 256 * 256)
+    rows.update(rng.choice(np.arange(last, m), size=min(12, m - last), replace=False).tolist())
+    rows.add(m - 1)
+    return np.array(sorted(rows))
+
+
+def _inputs(torch, m, k, n, dt, seed, weights="normal"):
+    g = torch.Generator(device="cuda").manual_seed(seed)
+    A = torch.randn(m, k, device="cuda", generator=g, dtype=torch.float32)
+    if weights == "linear":  # nn.Linear default init
+        B = (torch.rand(k, n, device="cuda", generator=g) * 2 - 1) / k ** 0.5
+    else:
+        B = torch.randn(k, n, device="cuda", generator=g, dtype=torch.float32)
+    if dt == torch.float64:
+        return A.double(), B.double()
+    return A.to(dt), B.to(dt)
+
+
+def _run_config(env, m, k, n, fmt, mode, seed, weights="normal", faulted_fraction=0.5, tf32_passes=3):
+    torch, O = env
+    from paper_2602_08043_b200.fused import FusedAbftGemm
+    dt = {"bf16": torch.bfloat16, "fp16": torch.float16, "fp32": torch.float32, "fp64": torch.float64}[fmt]
+    dA, dB = _inputs(torch, m, k, n, dt, seed, weights)
+    rng = np.random.default_rng(seed)
+    S = _sample_rows(m, rng)
+    g = FusedAbftGemm(dB, mode=mode, tf32_passes=tf32_passes)
+    wide = fmt in ("fp32", "fp64")
+    if not wide:
+        assert g.uses_cta_pairs(m), "the default launch must be the CTA-pair kernel"
+    # planted faults in a subset of the sampled rows
+    fr = S[rng.random(len(S)) < faulted_fraction]
+    bits = BITS_ONLINE if (mode == "online" or fmt == "fp32") else BITS_OFFLINE
+    if fmt == "fp64":
+        bits = [0, 20, 40, 45, 50, 52, 55, 58, 60, 62]
+    col = torch.full((m,), -1, dtype=torch.int32)
+    bit = torch.zeros(m, dtype=torch.int32)
+    fcols = rng.integers(0, n, len(fr))
+    fbits = rng.choice(bits, len(fr))
+    col[torch.from_numpy(fr)] = torch.from_numpy(fcols.astype(np.int32))
+    bit[torch.from_numpy(fr)] = torch.from_numpy(fbits.astype(np.int32))
+    faults = {"col": col.cuda(), "bit": bit.cuda(), "dir": torch.zeros(m, dtype=torch.int32, device="cuda")}
+    counts = torch.zeros(6, dtype=torch.int64, device="cuda")
+    acc = None if wide else torch.empty(m, n, dtype=torch.float32, device="cuda")
+    r = g(dA, counts=counts, checksums=True, faults=faults, accum_out=acc)
+    torch.cuda.synchronize()
+    e_max = g.opts.e_max
+    Sd = torch.from_numpy(S).cuda()
+    A_s = dA[Sd].double().cpu().numpy()
+    B_h = dB.double().cpu().numpy()
+    dev = {k_: getattr(r, k_)[Sd].cpu().numpy() for k_ in ("T", "diff1", "diff2", "residual", "location",
+                                                           "row_check1", "row_check2")}
+    det = r.detected.cpu().numpy().astype(bool)
+    # --- oracle on the row sample
+    T_ref, _ = O.vabft_thresholds(A_s, B_h, e_max, fmt=fmt)
+    assert _same(dev["T"], T_ref), ("thresholds", S[np.flatnonzero(dev["T"] != T_ref)][:8])
+    rc1, rc2 = O.blocked_row_checksums(A_s, B_h, fmt, mode)
+    assert _same(dev["row_check1"], rc1) and _same(dev["row_check2"], rc2), "row checksums"
+    if wide:
+        src = r.C[Sd].double().cpu().numpy()
+        v = O.verify(src, rc1, rc2, T_ref, fmt, "online", accum=(2, 128))
+    else:
+        src = (acc[Sd] if mode == "online" else r.C[Sd]).double().cpu().numpy()
+        v = O.verify(src, rc1, rc2, T_ref, "fp32", "offline", accum=(2, 128))
+    for key in ("diff1", "diff2", "residual"):
+        assert _same(dev[key], v[key]), key
+    assert np.array_equal(det[S], v["detected"]), ("detected", S[det[S] != v["detected"]][:8])
+    assert np.array_equal(dev["location"], v["location"]), "location"
+    # --- FPR over the full matrix: only planted rows may be flagged
+    clean = np.ones(m, dtype=bool)
+    clean[fr] = False
+    assert not det[clean].any(), ("false positives", np.flatnonzero(det & clean)[:8])
+    assert int(counts[0].item()) == m and int(counts[1].item()) == int(det.sum())
+    # --- C: FP32-accumulate bound against the exact product (unfaulted elements)
+    exact = A_s @ B_h
+    bound = (k + 1) * 2.0**-24 * (np.abs(A_s) @ np.abs(B_h))
+    got = src if (wide or mode == "online") else acc[Sd].double().cpu().numpy()
+    mask = np.ones_like(got, dtype=bool)
+    for i_s, row in enumerate(S):
+        if col[row] >= 0:
+            mask[i_s, int(col[row])] = False
+    assert np.all(np.abs(got - exact)[mask] <= bound[mask])
+    if not wide:  # C is the saturating RNE quantization (precision.cpp:129-159) of the post-injection accumulator
+        fmax = 65504.0 if fmt == "fp16" else float(torch.finfo(torch.bfloat16).max)
+        q = acc.clamp(-fmax, fmax).to(dt)
+        if mode == "offline":  # output-bit faults land after quantization
+            q[torch.from_numpy(fr).cuda(), torch.from_numpy(fcols).cuda()] = r.C[torch.from_numpy(fr).cuda(),
+                                                                                  torch.from_numpy(fcols).cuda()]
+        nan = torch.isnan(q)
+        assert torch.equal(torch.isnan(r.C), nan)
+        assert torch.equal(r.C.view(torch.int16)[~nan], q.view(torch.int16)[~nan])
+    located = v["location"][np.isin(S, fr)]
+    want = fcols[np.searchsorted(fr, S[np.isin(S, fr)])]
+    g.close()
+    return {"rows": len(S), "faulted": len(fr), "detected": int(v["detected"][np.isin(S, fr)].sum()),
+            "located": int((located == want).sum())}
+
+
+@pytest.mark.parametrize("mode", ["online", "offline"])
+def test_c2_bf16_4096_cubed(env, mode):
+    out = _run_config(env, 4096, 4096, 4096, "bf16", mode, seed=2)
+    assert out["detected"] > 0 and out["located"] > 0
+
+
+@pytest.mark.parametrize("k,n", [(4096, 11008), (11008, 4096)])
+def test_c4_llama_layer_shapes(env, k, n):
+    out = _run_config(env, 8192, k, n, "bf16", "online", seed=k + n, weights="linear")
+    assert out["detected"] > 0
+
+
+@pytest.mark.parametrize("m,k,n", [(6304, 768, 3072), (6304, 3072, 768), (6304, 768, 2304), (1024, 768, 2304),
+                                   (1024, 3072, 768)])
+def test_c5_vit_gpt2_shapes(env, m, k, n):
+    _run_config(env, m, k, n, "bf16", "online", seed=m + k + n)
+
+
+def test_c1_fp32_1024_cubed_bit_flips(env):
+    """C1: FP32 1024^3 N(0,1), 3xTF32 on tcgen05, single bit flips over bits
+    0..31 in half of all rows (every row is sampled)."""
+    out = _run_config(env, 1024, 1024, 1024, "fp32", "online", seed=1, faulted_fraction=0.5)
+    assert out["detected"] > 0 and out["located"] > 0
+
+
+@pytest.mark.parametrize("fmt", ["fp16", "fp64"])
+def test_c3_other_formats_2048(env, fmt):
+    _run_config(env, 2048, 2048, 2048, fmt, "online", seed=5)
+
+
+@pytest.mark.parametrize("mode", ["online", "offline"])
+def test_pair_half_tiles_match_one_cta_at_k4096(env, mode):
+    """4096^3 is 256 pair tiles = 3 waves of 74 + 34: the last 34 run as 68
+    half tiles, whose statistics warps take every other 128-k block of their
+    tile (K = 4096: 32 blocks over 16 N tiles, so the half-tile branch runs).
+    Thresholds, differences, verdicts and C equal the one-CTA kernel's."""
+    torch, _ = env
+    from paper_2602_08043_b200.fused import FusedAbftGemm
+    dA, dB = _inputs(torch, 4096, 4096, 4096, torch.bfloat16, 9)
+    g = FusedAbftGemm(dB, mode=mode)
+    out = {}
+    for cm in (0, 1):
+        g.opts.cta_mode = cm
+        r = g(dA, out=torch.empty(4096, 4096, device="cuda", dtype=torch.bfloat16), checksums=True)
+        torch.cuda.synchronize()
+        out[cm] = [x.clone() for x in (r.C.view(torch.int16), r.T, r.diff1, r.diff2, r.detected, r.row_check1)]
+    for a, b in zip(out[0], out[1]):
+        assert torch.equal(a, b)
+    g.close()

@@ -95,3 +95,23 @@ def test_gloo_two_ranks_nshard_and_counts():
 
 def test_merge_counts():
     assert merge_counts([[1, 2, 3, 4], [10, 20, 30, 40]]) == [11, 22, 33, 44]
+
+
+def test_bench_spawns_ranks_dry_run():
+    """bench.py --gpus 2 starts two ranks itself (torch.distributed.run) when
+    WORLD_SIZE is unset; --dry-run exercises the plan / slices / counter
+    all-reduce over gloo without a GPU."""
+    import json
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = {k: v for k, v in os.environ.items() if k not in ("WORLD_SIZE", "RANK", "LOCAL_RANK")}
+    for cfg, gemms in (("llama", 112), ("c2", 1), ("nsplit", 1)):
+        out = subprocess.run([sys.executable, os.path.join(root, "bench.py"), "--gpus", "2", "--dry-run",
+                              "--config", cfg], capture_output=True, text=True, timeout=240, env=env)
+        assert out.returncode == 0, out.stderr[-2000:]
+        line = json.loads([ln for ln in out.stdout.splitlines() if ln.startswith("{")][-1])
+        assert line["n_gpus"] == 2 and line["rank0_gemms"] == gemms
+        assert line["all_reduced_gemms"] == (224 if cfg == "llama" else 2)
+        if cfg == "nsplit":
+            assert line["rank0_columns"] == [0, 5504]

@@ -290,3 +290,42 @@ def test_port_matches_reference_when_built(port):
             for mode in ("offline", "online"):
                 a, b = R.encode_and_multiply(A, B, fmt, mode), port.encode_and_multiply(A, B, fmt, mode)
                 assert same(a.c_accum, b.c_accum) and same(a.row_check2, b.row_check2)
+
+
+@pytest.mark.parametrize("fmt", FMTS)
+@pytest.mark.parametrize("mode", ["offline", "online"])
+def test_blocked_row_checksums_composition(ref_or_port, fmt, mode):
+    """The config-scale checksum oracle (row_sums composition, no emulated
+    GEMM) equals encode_impl's row checksums with a NativeBlocked(128)
+    checksum precision: checked against a direct restatement of the
+    contract (checksum.cpp:74-79) in the working type."""
+    O = ref_or_port
+    A, B = O.trial_inputs(23, 300, 260, fmt, "normal:0,1", 77, 1)
+    c1, c2 = O.blocked_row_checksums(A, B, fmt, mode)
+    wt = np.float64 if fmt == "fp64" else np.float32
+
+    def blocked(terms):
+        tot = wt(0)
+        for b0 in range(0, len(terms), 128):
+            part = wt(0)
+            for t in terms[b0:b0 + 128]:
+                part = wt(part + t)
+            tot = wt(tot + part)
+        return tot
+    w = np.arange(1, B.shape[1] + 1, dtype=wt)
+    Bw = B.astype(wt)
+    br1 = np.array([blocked(Bw[q]) for q in range(B.shape[0])], dtype=wt)
+    br2 = np.array([blocked((w * Bw[q]).astype(wt)) for q in range(B.shape[0])], dtype=wt)
+    if mode == "offline":
+        br1 = np.array([O.quantize(float(x), fmt) for x in br1], dtype=wt)
+        br2 = np.array([O.quantize(float(x), fmt) for x in br2], dtype=wt)
+    Aw = A.astype(wt)
+    for br, got in ((br1, c1), (br2, c2)):
+        want = np.array([blocked((br * Aw[i]).astype(wt)) for i in range(A.shape[0])], dtype=np.float64)
+        if mode == "offline":
+            want = np.array([O.quantize(x, fmt) for x in want])
+        assert same(got, want)
+    if fmt in ("fp32", "fp64"):
+        # native formats: the reference's own encode with the strategy override
+        e = O.encode_and_multiply(A, B, fmt, mode, accum=(2, 128))
+        assert same(c1, e.row_check1) and same(c2, e.row_check2)
