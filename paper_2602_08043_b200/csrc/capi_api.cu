@@ -52,6 +52,23 @@ void check_weights(int64_t n, int fmt, int kind) {
              "ChecksumVectors: position weights exceed the exact-integer range of the checksum precision");
 }
 
+// Stream-ordered B-side buffers for one call (the handle-less entry points).
+BsideBuffers tmp_bside(Tmp& tmp, int fmt, int64_t k, int64_t n, cudaStream_t s) {
+    BsideBuffers buf;
+    buf.mean = tmp.get<double>(k);
+    buf.vb = tmp.get<double>(k);
+    buf.rowsum_abs = tmp.get<double>(k);
+    buf.br1 = tmp.get<float>(size_t(br_storage_floats(k)));
+    buf.br2 = tmp.get<float>(size_t(br_storage_floats(k)));
+    buf.summary = tmp.get<double>(4);
+    buf.nonfinite = tmp.get<int>(1);
+    buf.groups = tmp.get<unsigned>(bside_group_words(k));
+    buf.work = tmp.get<char>(bside_work_bytes(fmt, k, n));
+    check_cuda(cudaMemsetAsync(buf.nonfinite, 0, sizeof(int), s), "memset");
+    check_cuda(cudaMemsetAsync(buf.groups, 0, sizeof(unsigned) * bside_group_words(k), s), "memset");
+    return buf;
+}
+
 __global__ void thresholds_from_stats_kernel(int64_t m, int64_t n, const double* mean,
                                              const double* vb, const double* bsum, double e_max,
                                              double c_sigma, double* T) {
@@ -144,14 +161,7 @@ extern "C" vabft_status vabft_encode_and_multiply(const vabft_precision* spec, i
             epi.accum_out = static_cast<float*>(C_accum);
             tc_gemm_launch(f, false, m, n, k, A, B, c, epi, s);
             if (rc1 || rc2) {
-                BsideBuffers buf;
-                buf.mean = tmp.get<double>(k);
-                buf.vb = tmp.get<double>(k);
-                buf.rowsum_abs = tmp.get<double>(k);
-                buf.br1 = tmp.get<float>(size_t(br_storage_floats(k)));
-                buf.br2 = tmp.get<float>(size_t(br_storage_floats(k)));
-                buf.summary = tmp.get<double>(4);
-                buf.nonfinite = tmp.get<int>(1);
+                BsideBuffers buf = tmp_bside(tmp, f, k, n, s);
                 launch_bside(f, k, n, B, mode == VABFT_OFFLINE, buf, s);
                 double* T = tmp.get<double>(m);
                 double* mx = tmp.get<double>(1);
@@ -226,15 +236,7 @@ extern "C" vabft_status vabft_vabft_thresholds(int32_t format, int64_t m, int64_
         if (m < 1 || n < 1 || k < 1) fail(VABFT_INVALID_ARGUMENT, "dims must be >= 1");
         cudaStream_t s = as_stream(stream);
         Tmp tmp(s);
-        BsideBuffers buf;
-        buf.mean = tmp.get<double>(k);
-        buf.vb = tmp.get<double>(k);
-        buf.rowsum_abs = tmp.get<double>(k);
-        buf.br1 = tmp.get<float>(size_t(br_storage_floats(k)));
-        buf.br2 = tmp.get<float>(size_t(br_storage_floats(k)));
-        buf.summary = tmp.get<double>(4);
-        buf.nonfinite = tmp.get<int>(1);
-        check_cuda(cudaMemsetAsync(buf.nonfinite, 0, sizeof(int), s), "memset");
+        BsideBuffers buf = tmp_bside(tmp, format, k, n, s);
         launch_bside(format, k, n, B, 0, buf, s);
         double* mean = tmp.get<double>(m);
         double* vb = tmp.get<double>(m);
@@ -265,16 +267,10 @@ extern "C" vabft_status vabft_aabft_threshold(int32_t format, int64_t m, int64_t
         if (std::isnan(fixed_y)) {
             // computed y = max|A| * max_k |sum_j B[k][j]| (threshold_aabft.cpp:38-48)
             Tmp tmp(s);
-            BsideBuffers buf;
-            buf.mean = tmp.get<double>(k);
-            buf.vb = tmp.get<double>(k);
-            buf.rowsum_abs = tmp.get<double>(k);
-            buf.br1 = tmp.get<float>(size_t(br_storage_floats(k)));
-            buf.br2 = tmp.get<float>(size_t(br_storage_floats(k)));
-            buf.summary = tmp.get<double>(4);
-            buf.nonfinite = tmp.get<int>(1);
-            check_cuda(cudaMemsetAsync(buf.nonfinite, 0, sizeof(int), s), "memset");
+            BsideBuffers buf = tmp_bside(tmp, format, k, n, s);
             launch_bside(format, k, n, B, 0, buf, s);
+            if (format == VABFT_FP32 || format == VABFT_FP64)  // plain row sums on demand (bside.cu)
+                launch_bside_rowsum(format, k, n, B, buf, s);
             double* mx = tmp.get<double>(m);
             double* mn = tmp.get<double>(m);
             launch_row_stats(format, m, k, A, nullptr, mx, mn, nullptr, buf.nonfinite, s);

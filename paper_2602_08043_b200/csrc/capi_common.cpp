@@ -1,4 +1,5 @@
 // C-ABI plumbing: thread-local last error, status mapping, device info.
+#include <array>
 #include <atomic>
 #include <cstring>
 #include <map>
@@ -52,6 +53,19 @@ void ensure_smem_attr(const void* fn, int bytes) {
     check_cuda(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes),
                "cudaFuncSetAttribute(max dynamic shared memory)");
     g_attr_done.insert(key);
+}
+
+int cached_occupancy(const void* fn, int threads, int smem) {
+    return cached_cluster_count(
+        fn,
+        [](const void* f, void* ctx) {
+            const int* a = static_cast<const int*>(ctx);
+            int n = 0;
+            check_cuda(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, f, a[0], size_t(a[1])),
+                       "cudaOccupancyMaxActiveBlocksPerMultiprocessor");
+            return n;
+        },
+        const_cast<int*>(std::array<int, 2>{threads, smem}.data()));
 }
 
 int cached_cluster_count(const void* fn, int (*compute)(const void*, void*), void* ctx) {

@@ -46,6 +46,7 @@ struct vabft_bside {
     unsigned int* gbar;  // grid-barrier state of the fused kernel (inside storage)
     // wide formats (FP32 / FP64): B r1 / B r2 in the working type (held as doubles)
     double* brd = nullptr;  // [2][K]
+    bool rowsum_ready = false;  // wide formats: rowsum_abs / summary[3] (A-ABFT computed y) built
     // FP32 (3xTF32): the weight split once into hi / lo parts, transposed
     // ([2][N][K], K-major for kind::tf32), and
     // the activation's split buffers [2][M][K], grown on demand
@@ -192,17 +193,10 @@ WideWs carve_wide(void* base, int64_t M, int64_t N, int64_t K) {
 
 bool is_wide(int fmt) { return fmt == VABFT_FP32 || fmt == VABFT_FP64; }
 
-// TENSOR-engine checksum precision of the wide formats: the working type in
-// NativeBlocked(128) order.
-const vabft_accum kBlocked128{VABFT_ACCUM_BLOCKED, 0, 128};
-
-// B r1 / B r2 (checksum.cpp:110-115) of a wide-format weight.
-void wide_bside(vabft_bside* h, cudaStream_t s) {
-    launch_row_reduce(h->fmt, h->fmt == VABFT_FP32, 0, kBlocked128, h->k, h->n, h->B, nullptr, nullptr,
-                      h->mode == VABFT_OFFLINE ? h->fmt : -1, h->brd, h->brd + h->k, s);
-    if (h->fmt == VABFT_FP32)
-        split_tf32_t(static_cast<const float*>(h->B), h->b_split, h->b_split + size_t(h->k) * size_t(h->n), h->k,
-                     h->n, s);
+// FP32 weights: the TF32 hi / lo split, transposed for the kind::tf32 operand.
+// (B r1 / B r2 in the working type come from the B-side pass, buf.brd1/2.)
+void wide_split(vabft_bside* h, cudaStream_t s) {
+    split_tf32_t(static_cast<const float*>(h->B), h->b_split, h->b_split + size_t(h->k) * size_t(h->n), h->k, h->n, s);
 }
 
 // vabft_fused_gemm for FP32 / FP64: the GEMM with the ABFT epilogue, the
@@ -288,6 +282,10 @@ void wide_fused(const vabft_fused_opts* o, vabft_bside* h, int64_t m, const void
     // A-ABFT computed y needs the global max|A| first: combine in a separate
     // pass; otherwise the tail combines the A partials itself
     const bool global_y = o->threshold_method == 2;
+    if (global_y && !h->rowsum_ready) {  // max_k |sum_j B[k][j]| on first use (bside.cu)
+        launch_bside_rowsum(h->fmt, h->k, h->n, h->B, h->buf, s);
+        h->rowsum_ready = true;
+    }
     launch_wide_aside(h->fmt, m, k, A, h->brd, h->brd + k, o->mode == VABFT_OFFLINE ? h->fmt : -1, ws.mean, ws.vb,
                       ws.mx, ws.mn, ws.cr1, ws.cr2, ws.cpart, ws.ld, counts, global_y, s);
     if (global_y) {
@@ -356,8 +354,9 @@ extern "C" vabft_status vabft_bside_create(int32_t format, int32_t mode, int64_t
         h->B = B;
         const size_t K = size_t(k);
         const size_t KB = size_t(br_storage_floats(k));
+        const size_t gw = bside_group_words(k);
         const size_t bytes = align_up(8 * K) * 3 + align_up(4 * KB) * 2 + align_up(8 * 4) + align_up(4) + align_up(8) +
-                             align_up(4);
+                             align_up(4 * gw) + align_up(bside_work_bytes(format, k, n));
         check_cuda(cudaMalloc(&h->storage, bytes), "cudaMalloc(bside)");
         char* p = static_cast<char*>(h->storage);
         h->buf.mean = reinterpret_cast<double*>(p); p += align_up(8 * K);
@@ -368,19 +367,22 @@ extern "C" vabft_status vabft_bside_create(int32_t format, int32_t mode, int64_t
         h->buf.summary = reinterpret_cast<double*>(p); p += align_up(32);
         h->buf.nonfinite = reinterpret_cast<int*>(p); p += align_up(4);
         h->gbar = reinterpret_cast<unsigned int*>(p); p += align_up(8);
-        h->buf.done = reinterpret_cast<unsigned int*>(p);
-        check_cuda(cudaMemset(h->gbar, 0, 2 * sizeof(unsigned int)), "memset(grid barrier)");
-        check_cuda(cudaMemset(h->buf.done, 0, sizeof(unsigned int)), "memset(bside counter)");
+        h->buf.groups = reinterpret_cast<unsigned int*>(p); p += align_up(4 * gw);
+        h->buf.work = p;
+        // grid barrier, B-side group counters / flags and the non-finite flag start at zero
+        check_cuda(cudaMemset(h->buf.nonfinite, 0, size_t(p - reinterpret_cast<char*>(h->buf.nonfinite))),
+                   "memset(bside state)");
         if (is_wide(format)) {
             check_cuda(cudaMalloc(&h->brd, 2 * sizeof(double) * K), "cudaMalloc(bside B r)");
+            h->buf.brd1 = h->brd;
+            h->buf.brd2 = h->brd + K;
             if (format == VABFT_FP32) {
                 check_cuda(cudaMalloc(&h->b_split, 2 * sizeof(float) * K * size_t(n)), "cudaMalloc(B split)");
             }
         }
         if (B) {
-            check_cuda(cudaMemsetAsync(h->buf.nonfinite, 0, sizeof(int), as_stream(stream)), "memset");
             launch_bside(format, k, n, B, mode == VABFT_OFFLINE ? 1 : 0, h->buf, as_stream(stream));
-            if (is_wide(format)) wide_bside(h, as_stream(stream));
+            if (format == VABFT_FP32) wide_split(h, as_stream(stream));
         }
         *out = hp.release();
     });
@@ -390,9 +392,9 @@ extern "C" vabft_status vabft_bside_update(vabft_bside_t h, const void* B, void*
     return guarded([&] {
         if (!h || !B) fail(VABFT_INVALID_ARGUMENT, "vabft_bside_update: null argument");
         h->B = B;
-        check_cuda(cudaMemsetAsync(h->buf.nonfinite, 0, sizeof(int), as_stream(stream)), "memset");
+        h->rowsum_ready = false;
         launch_bside(h->fmt, h->k, h->n, B, h->mode == VABFT_OFFLINE ? 1 : 0, h->buf, as_stream(stream));
-        if (is_wide(h->fmt)) wide_bside(h, as_stream(stream));
+        if (h->fmt == VABFT_FP32) wide_split(h, as_stream(stream));
     });
 }
 

@@ -31,6 +31,8 @@ int sm_count();  // of the current device
 void ensure_smem_attr(const void* fn, int bytes);
 // per-(kernel, device) cache of an occupancy query: compute(fn, ctx) on a miss
 int cached_cluster_count(const void* fn, int (*compute)(const void*, void*), void* ctx);
+// per-(kernel, device) cudaOccupancyMaxActiveBlocksPerMultiprocessor
+int cached_occupancy(const void* fn, int threads, int smem);
 size_t elem_size(int fmt);
 
 // ---- verify tail (tail.cuh): inputs of one fused launch

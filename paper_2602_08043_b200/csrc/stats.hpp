@@ -16,17 +16,26 @@ struct BsideBuffers {
     double* rowsum_abs = nullptr;  // [K] |sum_j B[k][j]|
     double* summary = nullptr;     // [4] sum|mu|, sum mu^2, sum var, max_k |sum_j B|
     int* nonfinite = nullptr;      // [1] set when B holds NaN/Inf
-    unsigned int* done = nullptr;  // [1] zero-initialised CTA counter: the last CTA of the
-                                   // 16-bit row pass computes the summary (else a 2nd launch)
+    double* brd1 = nullptr;        // wide formats (optional): B r1 / B r2 in the working type, as doubles
+    double* brd2 = nullptr;
+    void* work = nullptr;          // bside_work_bytes(): per-(128-column block, row) partials
+    unsigned* groups = nullptr;    // bside_group_words(): arrival counters + ready flags, zero-initialised
+    unsigned epoch = 0;            // bumped by every launch (the ready-flag value)
 };
 
-// Floats of storage for one interleaved B r vector (K padded to 128).
+// Floats of storage for one B r vector (K padded to 128, zero padding).
 int64_t br_storage_floats(int64_t K);
+size_t bside_work_bytes(int fmt, int64_t K, int64_t N);
+size_t bside_group_words(int64_t K);
 
 void launch_row_stats(int fmt, int64_t rows, int64_t cols, const void* X, double* mean, double* mx,
                       double* mn, double* vb, int* nonfinite, cudaStream_t s);
+// The B-side pass (bside.cu). rowsum_abs / summary[3] (A-ABFT computed y)
+// are part of it for BF16 / FP16; the wide formats build them on demand with
+// launch_bside_rowsum.
 void launch_bside(int fmt, int64_t K, int64_t N, const void* B, int quantize_br, BsideBuffers& buf,
                   cudaStream_t s);
+void launch_bside_rowsum(int fmt, int64_t K, int64_t N, const void* B, BsideBuffers& buf, cudaStream_t s);
 void launch_aside(int fmt, int64_t M, int64_t K, int64_t N, const void* A, const BsideBuffers& buf,
                   int quantize_cr, double e_max, double c_sigma, double* T, double* cr1, double* cr2,
                   double* max_abs_a, cudaStream_t s);
