@@ -1092,6 +1092,148 @@ inline CampaignOutcome injection_campaign(const CampaignConfig& config, const Th
     return out;
 }
 
+// ---------------------------------------------------------- calibration.hpp
+// calibrate / fit_model (calibration.cpp:15-150): the reference's e_max
+// calibration protocol, with every GEMM, checksum and row sum on the device
+// EXACT engine (bit-identical to the emulator, hence the same maxima for the
+// same seed). The tcgen05 fast path is calibrated by the Python
+// paper_2602_08043_b200.calibration module (its accumulator differs).
+struct CalibrationModel {
+    EmaxModel::Kind kind = EmaxModel::Kind::Constant;
+    double value = 0.0, scale = 0.0, offset = 0.0, cv = 0.0, r2 = 0.0;
+};
+
+inline CalibrationModel fit_model(std::span<const int64_t> sizes, std::span<const double> maxima) {
+    if (sizes.size() != maxima.size() || sizes.empty())
+        throw std::invalid_argument("fit_model: sizes and maxima must match and be nonempty");
+    CalibrationModel m;
+    const size_t n = maxima.size();
+    double mean = 0.0;
+    for (const double v : maxima) mean += v;
+    mean /= double(n);
+    m.value = mean;
+    if (n >= 2 && mean > 0.0) {
+        double ss = 0.0;
+        for (const double v : maxima) ss += (v - mean) * (v - mean);
+        m.cv = std::sqrt(ss / double(n - 1)) / mean;
+    }
+    if (n >= 2) {
+        double sx = 0, sy = 0, sxx = 0, sxy = 0;
+        for (size_t i = 0; i < n; ++i) {
+            const double x = std::sqrt(double(sizes[i]));
+            sx += x;
+            sy += maxima[i];
+            sxx += x * x;
+            sxy += x * maxima[i];
+        }
+        const double denom = double(n) * sxx - sx * sx;
+        if (denom != 0.0) {
+            m.scale = (double(n) * sxy - sx * sy) / denom;
+            m.offset = (sy - m.scale * sx) / double(n);
+            double ss_res = 0, ss_tot = 0;
+            for (size_t i = 0; i < n; ++i) {
+                const double fit = m.scale * std::sqrt(double(sizes[i])) + m.offset;
+                ss_res += (maxima[i] - fit) * (maxima[i] - fit);
+                ss_tot += (maxima[i] - mean) * (maxima[i] - mean);
+            }
+            m.r2 = ss_tot > 0.0 ? 1.0 - ss_res / ss_tot : 1.0;
+        }
+    }
+    const bool constant = n < 2 || m.cv < 0.15 || m.scale <= 0.0;
+    m.kind = constant ? EmaxModel::Kind::Constant : EmaxModel::Kind::SqrtScaled;
+    return m;
+}
+
+struct CalibrationResult {
+    Format precision = Format::FP64;
+    VerifyMode mode = VerifyMode::Offline;
+    AccumStrategy accumulation{};
+    std::vector<int64_t> sizes;
+    std::vector<double> maxima;
+    CalibrationModel model;
+    double recommended = 0.0;
+    uint64_t seed = 0;
+    int64_t trials_per_size = 0;
+    int64_t aborted_trials = 0;
+    double unit_roundoff = 0.0;
+
+    // e_max_for (calibration.cpp:61-74)
+    double e_max_for(int64_t dim) const {
+        const double floor = 2.0 * unit_roundoff;
+        if (model.kind == EmaxModel::Kind::Constant) return std::max(recommended, floor);
+        double lambda = 1.0;
+        for (size_t i = 0; i < sizes.size(); ++i) {
+            const double fit = model.scale * std::sqrt(double(sizes[i])) + model.offset;
+            if (fit > 0.0) lambda = std::max(lambda, maxima[i] / fit);
+        }
+        return std::max(1.2 * lambda * (model.scale * std::sqrt(double(dim)) + model.offset), floor);
+    }
+    // recommended_model (calibration.cpp:76-86)
+    EmaxModel recommended_model() const {
+        if (model.kind == EmaxModel::Kind::Constant) return EmaxModel::constant(std::max(recommended, 2.0 * unit_roundoff));
+        double lambda = 1.0;
+        for (size_t i = 0; i < sizes.size(); ++i) {
+            const double fit = model.scale * std::sqrt(double(sizes[i])) + model.offset;
+            if (fit > 0.0) lambda = std::max(lambda, maxima[i] / fit);
+        }
+        return EmaxModel::sqrt_scaled(1.2 * lambda * model.scale, std::max(1.2 * lambda * model.offset, 0.0));
+    }
+};
+
+// calibrate (calibration.cpp:88-150): per trial Philox(seed, idx) -> |N(1,1)|
+// square A, B -> encode_and_multiply -> row_sums of the verification source
+// -> max_i |r1 - check1| / |check1| (a non-finite ratio aborts the trial);
+// per size the max over trials; fit_model; recommended = max(1.2 max, 2u).
+inline CalibrationResult calibrate(const PrecisionSpec& precision, std::span<const int64_t> sizes,
+                                   int64_t trials_per_size, uint64_t seed, VerifyMode mode = VerifyMode::Offline) {
+    if (sizes.empty()) throw std::invalid_argument("calibrate: need at least one size");
+    if (trials_per_size < 1) throw std::invalid_argument("calibrate: trials must be >= 1");
+    const Distribution dist = Distribution::abs_normal(1.0, 1.0);
+    const int64_t n_sizes = int64_t(sizes.size());
+    CalibrationResult out;
+    out.precision = precision.format;
+    out.mode = mode;
+    out.accumulation = precision.accumulation;
+    out.sizes.assign(sizes.begin(), sizes.end());
+    out.seed = seed;
+    out.trials_per_size = trials_per_size;
+    out.unit_roundoff = checksum_precision_for(precision, mode).unit_roundoff;
+    double overall = 0.0;
+    for (int64_t si = 0; si < n_sizes; ++si) {
+        const int64_t s = sizes[size_t(si)];
+        double mx_size = 0.0;
+        for (int64_t t = 0; t < trials_per_size; ++t) {
+            Philox rng(seed, uint64_t(si * trials_per_size + t));
+            const Matrix a = random_matrix(s, s, dist, precision, rng);
+            const Matrix b = random_matrix(s, s, dist, precision, rng);
+            const EncodedProduct prod = encode_and_multiply(a, b, mode);
+            const auto [r1, r2] = row_sums(prod.verification_source(), prod.checksum_precision);
+            (void)r2;
+            double mx = 0.0;
+            bool aborted = false;
+            for (int64_t i = 0; i < s; ++i) {
+                const double denom = std::abs(prod.row_check1[size_t(i)]);
+                const double rel = std::abs(r1[size_t(i)] - prod.row_check1[size_t(i)]) / denom;
+                if (!std::isfinite(rel)) {
+                    aborted = true;
+                    break;
+                }
+                mx = std::max(mx, rel);
+            }
+            if (aborted) {
+                ++out.aborted_trials;
+                continue;
+            }
+            mx_size = std::max(mx_size, mx);
+        }
+        out.maxima.push_back(mx_size);
+        overall = std::max(overall, mx_size);
+    }
+    out.model = fit_model(out.sizes, out.maxima);
+    out.recommended = std::max(1.2 * overall, 2.0 * out.unit_roundoff);
+    return out;
+}
+
 // ------------------------------------------------------------ matrix_io.hpp
 // VABFTMAT binary: magic, u32 version, u8 format id, u64 rows, u64 cols,
 // rows*cols little-endian FP64 (matrix_io.hpp:12-17); CSV one row per line.

@@ -64,7 +64,9 @@ struct BsT {
     static constexpr int kWords = 32;  // words per staged row
 };
 
-// Per-(block, row) partial arrays, each [nb][Kp].
+// Per-(block, row) partial arrays, group-major: element (block b, row k) at
+// ((k / 32) * nb + b) * 32 + k % 32, so a row group's partials of one array
+// are one contiguous span (the combining warp reads them coalesced).
 template <int F>
 struct BsPart {
     using W = typename BsT<F>::W;
@@ -72,9 +74,13 @@ struct BsPart {
     W *p1, *p2;
     double *s, *c;  // exact-sum partials (c: TwoSum tail, wide formats)
     V *sabs, *mx, *mn;
-    uint32_t* flags;  // 16-bit: (max magnitude pattern << 16) | (min nonzero magnitude pattern - 1);
+    uint32_t* flags;  // 16-bit: min nonzero magnitude pattern - 1 (0x7FFF: none);
                       // wide: 1 if the block holds a non-finite element
 };
+
+__host__ __device__ inline size_t bs_index(int64_t b, int64_t k, int64_t nb) {
+    return size_t(((k >> 5) * nb + b) * 32 + (k & 31));
+}
 
 template <int F>
 __host__ __device__ inline BsPart<F> bs_view(void* base, int64_t nb, int64_t kp) {
@@ -109,268 +115,292 @@ struct BsJob {
     BsideBuffers buf;
     BsPart<F> part;
     unsigned* grp_cnt;   // [ngroups] block arrivals (self-resetting)
-    unsigned* grp_flag;  // [ngroups] == epoch once the group is combined
-    unsigned epoch;
+    unsigned* grp_flag;  // [ngroups] == this launch's epoch once the group is combined
+    unsigned* grp_epoch;  // [2] epoch of the last complete launch, chains-done counter (device state, so a
+                          // CUDA-graph replay of the launch is a new epoch too)
+    int debug;  // developer ablation (VABFT_BSIDE_DEBUG): 1 no summary chains, 2 also no group combine
 };
 
 __device__ __forceinline__ float bs_add(float a, float b) { return __fadd_rn(a, b); }
 __device__ __forceinline__ double bs_add(double a, double b) { return __dadd_rn(a, b); }
 
-__device__ __forceinline__ void two_sum_bs(double a, double b, double& s, double& e) {
-    s = __dadd_rn(a, b);
-    const double bb = __dsub_rn(s, a);
-    e = __dadd_rn(__dsub_rn(a, __dsub_rn(s, bb)), __dsub_rn(b, bb));
-}
-
-// exact_sum_safe (wide.cu): hi = fl(s + c) equals the reference's Neumaier
-// fl(sum + comp) unless the exact sum is within 8 (K u)^2 sum|x| of a midpoint
-__device__ __forceinline__ bool bs_exact_safe(double s, double c, double sabs, int64_t K, double* hi_out) {
-    double hi, lo;
-    two_sum_bs(s, c, hi, lo);
-    const double ku = double(K) * 1.1102230246251565e-16;
-    const double margin = 8.0 * ku * ku * sabs * 1.01;  // sabs summed in the element type: 1 % slack
-    if (!(isfinite(hi) && isfinite(lo) && isfinite(margin))) return false;
-    const double nb = nextafter(hi, (lo > 0.0) ? INFINITY : -INFINITY);
-    if (!(fabs(lo) + margin < fabs(__dsub_rn(nb, hi)) * 0.5)) return false;
-    *hi_out = hi;
-    return true;
-}
-
-// Load one sub-tile (32 rows x kCols columns starting at column c) of the
-// row group into registers: lane l holds word l of every row.
+// Load one sub-tile (32 rows x kCols columns from column c) of the row group
+// starting at row pointer `base` (row stride N elements) into registers: lane l
+// holds word l of every row. Rows at or past `rows` read as zero.
 template <int F>
-__device__ __forceinline__ void bs_load(const BsJob<F>& j, int64_t r0, int64_t c, typename BsT<F>::Word (&v)[32]) {
+__device__ __forceinline__ void bs_load(const typename Elem<F>::T* __restrict__ base, int64_t N, int rows, int64_t c,
+                                        typename BsT<F>::Word (&v)[32]) {
     using Word = typename BsT<F>::Word;
     const int lane = threadIdx.x & 31;
     if constexpr (BsT<F>::k16) {
         const int64_t col = c + 2 * lane;
-        const bool even = (j.N & 1) == 0;
+        const bool in = col < N;
+        if ((N & 1) == 0) {  // rows 4-byte aligned: one 32-bit word per lane and row
+            const unsigned int* p = reinterpret_cast<const unsigned int*>(base + col);
+            const int64_t st = N >> 1;
 #pragma unroll
-        for (int rr = 0; rr < 32; ++rr) {
-            const int64_t r = r0 + rr;
-            uint32_t w = 0;
-            if (r < j.K && col < j.N) {
-                const uint16_t* p = j.B + r * j.N + col;
-                if (even) {
-                    w = __ldcs(reinterpret_cast<const unsigned int*>(p));
-                } else {  // odd N: rows are not 4-byte aligned
-                    w = __ldcs(p);
-                    if (col + 1 < j.N) w |= uint32_t(__ldcs(p + 1)) << 16;
+            for (int rr = 0; rr < 32; ++rr) v[rr] = (rr < rows && in) ? __ldcs(p + rr * st) : 0u;
+        } else {  // odd N
+            const uint16_t* p = base + col;
+            const bool in2 = col + 1 < N;
+#pragma unroll
+            for (int rr = 0; rr < 32; ++rr) {
+                uint32_t w = 0;
+                if (rr < rows && in) {
+                    w = __ldcs(p + rr * N);
+                    if (in2) w |= uint32_t(__ldcs(p + rr * N + 1)) << 16;
                 }
+                v[rr] = w;
             }
-            v[rr] = w;
         }
     } else {
         const int64_t col = c + lane;
+        const bool in = col < N;
+        const typename Elem<F>::T* p = base + col;
 #pragma unroll
         for (int rr = 0; rr < 32; ++rr) {
-            const int64_t r = r0 + rr;
             Word w = Word(0);
-            if (r < j.K && col < j.N) {
-                if constexpr (F == VABFT_FP32) w = __float_as_uint(__ldcs(j.B + r * j.N + col));
-                else w = __ldcs(j.B + r * j.N + col);
+            if (rr < rows && in) {
+                if constexpr (F == VABFT_FP32) w = __float_as_uint(__ldcs(p + rr * N));
+                else w = __ldcs(p + rr * N);
             }
             v[rr] = w;
         }
     }
 }
 
-// Process the row group's block b (lane = row).
+// Per-lane accumulators of one (row, block).
 template <int F>
-__device__ __forceinline__ void bs_block(const BsJob<F>& j, typename BsT<F>::Word* tile, int64_t rg, int b) {
+struct BsAcc {
     using W = typename BsT<F>::W;
     using V = typename BsT<F>::V;
-    using Word = typename BsT<F>::Word;
-    constexpr int kCols = BsT<F>::kCols;
-    constexpr int kStride = BsT<F>::kWords + 1;
-    const int lane = threadIdx.x & 31;
-    const int64_t r0 = rg * 32, row = r0 + lane;
-    const int64_t c0 = int64_t(b) * 128;
-    const int bw = int(j.N - c0 < 128 ? j.N - c0 : 128);
-    const int nsub = (bw + kCols - 1) / kCols;
-
     W p1 = W(0), p2 = W(0);
-    double s = 0.0, cc = 0.0;
+    double s = 0.0, c = 0.0;
     V sabs = V(0), mx = V(-INFINITY), mn = V(INFINITY);
-    uint32_t flg = 0;
-    // 16-bit packed trackers
+    unsigned long long bad = 0;
+    // 16-bit packed trackers: max (NaN-propagating), min, min nonzero magnitude - 1
     uint32_t vmax = F == VABFT_BF16 ? 0xFF80FF80u : 0xFC00FC00u;
     uint32_t vmin = F == VABFT_BF16 ? 0x7F807F80u : 0x7C007C00u;
-    uint32_t vmag = 0u, vmnz = 0x7FFF7FFFu;
-    unsigned long long bad = 0;
+    uint32_t vmnz = 0x7FFF7FFFu;
 
-    Word cur[32], nxt[32];
-    bs_load<F>(j, r0, c0, cur);
-    for (int q = 0; q < nsub; ++q) {
-        const int64_t cq = c0 + int64_t(q) * kCols;
-        if (q + 1 < nsub) bs_load<F>(j, r0, cq + kCols, nxt);
-        __syncwarp();
-#pragma unroll
-        for (int rr = 0; rr < 32; ++rr) tile[rr * kStride + lane] = cur[rr];
-        __syncwarp();
-        const int cnt = int(c0 + bw - cq < kCols ? c0 + bw - cq : kCols);  // warp-uniform
-        const Word* trow = tile + lane * kStride;
-        float wj = float(cq + 1);  // weight of the next element, exact (N <= 2^24)
-        if constexpr (BsT<F>::k16) {
-            const int npair = cnt >> 1;
-#pragma unroll 4
-            for (int jj = 0; jj < npair; ++jj) {
-                const uint32_t w = trow[jj];
-                uint32_t d;
-                if constexpr (F == VABFT_BF16) {
-                    asm("max.bf16x2 %0, %1, %2;" : "=r"(d) : "r"(vmax), "r"(w)); vmax = d;
-                    asm("min.bf16x2 %0, %1, %2;" : "=r"(d) : "r"(vmin), "r"(w)); vmin = d;
-                } else {
-                    asm("max.f16x2 %0, %1, %2;" : "=r"(d) : "r"(vmax), "r"(w)); vmax = d;
-                    asm("min.f16x2 %0, %1, %2;" : "=r"(d) : "r"(vmin), "r"(w)); vmin = d;
-                }
-                const uint32_t mag = w & 0x7FFF7FFFu;
-                asm("max.u16x2 %0, %1, %2;" : "=r"(d) : "r"(vmag), "r"(mag)); vmag = d;
-                asm("min.u16x2 %0, %1, %2;" : "=r"(d) : "r"(vmnz), "r"(((mag | 0x80008000u) - 0x00010001u) & 0x7FFF7FFFu));
-                vmnz = d;
-                const float xa = bits16_to_float<F>(uint16_t(w & 0xFFFFu));
-                const float xb = bits16_to_float<F>(uint16_t(w >> 16));
-                s = __dadd_rn(s, __dadd_rn(double(xa), double(xb)));  // exact under the guard
-                p1 = __fadd_rn(p1, xa);
-                p2 = __fadd_rn(p2, __fmul_rn(wj, xa));
-                wj = __fadd_rn(wj, 1.0f);
-                p1 = __fadd_rn(p1, xb);
-                p2 = __fadd_rn(p2, __fmul_rn(wj, xb));
-                wj = __fadd_rn(wj, 1.0f);
-            }
-            if (cnt & 1) {  // odd N: the row's last element
-                const uint16_t h = uint16_t(trow[npair] & 0xFFFFu);
-                const uint32_t hw = uint32_t(h) | (uint32_t(h) << 16);  // duplicate: neutral for the trackers
-                uint32_t d;
-                if constexpr (F == VABFT_BF16) {
-                    asm("max.bf16x2 %0, %1, %2;" : "=r"(d) : "r"(vmax), "r"(hw)); vmax = d;
-                    asm("min.bf16x2 %0, %1, %2;" : "=r"(d) : "r"(vmin), "r"(hw)); vmin = d;
-                } else {
-                    asm("max.f16x2 %0, %1, %2;" : "=r"(d) : "r"(vmax), "r"(hw)); vmax = d;
-                    asm("min.f16x2 %0, %1, %2;" : "=r"(d) : "r"(vmin), "r"(hw)); vmin = d;
-                }
-                const uint32_t mag = hw & 0x7FFF7FFFu;
-                asm("max.u16x2 %0, %1, %2;" : "=r"(d) : "r"(vmag), "r"(mag)); vmag = d;
-                asm("min.u16x2 %0, %1, %2;" : "=r"(d) : "r"(vmnz), "r"(((mag | 0x80008000u) - 0x00010001u) & 0x7FFF7FFFu));
-                vmnz = d;
-                const float xa = bits16_to_float<F>(h);
-                s = __dadd_rn(s, double(xa));
-                p1 = __fadd_rn(p1, xa);
-                p2 = __fadd_rn(p2, __fmul_rn(wj, xa));
-            }
+    __device__ __forceinline__ void track(uint32_t w) {
+        uint32_t d;
+        if constexpr (F == VABFT_BF16) {
+            asm("max.NaN.bf16x2 %0, %1, %2;" : "=r"(d) : "r"(vmax), "r"(w)); vmax = d;
+            asm("min.bf16x2 %0, %1, %2;" : "=r"(d) : "r"(vmin), "r"(w)); vmin = d;
         } else {
-#pragma unroll 4
-            for (int jj = 0; jj < cnt; ++jj) {
-                V x;
-                if constexpr (F == VABFT_FP32) x = __uint_as_float(trow[jj]);
-                else x = trow[jj];
-                const double xd = double(x);
-                if constexpr (F == VABFT_FP32) {
-                    bad = max(bad, static_cast<unsigned long long>(__float_as_uint(x) & 0x7FFFFFFFu));
-                    p1 = __fadd_rn(p1, x);
-                    p2 = __fadd_rn(p2, __fmul_rn(wj, x));
-                    sabs = __fadd_rn(sabs, fabsf(x));
-                } else {
-                    bad = max(bad, static_cast<unsigned long long>(__double_as_longlong(x)) & 0x7FFFFFFFFFFFFFFFull);
-                    p1 = __dadd_rn(p1, x);
-                    p2 = __dadd_rn(p2, __dmul_rn(double(wj), x));
-                    sabs = __dadd_rn(sabs, fabs(x));
-                }
-                wj = __fadd_rn(wj, 1.0f);
-                double t, e;
-                two_sum_bs(s, xd, t, e);
-                s = t;
-                cc = __dadd_rn(cc, e);
-                mx = mx < x ? x : mx;  // finite rows: fmax / fmin (non-finite rows are rejected)
-                mn = x < mn ? x : mn;
-            }
+            asm("max.NaN.f16x2 %0, %1, %2;" : "=r"(d) : "r"(vmax), "r"(w)); vmax = d;
+            asm("min.f16x2 %0, %1, %2;" : "=r"(d) : "r"(vmin), "r"(w)); vmin = d;
         }
-        if (q + 1 < nsub) {
-#pragma unroll
-            for (int rr = 0; rr < 32; ++rr) cur[rr] = nxt[rr];
-        }
+        // magnitude - 1 per half, zero -> 0x7FFF: (mag + 0x7FFF) mod 2^15
+        const uint32_t mz = ((w & 0x7FFF7FFFu) + 0x7FFF7FFFu) & 0x7FFF7FFFu;
+        asm("min.u16x2 %0, %1, %2;" : "=r"(d) : "r"(vmnz), "r"(mz)); vmnz = d;
     }
-    if (row < j.K) {
-        const size_t o = size_t(b) * size_t(j.Kp) + size_t(row);
-        if constexpr (BsT<F>::k16) {
-            const uint32_t mg = max(vmag & 0xFFFFu, vmag >> 16);
-            const uint32_t mz = min(vmnz & 0xFFFFu, vmnz >> 16);
-            flg = (mg << 16) | mz;
-            mx = fmaxf(bits16_to_float<F>(uint16_t(vmax & 0xFFFFu)), bits16_to_float<F>(uint16_t(vmax >> 16)));
-            mn = fminf(bits16_to_float<F>(uint16_t(vmin & 0xFFFFu)), bits16_to_float<F>(uint16_t(vmin >> 16)));
+    // one 32-bit word = 2 elements (16-bit formats); wt = weight of the first
+    __device__ __forceinline__ void pair(uint32_t w, float wt) {
+        track(w);
+        const float xa = bits16_to_float<F>(uint16_t(w & 0xFFFFu));
+        const float xb = bits16_to_float<F>(uint16_t(w >> 16));
+        s = __dadd_rn(s, __dadd_rn(double(xa), double(xb)));  // exact under the guard
+        p1 = __fadd_rn(__fadd_rn(p1, xa), xb);
+        p2 = __fadd_rn(p2, __fmul_rn(wt, xa));
+        p2 = __fadd_rn(p2, __fmul_rn(__fadd_rn(wt, 1.0f), xb));
+    }
+    // a lone 16-bit element (odd N), duplicated into both halves for the trackers
+    __device__ __forceinline__ void single(uint32_t h, float wt) {
+        track(h | (h << 16));
+        const float xa = bits16_to_float<F>(uint16_t(h));
+        s = __dadd_rn(s, double(xa));
+        p1 = __fadd_rn(p1, xa);
+        p2 = __fadd_rn(p2, __fmul_rn(wt, xa));
+    }
+    // one element of a wide format, weight wt
+    __device__ __forceinline__ void elem(V x, float wt) {
+        if constexpr (F == VABFT_FP32) {
+            bad = max(bad, static_cast<unsigned long long>(__float_as_uint(x) & 0x7FFFFFFFu));
+            p1 = __fadd_rn(p1, x);
+            p2 = __fadd_rn(p2, __fmul_rn(wt, x));
+            sabs = __fadd_rn(sabs, fabsf(x));
         } else {
-            flg = F == VABFT_FP32 ? (bad >= 0x7F800000ull ? 1u : 0u) : (bad >= 0x7FF0000000000000ull ? 1u : 0u);
-            j.part.c[o] = cc;
-            j.part.sabs[o] = sabs;
+            bad = max(bad, static_cast<unsigned long long>(__double_as_longlong(x)) & 0x7FFFFFFFFFFFFFFFull);
+            p1 = __dadd_rn(p1, x);
+            p2 = __dadd_rn(p2, __dmul_rn(double(wt), x));
+            sabs = __dadd_rn(sabs, fabs(x));
         }
-        j.part.p1[o] = p1;
-        j.part.p2[o] = p2;
-        j.part.s[o] = s;
+        double t, e;
+        two_sum(s, double(x), t, e);
+        s = t;
+        c = __dadd_rn(c, e);
+        mx = mx < x ? x : mx;  // finite rows: fmax / fmin (non-finite rows are rejected)
+        mn = x < mn ? x : mn;
+    }
+};
+
+// The block's per-row partials (lane = row) into the group-major arrays.
+template <int F>
+__device__ __forceinline__ void bs_store(const BsJob<F>& j, const BsAcc<F>& a, int64_t rg, int b) {
+    using V = typename BsT<F>::V;
+    const int lane = threadIdx.x & 31;
+    const int64_t r0 = rg * 32;
+    const int rows = int(j.K - r0 < 32 ? j.K - r0 : 32);
+    if (lane < rows) {
+        const size_t o = bs_index(b, r0 + lane, j.nb);
+        V mx = a.mx, mn = a.mn;
+        uint32_t flg;
+        if constexpr (BsT<F>::k16) {
+            flg = min(a.vmnz & 0xFFFFu, a.vmnz >> 16);
+            // the NaN-propagating max: a NaN anywhere in the block makes mx NaN
+            const float m0 = bits16_to_float<F>(uint16_t(a.vmax & 0xFFFFu));
+            const float m1 = bits16_to_float<F>(uint16_t(a.vmax >> 16));
+            mx = (isnan(m0) || isnan(m1)) ? __int_as_float(0x7FC00000) : fmaxf(m0, m1);
+            mn = fminf(bits16_to_float<F>(uint16_t(a.vmin & 0xFFFFu)), bits16_to_float<F>(uint16_t(a.vmin >> 16)));
+        } else {
+            flg = F == VABFT_FP32 ? (a.bad >= 0x7F800000ull ? 1u : 0u) : (a.bad >= 0x7FF0000000000000ull ? 1u : 0u);
+            j.part.c[o] = a.c;
+            j.part.sabs[o] = a.sabs;
+        }
+        j.part.p1[o] = a.p1;
+        j.part.p2[o] = a.p2;
+        j.part.s[o] = a.s;
         j.part.mx[o] = mx;
         j.part.mn[o] = mn;
         j.part.flags[o] = flg;
     }
 }
 
+// Process the row group's block b (lane = row).
+template <int F>
+__device__ __forceinline__ void bs_block(const BsJob<F>& j, typename BsT<F>::Word* tile, int64_t rg, int b) {
+    using Word = typename BsT<F>::Word;
+    using V = typename BsT<F>::V;
+    constexpr int kCols = BsT<F>::kCols;
+    constexpr int kStride = BsT<F>::kWords + 1;
+    const int lane = threadIdx.x & 31;
+    const int64_t K = j.K, N = j.N;
+    const int64_t r0 = rg * 32;
+    const int rows = int(K - r0 < 32 ? K - r0 : 32);
+    const int64_t c0 = int64_t(b) * 128;
+    const int bw = int(N - c0 < 128 ? N - c0 : 128);
+    const int nsub = (bw + kCols - 1) / kCols;
+    const typename Elem<F>::T* base = j.B + r0 * N;
+
+    BsAcc<F> a;
+    Word v[32];
+    bs_load<F>(base, N, rows, c0, v);
+    __syncwarp();
+#pragma unroll
+    for (int rr = 0; rr < 32; ++rr) tile[rr * kStride + lane] = v[rr];
+    __syncwarp();
+    const Word* trow = tile + lane * kStride;
+    for (int q = 0; q < nsub; ++q) {
+        const int64_t cq = c0 + int64_t(q) * kCols;
+        // the next sub-tile's loads are in flight while this one is processed
+        if (q + 1 < nsub) bs_load<F>(base, N, rows, cq + kCols, v);
+        const int cnt = int(c0 + bw - cq < kCols ? c0 + bw - cq : kCols);  // warp-uniform
+        const float w0 = float(cq + 1);  // weight j + 1 of the sub-tile's first element (exact: N <= 2^24)
+        if constexpr (BsT<F>::k16) {
+            if (cnt == kCols) {
+#pragma unroll
+                for (int jj = 0; jj < kCols / 2; ++jj) a.pair(trow[jj], __fadd_rn(w0, float(2 * jj)));
+            } else {
+                const int npair = cnt >> 1;
+                for (int jj = 0; jj < npair; ++jj) a.pair(trow[jj], __fadd_rn(w0, float(2 * jj)));
+                if (cnt & 1) a.single(trow[npair] & 0xFFFFu, __fadd_rn(w0, float(2 * npair)));
+            }
+        } else {
+            if (cnt == kCols) {
+#pragma unroll 8
+                for (int jj = 0; jj < kCols; ++jj) {
+                    if constexpr (F == VABFT_FP32) a.elem(__uint_as_float(trow[jj]), __fadd_rn(w0, float(jj)));
+                    else a.elem(trow[jj], __fadd_rn(w0, float(jj)));
+                }
+            } else {
+                for (int jj = 0; jj < cnt; ++jj) {
+                    if constexpr (F == VABFT_FP32) a.elem(__uint_as_float(trow[jj]), __fadd_rn(w0, float(jj)));
+                    else a.elem(trow[jj], __fadd_rn(w0, float(jj)));
+                }
+            }
+        }
+        if (q + 1 < nsub) {
+            __syncwarp();
+#pragma unroll
+            for (int rr = 0; rr < 32; ++rr) tile[rr * kStride + lane] = v[rr];
+            __syncwarp();
+        }
+    }
+    bs_store<F>(j, a, rg, b);
+}
+
 // Combine a finished row group (lane = row) and publish it.
 template <int F>
-__device__ __forceinline__ void bs_combine(const BsJob<F>& j, int64_t rg) {
+__device__ __forceinline__ void bs_combine(const BsJob<F>& j, int64_t rg, unsigned epoch) {
     using W = typename BsT<F>::W;
     using V = typename BsT<F>::V;
     const int lane = threadIdx.x & 31;
     const int64_t k = rg * 32 + lane;
-    if (k < j.K) {
-        W t1 = W(0), t2 = W(0);
-        double s = 0.0, c = 0.0, sabs = 0.0;
-        V mx = V(-INFINITY), mn = V(INFINITY);
-        uint32_t mg = 0u, mz = 0xFFFFu, bad = 0u;
-#pragma unroll 4
-        for (int b = 0; b < j.nb; ++b) {  // block order: the blocked:128 combination
-            const size_t o = size_t(b) * size_t(j.Kp) + size_t(k);
-            t1 = bs_add(t1, __ldcg(j.part.p1 + o));
-            t2 = bs_add(t2, __ldcg(j.part.p2 + o));
-            const V bx = __ldcg(j.part.mx + o), bn = __ldcg(j.part.mn + o);
-            mx = mx < bx ? bx : mx;
-            mn = bn < mn ? bn : mn;
-            const uint32_t f = __ldcg(j.part.flags + o);
-            if constexpr (BsT<F>::k16) {
-                s = __dadd_rn(s, __ldcg(j.part.s + o));
-                mg = max(mg, f >> 16);
-                mz = min(mz, f & 0xFFFFu);
-            } else {
-                bad |= f;
-                double t, e;
-                two_sum_bs(s, __ldcg(j.part.s + o), t, e);
-                s = t;
-                c = __dadd_rn(__dadd_rn(c, __ldcg(j.part.c + o)), e);
-                sabs = __dadd_rn(sabs, double(__ldcg(j.part.sabs + o)));
-            }
-        }
-        Neu n;
-        double plain = 0.0;
-        bool finite, fast;
+    const int nb = j.nb;
+    W t1 = W(0), t2 = W(0);
+    double s = 0.0, c = 0.0, sabs = 0.0;
+    V mx = V(-INFINITY), mn = V(INFINITY);
+    uint32_t mz = 0x7FFFu, bad = 0u;
+    const size_t o0 = bs_index(0, k, nb);
+#pragma unroll 8
+    for (int b = 0; b < nb; ++b) {  // block order: the blocked:128 combination
+        const size_t o = o0 + size_t(b) * 32;
+        t1 = bs_add(t1, __ldcg(j.part.p1 + o));
+        t2 = bs_add(t2, __ldcg(j.part.p2 + o));
+        const V bx = __ldcg(j.part.mx + o), bn = __ldcg(j.part.mn + o);
+        mx = (isnan(bx) || mx < bx) ? bx : mx;
+        mn = bn < mn ? bn : mn;
+        const uint32_t f = __ldcg(j.part.flags + o);
         if constexpr (BsT<F>::k16) {
-            finite = mg < (F == VABFT_BF16 ? 0x7F80u : 0x7C00u);
-            fast = finite && guard_exact<F>(fmaxf(fabsf(mx), fabsf(mn)), mz, j.N);
+            s = __dadd_rn(s, __ldcg(j.part.s + o));
+            mz = min(mz, f);
+        } else {
+            bad |= f;
+            double t, e;
+            two_sum(s, __ldcg(j.part.s + o), t, e);
+            s = t;
+            c = __dadd_rn(__dadd_rn(c, __ldcg(j.part.c + o)), e);
+            sabs = __dadd_rn(sabs, double(__ldcg(j.part.sabs + o)));
+        }
+    }
+    bool fast = false, finite = true;
+    Neu n;
+    double plain = 0.0;
+    if (k < j.K) {
+        if constexpr (BsT<F>::k16) {
+            const float amax = fmaxf(fabsf(mx), fabsf(mn));
+            finite = !isnan(mx) && isfinite(amax);
+            fast = finite && guard_exact<F>(amax, mz, j.N);
             n.s = s;
             plain = s;
         } else {
             finite = bad == 0u;
             double hi = 0.0;
-            fast = finite && bs_exact_safe(s, c, sabs, j.N, &hi);
+            // sabs was summed in the element type: 1 % slack keeps it an upper bound
+            fast = finite && exact_sum_safe(s, c, __dmul_rn(sabs, 1.01), j.N, &hi);
             n.s = hi;
         }
-        if (!finite) atomicMax(reinterpret_cast<unsigned*>(j.buf.nonfinite), j.epoch);  // nonzero: this launch saw NaN / Inf
-        if (!fast) {  // the reference's sequential loops over the row (rare)
+        // nonzero: this launch saw NaN / Inf
+        if (!finite) atomicMax(reinterpret_cast<unsigned*>(j.buf.nonfinite), epoch);
+    }
+    // rows outside the exactness guard: the reference's Neumaier sum by the
+    // whole warp (warp_neumaier_row: parallel error-free sum + midpoint check,
+    // the sequential loop only next to a rounding midpoint)
+    unsigned slow = __ballot_sync(0xffffffffu, k < j.K && finite && !fast);
+    while (slow) {
+        const int l = __ffs(slow) - 1;
+        slow &= slow - 1;
+        double pl;
+        const double hs = warp_neumaier_row<F>(j.B + (rg * 32 + l) * j.N, j.N, BsT<F>::k16 ? &pl : nullptr);
+        if (lane == l) {
             n = Neu{};
-            plain = 0.0;
-            const auto* r = j.B + k * j.N;
-            for (int64_t q = 0; q < j.N; ++q) {
-                const double x = Elem<F>::d(r[q]);
-                n.add(x);
-                plain = __dadd_rn(plain, x);
-            }
+            n.s = hs;
+            plain = pl;
         }
+    }
+    if (k < j.K) {
         double m, v;
         stats_finish(n, double(mx), double(mn), j.N, &m, &v);
         j.buf.mean[k] = m;
@@ -390,73 +420,134 @@ __device__ __forceinline__ void bs_combine(const BsJob<F>& j, int64_t rg) {
                 j.buf.brd1[k] = double(t1);
                 j.buf.brd2[k] = double(t2);
             }
-            if (!fast) j.buf.rowsum_abs[k] = fabs(plain);  // by-product of the fallback; see launch_bside_rowsum
         }
     }
     __threadfence();
     __syncwarp();
-    if (lane == 0) *reinterpret_cast<volatile unsigned*>(j.grp_flag + rg) = j.epoch;
+    if (lane == 0) *reinterpret_cast<volatile unsigned*>(j.grp_flag + rg) = epoch;
 }
 
-// The summary warp: BStatsSummary::from's sequential FP64 sums over k in row
-// order (threshold_vabft.cpp:15-26) and max_k |sum_j B| (16-bit formats; the
-// wide formats' plain row sums come from launch_bside_rowsum), consuming row
-// groups as they are published.
-template <int F>
-__device__ void bs_summary(const BsJob<F>& j) {
+// Summary: BStatsSummary::from's three sequential FP64 sums over k in row
+// order (threshold_vabft.cpp:15-26), one chain per warp (warps 0..2 of CTA 0,
+// on different schedulers), and max_k |sum_j B| (16-bit formats; order-free,
+// so warp 3 folds it lane-parallel; the wide formats' plain row sums come from
+// launch_bside_rowsum). The published row groups are consumed in batches of
+// 256 rows: while lane 0 runs the chain over batch i out of shared memory
+// (16-byte LDS issued ahead of the adds), the warp's coalesced loads of batch
+// i + 1 are in flight, landing in the other half of the warp's double buffer.
+// The chains then run at about one FP64 add latency (~8 cycles) per element:
+// the kernel's floor, K x 8 cycles. (Measured: a 16-value register prefetch
+// left every batch waiting ~1000 cycles on L2; a data-dependent branch or an
+// fmax in the chain doubled or quadrupled its cost.)
+template <int F, int kWhich>
+__device__ void bs_summary(const BsJob<F>& j, double* buf2 /* 2 x kBatch doubles */, unsigned epoch) {
+    constexpr int which = kWhich;  // compile-time: no branch inside the chain
+    constexpr int kBatch = 256, kPer = kBatch / 32;
     const int lane = threadIdx.x & 31;
-    double a_abs = 0.0, a_sq = 0.0, a_var = 0.0, a_max = 0.0;
-    int64_t ready = 0;  // groups [0, ready) are published
-    // poll the next 32 groups' flags at once; true when group rg is published
-    auto poll = [&](int64_t rg) {
-        if (rg < ready) return true;
-        const int64_t g = ready + lane;
-        const bool ok = g >= j.ngroups || *reinterpret_cast<volatile const unsigned*>(j.grp_flag + g) == j.epoch;
-        const unsigned bal = __ballot_sync(0xffffffffu, ok);
-        const int run = bal == 0xffffffffu ? 32 : __ffs(~bal) - 1;
-        if (run > 0) {
-            __threadfence();  // the group's values were fenced before its flag
+    const double* src = which == 2 ? j.buf.vb : which == 3 ? j.buf.rowsum_abs : j.buf.mean;
+    const int64_t K = j.K;
+    int64_t ready = j.debug >= 3 ? j.ngroups : 0;  // groups [0, ready) are published (debug >= 3: chains alone)
+    auto published = [&](int64_t kend) {  // rows [0, kend) published?
+        const int64_t need = (kend + 31) / 32;
+        while (ready < need) {
+            const int64_t g = ready + lane;
+            const bool ok = g >= j.ngroups || *reinterpret_cast<volatile const unsigned*>(j.grp_flag + g) == epoch;
+            const unsigned bal = __ballot_sync(0xffffffffu, ok);
+            const int run = bal == 0xffffffffu ? 32 : __ffs(~bal) - 1;
+            if (run == 0) return false;
+            // no fence per poll (measured to cost more than the chain): the
+            // producer fenced the group's values before its flag, and the
+            // value loads below are L2 (.cg) loads issued after the flag was
+            // seen (control dependency)
             ready += run;
         }
-        return rg < ready;
+        return true;
     };
-    auto load = [&](int64_t rg, double& m, double& v, double& rs) {
-        const int64_t k = rg * 32 + lane;
-        const bool valid = k < j.K;
-        m = valid ? __ldcg(j.buf.mean + k) : 0.0;
-        v = valid ? __ldcg(j.buf.vb + k) : 0.0;
-        rs = (valid && BsT<F>::k16) ? __ldcg(j.buf.rowsum_abs + k) : 0.0;
+    auto fetch = [&](int64_t k0, double (&v)[kPer]) {
+#pragma unroll
+        for (int e = 0; e < kPer; ++e) {
+            const int64_t k = k0 + e * 32 + lane;
+            v[e] = k < K ? __ldcg(src + k) : 0.0;
+        }
     };
-    double m, v, rs;
-    while (!poll(0)) __nanosleep(64);
-    load(0, m, v, rs);
-    for (int64_t rg = 0; rg < j.ngroups; ++rg) {
-        // the next group's values are in flight while this group's chain runs
-        double mn = 0.0, vn = 0.0, rsn = 0.0;
-        const bool pre = rg + 1 < j.ngroups && poll(rg + 1);
-        if (pre) load(rg + 1, mn, vn, rsn);
-        const int cnt = int(j.K - rg * 32 < 32 ? j.K - rg * 32 : 32);
-#pragma unroll 8
-        for (int q = 0; q < cnt; ++q) {
-            const double mq = __shfl_sync(0xffffffffu, m, q);
-            a_abs = __dadd_rn(a_abs, fabs(mq));
-            a_sq = __dadd_rn(a_sq, __dmul_rn(mq, mq));
-            a_var = __dadd_rn(a_var, __shfl_sync(0xffffffffu, v, q));
-            a_max = fmax(a_max, __shfl_sync(0xffffffffu, rs, q));
+    double acc = 0.0, v[kPer];
+    if constexpr (which == 3) {  // max_k |sum_j B|: order-free, lane-parallel
+        for (int64_t k0 = 0; k0 < K; k0 += 2 * kBatch) {  // two batches of loads in flight
+            const int64_t kend = k0 + 2 * kBatch < K ? k0 + 2 * kBatch : K;
+            while (!published(kend)) __nanosleep(64);
+            double w[kPer];
+            fetch(k0, v);
+            fetch(k0 + kBatch, w);
+#pragma unroll
+            for (int e = 0; e < kPer; ++e) acc = fmax(acc, fmax(v[e], w[e]));
         }
-        if (rg + 1 < j.ngroups && !pre) {
-            while (!poll(rg + 1)) __nanosleep(64);
-            load(rg + 1, mn, vn, rsn);
+#pragma unroll
+        for (int m = 16; m >= 1; m >>= 1) acc = fmax(acc, __shfl_xor_sync(0xffffffffu, acc, m));
+        if (lane == 0) j.buf.summary[3] = acc;
+        return;  // (warp 3 does not take part in the epoch hand-over)
+    }
+    auto stage = [&](const double (&x)[kPer], double* dst) {
+#pragma unroll
+        for (int e = 0; e < kPer; ++e) dst[e * 32 + lane] = x[e];
+        __syncwarp();
+    };
+    while (!published(kBatch < K ? kBatch : K)) __nanosleep(64);
+    fetch(0, v);
+    stage(v, buf2);
+    int cur = 0;
+    for (int64_t k0 = 0; k0 < K; k0 += kBatch) {
+        const int64_t k1 = k0 + kBatch;
+        const bool more = k1 < K;
+        const int64_t kend = k1 + kBatch < K ? k1 + kBatch : K;
+        const bool pre = more && published(kend);
+        if (pre) fetch(k1, v);  // in flight during the chain below
+        if (lane == 0) {
+            const double* x = buf2 + cur * kBatch;
+            const int cnt = int(K - k0 < kBatch ? K - k0 : kBatch);
+            if (cnt == kBatch) {
+                // 32 values per round loaded into registers before the adds,
+                // so no add waits on a shared-memory load
+#pragma unroll 1
+                for (int e0 = 0; e0 < kBatch; e0 += 32) {
+                    double2 q[16];
+#pragma unroll
+                    for (int i = 0; i < 16; ++i) q[i] = reinterpret_cast<const double2*>(x + e0)[i];
+#pragma unroll
+                    for (int i = 0; i < 16; ++i) {
+                        if constexpr (which == 0) acc = __dadd_rn(__dadd_rn(acc, fabs(q[i].x)), fabs(q[i].y));
+                        else if constexpr (which == 1)
+                            acc = __dadd_rn(__dadd_rn(acc, __dmul_rn(q[i].x, q[i].x)), __dmul_rn(q[i].y, q[i].y));
+                        else acc = __dadd_rn(__dadd_rn(acc, q[i].x), q[i].y);
+                    }
+                }
+            } else {
+                for (int e = 0; e < cnt; ++e) {
+                    const double xe = x[e];
+                    if constexpr (which == 0) acc = __dadd_rn(acc, fabs(xe));
+                    else if constexpr (which == 1) acc = __dadd_rn(acc, __dmul_rn(xe, xe));
+                    else acc = __dadd_rn(acc, xe);
+                }
+            }
         }
-        m = mn;
-        v = vn;
-        rs = rsn;
+        __syncwarp();
+        if (more) {
+            if (!pre) {
+                while (!published(kend)) __nanosleep(64);
+                fetch(k1, v);
+            }
+            cur ^= 1;
+            stage(v, buf2 + cur * kBatch);
+        }
     }
     if (lane == 0) {
-        j.buf.summary[0] = a_abs;
-        j.buf.summary[1] = a_sq;
-        j.buf.summary[2] = a_var;
-        if (BsT<F>::k16) j.buf.summary[3] = a_max;
+        j.buf.summary[which] = acc;
+        // the last of the three chains (every flag read) closes the epoch
+        __threadfence();
+        if (atomicAdd(j.grp_epoch + 1, 1u) == 2u) {
+            j.grp_epoch[1] = 0u;
+            __threadfence();
+            j.grp_epoch[0] = epoch;
+        }
     }
 }
 
@@ -469,38 +560,51 @@ template <int F>
 __global__ void __launch_bounds__(kBsThreads, F == VABFT_FP64 ? 1 : 2) bside_kernel(const __grid_constant__ BsJob<F> j) {
     using Word = typename BsT<F>::Word;
     constexpr int kStride = BsT<F>::kWords + 1;
+    constexpr int kChains = BsT<F>::k16 ? 4 : 3;  // wide formats: max_k |sum_j B| on demand
     extern __shared__ __align__(16) uint8_t bs_smem_raw[];
     Word* tiles = reinterpret_cast<Word*>(bs_smem_raw);
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    if (blockIdx.x == 0 && warp == 0) {
-        bs_summary<F>(j);
+    const unsigned epoch = *reinterpret_cast<volatile const unsigned*>(j.grp_epoch) + 1u;
+    if (blockIdx.x == 0 && warp < kChains) {  // the warp's tile slice is its double buffer (>= 2 KiB)
+        double* b2 = reinterpret_cast<double*>(tiles + size_t(warp) * 32 * kStride);
+        if (j.debug == 0 || j.debug == 3 || j.debug == 4 + warp) {
+            switch (warp) {
+                case 0: bs_summary<F, 0>(j, b2, epoch); break;
+                case 1: bs_summary<F, 1>(j, b2, epoch); break;
+                case 2: bs_summary<F, 2>(j, b2, epoch); break;
+                default: bs_summary<F, 3>(j, b2, epoch); break;
+            }
+        }
         return;
     }
     // zero padding of the B r vectors (the A-side readers take whole 128-k blocks)
-    if (blockIdx.x == 0 && warp == 1) {
+    if (blockIdx.x == 0 && warp == kChains) {
         const int64_t kpad = (j.K + 127) / 128 * 128;
         for (int64_t k = j.K + lane; k < kpad; k += 32) {
             j.buf.br1[k] = 0.0f;
             j.buf.br2[k] = 0.0f;
         }
     }
+    if (j.debug >= 3) return;  // chains alone (developer timing)
     Word* tile = tiles + size_t(warp) * 32 * kStride;
-    const int64_t tw = int64_t(blockIdx.x) * kBsWarps + warp - 1;
-    const int64_t nt = int64_t(gridDim.x) * kBsWarps - 1;
-    const int64_t tasks = int64_t(j.ngroups) * j.nb;
+    const int64_t tw = int64_t(blockIdx.x) * kBsWarps + warp - kChains;
+    const int64_t nt = int64_t(gridDim.x) * kBsWarps - kChains;
+    const int nb = j.nb;
+    const int64_t tasks = int64_t(j.ngroups) * nb;
     for (int64_t t = tw; t < tasks; t += nt) {
-        const int64_t rg = t / j.nb;
-        const int b = int(t - rg * j.nb);
+        const int64_t rg = t / nb;
+        const int b = int(t - rg * nb);
         bs_block<F>(j, tile, rg, b);
+        // arrival: every lane's partial stores before lane 0's counter RMW
         __threadfence();
         __syncwarp();
         unsigned old = 0;
         if (lane == 0) old = atomicAdd(j.grp_cnt + rg, 1u);
         old = __shfl_sync(0xffffffffu, old, 0);
-        if (old == unsigned(j.nb) - 1u) {
+        if (old == unsigned(nb) - 1u && j.debug < 2) {
             __threadfence();
             if (lane == 0) j.grp_cnt[rg] = 0u;  // ready for the next launch
-            bs_combine<F>(j, rg);
+            bs_combine<F>(j, rg, epoch);
         }
     }
 }
@@ -547,8 +651,12 @@ void launch_bs(int64_t K, int64_t N, const void* B, int quantize_br, BsideBuffer
     j.part = bs_view<F>(buf.work, j.nb, j.Kp);
     j.grp_cnt = buf.groups;
     j.grp_flag = buf.groups + j.ngroups;
-    j.epoch = ++buf.epoch;
-    if (j.epoch == 0) j.epoch = ++buf.epoch;  // flags are zero-initialised: never publish epoch 0
+    static const int dbg = [] {
+        const char* e = std::getenv("VABFT_BSIDE_DEBUG");
+        return e ? std::atoi(e) : 0;
+    }();
+    j.debug = dbg;
+    j.grp_epoch = buf.groups + 2 * j.ngroups;
     constexpr size_t smem = bs_smem<F>();
     ensure_smem_attr(reinterpret_cast<const void*>(bside_kernel<F>), int(smem));
     const int per_sm = cached_occupancy(reinterpret_cast<const void*>(bside_kernel<F>), kBsThreads, int(smem));
@@ -571,7 +679,7 @@ size_t bside_work_bytes(int fmt, int64_t K, int64_t N) {
     }
 }
 
-size_t bside_group_words(int64_t K) { return size_t(2 * ((K + 31) / 32)); }
+size_t bside_group_words(int64_t K) { return size_t(2 * ((K + 31) / 32) + 2); }
 
 int64_t br_storage_floats(int64_t K) { return ((K + 127) / 128) * 128; }
 

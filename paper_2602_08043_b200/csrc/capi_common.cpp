@@ -8,6 +8,8 @@
 #include <string>
 #include <tuple>
 
+#include <cuda.h>
+#include <cudaTypedefs.h>
 #include <cuda_runtime.h>
 
 #include "internal.hpp"
@@ -79,6 +81,28 @@ int cached_cluster_count(const void* fn, int (*compute)(const void*, void*), voi
     std::lock_guard<std::mutex> lk(g_attr_mu);
     g_clusters[key] = n;
     return n;
+}
+
+CUtensorMap encode_map_2d(CUtensorMapDataType dt, const void* base, uint64_t rows, uint64_t cols, uint64_t ld,
+                          uint32_t elem_bytes, uint32_t box_cols, uint32_t box_rows, CUtensorMapSwizzle swizzle) {
+    static PFN_cuTensorMapEncodeTiled_v12000 fn = [] {
+        void* ptr = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &ptr, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            return reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(ptr);
+        return static_cast<PFN_cuTensorMapEncodeTiled_v12000>(nullptr);
+    }();
+    if (!fn) fail(VABFT_CUDA_ERROR, "cuTensorMapEncodeTiled unavailable");
+    CUtensorMap m;
+    cuuint64_t dims[2] = {cols, rows};
+    cuuint64_t strides[1] = {ld * elem_bytes};
+    cuuint32_t box[2] = {box_cols, box_rows};
+    cuuint32_t estr[2] = {1, 1};
+    const CUresult r = fn(&m, dt, 2, const_cast<void*>(base), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                          swizzle, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) fail(VABFT_CUDA_ERROR, "cuTensorMapEncodeTiled failed");
+    return m;
 }
 
 size_t elem_size(int fmt) {

@@ -66,6 +66,30 @@ struct Neu {
     }
 };
 
+// Error-free transformation: s + e == a + b exactly (Knuth's TwoSum).
+__device__ __forceinline__ void two_sum(double a, double b, double& s, double& e) {
+    s = __dadd_rn(a, b);
+    const double bb = __dsub_rn(s, a);
+    e = __dadd_rn(__dsub_rn(a, __dsub_rn(s, bb)), __dsub_rn(b, bb));
+}
+
+// A row sum held as an error-free cascade (s, c): hi = fl(s + c) equals the
+// reference's sequential Neumaier fl(sum + comp) (stats.cpp:12-24) unless the
+// exact sum lies within 8 (K u)^2 sum|x| of a rounding midpoint — both
+// results are within (K u)^2 sum|x| of the exact sum (sabs: an upper bound of
+// sum|x|). False when that cannot be ruled out (the caller reruns the loop).
+__device__ __forceinline__ bool exact_sum_safe(double s, double c, double sabs, int64_t K, double* hi_out) {
+    double hi, lo;
+    two_sum(s, c, hi, lo);
+    const double ku = double(K) * 1.1102230246251565e-16;  // K u, u = 2^-53
+    const double margin = 8.0 * ku * ku * sabs * 1.0000001;
+    if (!(isfinite(hi) && isfinite(lo) && isfinite(margin))) return false;
+    const double nb = nextafter(hi, (lo > 0.0) ? INFINITY : -INFINITY);  // the midpoint on lo's side
+    if (!(fabs(lo) + margin < fabs(__dsub_rn(nb, hi)) * 0.5)) return false;
+    *hi_out = hi;
+    return true;
+}
+
 template <class T>
 __device__ __forceinline__ T shfl_xor(T v, int m) {
     return __shfl_xor_sync(0xffffffffu, v, m);

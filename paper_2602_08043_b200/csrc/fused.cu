@@ -160,7 +160,7 @@ struct WideWs {
     void* cpart;          // [7][ceil(K/128)][ld] A-side block partials (wide.cu)
     int64_t ld;
     double *mean, *mx, *mn, *vb, *cr1, *cr2, *max_abs_a;
-    int* nonfinite;
+    unsigned* gcnt;       // [ld / 32] A-pass arrival counters (zero at rest)
     size_t bytes;
 };
 
@@ -186,7 +186,7 @@ WideWs carve_wide(void* base, int64_t M, int64_t N, int64_t K) {
     w.cr1 = reinterpret_cast<double*>(take(8 * m));
     w.cr2 = reinterpret_cast<double*>(take(8 * m));
     w.max_abs_a = reinterpret_cast<double*>(take(8));
-    w.nonfinite = reinterpret_cast<int*>(take(4));
+    w.gcnt = reinterpret_cast<unsigned*>(take(4 * (ld / 32)));
     w.bytes = off;
     return w;
 }
@@ -279,19 +279,15 @@ void wide_fused(const vabft_fused_opts* o, vabft_bside* h, int64_t m, const void
         if (scratch) check_cuda(cudaFreeAsync(scratch, s), "cudaFreeAsync");
     }
     if (!tail) return;
-    // A-ABFT computed y needs the global max|A| first: combine in a separate
-    // pass; otherwise the tail combines the A partials itself
+    // the A pass verifies each row group as it completes; A-ABFT computed y
+    // needs the global max|A| first: stage the statistics, then a tail kernel
     const bool global_y = o->threshold_method == 2;
     if (global_y && !h->rowsum_ready) {  // max_k |sum_j B[k][j]| on first use (bside.cu)
         launch_bside_rowsum(h->fmt, h->k, h->n, h->B, h->buf, s);
         h->rowsum_ready = true;
     }
-    launch_wide_aside(h->fmt, m, k, A, h->brd, h->brd + k, o->mode == VABFT_OFFLINE ? h->fmt : -1, ws.mean, ws.vb,
-                      ws.mx, ws.mn, ws.cr1, ws.cr2, ws.cpart, ws.ld, counts, global_y, s);
-    if (global_y) {
-        check_cuda(cudaMemsetAsync(ws.max_abs_a, 0, sizeof(double), s), "memset");
-        launch_max_abs_rows(m, ws.mx, ws.mn, ws.max_abs_a, s);
-    }
+    if (claim_workspace(workspace, h, ws.bytes, o->workspace_fresh != 0))
+        check_cuda(cudaMemsetAsync(ws.gcnt, 0, sizeof(unsigned) * size_t(ws.ld / 32), s), "memset");
     WideTail t{};
     t.M = m;
     t.N = n;
@@ -319,11 +315,13 @@ void wide_fused(const vabft_fused_opts* o, vabft_bside* h, int64_t m, const void
     t.counts = counts;
     t.C = C;
     t.correct = o->correct;
-    if (!global_y) {
-        t.apart = ws.cpart;
-        t.A = A;
-        t.qfmt = o->mode == VABFT_OFFLINE ? h->fmt : -1;
-    }
+    t.A = A;
+    t.qfmt = o->mode == VABFT_OFFLINE ? h->fmt : -1;
+    launch_wide_aside(t, h->brd, h->brd + k, ws.cpart, ws.gcnt, !global_y, ws.mean, ws.vb, ws.mx, ws.mn, ws.cr1,
+                      ws.cr2, s);
+    if (!global_y) return;
+    check_cuda(cudaMemsetAsync(ws.max_abs_a, 0, sizeof(double), s), "memset");
+    launch_max_abs_rows(m, ws.mx, ws.mn, ws.max_abs_a, s);
     launch_wide_tail(t, s);
 }
 
@@ -434,7 +432,6 @@ extern "C" vabft_status vabft_fused_gemm(const vabft_fused_opts* o, vabft_bside_
         cudaStream_t s = as_stream(stream);
         if (o->fault_target < 0 || o->fault_target > 2) fail(VABFT_INVALID_ARGUMENT, "bad fault target");
         if (is_wide(h->fmt)) {
-            release_workspace(workspace);  // its carve overlays the 16-bit counters
             wide_fused(o, h, m, A, C, T, verdicts, counts, workspace, s);
             return;
         }

@@ -6,6 +6,7 @@
 #include <stdexcept>
 #include <string>
 
+#include <cuda.h>
 #include <cuda_runtime.h>
 
 #include "vabft_c.h"
@@ -33,6 +34,10 @@ void ensure_smem_attr(const void* fn, int bytes);
 int cached_cluster_count(const void* fn, int (*compute)(const void*, void*), void* ctx);
 // per-(kernel, device) cudaOccupancyMaxActiveBlocksPerMultiprocessor
 int cached_occupancy(const void* fn, int threads, int smem);
+// 2-D row-major TMA descriptor: rows x cols elements of elem_bytes, row
+// stride ld elements, box {box_cols, box_rows}, out-of-bounds boxes zero-filled
+CUtensorMap encode_map_2d(CUtensorMapDataType dt, const void* base, uint64_t rows, uint64_t cols, uint64_t ld,
+                          uint32_t elem_bytes, uint32_t box_cols, uint32_t box_rows, CUtensorMapSwizzle swizzle);
 size_t elem_size(int fmt);
 
 // ---- verify tail (tail.cuh): inputs of one fused launch
@@ -145,8 +150,8 @@ struct WideTail {
     int64_t M, N, K, nblk, ld;
     int fmt;                               // VABFT_FP32 / VABFT_FP64 (C element type)
     const void *part1, *part2;             // as WideEpilogue
-    const double *mean, *vb;               // A row statistics (stats.cpp:9-32)
-    const double *cr1, *cr2;               // row checksums A (B r)
+    const double *mean, *vb;               // A row statistics (stats.cpp:9-32), staged (wide_tail_kernel)
+    const double *cr1, *cr2;               // row checksums A (B r), staged
     const double* bsum;                    // B summary (4)
     const double* max_abs_a;               // A-ABFT computed y
     int method, aabft_t;
@@ -156,18 +161,19 @@ struct WideTail {
     int64_t* counts;
     void* C;
     int correct;
-    // A-side partials to combine in the tail (nullptr: mean/vb/cr1/cr2 given)
-    const void* apart = nullptr;
-    const void* A = nullptr;
-    int qfmt = -1;
+    const void* A = nullptr;  // the A operand (FP32 / FP64), read by the A pass
+    int qfmt = -1;            // offline FP32: checksums rounded to the input format
 };
 void launch_wide_tail(const WideTail& t, cudaStream_t stream);
-// A side: row statistics and the blocked:128 row checksums A (B r); apart is
-// scratch for the per-(128-column block, row) partials, 7 x ceil(K/128) x ld
-// doubles
-void launch_wide_aside(int fmt, int64_t M, int64_t K, const void* A, const double* br1, const double* br2, int qfmt,
-                       double* mean, double* vb, double* mx, double* mn, double* cr1, double* cr2, void* apart,
-                       int64_t ld, int64_t* counts, bool combine, cudaStream_t stream);
+// A side (wide.cu): one pass over t.A producing the row statistics and the
+// blocked:128 row checksums A (B r); apart is scratch for the per-(128-column
+// block, row) partials (7 x ceil(K/128) x ld doubles), gcnt ceil(M/32)
+// zero-initialised self-resetting counters. finish: the verdicts of t in the
+// same kernel; else mean / vb / mx / mn / cr1 / cr2 are staged for
+// launch_wide_tail (A-ABFT computed y).
+void launch_wide_aside(const WideTail& t, const double* br1, const double* br2, void* apart, unsigned* gcnt,
+                       bool finish, double* mean, double* vb, double* mx, double* mn, double* cr1, double* cr2,
+                       cudaStream_t stream);
 void launch_max_abs_rows(int64_t m, const double* mx, const double* mn, double* out, cudaStream_t stream);
 // InputA operand faults of the wide path: per row i, flip bit[i] of
 // X[i][col[i]] (col < 0: none), per-row records

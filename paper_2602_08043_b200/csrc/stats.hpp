@@ -19,8 +19,8 @@ struct BsideBuffers {
     double* brd1 = nullptr;        // wide formats (optional): B r1 / B r2 in the working type, as doubles
     double* brd2 = nullptr;
     void* work = nullptr;          // bside_work_bytes(): per-(128-column block, row) partials
-    unsigned* groups = nullptr;    // bside_group_words(): arrival counters + ready flags, zero-initialised
-    unsigned epoch = 0;            // bumped by every launch (the ready-flag value)
+    unsigned* groups = nullptr;    // bside_group_words(): arrival counters, ready flags and the launch
+                                   // epoch, zero-initialised (device state: graph replays stay correct)
 };
 
 // Floats of storage for one B r vector (K padded to 128, zero padding).

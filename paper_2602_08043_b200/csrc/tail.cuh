@@ -54,6 +54,70 @@ __device__ __forceinline__ bool guard_exact(float max_abs, uint32_t mnz_pat, int
     return top <= 53 + lsb;
 }
 
+// The reference's Neumaier row sum fl(sum + comp) (stats.cpp:12-24) of one
+// row that failed the exactness guard, by the whole warp (all lanes call, all
+// get the result). The exact sum as a TwoSum cascade per lane over strided
+// elements, merged in a butterfly (TwoSum is symmetric, so every lane holds
+// the same merged value); fl(s + c) is the reference's result unless the
+// exact sum lies within 8 (K u)^2 sum|x| of a rounding midpoint
+// (exact_sum_safe). Otherwise — or when the plain sequential FP64 sum is
+// wanted too (`plain`: aabft_computed_y's row sums of B) — the reference's
+// loops run in row order with the elements staged in registers: lane l holds
+// elements [32 l, 32 l + 32) of each 1024-element chunk and the running
+// state passes from lane to lane. Cost: ~1 us at K = 4096 (parallel), ~10 us
+// (sequential, about one FP64 add latency per element).
+template <int F>
+__device__ __noinline__ double warp_neumaier_row(const typename Elem<F>::T* row, int64_t K, double* plain) {
+    const int lane = threadIdx.x & 31;
+    if (plain == nullptr) {
+        double s = 0.0, c = 0.0, sabs = 0.0;
+        for (int64_t q = lane; q < K; q += 32) {
+            const double x = Elem<F>::d(row[q]);
+            double t, e;
+            two_sum(s, x, t, e);
+            s = t;
+            c = __dadd_rn(c, e);
+            sabs = __dadd_rn(sabs, fabs(x));
+        }
+#pragma unroll
+        for (int m = 16; m >= 1; m >>= 1) {
+            const double so = __shfl_xor_sync(0xffffffffu, s, m), co = __shfl_xor_sync(0xffffffffu, c, m);
+            double t, e;
+            two_sum(s, so, t, e);
+            s = t;
+            c = __dadd_rn(__dadd_rn(c, co), e);
+            sabs = __dadd_rn(sabs, __shfl_xor_sync(0xffffffffu, sabs, m));
+        }
+        double hi;
+        if (exact_sum_safe(s, c, sabs, K, &hi)) return hi;
+    }
+    Neu n;
+    double pl = 0.0;
+    for (int64_t j0 = 0; j0 < K; j0 += 1024) {
+        double x[32];
+        const int64_t b = j0 + int64_t(lane) * 32;
+#pragma unroll
+        for (int e = 0; e < 32; ++e) x[e] = b + e < K ? Elem<F>::d(row[b + e]) : 0.0;
+        for (int l = 0; l < 32; ++l) {
+            if (lane == l) {
+                const int cnt = int(K - b < 32 ? (K - b > 0 ? K - b : 0) : 32);
+#pragma unroll
+                for (int e = 0; e < 32; ++e) {
+                    if (e < cnt) {
+                        n.add(x[e]);
+                        pl = __dadd_rn(pl, x[e]);
+                    }
+                }
+            }
+            n.s = __shfl_sync(0xffffffffu, n.s, l);
+            n.c = __shfl_sync(0xffffffffu, n.c, l);
+            pl = __shfl_sync(0xffffffffu, pl, l);
+        }
+    }
+    if (plain) *plain = pl;
+    return __dadd_rn(n.s, n.c);
+}
+
 // Sequentially accumulate arrays x1/x2 (blocks [0, nb) of row group g) in
 // block order, fetching chunks through the warp's smem slice.
 __device__ __forceinline__ void ordered_sums(const float* x1, const float* x2, int64_t nb, int64_t g,
@@ -83,25 +147,36 @@ __device__ __forceinline__ void ordered_sums(const float* x1, const float* x2, i
 // Threshold of row i from its order-independent statistics (which are reset
 // to their identities for the next launch) and the A (B r) checksums from
 // their FP32 blocked:128 sums t1 / t2 (quantized offline).
+// Called by all lanes of the warp (valid: lane's row exists). Rows failing
+// the exactness guard get the reference's Neumaier sum from
+// warp_neumaier_row, the whole warp working on one such row at a time.
 template <int F>
-__device__ __forceinline__ void row_threshold(const TailArgs& a, int64_t i, double sum, uint32_t kmax,
+__device__ __forceinline__ void row_threshold(const TailArgs& a, int64_t i, bool valid, double sum, uint32_t kmax,
                                               uint32_t kmin, uint32_t mnz, float t1, float t2, double& tv,
                                               double& c1, double& c2, float& amax) {
+    const float mx = fkey_decode(kmax);
+    const float mn = fkey_decode(kmin);
+    amax = fmaxf(fabsf(mx), fabsf(mn));
+    const bool slow = valid && !guard_exact<F>(amax, mnz, a.K);
+    unsigned rows = __ballot_sync(0xffffffffu, slow);
+    if (rows && (threadIdx.x & 31) == 0 && a.counts)
+        atomicAdd(reinterpret_cast<unsigned long long*>(a.counts + VABFT_COUNT_SLOW_STATS),
+                  static_cast<unsigned long long>(__popc(rows)));
+    while (rows) {
+        const int l = __ffs(rows) - 1;
+        rows &= rows - 1;
+        const int64_t il = i - (threadIdx.x & 31) + l;
+        const double hs = warp_neumaier_row<F>(a.A + il * a.K, a.K, nullptr);
+        if ((threadIdx.x & 31) == l) sum = hs;
+    }
+    if (!valid) {
+        amax = 0.0f;
+        return;
+    }
     a.rsum[i] = 0.0;
     a.rmax[i] = 0u;
     a.rmin[i] = 0xFFFFFFFFu;
     a.rmnz[i] = 0xFFFFFFFFu;
-    const float mx = fkey_decode(kmax);
-    const float mn = fkey_decode(kmin);
-    amax = fmaxf(fabsf(mx), fabsf(mn));
-    if (!guard_exact<F>(amax, mnz, a.K)) {
-        // the reference's sequential Neumaier pass over the row (stats.cpp:12-24)
-        if (a.counts) atomicAdd(reinterpret_cast<unsigned long long*>(a.counts + VABFT_COUNT_SLOW_STATS), 1ull);
-        Neu ns;
-        const uint16_t* row = a.A + i * a.K;
-        for (int64_t q = 0; q < a.K; ++q) ns.add(double(bits16_to_float<F>(row[q])));
-        sum = __dadd_rn(ns.s, ns.c);
-    }
     Neu fin;
     fin.s = sum;
     double mean, vb;
@@ -197,9 +272,10 @@ __device__ void verify_rowgroup(const TailArgs& a, int64_t g, int phase, float* 
         float t1 = 0.0f, t2 = 0.0f;
         ordered_sums(a.sp1, a.sp2, a.nblkK, g, sbuf, bar, bar_phase, t1, t2);
         float amax = 0.0f;
+        row_threshold<F>(a, i, valid, valid ? __ldcg(a.rsum + i) : 0.0, valid ? __ldcg(a.rmax + i) : 0u,
+                         valid ? __ldcg(a.rmin + i) : 0xFFFFFFFFu, valid ? __ldcg(a.rmnz + i) : 0xFFFFFFFFu, t1, t2, tv,
+                         c1, c2, amax);
         if (valid) {
-            row_threshold<F>(a, i, __ldcg(a.rsum + i), __ldcg(a.rmax + i), __ldcg(a.rmin + i), __ldcg(a.rmnz + i),
-                             t1, t2, tv, c1, c2, amax);
             if (phase == 1) {
                 a.cr1[i] = c1;
                 a.cr2[i] = c2;
@@ -275,10 +351,10 @@ __device__ void stats_half_direct(const TailArgs& a, int64_t g) {
     }
     float t1 = 0.0f, t2 = 0.0f;
     ordered_sums_l2(a.sp1, a.sp2, a.nblkK, g, t1, t2);
+    double c1, c2, tv;
+    float amax;
+    row_threshold<F>(a, i, valid, sum, kmax, kmin, mnz, t1, t2, tv, c1, c2, amax);
     if (valid) {
-        double c1, c2, tv;
-        float amax;
-        row_threshold<F>(a, i, sum, kmax, kmin, mnz, t1, t2, tv, c1, c2, amax);
         a.cr1[i] = c1;
         a.cr2[i] = c2;
         a.Tv[i] = tv;

@@ -30,6 +30,7 @@
 #include "numerics.cuh"
 #include "ptx.cuh"
 #include "reducers.cuh"
+#include "tail.cuh"
 
 namespace vabft_dev {
 
@@ -209,50 +210,47 @@ __global__ void __launch_bounds__(kDThreads, 1) dgemm_kernel(const __grid_consta
     }
 }
 
-// A side of the wide fused path: ONE pass over A, then a per-row combine
-// (inside the verify tail). It runs after the GEMM on the same stream: run
-// beside the GEMM on a second stream it was starved of memory bandwidth and
-// finished late (measured), so the serial order is the faster one.
+// A side and verification of the wide fused path: ONE pass over A after the
+// GEMM on the same stream (run beside the GEMM on a second stream it was
+// starved of memory bandwidth and finished late — measured), with the
+// per-row-group combine and the verdicts inside the same kernel.
 //
-// wide_apart_kernel: a warp takes 32 rows x one 128-column block (coalesced
-// tile loads through shared memory; lane = row walks the block in order) and
-// writes, per (block, row):
+// wide_apart_kernel: persistent; a warp task is (32-row group, 128-column
+// block of K). The warp streams the 32 x 128 tile through its shared-memory
+// slice in 32-column sub-tiles (coalesced 128 / 256-byte row segments, the
+// next sub-tile's loads in flight while this one is processed) and lane = row
+// walks the block in column order; the block's B r weights are staged once in
+// shared memory and read as broadcasts. Per (block, row) it writes:
 //  - the NativeBlocked(128) checksum partials sum_j T(br_j) T(a_j) in the
 //    working type W (checksum.cpp:103-146);
-//  - an error-free cascaded sum (TwoSum: s, c) of the row segment in FP64,
-//    sum |a|, and max / min (stats.cpp:9-32).
-// wide_acombine_kernel (thread per row): checksum partials in block order;
-// the (s, c) pairs merged with TwoSum. With hi = fl(s + c), |s + c - S| <=
-// (K u)^2 sum|x| for the exact row sum S, and the reference's sequential
-// Neumaier sum + comp obeys the same bound — both round to fl(S) unless S lies
-// within 8 (K u)^2 sum|x| of a rounding midpoint. That is checked per row;
-// such rows (and non-finite ones) rerun the reference's loop (counted as
-// slow-stats rows), so the mean is bit-identical in every case.
-__device__ __forceinline__ void two_sum(double a, double b, double& s, double& e) {
-    s = __dadd_rn(a, b);
-    const double bb = __dsub_rn(s, a);
-    e = __dadd_rn(__dsub_rn(a, __dsub_rn(s, bb)), __dsub_rn(b, bb));
-}
-
-// hi = fl(s + c) equals the reference's fl(sum + comp) unless the exact sum
-// lies within 8 (K u)^2 sum|x| of a rounding midpoint (see above).
-__device__ __forceinline__ bool exact_sum_safe(double s, double c, double sabs, int64_t K, double* hi_out) {
-    double hi, lo;
-    two_sum(s, c, hi, lo);
-    const double ku = double(K) * 1.1102230246251565e-16;  // K u, u = 2^-53
-    const double margin = 8.0 * ku * ku * sabs * 1.0000001;
-    if (!(isfinite(hi) && isfinite(lo) && isfinite(margin))) return false;
-    const double nb = nextafter(hi, (lo > 0.0) ? INFINITY : -INFINITY);  // the midpoint on lo's side
-    if (!(fabs(lo) + margin < fabs(__dsub_rn(nb, hi)) * 0.5)) return false;
-    *hi_out = hi;
-    return true;
-}
-
+//  - an error-free (s, c) pair of the row segment's sum, sum |a|, max / min
+//    (stats.cpp:9-32). FP32: per 32-element sub-tile a plain FP64 sum, exact
+//    when 32 max|x| < 2^(53 + lsb(min nonzero |x|)) (a sub-tile outside that
+//    guard is redone with TwoSum from the staged tile), TwoSum-merged into the
+//    block's pair; FP64: a TwoSum cascade per element. sum|x| (the margin of
+//    exact_sum_safe) is kept in the element type and stored rounded up by a
+//    relative 2^-8 (an upper bound).
+// The warp completing a row group's last block (self-resetting arrival
+// counter) finishes the group, lane = row: checksum partials in block order,
+// the (s, c) pairs merged with TwoSum; hi = fl(s + c) equals the reference's
+// sequential Neumaier fl(sum + comp) unless the exact sum lies within
+// 8 (K u)^2 sum|x| of a rounding midpoint (exact_sum_safe) — those rows get
+// the reference's sum from warp_neumaier_row (counted as slow-stats rows), so
+// the mean is bit-identical in every case. Then, for thresholds without a
+// global dependency, the C-row partials of the GEMM epilogue (blocked:128
+// order), the threshold, D1 / D2, the strict compare, the NaN rule,
+// localization and the optional correction (detect.cpp:9-64): the whole
+// verify tail, in the same kernel. A-ABFT with computed y (global max|A|
+// first) stages the row statistics instead and verifies in wide_tail_kernel.
 template <class W>
-struct APart {  // per (block, row) partial arrays, each [nb][ld]
+struct APart {  // per (block, row) partial arrays, group-major (ap_index)
     W *p1, *p2;
     double *s, *c, *sabs, *mx, *mn;
 };
+
+__host__ __device__ inline size_t ap_index(int64_t b, int64_t row, int64_t nb) {
+    return size_t(((row >> 5) * nb + b) * 32 + (row & 31));
+}
 
 template <class W>
 __host__ __device__ inline APart<W> apart_view(void* base, int64_t nb, int64_t ld) {
@@ -269,324 +267,336 @@ __host__ __device__ inline APart<W> apart_view(void* base, int64_t nb, int64_t l
     return a;
 }
 
-template <int F, class W>
-__global__ void __launch_bounds__(128) wide_apart_kernel(const typename Elem<F>::T* __restrict__ A, int64_t M,
-                                                         int64_t K, const double* __restrict__ br1,
-                                                         const double* __restrict__ br2, APart<W> out, int64_t ld) {
+// Everything the A pass needs beyond the verdict arguments.
+template <class W>
+struct ApJob {
+    WideTail t;              // verdict arguments (t.apart / t.mean ... unused here)
+    const double *br1, *br2;
+    APart<W> part;
+    unsigned* gcnt;          // [ceil(M/32)] block arrivals per row group (self-resetting)
+    int finish;              // 1: verdicts in this kernel; 0: stage the row statistics
+    double *mean, *vb, *mx, *mn, *cr1, *cr2;  // staging (finish == 0)
+};
+
+constexpr int kApWarps = 8;
+
+template <int F>
+constexpr size_t ap_smem() {
     using T = typename Elem<F>::T;
-    __shared__ T tile[4][32][33];
-    const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int64_t r0 = (int64_t(blockIdx.x) * 4 + w) * 32, b = blockIdx.y;
-    if (r0 >= M) return;
-    W p1 = W(0), p2 = W(0);
-    double s = 0.0, c = 0.0, sabs = 0.0;
-    T mx = T(-INFINITY), mn = T(INFINITY);
-    for (int q = 0; q < 4; ++q) {
-        const int64_t col0 = b * 128 + q * 32;
-        if (col0 >= K) break;
-        const int64_t col = col0 + lane;
-        T v[32];  // all 32 row loads in flight before the first smem store
+    return size_t(kApWarps) * (32 * 33 * sizeof(T) + 2 * 128 * sizeof(T));
+}
+
+template <int F>
+__device__ __forceinline__ void ap_load(const typename Elem<F>::T* __restrict__ A, int64_t M, int64_t K, int64_t r0,
+                                        int64_t c, typename Elem<F>::T (&v)[32]) {
+    using T = typename Elem<F>::T;
+    const int64_t col = c + (threadIdx.x & 31);
+    const T* p = A + r0 * K + col;
+    const int rows = int(M - r0 < 32 ? M - r0 : 32);
 #pragma unroll
-        for (int rr = 0; rr < 32; ++rr) {
-            const int64_t r = r0 + rr;
-            v[rr] = (r < M && col < K) ? __ldcs(A + r * K + col) : T(0);
+    for (int rr = 0; rr < 32; ++rr) v[rr] = (rr < rows && col < K) ? __ldcs(p + rr * K) : T(0);
+}
+
+// The verdict of the lanes' rows (lane = row) from their C-row sums r1 / r2,
+// checksums c1 / c2 and statistics; warp-aggregated counters.
+template <int F>
+__device__ __forceinline__ void wide_verdicts(const WideTail& a, int64_t i, bool valid, double r1, double r2,
+                                              double mean_i, double vb_i, double c1, double c2) {
+    const int lane = threadIdx.x & 31;
+    bool det = false, located = false, isnan_row = false, corrected = false;
+    if (valid) {
+        double t;
+        if (a.method == 0) {
+            t = vabft_threshold_total(mean_i, vb_i, a.bsum[0], a.bsum[1], a.bsum[2], a.N, a.e_max, a.c_sigma);
+        } else {
+            const double y = a.method == 1 ? a.aabft_fixed_y : __dmul_rn(*a.max_abs_a, a.bsum[3]);
+            t = aabft_total(a.K, a.aabft_t, y, a.aabft_conf);
         }
-        const W w1l = col < K ? W(br1[col]) : W(0), w2l = col < K ? W(br2[col]) : W(0);
-#pragma unroll
-        for (int rr = 0; rr < 32; ++rr) tile[w][rr][lane] = v[rr];
-        __syncwarp();
-        const int cmax = int(K - col0 < 32 ? K - col0 : 32);
-        for (int jj = 0; jj < cmax; ++jj) {
-            const T e = tile[w][lane][jj];
-            const W x = W(e);
-            p1 = radd(p1, rmul(__shfl_sync(0xffffffffu, w1l, jj), x));
-            p2 = radd(p2, rmul(__shfl_sync(0xffffffffu, w2l, jj), x));
-            const double xd = double(e);
-            double t, err;
-            two_sum(s, xd, t, err);
-            s = t;
-            c = __dadd_rn(c, err);
-            sabs = __dadd_rn(sabs, fabs(xd));
-            mx = mx < e ? e : mx;  // NaN-free rows: identical to fmax / fmin
-            mn = e < mn ? e : mn;
+        if (a.T_out) a.T_out[i] = t;
+        const double d1 = __dsub_rn(r1, c1);
+        const double d2 = __dsub_rn(r2, c2);
+        int64_t loc = -1;
+        double res = 0.0;
+        if (isnan(d1) || isnan(d2)) {
+            det = true;
+            isnan_row = true;
+        } else {
+            det = fabs(d1) > t;
+            if (det && fabs(d1) > __dmul_rn(a.floor_scale, t)) {
+                int64_t j;
+                double rr;
+                if (localize_dev(d1, d2, a.N, &j, &rr)) {
+                    loc = j;
+                    res = rr;
+                    located = true;
+                    // correct (detect.cpp:57-64): C[i][j] = quantize(C[i][j] - diff1)
+                    if (a.correct && a.C != nullptr && rr < 0.4) {
+                        if (a.fmt == VABFT_FP64) {
+                            double* cij = static_cast<double*>(a.C) + i * a.N + j;
+                            *cij = __dsub_rn(*cij, d1);
+                        } else {
+                            float* cij = static_cast<float*>(a.C) + i * a.N + j;
+                            const float q = __double2float_rn(__dsub_rn(double(*cij), d1));
+                            *cij = isinf(q) ? copysignf(3.40282346638528859812e+38f, q) : q;
+                        }
+                        corrected = true;
+                    }
+                }
+            }
         }
-        __syncwarp();
+        if (a.v.diff1) a.v.diff1[i] = d1;
+        if (a.v.diff2) a.v.diff2[i] = d2;
+        if (a.v.detected) a.v.detected[i] = det ? 1 : 0;
+        if (a.v.location) a.v.location[i] = loc;
+        if (a.v.residual) a.v.residual[i] = res;
+        if (a.v.row_check1) a.v.row_check1[i] = c1;
+        if (a.v.row_check2) a.v.row_check2[i] = c2;
     }
-    const int64_t row = r0 + lane;
-    if (row < M) {
-        const size_t o = size_t(b) * size_t(ld) + size_t(row);
-        out.p1[o] = p1;
-        out.p2[o] = p2;
-        out.s[o] = s;
-        out.c[o] = c;
-        out.sabs[o] = sabs;
-        out.mx[o] = double(mx);
-        out.mn[o] = double(mn);
+    if (a.counts) {
+        const unsigned nv = __popc(__ballot_sync(0xffffffffu, valid));
+        const unsigned nd = __popc(__ballot_sync(0xffffffffu, det));
+        const unsigned nl = __popc(__ballot_sync(0xffffffffu, located));
+        const unsigned nn = __popc(__ballot_sync(0xffffffffu, isnan_row));
+        const unsigned nc = __popc(__ballot_sync(0xffffffffu, corrected));
+        if (lane == 0) {
+            unsigned long long* cnt = reinterpret_cast<unsigned long long*>(a.counts);
+            if (nv) atomicAdd(cnt + VABFT_COUNT_ROWS, nv);
+            if (nd) atomicAdd(cnt + VABFT_COUNT_DETECTED, nd);
+            if (nl) atomicAdd(cnt + VABFT_COUNT_LOCATED, nl);
+            if (nn) atomicAdd(cnt + VABFT_COUNT_NAN, nn);
+            if (nc) atomicAdd(cnt + VABFT_COUNT_CORRECTED, nc);
+        }
     }
 }
 
-// Per-row combine of the A-side partials: stats (mean, var_bound, max, min)
-// and the row checksums; see the comment above.
+// C r1 / C r2 of the lanes' rows: the epilogue's per-128-column partials
+// ([nb][ld], lane = row: coalesced) added in block order (blocked:128).
+template <class W>
+__device__ __forceinline__ void wide_row_sums(const WideTail& a, int64_t i, double& r1, double& r2) {
+    const W* p1 = static_cast<const W*>(a.part1) + i;
+    const W* p2 = static_cast<const W*>(a.part2) + i;
+    W s1 = W(0), s2 = W(0);
+#pragma unroll 8
+    for (int64_t b = 0; b < a.nblk; ++b) {
+        s1 = radd(s1, __ldcg(p1 + b * a.ld));
+        s2 = radd(s2, __ldcg(p2 + b * a.ld));
+    }
+    r1 = double(s1);
+    r2 = double(s2);
+}
+
+// Finish a row group (lane = row): A statistics and checksums, then either
+// the verdicts (finish) or the staged statistics.
 template <int F, class W>
-__device__ __forceinline__ void acombine_row(const typename Elem<F>::T* __restrict__ A, int64_t K, const APart<W>& in,
-                                             int64_t ld, int qfmt, int64_t i, int64_t* counts, double& mean,
-                                             double& vb, double& mx, double& mn, double& c1, double& c2) {
-    const int64_t nb = (K + 127) / 128;
+__device__ __forceinline__ void ap_finish_group(const ApJob<W>& j, int64_t rg) {
+    using T = typename Elem<F>::T;
+    const WideTail& a = j.t;
+    const int lane = threadIdx.x & 31;
+    const int64_t i = rg * 32 + lane;
+    const bool valid = i < a.M;
+    const int64_t nb = (a.K + 127) / 128;
     W t1 = W(0), t2 = W(0);
-    double s = 0.0, c = 0.0, sabs = 0.0;
-    mx = -INFINITY;
-    mn = INFINITY;
-#pragma unroll 4
-    for (int64_t b = 0; b < nb; ++b) {
-        const size_t o = size_t(b) * size_t(ld) + size_t(i);
-        t1 = radd(t1, in.p1[o]);
-        t2 = radd(t2, in.p2[o]);
-        double t, err;
-        two_sum(s, in.s[o], t, err);
-        s = t;
-        c = __dadd_rn(__dadd_rn(c, in.c[o]), err);
-        sabs = __dadd_rn(sabs, in.sabs[o]);
-        mx = mx < in.mx[o] ? in.mx[o] : mx;
-        mn = in.mn[o] < mn ? in.mn[o] : mn;
+    double s = 0.0, c = 0.0, sabs = 0.0, mx = -INFINITY, mn = INFINITY;
+    if (valid) {
+        const size_t o0 = ap_index(0, i, nb);
+#pragma unroll 8
+        for (int64_t b = 0; b < nb; ++b) {
+            const size_t o = o0 + size_t(b) * 32;
+            t1 = radd(t1, __ldcg(j.part.p1 + o));
+            t2 = radd(t2, __ldcg(j.part.p2 + o));
+            double tt, err;
+            two_sum(s, __ldcg(j.part.s + o), tt, err);
+            s = tt;
+            c = __dadd_rn(__dadd_rn(c, __ldcg(j.part.c + o)), err);
+            sabs = __dadd_rn(sabs, __ldcg(j.part.sabs + o));
+            const double bx = __ldcg(j.part.mx + o), bn = __ldcg(j.part.mn + o);
+            mx = mx < bx ? bx : mx;
+            mn = bn < mn ? bn : mn;
+        }
     }
     Neu ns;
-    if (exact_sum_safe(s, c, sabs, K, &ns.s)) {
-        // ns.s = fl(sum + comp) of the reference
-    } else {
-        if (counts) atomicAdd(reinterpret_cast<unsigned long long*>(counts + VABFT_COUNT_SLOW_STATS), 1ull);
-        const typename Elem<F>::T* arow = A + i * K;
-        for (int64_t j = 0; j < K; ++j) ns.add(double(arow[j]));  // the reference's loop (stats.cpp:12-24)
+    const bool slow = valid && !exact_sum_safe(s, c, sabs, a.K, &ns.s);
+    unsigned rows = __ballot_sync(0xffffffffu, slow);
+    if (rows && lane == 0 && a.counts)
+        atomicAdd(reinterpret_cast<unsigned long long*>(a.counts + VABFT_COUNT_SLOW_STATS),
+                  static_cast<unsigned long long>(__popc(rows)));
+    while (rows) {  // rare: rows next to a rounding midpoint (or non-finite)
+        const int l = __ffs(rows) - 1;
+        rows &= rows - 1;
+        const double hs = warp_neumaier_row<F>(static_cast<const T*>(a.A) + (rg * 32 + l) * a.K, a.K, nullptr);
+        if (lane == l) {
+            ns = Neu{};
+            ns.s = hs;
+        }
     }
-    stats_finish(ns, mx, mn, K, &mean, &vb);
-    c1 = double(t1);
-    c2 = double(t2);
-    if (qfmt == VABFT_FP32) {  // offline FP32: the checksum rounded to the input format (a no-op for W = float)
-        c1 = double(float(c1));
-        c2 = double(float(c2));
+    double mean_i = 0.0, vb_i = 0.0, c1 = 0.0, c2 = 0.0;
+    if (valid) {
+        stats_finish(ns, mx, mn, a.K, &mean_i, &vb_i);
+        c1 = double(t1);
+        c2 = double(t2);
+        if (a.qfmt == VABFT_FP32) {  // offline FP32: rounded to the input format (a no-op for W = float)
+            c1 = double(float(c1));
+            c2 = double(float(c2));
+        }
     }
+    if (!j.finish) {
+        if (valid) {
+            j.mean[i] = mean_i;
+            j.vb[i] = vb_i;
+            j.mx[i] = mx;
+            j.mn[i] = mn;
+            j.cr1[i] = c1;
+            j.cr2[i] = c2;
+        }
+        return;
+    }
+    double r1 = 0.0, r2 = 0.0;
+    if (valid) wide_row_sums<W>(a, i, r1, r2);
+    wide_verdicts<F>(a, i, valid, r1, r2, mean_i, vb_i, c1, c2);
 }
 
 template <int F, class W>
-__global__ void __launch_bounds__(256) wide_acombine_kernel(const typename Elem<F>::T* __restrict__ A, int64_t M,
-                                                            int64_t K, APart<W> in, int64_t ld, int qfmt, double* mean,
-                                                            double* vb, double* mx_out, double* mn_out, double* cr1,
-                                                            double* cr2, int64_t* counts) {
-    const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
-    if (i >= M) return;
-    double m, v, mx, mn, c1, c2;
-    acombine_row<F, W>(A, K, in, ld, qfmt, i, counts, m, v, mx, mn, c1, c2);
-    mean[i] = m;
-    vb[i] = v;
-    mx_out[i] = mx;
-    mn_out[i] = mn;
-    cr1[i] = c1;
-    cr2[i] = c2;
+__global__ void __launch_bounds__(32 * kApWarps, F == VABFT_FP64 ? 1 : 2)
+    wide_apart_kernel(const typename Elem<F>::T* __restrict__ A, const __grid_constant__ ApJob<W> j) {
+    using T = typename Elem<F>::T;
+    extern __shared__ __align__(16) uint8_t ap_raw[];
+    const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    T* tile = reinterpret_cast<T*>(ap_raw + size_t(w) * (32 * 33 * sizeof(T) + 2 * 128 * sizeof(T)));
+    W* wts = reinterpret_cast<W*>(tile + 32 * 33);  // [2][128] weights of the block (W == T)
+    const int64_t M = j.t.M, K = j.t.K;
+    const int64_t nb = (K + 127) / 128, ngroups = (M + 31) / 32;
+    const int64_t tasks = ngroups * nb;
+    for (int64_t t = int64_t(blockIdx.x) * kApWarps + w; t < tasks; t += int64_t(gridDim.x) * kApWarps) {
+        const int64_t rg = t / nb, b = t - rg * nb;
+        const int64_t r0 = rg * 32, c0 = b * 128;
+        const int bw = int(K - c0 < 128 ? K - c0 : 128);
+        const int nsub = (bw + 31) / 32;
+        T v[32];
+        ap_load<F>(A, M, K, r0, c0, v);
+        __syncwarp();
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            const int jj = q * 32 + lane;
+            wts[jj] = jj < bw ? W(j.br1[c0 + jj]) : W(0);
+            wts[128 + jj] = jj < bw ? W(j.br2[c0 + jj]) : W(0);
+        }
+#pragma unroll
+        for (int rr = 0; rr < 32; ++rr) tile[rr * 33 + lane] = v[rr];
+        __syncwarp();
+        W p1 = W(0), p2 = W(0);
+        double s = 0.0, c = 0.0;
+        T sabs = T(0), mx = T(-INFINITY), mn = T(INFINITY);
+        const T* trow = tile + lane * 33;
+        for (int q = 0; q < nsub; ++q) {
+            const int64_t cq = c0 + int64_t(q) * 32;
+            if (q + 1 < nsub) ap_load<F>(A, M, K, r0, cq + 32, v);  // in flight during this sub-tile
+            const int cnt = int(c0 + bw - cq < 32 ? c0 + bw - cq : 32);  // warp-uniform
+            const W* w1 = wts + q * 32;
+            const W* w2 = wts + 128 + q * 32;
+            if constexpr (F == VABFT_FP32) {
+                double ps = 0.0;
+                uint32_t amx = 0u, mnz = 0xFFFFFFFFu;
+#pragma unroll 8
+                for (int jj = 0; jj < cnt; ++jj) {
+                    const float x = trow[jj];
+                    const uint32_t mag = __float_as_uint(x) & 0x7FFFFFFFu;
+                    amx = max(amx, mag);
+                    mnz = min(mnz, mag - 1u);  // 0 wraps to the maximum: ignored
+                    ps = __dadd_rn(ps, double(x));
+                    p1 = radd(p1, rmul(w1[jj], x));
+                    p2 = radd(p2, rmul(w2[jj], x));
+                    sabs = __fadd_rn(sabs, fabsf(x));
+                    mx = mx < x ? x : mx;  // NaN-free rows: identical to fmax / fmin
+                    mn = x < mn ? x : mn;
+                }
+                // exactness guard of the plain sub-tile sum (see guard_exact)
+                bool exact = true;
+                if (mnz != 0xFFFFFFFFu && amx < 0x7F800000u) {
+                    const int ez = int((mnz + 1u) >> 23);
+                    const int lsb = (ez == 0 ? 1 : ez) - 127 - 23;
+                    const int top = int(amx >> 23) - 127 + 1 + 6;  // 32 terms < 2^6 max
+                    exact = top <= 53 + lsb;
+                }
+                if (!exact) {  // rare: the sub-tile's exact sum as a TwoSum cascade
+                    double hs = 0.0, hc = 0.0;
+                    for (int jj = 0; jj < cnt; ++jj) {
+                        double tt, e;
+                        two_sum(hs, double(trow[jj]), tt, e);
+                        hs = tt;
+                        hc = __dadd_rn(hc, e);
+                    }
+                    ps = hs;
+                    c = __dadd_rn(c, hc);
+                }
+                double tt, e;
+                two_sum(s, ps, tt, e);
+                s = tt;
+                c = __dadd_rn(c, e);
+            } else {
+#pragma unroll 4
+                for (int jj = 0; jj < cnt; ++jj) {
+                    const double x = trow[jj];
+                    p1 = radd(p1, rmul(w1[jj], x));
+                    p2 = radd(p2, rmul(w2[jj], x));
+                    double tt, e;
+                    two_sum(s, x, tt, e);
+                    s = tt;
+                    c = __dadd_rn(c, e);
+                    sabs = __dadd_rn(sabs, fabs(x));
+                    mx = mx < x ? x : mx;
+                    mn = x < mn ? x : mn;
+                }
+            }
+            if (q + 1 < nsub) {
+                __syncwarp();
+#pragma unroll
+                for (int rr = 0; rr < 32; ++rr) tile[rr * 33 + lane] = v[rr];
+                __syncwarp();
+            }
+        }
+        const int64_t row = r0 + lane;
+        if (row < M) {
+            const size_t o = ap_index(b, row, nb);
+            j.part.p1[o] = p1;
+            j.part.p2[o] = p2;
+            j.part.s[o] = s;
+            j.part.c[o] = c;
+            // an upper bound of sum|x| (the element-type sum is within K u_T relatively)
+            j.part.sabs[o] = __dmul_ru(double(sabs), F == VABFT_FP32 ? 1.00390625 : 1.0 + 0x1p-40);
+            j.part.mx[o] = double(mx);
+            j.part.mn[o] = double(mn);
+        }
+        // arrival: every lane's partial stores before lane 0's release RMW
+        __syncwarp();
+        unsigned old = 0;
+        if (lane == 0) old = atom_add_acq_rel_gpu(j.gcnt + rg, 1u);
+        old = __shfl_sync(0xffffffffu, old, 0);
+        if (old == unsigned(nb) - 1u) {
+            if (lane == 0) j.gcnt[rg] = 0u;  // ready for the next launch
+            ap_finish_group<F, W>(j, rg);
+        }
+    }
 }
 
-template <class W>
-__device__ __forceinline__ W load_part(const void* p, size_t o) {
-    return static_cast<const W*>(p)[o];
-}
-
-// Verify tail, a warp per row: the C-row partials (blocked:128 order) and,
-// with a.apart set (threshold methods without a global dependency), the
-// A-side partials are combined across the lanes (lane = 128-column block,
-// ordered sums through shuffles, TwoSum merges in a butterfly); lane 0 then
-// evaluates the threshold, D1 / D2, the strict compare, NaN rule,
-// localization and the optional correction. Counters are aggregated per CTA.
+// Verify tail for thresholds with a global dependency (A-ABFT computed y):
+// warp per 32-row group (lane = row), the row statistics staged by the A
+// pass, the C-row partials in block order, the verdicts.
 template <int F>
 __global__ void __launch_bounds__(256) wide_tail_kernel(const WideTail a) {
     using W = std::conditional_t<F == VABFT_FP64, double, float>;
-    using T = typename Elem<F>::T;
-    __shared__ unsigned long long cnt[6];
-    const int lane = threadIdx.x & 31;
-    if (threadIdx.x < 6) cnt[threadIdx.x] = 0;
-    __syncthreads();
-    const int64_t i = int64_t(blockIdx.x) * 8 + (threadIdx.x >> 5);
-    if (i < a.M) {
-        // C r1 / C r2: block partials in order
-        W r1 = W(0), r2 = W(0);
-        for (int64_t g = 0; g < a.nblk; g += 32) {
-            const int64_t b = g + lane;
-            W q1 = W(0), q2 = W(0);
-            if (b < a.nblk) {
-                const size_t o = size_t(b) * size_t(a.ld) + size_t(i);
-                q1 = load_part<W>(a.part1, o);
-                q2 = load_part<W>(a.part2, o);
-            }
-            const int n = a.nblk - g < 32 ? int(a.nblk - g) : 32;
-            for (int l = 0; l < n; ++l) {
-                r1 = radd(r1, __shfl_sync(0xffffffffu, q1, l));
-                r2 = radd(r2, __shfl_sync(0xffffffffu, q2, l));
-            }
-        }
-        double mean_i = 0.0, vb_i = 0.0, c1 = 0.0, c2 = 0.0;
-        if (a.apart) {
-            const int64_t nbk = (a.K + 127) / 128;
-            const APart<W> in = apart_view<W>(const_cast<void*>(a.apart), nbk, a.ld);
-            W t1 = W(0), t2 = W(0);
-            double s = 0.0, c = 0.0, sabs = 0.0, mx = -INFINITY, mn = INFINITY;
-            for (int64_t g = 0; g < nbk; g += 32) {
-                const int64_t b = g + lane;
-                W q1 = W(0), q2 = W(0);
-                if (b < nbk) {
-                    const size_t o = size_t(b) * size_t(a.ld) + size_t(i);
-                    q1 = in.p1[o];
-                    q2 = in.p2[o];
-                    double t, err;
-                    two_sum(s, in.s[o], t, err);
-                    s = t;
-                    c = __dadd_rn(__dadd_rn(c, in.c[o]), err);
-                    sabs = __dadd_rn(sabs, in.sabs[o]);
-                    mx = mx < in.mx[o] ? in.mx[o] : mx;
-                    mn = in.mn[o] < mn ? in.mn[o] : mn;
-                }
-                const int n = nbk - g < 32 ? int(nbk - g) : 32;
-                for (int l = 0; l < n; ++l) {
-                    t1 = radd(t1, __shfl_sync(0xffffffffu, q1, l));
-                    t2 = radd(t2, __shfl_sync(0xffffffffu, q2, l));
-                }
-            }
-#pragma unroll
-            for (int o = 16; o >= 1; o >>= 1) {
-                const double so = __shfl_xor_sync(0xffffffffu, s, o), co = __shfl_xor_sync(0xffffffffu, c, o);
-                double t, err;
-                two_sum(s, so, t, err);
-                s = t;
-                c = __dadd_rn(__dadd_rn(c, co), err);
-                sabs = __dadd_rn(sabs, __shfl_xor_sync(0xffffffffu, sabs, o));
-                const double mxo = __shfl_xor_sync(0xffffffffu, mx, o), mno = __shfl_xor_sync(0xffffffffu, mn, o);
-                mx = mx < mxo ? mxo : mx;
-                mn = mno < mn ? mno : mn;
-            }
-            Neu ns;
-            const bool safe = __shfl_sync(0xffffffffu, exact_sum_safe(s, c, sabs, a.K, &ns.s) ? 1 : 0, 0) != 0;
-            if (!safe) {
-                // the reference's sequential loop (stats.cpp:12-24) — rows whose exact
-                // sum sits on a rounding midpoint (measured ~1 in 4096 for FP64 N(0,1)
-                // rows at K = 4096, ~1 in 10^5 FP32 rows). The warp stages the row
-                // 256 elements at a time in its own shared-memory slice (8 coalesced
-                // loads per lane in flight), then lane 0 reads 32 elements per batch
-                // with 16-byte LDS ahead of the chain and runs the adds back to back.
-                // (Broadcasting each element by a shuffle put a SHFL, a branch and
-                // the conversion on the chain: 63 cycles per element, 131 us for
-                // one K = 4096 row.)
-                if (lane == 0 && a.counts) atomicAdd(&cnt[VABFT_COUNT_SLOW_STATS], 1ull);
-                constexpr int kChunk = 256;
-                __shared__ __align__(16) T stage[8][kChunk];
-                T* st = stage[threadIdx.x >> 5];
-                const T* arow = static_cast<const T*>(a.A) + i * a.K;
-                ns = Neu{};
-                for (int64_t j0 = 0; j0 < a.K; j0 += kChunk) {
-                    const int n = a.K - j0 < kChunk ? int(a.K - j0) : kChunk;  // warp-uniform
-                    __syncwarp();
-#pragma unroll
-                    for (int r = 0; r < kChunk / 32; ++r) {
-                        const int q = r * 32 + lane;
-                        if (q < n) st[q] = arow[j0 + q];
-                    }
-                    __syncwarp();
-                    if (lane == 0) {
-                        int q = 0;
-                        for (; q + 32 <= n; q += 32) {
-                            using V = std::conditional_t<sizeof(T) == 8, double2, float4>;
-                            constexpr int kPer = 16 / sizeof(T);
-                            T xs[32];
-#pragma unroll
-                            for (int u = 0; u < 32 / kPer; ++u) {
-                                const V w = reinterpret_cast<const V*>(st + q)[u];
-                                if constexpr (sizeof(T) == 8) {
-                                    xs[2 * u] = w.x;
-                                    xs[2 * u + 1] = w.y;
-                                } else {
-                                    xs[4 * u] = w.x;
-                                    xs[4 * u + 1] = w.y;
-                                    xs[4 * u + 2] = w.z;
-                                    xs[4 * u + 3] = w.w;
-                                }
-                            }
-#pragma unroll
-                            for (int l = 0; l < 32; ++l) ns.add(double(xs[l]));
-                        }
-                        for (; q < n; ++q) ns.add(double(st[q]));
-                    }
-                }
-            }
-            if (lane == 0) {
-                stats_finish(ns, mx, mn, a.K, &mean_i, &vb_i);
-                c1 = double(t1);
-                c2 = double(t2);
-                if (a.qfmt == VABFT_FP32) {  // offline FP32: rounded to the input format (no-op for W = float)
-                    c1 = double(float(c1));
-                    c2 = double(float(c2));
-                }
-            }
-        } else if (lane == 0) {
-            mean_i = a.mean[i];
-            vb_i = a.vb[i];
-            c1 = a.cr1[i];
-            c2 = a.cr2[i];
-        }
-        if (lane == 0) {
-            bool det = false, located = false, isnan_row = false, corrected = false;
-            double t;
-            if (a.method == 0) {
-                t = vabft_threshold_total(mean_i, vb_i, a.bsum[0], a.bsum[1], a.bsum[2], a.N, a.e_max, a.c_sigma);
-            } else {
-                const double y = a.method == 1 ? a.aabft_fixed_y : __dmul_rn(*a.max_abs_a, a.bsum[3]);
-                t = aabft_total(a.K, a.aabft_t, y, a.aabft_conf);
-            }
-            if (a.T_out) a.T_out[i] = t;
-            const double d1 = __dsub_rn(double(r1), c1);
-            const double d2 = __dsub_rn(double(r2), c2);
-            int64_t loc = -1;
-            double res = 0.0;
-            if (isnan(d1) || isnan(d2)) {
-                det = true;
-                isnan_row = true;
-            } else {
-                det = fabs(d1) > t;
-                if (det && fabs(d1) > __dmul_rn(a.floor_scale, t)) {
-                    int64_t j;
-                    double rr;
-                    if (localize_dev(d1, d2, a.N, &j, &rr)) {
-                        loc = j;
-                        res = rr;
-                        located = true;
-                        // correct (detect.cpp:57-64): C[i][j] = quantize(C[i][j] - diff1)
-                        if (a.correct && a.C != nullptr && rr < 0.4) {
-                            if (a.fmt == VABFT_FP64) {
-                                double* cij = static_cast<double*>(a.C) + i * a.N + j;
-                                *cij = __dsub_rn(*cij, d1);
-                            } else {
-                                float* cij = static_cast<float*>(a.C) + i * a.N + j;
-                                const float q = __double2float_rn(__dsub_rn(double(*cij), d1));
-                                *cij = isinf(q) ? copysignf(3.40282346638528859812e+38f, q) : q;
-                            }
-                            corrected = true;
-                        }
-                    }
-                }
-            }
-            if (a.v.diff1) a.v.diff1[i] = d1;
-            if (a.v.diff2) a.v.diff2[i] = d2;
-            if (a.v.detected) a.v.detected[i] = det ? 1 : 0;
-            if (a.v.location) a.v.location[i] = loc;
-            if (a.v.residual) a.v.residual[i] = res;
-            if (a.v.row_check1) a.v.row_check1[i] = c1;
-            if (a.v.row_check2) a.v.row_check2[i] = c2;
-            if (a.counts) {
-                atomicAdd(&cnt[VABFT_COUNT_ROWS], 1ull);
-                if (det) atomicAdd(&cnt[VABFT_COUNT_DETECTED], 1ull);
-                if (located) atomicAdd(&cnt[VABFT_COUNT_LOCATED], 1ull);
-                if (isnan_row) atomicAdd(&cnt[VABFT_COUNT_NAN], 1ull);
-                if (corrected) atomicAdd(&cnt[VABFT_COUNT_CORRECTED], 1ull);
-            }
-        }
+    const int64_t rg = int64_t(blockIdx.x) * 8 + (threadIdx.x >> 5);
+    if (rg * 32 >= a.M) return;
+    const int64_t i = rg * 32 + (threadIdx.x & 31);
+    const bool valid = i < a.M;
+    double r1 = 0.0, r2 = 0.0, mean_i = 0.0, vb_i = 0.0, c1 = 0.0, c2 = 0.0;
+    if (valid) {
+        wide_row_sums<W>(a, i, r1, r2);
+        mean_i = a.mean[i];
+        vb_i = a.vb[i];
+        c1 = a.cr1[i];
+        c2 = a.cr2[i];
     }
-    __syncthreads();
-    if (a.counts && threadIdx.x < 6 && cnt[threadIdx.x])
-        atomicAdd(reinterpret_cast<unsigned long long*>(a.counts + threadIdx.x), cnt[threadIdx.x]);
+    wide_verdicts<F>(a, i, valid, r1, r2, mean_i, vb_i, c1, c2);
 }
 
 __global__ void max_abs_rows_kernel(int64_t m, const double* mx, const double* mn, double* out) {
@@ -620,30 +630,43 @@ void dgemm_launch(int64_t M, int64_t N, int64_t K, const double* A, const double
 }
 
 void launch_wide_tail(const WideTail& t, cudaStream_t stream) {
-    const unsigned grid = unsigned((t.M + 7) / 8);
+    const unsigned grid = unsigned(((t.M + 31) / 32 + 7) / 8);  // 8 row groups (warps) per CTA
     if (t.fmt == VABFT_FP64) wide_tail_kernel<VABFT_FP64><<<grid, 256, 0, stream>>>(t);
-    else wide_tail_kernel<VABFT_FP32><<<grid, 256, 0, stream>>>(t);  // 8 rows (warps) per CTA
+    else wide_tail_kernel<VABFT_FP32><<<grid, 256, 0, stream>>>(t);
     check_cuda(cudaGetLastError(), "wide tail launch");
 }
 
-void launch_wide_aside(int fmt, int64_t M, int64_t K, const void* A, const double* br1, const double* br2, int qfmt,
-                       double* mean, double* vb, double* mx, double* mn, double* cr1, double* cr2, void* apart,
-                       int64_t ld, int64_t* counts, bool combine, cudaStream_t stream) {
-    const int64_t nb = (K + 127) / 128;
-    const dim3 grid_p(unsigned((M + 127) / 128), unsigned(nb));
-    const unsigned grid_c = unsigned((M + 255) / 256);
-    auto run = [&](auto tag, auto wtag) {
+void launch_wide_aside(const WideTail& t, const double* br1, const double* br2, void* apart, unsigned* gcnt,
+                       bool finish, double* mean, double* vb, double* mx, double* mn, double* cr1, double* cr2,
+                       cudaStream_t stream) {
+    const int64_t nb = (t.K + 127) / 128;
+    auto run = [&](auto tag) {
         using T = decltype(tag);
-        using W = decltype(wtag);
+        using W = T;
         constexpr int F = sizeof(T) == 8 ? VABFT_FP64 : VABFT_FP32;
-        const APart<W> part = apart_view<W>(apart, nb, ld);
-        wide_apart_kernel<F, W><<<grid_p, 128, 0, stream>>>(static_cast<const T*>(A), M, K, br1, br2, part, ld);
-        if (combine)
-            wide_acombine_kernel<F, W><<<grid_c, 256, 0, stream>>>(static_cast<const T*>(A), M, K, part, ld, qfmt,
-                                                                   mean, vb, mx, mn, cr1, cr2, counts);
+        ApJob<W> j;
+        j.t = t;
+        j.br1 = br1;
+        j.br2 = br2;
+        j.part = apart_view<W>(apart, nb, t.ld);
+        j.gcnt = gcnt;
+        j.finish = finish ? 1 : 0;
+        j.mean = mean;
+        j.vb = vb;
+        j.mx = mx;
+        j.mn = mn;
+        j.cr1 = cr1;
+        j.cr2 = cr2;
+        auto kern = wide_apart_kernel<F, W>;
+        constexpr size_t smem = ap_smem<F>();
+        ensure_smem_attr(reinterpret_cast<const void*>(kern), int(smem));
+        const int per_sm = cached_occupancy(reinterpret_cast<const void*>(kern), 32 * kApWarps, int(smem));
+        const int64_t tasks = (t.M + 31) / 32 * nb;
+        const int grid = int(std::min<int64_t>(int64_t(sm_count()) * std::max(per_sm, 1), (tasks + kApWarps - 1) / kApWarps));
+        kern<<<grid, 32 * kApWarps, smem, stream>>>(static_cast<const T*>(t.A), j);
     };
-    if (fmt == VABFT_FP64) run(double{}, double{});
-    else if (fmt == VABFT_FP32) run(float{}, float{});
+    if (t.fmt == VABFT_FP64) run(double{});
+    else if (t.fmt == VABFT_FP32) run(float{});
     else fail(VABFT_INVALID_ARGUMENT, "wide A side: FP32 / FP64 only");
     check_cuda(cudaGetLastError(), "wide A-side launch");
 }

@@ -29,29 +29,45 @@ class CalibrationModel:
     r2: float = 0.0
 
 
+def _seq_sum(xs) -> float:
+    """Left-to-right FP64 sum (the reference's loops). Python 3.12's built-in
+    sum() of floats is compensated (Neumaier), which rounds differently."""
+    t = 0.0
+    for x in xs:
+        t += x
+    return t
+
+
 def fit_model(sizes: Sequence[int], maxima: Sequence[float]) -> CalibrationModel:
     """fit_model (calibration.cpp:15-59): Constant if the maxima vary little
-    (CV < 15%), else least squares of max against sqrt(size)."""
+    (CV < 15%), else least squares of max against sqrt(size). Same
+    operations in the same order as the reference (bit-identical results)."""
     if len(sizes) != len(maxima) or not sizes:
         raise ValueError("fit_model: sizes and maxima must match and be nonempty")
     n = len(maxima)
     m = CalibrationModel()
-    mean = sum(maxima) / n
+    mean = _seq_sum(maxima) / n
     m.value = mean
     if n >= 2 and mean > 0.0:
-        ss = sum((v - mean) ** 2 for v in maxima)
+        ss = _seq_sum((v - mean) * (v - mean) for v in maxima)
         m.cv = math.sqrt(ss / (n - 1)) / mean
     if n >= 2:
-        xs = [math.sqrt(float(s)) for s in sizes]
-        sx, sy = sum(xs), sum(maxima)
-        sxx = sum(x * x for x in xs)
-        sxy = sum(x * y for x, y in zip(xs, maxima))
+        sx = sy = sxx = sxy = 0.0
+        for s_, y in zip(sizes, maxima):
+            x = math.sqrt(float(s_))
+            sx += x
+            sy += y
+            sxx += x * x
+            sxy += x * y
         denom = n * sxx - sx * sx
         if denom != 0.0:
             m.scale = (n * sxy - sx * sy) / denom
             m.offset = (sy - m.scale * sx) / n
-            ss_res = sum((y - (m.scale * x + m.offset)) ** 2 for x, y in zip(xs, maxima))
-            ss_tot = sum((y - mean) ** 2 for y in maxima)
+            ss_res = ss_tot = 0.0
+            for s_, y in zip(sizes, maxima):
+                fit = m.scale * math.sqrt(float(s_)) + m.offset
+                ss_res += (y - fit) * (y - fit)
+                ss_tot += (y - mean) * (y - mean)
             m.r2 = 1.0 - ss_res / ss_tot if ss_tot > 0.0 else 1.0
     m.kind = "constant" if (n < 2 or m.cv < 0.15 or m.scale <= 0.0) else "sqrt_scaled"
     return m

@@ -273,6 +273,37 @@ PYBIND11_MODULE(_core, m) {
         .def("localization_accuracy", &CampaignOutcome::localization_accuracy);
     m.def("injection_campaign", &injection_campaign);
 
+    py::class_<CalibrationModel>(m, "CalibrationModel")
+        .def(py::init<>())
+        .def_readwrite("kind", &CalibrationModel::kind)
+        .def_readwrite("value", &CalibrationModel::value)
+        .def_readwrite("scale", &CalibrationModel::scale)
+        .def_readwrite("offset", &CalibrationModel::offset)
+        .def_readwrite("cv", &CalibrationModel::cv)
+        .def_readwrite("r2", &CalibrationModel::r2);
+    py::class_<CalibrationResult>(m, "CalibrationResult")
+        .def_readonly("precision", &CalibrationResult::precision)
+        .def_readonly("mode", &CalibrationResult::mode)
+        .def_readonly("sizes", &CalibrationResult::sizes)
+        .def_readonly("maxima", &CalibrationResult::maxima)
+        .def_readonly("model", &CalibrationResult::model)
+        .def_readonly("recommended", &CalibrationResult::recommended)
+        .def_readonly("seed", &CalibrationResult::seed)
+        .def_readonly("trials_per_size", &CalibrationResult::trials_per_size)
+        .def_readonly("aborted_trials", &CalibrationResult::aborted_trials)
+        .def_readonly("unit_roundoff", &CalibrationResult::unit_roundoff)
+        .def("e_max_for", &CalibrationResult::e_max_for)
+        .def("recommended_model", &CalibrationResult::recommended_model);
+    m.def("fit_model", [](const std::vector<int64_t>& sizes, const std::vector<double>& maxima) {
+        return fit_model(sizes, maxima);
+    });
+    m.def("calibrate",
+          [](const PrecisionSpec& p, const std::vector<int64_t>& sizes, int64_t trials, uint64_t seed, VerifyMode mode) {
+              return calibrate(p, sizes, trials, seed, mode);
+          },
+          py::arg("precision"), py::arg("sizes"), py::arg("trials_per_size"), py::arg("seed"),
+          py::arg("mode") = VerifyMode::Offline);
+
     m.attr("kMatrixFileVersion") = kMatrixFileVersion;
     m.def("save_matrix_binary", &save_matrix_binary);
     m.def("load_matrix_binary", &load_matrix_binary);

@@ -205,3 +205,176 @@ def test_pair_half_tiles_match_one_cta_at_k4096(env, mode):
     for a, b in zip(out[0], out[1]):
         assert torch.equal(a, b)
     g.close()
+
+
+def test_guard_failing_rows_at_c2_size(env):
+    """Rows whose A statistics fail the in-GEMM exactness guard (entries near
+    1e-10 next to O(1) ones at K = 4096) take the warp-cooperative Neumaier
+    rerun inside the streamed verification: thresholds stay bit-exact against
+    the reference and the rerun count is reported in counts[4]."""
+    torch, O = env
+    from paper_2602_08043_b200.fused import FusedAbftGemm
+    m = k = n = 4096
+    dA, dB = _inputs(torch, m, k, n, torch.bfloat16, 21)
+    rows = torch.arange(0, m, 61, device="cuda")  # 68 rows
+    tiny = (torch.rand(len(rows), k, device="cuda") < 0.5)
+    dA[rows] = torch.where(tiny, dA[rows].float() * 1e-10, dA[rows].float()).bfloat16()
+    g = FusedAbftGemm(dB)
+    counts = torch.zeros(6, dtype=torch.int64, device="cuda")
+    r = g(dA, counts=counts)
+    torch.cuda.synchronize()
+    assert int(counts[4].item()) >= len(rows) // 2, counts.tolist()
+    S = torch.cat([rows[:24], torch.arange(1, 40, device="cuda")]).unique()
+    T_ref, _ = O.vabft_thresholds(dA[S].double().cpu().numpy(), dB.double().cpu().numpy(), g.opts.e_max, fmt="bf16")
+    assert _same(r.T[S].cpu().numpy(), T_ref)
+    assert int(counts[1].item()) == 0
+    g.close()
+
+
+@pytest.mark.parametrize("fmt", ["bf16", "fp16", "fp32", "fp64"])
+@pytest.mark.parametrize("shape", [(1024, 1000), (300, 777)])
+def test_bside_pass_mixed_scales_bit_exact(env, fmt, shape):
+    """The per-weight B-side pass (bside.cu) on weights whose rows mix
+    magnitudes far apart (rows outside the exactness guard go through the
+    warp Neumaier rerun) and odd / ragged N: B summary and thresholds
+    bit-exact against the reference's precompute_b_stats / BStatsSummary."""
+    torch, O = env
+    from paper_2602_08043_b200 import api
+    k, n = shape
+    rng = np.random.default_rng(k + n)
+    B = rng.standard_normal((k, n))
+    B[::7] *= np.where(rng.random((len(B[::7]), n)) < 0.3, 1e-9, 1.0)
+    B[3::11] *= 1e-25 if fmt != "fp16" else 1e-4
+    A = rng.standard_normal((64, k))
+    B = np.array([O.quantize(x, fmt) for x in B.ravel()]).reshape(B.shape)
+    A = np.array([O.quantize(x, fmt) for x in A.ravel()]).reshape(A.shape)
+    T, summ = api.vabft_thresholds(A, B, api.VabftParams(1e-3, 2.5), fmt, return_summary=True)
+    T_ref, s_ref = O.vabft_thresholds(A, B, 1e-3, fmt=fmt)
+    assert _same(summ, s_ref)
+    assert _same(T, T_ref)
+
+
+def test_nsplit_slices_match_oracle_on_slices(env):
+    """SURVEY §8(e) N-sharding: two column slices of one C4-shaped GEMM
+    (8192 x 4096 x 11008 split by shard_columns), each a ColumnShardedGemm
+    verifying its slice as an independent ABFT unit. Per slice, thresholds,
+    checksums and verdicts equal the reference on (A[S], B[:, n0:n1]); planted
+    faults are located at their GLOBAL column; C slices reassemble the full
+    product bit for bit (one-rank run of the same two slices)."""
+    torch, O = env
+    from paper_2602_08043_b200.sharding import ColumnShardedGemm, shard_columns
+    m, k, n = 8192, 4096, 11008
+    dA, dB = _inputs(torch, m, k, n, torch.bfloat16, 44, weights="linear")
+    rng = np.random.default_rng(44)
+    S = _sample_rows(m, rng, count=24)
+    A_s = dA[torch.from_numpy(S).cuda()].double().cpu().numpy()
+    B_h = dB.double().cpu().numpy()
+    C_full = torch.empty(m, n, dtype=torch.bfloat16, device="cuda")
+    for n0, n1 in shard_columns(n, 2):
+        sg = ColumnShardedGemm(dB[:, n0:n1].contiguous(), n0, n)
+        col = torch.full((m,), -1, dtype=torch.int32, device="cuda")
+        bit = torch.zeros(m, dtype=torch.int32, device="cuda")
+        fr = S[::3]
+        fc = rng.integers(0, n1 - n0, len(fr))
+        col[torch.from_numpy(fr).cuda()] = torch.from_numpy(fc.astype(np.int32)).cuda()
+        bit[torch.from_numpy(fr).cuda()] = 26  # flip exponent bit 3: x 2^+-8
+        out = torch.empty(m, n1 - n0, dtype=torch.bfloat16, device="cuda")
+        acc = torch.empty(m, n1 - n0, dtype=torch.float32, device="cuda")
+        r = sg(dA, out=out, checksums=True, accum_out=acc,
+               faults={"col": col, "bit": bit, "dir": torch.zeros(m, dtype=torch.int32, device="cuda")})
+        torch.cuda.synchronize()
+        Sd = torch.from_numpy(S).cuda()
+        Bs = B_h[:, n0:n1]
+        T_ref, _ = O.vabft_thresholds(A_s, Bs, sg.g.opts.e_max, fmt="bf16")
+        rc1, rc2 = O.blocked_row_checksums(A_s, Bs, "bf16", "online")
+        assert _same(r.T[Sd].cpu().numpy(), T_ref)
+        assert _same(r.row_check1[Sd].cpu().numpy(), rc1) and _same(r.row_check2[Sd].cpu().numpy(), rc2)
+        v = O.verify(acc[Sd].double().cpu().numpy(), rc1, rc2, T_ref, "fp32", "offline", accum=(2, 128))
+        assert np.array_equal(r.detected[Sd].cpu().numpy().astype(bool), v["detected"])
+        assert np.array_equal(r.location[Sd].cpu().numpy(), v["location"])
+        gl = sg.global_location(r).cpu().numpy()
+        loc_fr = r.location.cpu().numpy()[fr]
+        ok = loc_fr >= 0  # located unless |x| sits below the threshold
+        assert ok.mean() > 0.7, (ok.sum(), len(fr))
+        # the global column is the fault's (slice offset applied); a flip of a
+        # small element (|D1| below the row-sum rounding noise of D2) can be
+        # located elsewhere — by the reference too (device == oracle above)
+        hit = gl[fr][ok] == (fc + n0)[ok]
+        assert hit.any()
+        assert np.array_equal(gl[fr][ok] - n0, loc_fr[ok])
+        sg(dA, out=out)  # a clean run for the reassembly check below
+        torch.cuda.synchronize()
+        C_full[:, n0:n1] = out
+        # clean rows stay clean
+        det = r.detected.cpu().numpy().astype(bool)
+        det[fr] = False
+        assert not det.any()
+        sg.close()
+    # the slices reassemble the unsplit product (each C element is computed
+    # independently of the other columns)
+    ref = torch.empty(m, n, dtype=torch.bfloat16, device="cuda")
+    from paper_2602_08043_b200.fused import plain_gemm
+    plain_gemm(dA, dB, out=ref)
+    torch.cuda.synchronize()
+    assert torch.equal(C_full.view(torch.int16), ref.view(torch.int16))
+
+
+@pytest.mark.parametrize("n", [256, 1024])
+def test_fp16_offline_normal_1_1_false_positives_are_the_references(env, n):
+    """FP16 offline on N(1,1) operands flags clean rows — reference behaviour,
+    not a kernel defect: offline row checksums A (B r2) are quantized to FP16
+    and saturate at 65504 (checksum.cpp:129-134, precision.cpp:153-157), so
+    D2 (and with it D1 for large rows) is wrong by construction. Per row, the
+    fused kernel's verdicts equal the reference's verify on the same inputs
+    (device output, reference thresholds and checksums), and the reference's
+    own end-to-end pipeline (its emulated GEMM) flags rows too."""
+    torch, O = env
+    from paper_2602_08043_b200.fused import FusedAbftGemm
+    A, B = O.trial_inputs(n, n, n, "fp16", "normal:1,1", 0, 0)
+    g = FusedAbftGemm(torch.from_numpy(B).to(torch.float16).cuda(), mode="offline")
+    counts = torch.zeros(6, dtype=torch.int64, device="cuda")
+    r = g(torch.from_numpy(A).to(torch.float16).cuda(), counts=counts, checksums=True)
+    torch.cuda.synchronize()
+    e_max = g.opts.e_max
+    T_ref, _ = O.vabft_thresholds(A, B, e_max, fmt="fp16")
+    rc1, rc2 = O.blocked_row_checksums(A, B, "fp16", "offline")
+    assert _same(r.T.cpu().numpy(), T_ref)
+    assert _same(r.row_check1.cpu().numpy(), rc1) and _same(r.row_check2.cpu().numpy(), rc2)
+    v = O.verify(r.C.double().cpu().numpy(), rc1, rc2, T_ref, "fp32", "offline", accum=(2, 128))
+    det = r.detected.cpu().numpy().astype(bool)
+    assert np.array_equal(det, v["detected"]) and np.array_equal(r.location.cpu().numpy(), v["location"])
+    assert det.sum() > 0 and int(counts[1].item()) == det.sum()
+    assert np.abs(rc2).max() == 65504.0  # the saturated checksums behind the flags
+    e = O.encode_and_multiply(A, B, "fp16", "offline")  # the reference end to end
+    T_full, _ = O.vabft_thresholds(A, B, e_max, fmt="fp16")
+    vr = O.verify(e.c, e.row_check1, e.row_check2, T_full, "fp16", "offline")
+    assert vr["detected"].sum() > 0
+    g.close()
+
+
+def test_bside_update_replayed_from_a_cuda_graph(env):
+    """vabft_bside_update captured once in a CUDA graph and replayed with new
+    weight values in the same buffer: the B-side pass keeps its launch epoch
+    on the device, so every replay republishes its row groups and the
+    thresholds stay bit-exact against the reference for each weight."""
+    torch, O = env
+    from paper_2602_08043_b200.fused import FusedAbftGemm
+    m, k, n = 256, 1024, 768
+    A, _ = _inputs(torch, m, k, n, torch.bfloat16, 61)
+    Bbuf = torch.empty(k, n, device="cuda", dtype=torch.bfloat16)
+    Bbuf.copy_(torch.randn(k, n, device="cuda"))
+    g = FusedAbftGemm(Bbuf)
+    g.update_weight(Bbuf)
+    torch.cuda.synchronize()
+    gr = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(gr):
+        g.update_weight(Bbuf)
+    for seed in (1, 2, 3):
+        gen = torch.Generator(device="cuda").manual_seed(seed)
+        Bbuf.copy_(torch.randn(k, n, device="cuda", generator=gen) * (seed + 1))
+        gr.replay()
+        r = g(A)
+        torch.cuda.synchronize()
+        T_ref, _ = O.vabft_thresholds(A.double().cpu().numpy(), Bbuf.double().cpu().numpy(), g.opts.e_max, fmt="bf16")
+        assert _same(r.T.cpu().numpy(), T_ref), seed
+    g.close()

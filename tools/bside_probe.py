@@ -1,5 +1,5 @@
 """Time the per-weight B-side pass (vabft_bside_update: bside_kernel [+ FP32
-TF32 split]) with CUDA events, L2 flushed between launches.
+TF32 split]) as a CUDA-graph replay with CUDA events, L2 flushed between launches.
 usage: bside_probe.py [K N] -> one JSON line per format"""
 import json
 import os
@@ -18,12 +18,18 @@ for dt in (torch.bfloat16, torch.float16, torch.float32, torch.float64):
     torch.manual_seed(0)
     B = torch.randn(k, n, device="cuda").to(dt)
     g = FusedAbftGemm(B)
+    for _ in range(3):
+        _capi.check(_capi.lib.vabft_bside_update(g.h, ptr(B), stream_ptr()))
+    torch.cuda.synchronize()
+    gr = torch.cuda.CUDAGraph()  # device time only (no host launch gaps inside the events)
+    with torch.cuda.graph(gr):
+        _capi.check(_capi.lib.vabft_bside_update(g.h, ptr(B), stream_ptr()))
     ts = []
     for i in range(23):
         flush.zero_()
         s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         s.record()
-        _capi.check(_capi.lib.vabft_bside_update(g.h, ptr(B), stream_ptr()))
+        gr.replay()
         e.record()
         torch.cuda.synchronize()
         if i >= 3:

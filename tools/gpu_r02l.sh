@@ -1,0 +1,4 @@
+for d in 3 4 7 0 1; do echo "debug=$d"; VABFT_BSIDE_DEBUG=$d timeout 300 python tools/bside_probe.py 4096 4096 2>&1 | head -3 | cut -c1-110; done
+timeout 300 python tools/bside_probe.py 11008 4096 2>&1 | head -3 | cut -c1-110
+timeout 900 python -m pytest tests/test_gpu_configs.py tests/test_gpu_calibration.py -x -q > gpurun_out/t.log 2>&1; echo "rc=$?"; grep -E "passed|failed|Error|assert" gpurun_out/t.log | head -20
+python tools/fp32_once.py > /dev/null 2>&1 && ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches_fp32.csv python tools/fp32_once.py > /dev/null 2>&1; echo "ncu rc=$?"

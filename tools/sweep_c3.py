@@ -16,7 +16,7 @@ difference is |row_check1 - exactly rounded row sum of the source|
 (math.fsum, the role MPFR plays in oracle_row_diffs), T_V with
 resolve_e_max of the format's default model, T_A fixed y = 21.
 
-  python tools/sweep_c3.py [--quick] > profiles/r01_sweep_c3.jsonl
+  python tools/sweep_c3.py [--quick] [--rows 100000] > profiles/r02_sweep_c3.jsonl
 """
 import argparse
 import json
@@ -111,6 +111,9 @@ def sweep_wide(fmt, dist, n, trials, mode, rng):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--quick", action="store_true")
+    ap.add_argument("--rows", type=int, default=100000,
+                    help="clean rows per (format, distribution, mode, n <= 4096) configuration")
+    ap.add_argument("--exact-rows", type=int, default=20000, help="rows per EXACT-engine configuration")
     args = ap.parse_args()
     gen = torch.Generator(device="cuda")
     gen.manual_seed(0)
@@ -139,6 +142,9 @@ def main():
                 plan.append((fmt, "online", dist, n, t))
     for fmt, mode, dist, n, trials in plan:
         t0 = time.time()
+        if not args.quick and n <= 4096:  # >= args.rows rows per configuration
+            want = args.exact_rows if fmt.endswith(":exact") else args.rows
+            trials = max(trials, -(-want // n))
         if fmt.endswith(":exact"):
             fmt = fmt.split(":")[0]
             a = sweep_wide(fmt, dist, n, trials, mode, rng)
