@@ -301,6 +301,38 @@ def measure_formats(dev, flush, torch, n=4096, steps=20, warmup=3):
     return out
 
 
+def measure_exact_engine(torch, n=1024, reps=5):
+    """The order-exact SIMT engine (vabft_encode_and_multiply, ENGINE_EXACT:
+    the reference's sequential FP32 accumulation, bit for bit) on device
+    buffers, BF16 n^3 online: its throughput beside the tensor path's."""
+    import ctypes as C
+    from paper_2602_08043_b200 import _capi
+    from paper_2602_08043_b200.device import ptr, stream_ptr
+    spec = _capi.precision("bf16")
+    A = torch.randn(n, n, device="cuda").bfloat16()
+    B = torch.randn(n, n, device="cuda").bfloat16()
+    Cc = torch.empty(n, n, device="cuda", dtype=torch.bfloat16)
+    acc = torch.empty(n, n, device="cuda", dtype=torch.float32)
+    rc = torch.empty(2, n, device="cuda", dtype=torch.float64)
+
+    def run():
+        _capi.check(_capi.lib.vabft_encode_and_multiply(C.byref(spec), _capi.ONLINE, 0, n, n, n, ptr(A), ptr(B),
+                                                        ptr(Cc), ptr(acc), ptr(rc[0]), ptr(rc[1]), None, None, None,
+                                                        0, stream_ptr()))
+    run()
+    torch.cuda.synchronize()
+    s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    s.record()
+    for _ in range(reps):
+        run()
+    e.record()
+    torch.cuda.synchronize()
+    ms = s.elapsed_time(e) / reps
+    return {"shape": [n, n, n], "format": "bf16", "mode": "online", "ms": ms, "tflops": 2.0 * n ** 3 / ms / 1e9,
+            "note": "EXACT engine: C, C_accum and row checksums bit-identical to the reference (sequential FP32 "
+                    "k-loop, no FMA); the parity engine, not the hot path"}
+
+
 # ---------------------------------------------------------------- GPU arm
 class Workload:
     """The rank's resident share of the configured batch: weights (per GEMM,
@@ -544,9 +576,10 @@ def run_ours(args):
             for g in ln["g"]:
                 g.close()
 
-    formats = None
+    formats = exact = None
     if world == 1 and args.config == "c2" and not args.no_formats:
         formats = measure_formats(dev, flush, torch)
+        exact = measure_exact_engine(torch)
 
     value = total_flops / (ms_fused / args.steps / 1e3) / 1e12
     fused_int_tf = total_flops / (ms_f_int / (rounds * per) / 1e3) / 1e12
@@ -608,6 +641,7 @@ def run_ours(args):
         "gpu_launches": args.steps * n_own,  # one fused kernel per GEMM (per rank)
         "clocks": clocks,
         "formats": formats,
+        "exact_engine": exact,
     }
     print(json.dumps(line), flush=True)
     if world > 1:

@@ -41,6 +41,7 @@
 #include <cuda_runtime_api.h>
 
 #include <algorithm>
+#include <atomic>
 #include <array>
 #include <cmath>
 #include <cstdint>
@@ -509,8 +510,27 @@ struct EncodedProduct {
     const Matrix& verification_source() const { return mode == VerifyMode::Online ? c_accum : c; }
 };
 
+// Engine of the reference-signature entry points (encode_and_multiply and
+// what builds on it: verify of its product, calibrate, injection_campaign,
+// verify_files). Exact (default): the order-exact SIMT kernels, bit-identical
+// to the reference. Tensor: the B200 fast path — tcgen05 for BF16 / FP16
+// (FP32 accumulator in the tensor core's order), tcgen05 kind::tf32 3xTF32 for
+// FP32, SIMT DFMA for FP64 — with checksums and row sums in the accumulator's
+// working type in NativeBlocked(128) order (the fused kernels' checksum
+// precision), so verify() on its product compares like the fused path.
+namespace b200 {
+enum class Engine { Exact = VABFT_ENGINE_EXACT, Tensor = VABFT_ENGINE_TENSOR };
+inline std::atomic<int>& engine_slot() {
+    static std::atomic<int> e{VABFT_ENGINE_EXACT};
+    return e;
+}
+inline void set_engine(Engine e) { engine_slot().store(int(e)); }
+inline Engine engine() { return Engine(engine_slot().load()); }
+}  // namespace b200
+
 // encode_and_multiply (checksum.cpp:103-158): C, C_accum and all four
-// checksum vectors from one device call (EXACT engine: bit-identical).
+// checksum vectors from one device call (EXACT engine: bit-identical; see
+// b200::set_engine for the fast path).
 inline EncodedProduct encode_and_multiply(const Matrix& a, const Matrix& b, VerifyMode mode = VerifyMode::Offline) {
     if (a.cols() != b.rows()) throw std::invalid_argument("gemm_emulated: inner dimensions disagree");
     if (a.format().format != b.format().format) throw std::invalid_argument("gemm_emulated: operand formats disagree");
@@ -525,10 +545,11 @@ inline EncodedProduct encode_and_multiply(const Matrix& a, const Matrix& b, Veri
     size_t ws = 0;
     detail::check(vabft_encode_workspace_size(m, n, k, &cs, &ws));
     detail::DeviceBuffer dW(ws);
-    detail::check(vabft_encode_and_multiply(&cs, mode == VerifyMode::Online ? VABFT_ONLINE : VABFT_OFFLINE,
-                                            VABFT_ENGINE_EXACT, m, n, k, dA.get(), dB.get(), dC.get(), dAcc.get(),
-                                            rc1.as<double>(), rc2.as<double>(), cc1.as<double>(), cc2.as<double>(),
-                                            dW.get(), ws, nullptr));
+    const int eng = b200::engine_slot().load();
+    detail::check(vabft_encode_and_multiply(&cs, mode == VerifyMode::Online ? VABFT_ONLINE : VABFT_OFFLINE, eng, m,
+                                            n, k, dA.get(), dB.get(), dC.get(), dAcc.get(), rc1.as<double>(),
+                                            rc2.as<double>(), cc1.as<double>(), cc2.as<double>(), dW.get(), ws,
+                                            nullptr));
     detail::cuda_check(cudaDeviceSynchronize(), "encode_and_multiply");
     EncodedProduct out;
     out.c = detail::download(dC, m, n, spec.format, spec);
@@ -539,6 +560,9 @@ inline EncodedProduct encode_and_multiply(const Matrix& a, const Matrix& b, Veri
     out.col_check1 = cc1.to_vector<double>(size_t(n));
     out.col_check2 = cc2.to_vector<double>(size_t(n));
     out.checksum_precision = checksum_precision_for(spec, mode);
+    if (eng == VABFT_ENGINE_TENSOR)  // the fused kernels' checksum precision
+        out.checksum_precision = (spec.format == Format::FP64 ? PrecisionSpec::fp64() : PrecisionSpec::fp32())
+                                     .with_accumulation({AccumKind::NativeBlocked, 128});
     out.mode = mode;
     return out;
 }

@@ -61,7 +61,8 @@ struct BsT {
     // FP32) or 64-bit words, row stride padded by one word
     static constexpr int kCols = k16 ? 64 : 32;
     using Word = typename std::conditional<F == VABFT_FP64, double, uint32_t>::type;
-    static constexpr int kWords = 32;  // words per staged row
+    static constexpr int kWords = 32;   // words per staged row
+    static constexpr int kStride = 36;  // padded stride: 16-byte aligned rows, conflict-free 16-byte LDS
 };
 
 // Per-(block, row) partial arrays, group-major: element (block b, row k) at
@@ -274,7 +275,7 @@ __device__ __forceinline__ void bs_block(const BsJob<F>& j, typename BsT<F>::Wor
     using Word = typename BsT<F>::Word;
     using V = typename BsT<F>::V;
     constexpr int kCols = BsT<F>::kCols;
-    constexpr int kStride = BsT<F>::kWords + 1;
+    constexpr int kStride = BsT<F>::kStride;
     const int lane = threadIdx.x & 31;
     const int64_t K = j.K, N = j.N;
     const int64_t r0 = rg * 32;
@@ -299,20 +300,41 @@ __device__ __forceinline__ void bs_block(const BsJob<F>& j, typename BsT<F>::Wor
         const int cnt = int(c0 + bw - cq < kCols ? c0 + bw - cq : kCols);  // warp-uniform
         const float w0 = float(cq + 1);  // weight j + 1 of the sub-tile's first element (exact: N <= 2^24)
         if constexpr (BsT<F>::k16) {
-            if (cnt == kCols) {
+            if (cnt == kCols) {  // 16-byte LDS: 8 elements per load
 #pragma unroll
-                for (int jj = 0; jj < kCols / 2; ++jj) a.pair(trow[jj], __fadd_rn(w0, float(2 * jj)));
+                for (int u = 0; u < kCols / 8; ++u) {
+                    const uint4 q4 = reinterpret_cast<const uint4*>(trow)[u];
+                    const float wu = __fadd_rn(w0, float(8 * u));
+                    a.pair(q4.x, wu);
+                    a.pair(q4.y, __fadd_rn(wu, 2.0f));
+                    a.pair(q4.z, __fadd_rn(wu, 4.0f));
+                    a.pair(q4.w, __fadd_rn(wu, 6.0f));
+                }
             } else {
                 const int npair = cnt >> 1;
                 for (int jj = 0; jj < npair; ++jj) a.pair(trow[jj], __fadd_rn(w0, float(2 * jj)));
                 if (cnt & 1) a.single(trow[npair] & 0xFFFFu, __fadd_rn(w0, float(2 * npair)));
             }
         } else {
-            if (cnt == kCols) {
-#pragma unroll 8
-                for (int jj = 0; jj < kCols; ++jj) {
-                    if constexpr (F == VABFT_FP32) a.elem(__uint_as_float(trow[jj]), __fadd_rn(w0, float(jj)));
-                    else a.elem(trow[jj], __fadd_rn(w0, float(jj)));
+            if (cnt == kCols) {  // 16-byte LDS
+                if constexpr (F == VABFT_FP32) {
+#pragma unroll
+                    for (int u = 0; u < kCols / 4; ++u) {
+                        const uint4 q4 = reinterpret_cast<const uint4*>(trow)[u];
+                        const float wu = __fadd_rn(w0, float(4 * u));
+                        a.elem(__uint_as_float(q4.x), wu);
+                        a.elem(__uint_as_float(q4.y), __fadd_rn(wu, 1.0f));
+                        a.elem(__uint_as_float(q4.z), __fadd_rn(wu, 2.0f));
+                        a.elem(__uint_as_float(q4.w), __fadd_rn(wu, 3.0f));
+                    }
+                } else {
+#pragma unroll 4
+                    for (int u = 0; u < kCols / 2; ++u) {
+                        const double2 q2 = reinterpret_cast<const double2*>(trow)[u];
+                        const float wu = __fadd_rn(w0, float(2 * u));
+                        a.elem(q2.x, wu);
+                        a.elem(q2.y, __fadd_rn(wu, 1.0f));
+                    }
                 }
             } else {
                 for (int jj = 0; jj < cnt; ++jj) {
@@ -553,13 +575,13 @@ __device__ void bs_summary(const BsJob<F>& j, double* buf2 /* 2 x kBatch doubles
 
 template <int F>
 constexpr size_t bs_smem() {
-    return size_t(kBsWarps) * 32 * (BsT<F>::kWords + 1) * sizeof(typename BsT<F>::Word);
+    return size_t(kBsWarps) * 32 * BsT<F>::kStride * sizeof(typename BsT<F>::Word);
 }
 
 template <int F>
 __global__ void __launch_bounds__(kBsThreads, F == VABFT_FP64 ? 1 : 2) bside_kernel(const __grid_constant__ BsJob<F> j) {
     using Word = typename BsT<F>::Word;
-    constexpr int kStride = BsT<F>::kWords + 1;
+    constexpr int kStride = BsT<F>::kStride;
     constexpr int kChains = BsT<F>::k16 ? 4 : 3;  // wide formats: max_k |sum_j B| on demand
     extern __shared__ __align__(16) uint8_t bs_smem_raw[];
     Word* tiles = reinterpret_cast<Word*>(bs_smem_raw);
@@ -595,11 +617,11 @@ __global__ void __launch_bounds__(kBsThreads, F == VABFT_FP64 ? 1 : 2) bside_ker
         const int64_t rg = t / nb;
         const int b = int(t - rg * nb);
         bs_block<F>(j, tile, rg, b);
-        // arrival: every lane's partial stores before lane 0's counter RMW
-        __threadfence();
+        // arrival: every lane's partial stores before lane 0's release RMW;
+        // the last arriver reads the partials through L2 after a fence
         __syncwarp();
         unsigned old = 0;
-        if (lane == 0) old = atomicAdd(j.grp_cnt + rg, 1u);
+        if (lane == 0) old = atom_add_release_gpu(j.grp_cnt + rg, 1u);
         old = __shfl_sync(0xffffffffu, old, 0);
         if (old == unsigned(nb) - 1u && j.debug < 2) {
             __threadfence();

@@ -25,6 +25,13 @@ __device__ __forceinline__ unsigned int atom_add_acq_rel_gpu(unsigned int* addr,
     asm volatile("atom.add.acq_rel.gpu.global.u32 %0, [%1], %2;" : "=r"(old) : "l"(addr), "r"(v) : "memory");
     return old;
 }
+// Release-only RMW (no acquire, so no L1 invalidation): the arrival of a
+// producer whose partials are then read through L2 by the last arriver.
+__device__ __forceinline__ unsigned int atom_add_release_gpu(unsigned int* addr, unsigned int v) {
+    unsigned int old;
+    asm volatile("atom.add.release.gpu.global.u32 %0, [%1], %2;" : "=r"(old) : "l"(addr), "r"(v) : "memory");
+    return old;
+}
 __device__ __forceinline__ void fence_mbar_init() {
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
 }

@@ -279,11 +279,12 @@ struct ApJob {
 };
 
 constexpr int kApWarps = 8;
+constexpr int kApLd = 36;  // staged row stride (elements): 16-byte aligned rows, conflict-free 16-byte LDS
 
 template <int F>
 constexpr size_t ap_smem() {
     using T = typename Elem<F>::T;
-    return size_t(kApWarps) * (32 * 33 * sizeof(T) + 2 * 128 * sizeof(T));
+    return size_t(kApWarps) * (32 * kApLd * sizeof(T) + 2 * 128 * sizeof(T));
 }
 
 template <int F>
@@ -296,6 +297,25 @@ __device__ __forceinline__ void ap_load(const typename Elem<F>::T* __restrict__ 
 #pragma unroll
     for (int rr = 0; rr < 32; ++rr) v[rr] = (rr < rows && col < K) ? __ldcs(p + rr * K) : T(0);
 }
+
+// One element of the FP32 A pass: checksum products (no FMA), the plain FP64
+// sub-tile sum, sum|x|, max / min and the exactness-guard trackers.
+struct ApF32 {
+    float p1 = 0.0f, p2 = 0.0f, sabs = 0.0f, mx = -INFINITY, mn = INFINITY;
+    double ps = 0.0;
+    uint32_t amx = 0u, mnz = 0xFFFFFFFFu;
+    __device__ __forceinline__ void add(float x, float w1, float w2) {
+        const uint32_t mag = __float_as_uint(x) & 0x7FFFFFFFu;
+        amx = max(amx, mag);
+        mnz = min(mnz, mag - 1u);  // 0 wraps to the maximum: ignored
+        ps = __dadd_rn(ps, double(x));
+        p1 = __fadd_rn(p1, __fmul_rn(w1, x));
+        p2 = __fadd_rn(p2, __fmul_rn(w2, x));
+        sabs = __fadd_rn(sabs, fabsf(x));
+        mx = fmaxf(mx, x);  // finite rows (non-finite ones fail exact_sum_safe and rerun)
+        mn = fminf(mn, x);
+    }
+};
 
 // The verdict of the lanes' rows (lane = row) from their C-row sums r1 / r2,
 // checksums c1 / c2 and statistics; warp-aggregated counters.
@@ -461,8 +481,8 @@ __global__ void __launch_bounds__(32 * kApWarps, F == VABFT_FP64 ? 1 : 2)
     using T = typename Elem<F>::T;
     extern __shared__ __align__(16) uint8_t ap_raw[];
     const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    T* tile = reinterpret_cast<T*>(ap_raw + size_t(w) * (32 * 33 * sizeof(T) + 2 * 128 * sizeof(T)));
-    W* wts = reinterpret_cast<W*>(tile + 32 * 33);  // [2][128] weights of the block (W == T)
+    T* tile = reinterpret_cast<T*>(ap_raw + size_t(w) * (32 * kApLd * sizeof(T) + 2 * 128 * sizeof(T)));
+    W* wts = reinterpret_cast<W*>(tile + 32 * kApLd);  // [2][128] weights of the block (W == T)
     const int64_t M = j.t.M, K = j.t.K;
     const int64_t nb = (K + 127) / 128, ngroups = (M + 31) / 32;
     const int64_t tasks = ngroups * nb;
@@ -481,12 +501,12 @@ __global__ void __launch_bounds__(32 * kApWarps, F == VABFT_FP64 ? 1 : 2)
             wts[128 + jj] = jj < bw ? W(j.br2[c0 + jj]) : W(0);
         }
 #pragma unroll
-        for (int rr = 0; rr < 32; ++rr) tile[rr * 33 + lane] = v[rr];
+        for (int rr = 0; rr < 32; ++rr) tile[rr * kApLd + lane] = v[rr];
         __syncwarp();
         W p1 = W(0), p2 = W(0);
         double s = 0.0, c = 0.0;
         T sabs = T(0), mx = T(-INFINITY), mn = T(INFINITY);
-        const T* trow = tile + lane * 33;
+        const T* trow = tile + lane * kApLd;
         for (int q = 0; q < nsub; ++q) {
             const int64_t cq = c0 + int64_t(q) * 32;
             if (q + 1 < nsub) ap_load<F>(A, M, K, r0, cq + 32, v);  // in flight during this sub-tile
@@ -494,44 +514,55 @@ __global__ void __launch_bounds__(32 * kApWarps, F == VABFT_FP64 ? 1 : 2)
             const W* w1 = wts + q * 32;
             const W* w2 = wts + 128 + q * 32;
             if constexpr (F == VABFT_FP32) {
-                double ps = 0.0;
-                uint32_t amx = 0u, mnz = 0xFFFFFFFFu;
-#pragma unroll 8
-                for (int jj = 0; jj < cnt; ++jj) {
-                    const float x = trow[jj];
-                    const uint32_t mag = __float_as_uint(x) & 0x7FFFFFFFu;
-                    amx = max(amx, mag);
-                    mnz = min(mnz, mag - 1u);  // 0 wraps to the maximum: ignored
-                    ps = __dadd_rn(ps, double(x));
-                    p1 = radd(p1, rmul(w1[jj], x));
-                    p2 = radd(p2, rmul(w2[jj], x));
-                    sabs = __fadd_rn(sabs, fabsf(x));
-                    mx = mx < x ? x : mx;  // NaN-free rows: identical to fmax / fmin
-                    mn = x < mn ? x : mn;
+                ApF32 e;
+                e.p1 = p1;
+                e.p2 = p2;
+                e.sabs = sabs;
+                e.mx = mx;
+                e.mn = mn;
+                if (cnt == 32) {  // 16-byte LDS of 4 elements and of their weights
+#pragma unroll
+                    for (int u = 0; u < 8; ++u) {
+                        const float4 x4 = reinterpret_cast<const float4*>(trow)[u];
+                        const float4 a4 = reinterpret_cast<const float4*>(w1)[u];
+                        const float4 b4 = reinterpret_cast<const float4*>(w2)[u];
+                        e.add(x4.x, a4.x, b4.x);
+                        e.add(x4.y, a4.y, b4.y);
+                        e.add(x4.z, a4.z, b4.z);
+                        e.add(x4.w, a4.w, b4.w);
+                    }
+                } else {
+                    for (int jj = 0; jj < cnt; ++jj) e.add(trow[jj], w1[jj], w2[jj]);
                 }
+                p1 = e.p1;
+                p2 = e.p2;
+                sabs = e.sabs;
+                mx = e.mx;
+                mn = e.mn;
+                double ps = e.ps;
                 // exactness guard of the plain sub-tile sum (see guard_exact)
                 bool exact = true;
-                if (mnz != 0xFFFFFFFFu && amx < 0x7F800000u) {
-                    const int ez = int((mnz + 1u) >> 23);
+                if (e.mnz != 0xFFFFFFFFu && e.amx < 0x7F800000u) {
+                    const int ez = int((e.mnz + 1u) >> 23);
                     const int lsb = (ez == 0 ? 1 : ez) - 127 - 23;
-                    const int top = int(amx >> 23) - 127 + 1 + 6;  // 32 terms < 2^6 max
+                    const int top = int(e.amx >> 23) - 127 + 1 + 6;  // 32 terms < 2^6 max
                     exact = top <= 53 + lsb;
                 }
                 if (!exact) {  // rare: the sub-tile's exact sum as a TwoSum cascade
                     double hs = 0.0, hc = 0.0;
                     for (int jj = 0; jj < cnt; ++jj) {
-                        double tt, e;
-                        two_sum(hs, double(trow[jj]), tt, e);
+                        double tt, ee;
+                        two_sum(hs, double(trow[jj]), tt, ee);
                         hs = tt;
-                        hc = __dadd_rn(hc, e);
+                        hc = __dadd_rn(hc, ee);
                     }
                     ps = hs;
                     c = __dadd_rn(c, hc);
                 }
-                double tt, e;
-                two_sum(s, ps, tt, e);
+                double tt, ee;
+                two_sum(s, ps, tt, ee);
                 s = tt;
-                c = __dadd_rn(c, e);
+                c = __dadd_rn(c, ee);
             } else {
 #pragma unroll 4
                 for (int jj = 0; jj < cnt; ++jj) {
@@ -550,7 +581,7 @@ __global__ void __launch_bounds__(32 * kApWarps, F == VABFT_FP64 ? 1 : 2)
             if (q + 1 < nsub) {
                 __syncwarp();
 #pragma unroll
-                for (int rr = 0; rr < 32; ++rr) tile[rr * 33 + lane] = v[rr];
+                for (int rr = 0; rr < 32; ++rr) tile[rr * kApLd + lane] = v[rr];
                 __syncwarp();
             }
         }
@@ -566,12 +597,15 @@ __global__ void __launch_bounds__(32 * kApWarps, F == VABFT_FP64 ? 1 : 2)
             j.part.mx[o] = double(mx);
             j.part.mn[o] = double(mn);
         }
-        // arrival: every lane's partial stores before lane 0's release RMW
+        // arrival: every lane's partial stores before lane 0's release RMW;
+        // the last arriver then reads all partials through L2 (.cg) after a
+        // fence (acquire side)
         __syncwarp();
         unsigned old = 0;
-        if (lane == 0) old = atom_add_acq_rel_gpu(j.gcnt + rg, 1u);
+        if (lane == 0) old = atom_add_release_gpu(j.gcnt + rg, 1u);
         old = __shfl_sync(0xffffffffu, old, 0);
         if (old == unsigned(nb) - 1u) {
+            __threadfence();
             if (lane == 0) j.gcnt[rg] = 0u;  // ready for the next launch
             ap_finish_group<F, W>(j, rg);
         }

@@ -7,7 +7,7 @@ resolve_run_e_max: calibrate(precision, mode, {128, 256, 512, K}) then
 e_max_for(K)). Online verification compares the FP32 accumulator of the
 tensor core, whose rounding the CPU emulator does not reproduce, so the
 online defaults here come from the same protocol run on the B200 fused path
-(calibration.calibrate; raw data in profiles/r01_calibration_*_device.json):
+(calibration.calibrate; raw data in profiles/r02_calibration_device_100trials.jsonl):
 |N(1,1)| square operands, per size the max over trials and rows of
 |D1| / |row_check1|. Offline defaults are the reference's format constants
 (precision.cpp:44-62), which its own calibration reproduces (the 2u floor).
@@ -124,32 +124,34 @@ def unit_roundoff_for(precision: str, mode: str) -> float:
     return {"bf16": 2.0 ** -8, "fp16": 2.0 ** -11, "fp32": 2.0 ** -24, "fp64": 2.0 ** -53}[precision]
 
 
-# Device calibration of the fused tcgen05 path (B200, 6 trials per size,
-# seed 0; tools/calib_run.py). Maxima of |D1|/|row_check1| per square size.
+# Device calibration of the fused paths (B200, calibration.calibrate: the
+# reference protocol of calibration.cpp:88-150, 100 trials per size, seed 0;
+# tools/calib_run.py -> profiles/r02_calibration_device_100trials.jsonl).
+# Maxima of |D1| / |row_check1| per square size.
 DEVICE_CALIBRATION: Dict[Tuple[str, str], Tuple[List[int], List[float]]] = {
-    # 10 trials per size (profiles/r01_calibration_bf16_device_10trials.json)
+    # the tcgen05 FP32 accumulator, BF16 operands
     ("bf16", "online"): ([128, 256, 512, 1024, 2048, 4096, 8192, 16384],
-                         [1.04e-06, 9.20e-07, 1.41e-06, 2.55e-06, 6.05e-06, 1.49e-05, 3.61e-05, 8.41e-05]),
-    # profiles/r01_calibration_fp16_device.json. (FP16 OFFLINE is not tabled:
-    # with |N(1,1)| operands the FP16-quantized checksums saturate at 65504
-    # from size 256 on, so the protocol measures overflow, not rounding; the
-    # format constant stays.)
+                         [1.038e-06, 1.082e-06, 1.458e-06, 2.659e-06, 6.115e-06, 1.520e-05, 3.663e-05, 8.408e-05]),
+    # FP16 operands on the same accumulator. (FP16 OFFLINE is not tabled: with
+    # |N(1,1)| operands the FP16-quantized checksums saturate at 65504 from
+    # size 256 on, so the protocol measures overflow, not rounding; the format
+    # constant stays. BF16 offline maxima, 3.0e-3 .. 4.0e-3, sit below the 2u
+    # floor 7.8e-3, which the format constant 8e-3 covers.)
     ("fp16", "online"): ([128, 256, 512, 1024, 2048, 4096, 8192, 16384],
-                         [1.48e-06, 1.88e-06, 3.39e-06, 6.62e-06, 1.35e-05, 2.73e-05, 5.45e-05, 1.10e-04]),
+                         [1.547e-06, 1.982e-06, 3.472e-06, 6.654e-06, 1.350e-05, 2.733e-05, 5.475e-05, 1.097e-04]),
     # FP64 SIMT DFMA path (sequential FMA accumulation, FP64 blocked:128
-    # checksums; online == offline), 4 trials per size
-    # (profiles/r01_calibration_fp64_device.json)
+    # checksums; online == offline)
     ("fp64", "online"): ([128, 256, 512, 1024, 2048, 4096, 8192, 16384],
-                         [1.72e-15, 1.25e-15, 1.01e-15, 8.18e-16, 8.21e-16, 9.85e-16, 1.47e-15, 2.28e-15]),
-    # FP32 on tcgen05 with 3xTF32 (profiles/r01_calibration_fp32_3xtf32_device.json):
-    # the products are FP32-accurate but the tensor core's FP32 accumulation
-    # truncates, so |D1|/|r| grows linearly in n (as for BF16 online)
+                         [2.163e-15, 1.510e-15, 1.131e-15, 9.530e-16, 9.945e-16, 1.146e-15, 1.644e-15, 2.287e-15]),
+    # FP32 on tcgen05 with 3xTF32: the products are FP32-accurate but the
+    # tensor core's FP32 accumulation truncates, so |D1|/|r| grows linearly in
+    # n (as for BF16 online)
     ("fp32", "online"): ([128, 256, 512, 1024, 2048, 4096, 8192, 16384],
-                         [1.90e-06, 3.29e-06, 6.38e-06, 1.24e-05, 2.52e-05, 4.96e-05, 9.86e-05, 1.89e-04]),
-    # one TF32 pass (profiles/r01_calibration_tf32_device.json): TF32 operand
-    # rounding dominates, flat in n; the 2u floor (u = 2^-11) applies
+                         [2.276e-06, 3.471e-06, 6.409e-06, 1.272e-05, 2.514e-05, 5.010e-05, 9.896e-05, 1.900e-04]),
+    # one TF32 pass: TF32 operand rounding dominates, flat in n; the 2u floor
+    # (u = 2^-11) applies
     ("tf32", "online"): ([128, 256, 512, 1024, 2048, 4096, 8192, 16384],
-                         [4.18e-04, 4.17e-04, 3.93e-04, 3.90e-04, 3.91e-04, 3.99e-04, 4.26e-04, 4.86e-04]),
+                         [4.434e-04, 4.134e-04, 4.019e-04, 3.979e-04, 3.955e-04, 4.014e-04, 4.281e-04, 4.880e-04]),
 }
 
 # reference format defaults (PrecisionSpec::bf16/fp16, precision.cpp:44-62)
@@ -165,7 +167,7 @@ def device_calibration(precision: str, mode: str) -> CalibrationResult:
     if key not in DEVICE_CALIBRATION:
         raise KeyError(f"no device calibration for {precision}/{mode}")
     sizes, maxima = DEVICE_CALIBRATION[key]
-    return CalibrationResult.from_maxima(precision, mode, sizes, maxima, trials=6)
+    return CalibrationResult.from_maxima(precision, mode, sizes, maxima, trials=100)
 
 
 def measured_max(precision: str, mode: str, size: int) -> float:
@@ -194,7 +196,7 @@ def resolve_run_e_max(precision: str, mode: str, k: int) -> float:
     if k < 128:
         sizes.insert(0, k)
     maxima = [measured_max(precision, mode, s) for s in sizes]
-    return CalibrationResult.from_maxima(precision, mode, sizes, maxima, trials=6).e_max_for(k)
+    return CalibrationResult.from_maxima(precision, mode, sizes, maxima, trials=100).e_max_for(k)
 
 
 def default_e_max(precision: str, mode: str, k: int) -> float:

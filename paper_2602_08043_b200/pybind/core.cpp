@@ -273,6 +273,10 @@ PYBIND11_MODULE(_core, m) {
         .def("localization_accuracy", &CampaignOutcome::localization_accuracy);
     m.def("injection_campaign", &injection_campaign);
 
+    py::enum_<b200::Engine>(m, "Engine").value("Exact", b200::Engine::Exact).value("Tensor", b200::Engine::Tensor);
+    m.def("set_engine", &b200::set_engine);
+    m.def("engine", &b200::engine);
+
     py::class_<CalibrationModel>(m, "CalibrationModel")
         .def(py::init<>())
         .def_readwrite("kind", &CalibrationModel::kind)

@@ -278,3 +278,47 @@ def test_cpp_fused_gemm_matches_python_path(fmt):
     assert torch.equal(C.view(torch.uint8), r.C.view(torch.uint8))
     assert torch.equal(T, r.T) and torch.equal(det, r.detected) and torch.equal(loc, r.location)
     assert int(counts[0]) == m and int(counts[1]) == 0
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("fmt", list(FMTS))
+@pytest.mark.parametrize("mode", ["offline", "online"])
+def test_reference_signature_reaches_the_fast_path(ref_or_port, fmt, mode):
+    """b200::set_engine(Tensor): the reference-signature encode_and_multiply
+    runs the B200 kernels (tcgen05 / 3xTF32 / DFMA). C_accum is the tensor
+    core's, within the FP32-accumulate bound of the exact product; the
+    checksums are the fused path's (working type, NativeBlocked(128)) and
+    equal the reference's row_sums composition bit for bit; verify() on the
+    product flags and locates a planted fault exactly as the reference's
+    verify does on the same data."""
+    A, B = ref_or_port.trial_inputs(64, 256, 96, fmt, "normal:0,1", 23, 1)
+    s = SPEC[fmt]()
+    a, b = core.Matrix.from_numpy(A, s, False), core.Matrix.from_numpy(B, s, False)
+    vm = core.VerifyMode.Online if mode == "online" else core.VerifyMode.Offline
+    core.set_engine(core.Engine.Tensor)
+    try:
+        e = core.encode_and_multiply(a, b, vm)
+    finally:
+        core.set_engine(core.Engine.Exact)
+    assert core.engine() == core.Engine.Exact
+    exact = A @ B
+    bound = (A.shape[1] + 1) * 2.0**-24 * (np.abs(A) @ np.abs(B))
+    assert np.all(np.abs(e.c_accum.values() - exact) <= bound)
+    c1, c2 = ref_or_port.blocked_row_checksums(A, B, fmt, mode)
+    assert same(e.row_check1, c1) and same(e.row_check2, c2)
+    T = np.full(A.shape[0], 1e-2 if fmt in ("bf16", "fp16") else 1e-6)
+    f = core.FaultSpec()
+    f.bit_index = 60 if fmt == "fp64" else (28 if (mode == "online" or fmt == "fp32") else 13)
+    f.direction, f.position = core.FlipDirection.Flip, (7, 33)
+    src = e.c_accum if mode == "online" else e.c
+    bad, rec = core.inject(src, f, core.Philox(3))
+    if mode == "online":
+        e.c_accum = bad
+    else:
+        e.c = bad
+    v = core.verify(e, T)
+    wf = "fp64" if fmt == "fp64" else "fp32"
+    vr = ref_or_port.verify(bad.values(), e.row_check1, e.row_check2, T, wf, "offline", accum=(2, 128))
+    assert [x.detected for x in v] == list(vr["detected"].astype(bool))
+    assert [(-1 if x.location is None else x.location) for x in v] == list(vr["location"])
+    assert v[7].detected and v[7].location == 33
