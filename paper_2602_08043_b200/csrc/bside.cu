@@ -170,6 +170,30 @@ __device__ __forceinline__ void bs_load(const typename Elem<F>::T* __restrict__ 
     }
 }
 
+// 16-byte variant for 4-byte words (16-bit pairs, FP32) when the row stride
+// is a multiple of 16 bytes and B is 16-byte aligned: lane l holds words
+// 4 (l % 8) .. + 3 of row 4 i + l / 8 (8 lanes per 128-byte row segment);
+// stored into the staged tile with 16-byte stores.
+template <int F>
+__device__ __forceinline__ void bs_load_v4(const typename Elem<F>::T* __restrict__ base, int64_t N, int rows, int64_t c,
+                                           uint4 (&v)[8]) {
+    constexpr int kPerWord = BsT<F>::k16 ? 2 : 1;  // elements per 32-bit word
+    const int lane = threadIdx.x & 31;
+    const int64_t col = c + int64_t(4 * kPerWord) * (lane & 7);
+    const int rs = lane >> 3;
+    const typename Elem<F>::T* p = base + int64_t(rs) * N + col;
+#pragma unroll
+    for (int i = 0; i < 8; ++i)
+        v[i] = (4 * i + rs < rows && col < N) ? __ldcs(reinterpret_cast<const uint4*>(p + int64_t(4 * i) * N))
+                                              : make_uint4(0u, 0u, 0u, 0u);
+}
+__device__ __forceinline__ void bs_stage_v4(uint32_t* tile, int stride, const uint4 (&v)[8]) {
+    const int lane = threadIdx.x & 31;
+#pragma unroll
+    for (int i = 0; i < 8; ++i)
+        *reinterpret_cast<uint4*>(tile + (4 * i + (lane >> 3)) * stride + 4 * (lane & 7)) = v[i];
+}
+
 // Per-lane accumulators of one (row, block).
 template <int F>
 struct BsAcc {
@@ -270,7 +294,7 @@ __device__ __forceinline__ void bs_store(const BsJob<F>& j, const BsAcc<F>& a, i
 }
 
 // Process the row group's block b (lane = row).
-template <int F>
+template <int F, bool kVec>
 __device__ __forceinline__ void bs_block(const BsJob<F>& j, typename BsT<F>::Word* tile, int64_t rg, int b) {
     using Word = typename BsT<F>::Word;
     using V = typename BsT<F>::V;
@@ -286,17 +310,26 @@ __device__ __forceinline__ void bs_block(const BsJob<F>& j, typename BsT<F>::Wor
     const typename Elem<F>::T* base = j.B + r0 * N;
 
     BsAcc<F> a;
-    Word v[32];
-    bs_load<F>(base, N, rows, c0, v);
+    Word v[kVec ? 1 : 32];
+    uint4 v4[kVec ? 8 : 1];
+    if constexpr (kVec) bs_load_v4<F>(base, N, rows, c0, v4);
+    else bs_load<F>(base, N, rows, c0, v);
     __syncwarp();
+    if constexpr (kVec) {
+        bs_stage_v4(reinterpret_cast<uint32_t*>(tile), kStride, v4);
+    } else {
 #pragma unroll
-    for (int rr = 0; rr < 32; ++rr) tile[rr * kStride + lane] = v[rr];
+        for (int rr = 0; rr < 32; ++rr) tile[rr * kStride + lane] = v[rr];
+    }
     __syncwarp();
     const Word* trow = tile + lane * kStride;
     for (int q = 0; q < nsub; ++q) {
         const int64_t cq = c0 + int64_t(q) * kCols;
         // the next sub-tile's loads are in flight while this one is processed
-        if (q + 1 < nsub) bs_load<F>(base, N, rows, cq + kCols, v);
+        if (q + 1 < nsub) {
+            if constexpr (kVec) bs_load_v4<F>(base, N, rows, cq + kCols, v4);
+            else bs_load<F>(base, N, rows, cq + kCols, v);
+        }
         const int cnt = int(c0 + bw - cq < kCols ? c0 + bw - cq : kCols);  // warp-uniform
         const float w0 = float(cq + 1);  // weight j + 1 of the sub-tile's first element (exact: N <= 2^24)
         if constexpr (BsT<F>::k16) {
@@ -345,8 +378,12 @@ __device__ __forceinline__ void bs_block(const BsJob<F>& j, typename BsT<F>::Wor
         }
         if (q + 1 < nsub) {
             __syncwarp();
+            if constexpr (kVec) {
+                bs_stage_v4(reinterpret_cast<uint32_t*>(tile), kStride, v4);
+            } else {
 #pragma unroll
-            for (int rr = 0; rr < 32; ++rr) tile[rr * kStride + lane] = v[rr];
+                for (int rr = 0; rr < 32; ++rr) tile[rr * kStride + lane] = v[rr];
+            }
             __syncwarp();
         }
     }
@@ -578,7 +615,7 @@ constexpr size_t bs_smem() {
     return size_t(kBsWarps) * 32 * BsT<F>::kStride * sizeof(typename BsT<F>::Word);
 }
 
-template <int F>
+template <int F, bool kVec>
 __global__ void __launch_bounds__(kBsThreads, F == VABFT_FP64 ? 1 : 2) bside_kernel(const __grid_constant__ BsJob<F> j) {
     using Word = typename BsT<F>::Word;
     constexpr int kStride = BsT<F>::kStride;
@@ -616,7 +653,7 @@ __global__ void __launch_bounds__(kBsThreads, F == VABFT_FP64 ? 1 : 2) bside_ker
     for (int64_t t = tw; t < tasks; t += nt) {
         const int64_t rg = t / nb;
         const int b = int(t - rg * nb);
-        bs_block<F>(j, tile, rg, b);
+        bs_block<F, kVec>(j, tile, rg, b);
         // arrival: every lane's partial stores before lane 0's release RMW;
         // the last arriver reads the partials through L2 after a fence
         __syncwarp();
@@ -680,12 +717,16 @@ void launch_bs(int64_t K, int64_t N, const void* B, int quantize_br, BsideBuffer
     j.debug = dbg;
     j.grp_epoch = buf.groups + 2 * j.ngroups;
     constexpr size_t smem = bs_smem<F>();
-    ensure_smem_attr(reinterpret_cast<const void*>(bside_kernel<F>), int(smem));
-    const int per_sm = cached_occupancy(reinterpret_cast<const void*>(bside_kernel<F>), kBsThreads, int(smem));
+    // 16-byte loads when rows are 16-byte multiples and B is aligned (4-byte words only)
+    const bool vec = F != VABFT_FP64 && (N * int64_t(sizeof(typename Elem<F>::T))) % 16 == 0 &&
+                     reinterpret_cast<uintptr_t>(B) % 16 == 0;
+    auto kern = vec ? bside_kernel<F, F != VABFT_FP64> : bside_kernel<F, false>;
+    ensure_smem_attr(reinterpret_cast<const void*>(kern), int(smem));
+    const int per_sm = cached_occupancy(reinterpret_cast<const void*>(kern), kBsThreads, int(smem));
     const int64_t tasks = int64_t(j.ngroups) * j.nb;
     const int64_t want = (tasks + kBsWarps - 1) / kBsWarps + 1;
     const int grid = int(std::min<int64_t>(int64_t(sm_count()) * std::max(per_sm, 1), want));
-    bside_kernel<F><<<grid, kBsThreads, smem, s>>>(j);
+    kern<<<grid, kBsThreads, smem, s>>>(j);
     check_cuda(cudaGetLastError(), "bside launch");
 }
 

@@ -298,6 +298,28 @@ __device__ __forceinline__ void ap_load(const typename Elem<F>::T* __restrict__ 
     for (int rr = 0; rr < 32; ++rr) v[rr] = (rr < rows && col < K) ? __ldcs(p + rr * K) : T(0);
 }
 
+// FP32 with K % 4 == 0 and A 16-byte aligned: 16-byte loads, lane l holding
+// row 4 i + l / 8, columns c + 4 (l % 8) .. + 3 of the sub-tile (8 lanes per
+// 128-byte row segment), and 16-byte stores into the staged tile.
+__device__ __forceinline__ void ap_load_v4(const float* __restrict__ A, int64_t M, int64_t K, int64_t r0, int64_t c,
+                                           float4 (&v)[8]) {
+    const int lane = threadIdx.x & 31;
+    const int64_t col = c + 4 * (lane & 7);
+    const int rs = lane >> 3;
+    const float* p = A + (r0 + rs) * K + col;
+    const int rows = int(M - r0 < 32 ? M - r0 : 32);
+#pragma unroll
+    for (int i = 0; i < 8; ++i)
+        v[i] = (4 * i + rs < rows && col < K) ? __ldcs(reinterpret_cast<const float4*>(p + int64_t(4 * i) * K))
+                                              : make_float4(0.f, 0.f, 0.f, 0.f);
+}
+__device__ __forceinline__ void ap_stage_v4(float* tile, const float4 (&v)[8]) {
+    const int lane = threadIdx.x & 31;
+#pragma unroll
+    for (int i = 0; i < 8; ++i)
+        *reinterpret_cast<float4*>(tile + (4 * i + (lane >> 3)) * kApLd + 4 * (lane & 7)) = v[i];
+}
+
 // One element of the FP32 A pass: checksum products (no FMA), the plain FP64
 // sub-tile sum, sum|x|, max / min and the exactness-guard trackers.
 struct ApF32 {
@@ -475,7 +497,7 @@ __device__ __forceinline__ void ap_finish_group(const ApJob<W>& j, int64_t rg) {
     wide_verdicts<F>(a, i, valid, r1, r2, mean_i, vb_i, c1, c2);
 }
 
-template <int F, class W>
+template <int F, class W, bool kVec>
 __global__ void __launch_bounds__(32 * kApWarps, F == VABFT_FP64 ? 1 : 2)
     wide_apart_kernel(const typename Elem<F>::T* __restrict__ A, const __grid_constant__ ApJob<W> j) {
     using T = typename Elem<F>::T;
@@ -491,8 +513,10 @@ __global__ void __launch_bounds__(32 * kApWarps, F == VABFT_FP64 ? 1 : 2)
         const int64_t r0 = rg * 32, c0 = b * 128;
         const int bw = int(K - c0 < 128 ? K - c0 : 128);
         const int nsub = (bw + 31) / 32;
-        T v[32];
-        ap_load<F>(A, M, K, r0, c0, v);
+        T v[kVec ? 1 : 32];
+        float4 v4[kVec ? 8 : 1];
+        if constexpr (kVec) ap_load_v4(reinterpret_cast<const float*>(A), M, K, r0, c0, v4);
+        else ap_load<F>(A, M, K, r0, c0, v);
         __syncwarp();
 #pragma unroll
         for (int q = 0; q < 4; ++q) {
@@ -500,8 +524,12 @@ __global__ void __launch_bounds__(32 * kApWarps, F == VABFT_FP64 ? 1 : 2)
             wts[jj] = jj < bw ? W(j.br1[c0 + jj]) : W(0);
             wts[128 + jj] = jj < bw ? W(j.br2[c0 + jj]) : W(0);
         }
+        if constexpr (kVec) {
+            ap_stage_v4(reinterpret_cast<float*>(tile), v4);
+        } else {
 #pragma unroll
-        for (int rr = 0; rr < 32; ++rr) tile[rr * kApLd + lane] = v[rr];
+            for (int rr = 0; rr < 32; ++rr) tile[rr * kApLd + lane] = v[rr];
+        }
         __syncwarp();
         W p1 = W(0), p2 = W(0);
         double s = 0.0, c = 0.0;
@@ -509,7 +537,10 @@ __global__ void __launch_bounds__(32 * kApWarps, F == VABFT_FP64 ? 1 : 2)
         const T* trow = tile + lane * kApLd;
         for (int q = 0; q < nsub; ++q) {
             const int64_t cq = c0 + int64_t(q) * 32;
-            if (q + 1 < nsub) ap_load<F>(A, M, K, r0, cq + 32, v);  // in flight during this sub-tile
+            if (q + 1 < nsub) {  // in flight during this sub-tile
+                if constexpr (kVec) ap_load_v4(reinterpret_cast<const float*>(A), M, K, r0, cq + 32, v4);
+                else ap_load<F>(A, M, K, r0, cq + 32, v);
+            }
             const int cnt = int(c0 + bw - cq < 32 ? c0 + bw - cq : 32);  // warp-uniform
             const W* w1 = wts + q * 32;
             const W* w2 = wts + 128 + q * 32;
@@ -580,8 +611,12 @@ __global__ void __launch_bounds__(32 * kApWarps, F == VABFT_FP64 ? 1 : 2)
             }
             if (q + 1 < nsub) {
                 __syncwarp();
+                if constexpr (kVec) {
+                    ap_stage_v4(reinterpret_cast<float*>(tile), v4);
+                } else {
 #pragma unroll
-                for (int rr = 0; rr < 32; ++rr) tile[rr * kApLd + lane] = v[rr];
+                    for (int rr = 0; rr < 32; ++rr) tile[rr * kApLd + lane] = v[rr];
+                }
                 __syncwarp();
             }
         }
@@ -691,7 +726,8 @@ void launch_wide_aside(const WideTail& t, const double* br1, const double* br2, 
         j.mn = mn;
         j.cr1 = cr1;
         j.cr2 = cr2;
-        auto kern = wide_apart_kernel<F, W>;
+        const bool vec = F == VABFT_FP32 && t.K % 4 == 0 && reinterpret_cast<uintptr_t>(t.A) % 16 == 0;
+        auto kern = vec ? wide_apart_kernel<F, W, F == VABFT_FP32> : wide_apart_kernel<F, W, false>;
         constexpr size_t smem = ap_smem<F>();
         ensure_smem_attr(reinterpret_cast<const void*>(kern), int(smem));
         const int per_sm = cached_occupancy(reinterpret_cast<const void*>(kern), 32 * kApWarps, int(smem));
