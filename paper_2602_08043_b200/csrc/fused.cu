@@ -317,8 +317,10 @@ void wide_fused(const vabft_fused_opts* o, vabft_bside* h, int64_t m, const void
     t.correct = o->correct;
     t.A = A;
     t.qfmt = o->mode == VABFT_OFFLINE ? h->fmt : -1;
-    launch_wide_aside(t, h->brd, h->brd + k, ws.cpart, ws.gcnt, !global_y, ws.mean, ws.vb, ws.mx, ws.mn, ws.cr1,
-                      ws.cr2, s);
+    const bool f32 = h->fmt == VABFT_FP32;  // B r in the working type: the pass's float copies for FP32
+    launch_wide_aside(t, f32 ? static_cast<const void*>(h->buf.br1) : h->brd,
+                      f32 ? static_cast<const void*>(h->buf.br2) : h->brd + k, ws.cpart, ws.gcnt, !global_y, ws.mean,
+                      ws.vb, ws.mx, ws.mn, ws.cr1, ws.cr2, s);
     if (!global_y) return;
     check_cuda(cudaMemsetAsync(ws.max_abs_a, 0, sizeof(double), s), "memset");
     launch_max_abs_rows(m, ws.mx, ws.mn, ws.max_abs_a, s);

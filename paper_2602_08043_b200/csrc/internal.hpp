@@ -166,12 +166,13 @@ struct WideTail {
 };
 void launch_wide_tail(const WideTail& t, cudaStream_t stream);
 // A side (wide.cu): one pass over t.A producing the row statistics and the
-// blocked:128 row checksums A (B r); apart is scratch for the per-(128-column
+// blocked:128 row checksums A (B r) (br1 / br2 in the working type: float
+// for FP32, double for FP64); apart is scratch for the per-(128-column
 // block, row) partials (7 x ceil(K/128) x ld doubles), gcnt ceil(M/32)
 // zero-initialised self-resetting counters. finish: the verdicts of t in the
 // same kernel; else mean / vb / mx / mn / cr1 / cr2 are staged for
 // launch_wide_tail (A-ABFT computed y).
-void launch_wide_aside(const WideTail& t, const double* br1, const double* br2, void* apart, unsigned* gcnt,
+void launch_wide_aside(const WideTail& t, const void* br1, const void* br2, void* apart, unsigned* gcnt,
                        bool finish, double* mean, double* vb, double* mx, double* mn, double* cr1, double* cr2,
                        cudaStream_t stream);
 void launch_max_abs_rows(int64_t m, const double* mx, const double* mn, double* out, cudaStream_t stream);

@@ -271,7 +271,7 @@ __host__ __device__ inline APart<W> apart_view(void* base, int64_t nb, int64_t l
 template <class W>
 struct ApJob {
     WideTail t;              // verdict arguments (t.apart / t.mean ... unused here)
-    const double *br1, *br2;
+    const W *br1, *br2;      // B r1 / B r2 in the working type (FP32: the handle's float copies)
     APart<W> part;
     unsigned* gcnt;          // [ceil(M/32)] block arrivals per row group (self-resetting)
     int finish;              // 1: verdicts in this kernel; 0: stage the row statistics
@@ -705,7 +705,7 @@ void launch_wide_tail(const WideTail& t, cudaStream_t stream) {
     check_cuda(cudaGetLastError(), "wide tail launch");
 }
 
-void launch_wide_aside(const WideTail& t, const double* br1, const double* br2, void* apart, unsigned* gcnt,
+void launch_wide_aside(const WideTail& t, const void* br1, const void* br2, void* apart, unsigned* gcnt,
                        bool finish, double* mean, double* vb, double* mx, double* mn, double* cr1, double* cr2,
                        cudaStream_t stream) {
     const int64_t nb = (t.K + 127) / 128;
@@ -715,8 +715,8 @@ void launch_wide_aside(const WideTail& t, const double* br1, const double* br2, 
         constexpr int F = sizeof(T) == 8 ? VABFT_FP64 : VABFT_FP32;
         ApJob<W> j;
         j.t = t;
-        j.br1 = br1;
-        j.br2 = br2;
+        j.br1 = static_cast<const W*>(br1);
+        j.br2 = static_cast<const W*>(br2);
         j.part = apart_view<W>(apart, nb, t.ld);
         j.gcnt = gcnt;
         j.finish = finish ? 1 : 0;
