@@ -234,6 +234,10 @@ typedef struct vabft_bside* vabft_bside_t;
  * checksum.cpp:110-115) with the checksum precision of `mode`. */
 vabft_status vabft_bside_create(int32_t format, int32_t mode, int64_t k, int64_t n, const void* B,
                                 vabft_bside_t* out, void* stream);
+/* [v2] The same for a weight stored with row stride ldb >= n elements (0 = n;
+ * BF16 / FP16, a multiple of 8), e.g. a column slice of a wider matrix. */
+vabft_status vabft_bside_create_ld(int32_t format, int32_t mode, int64_t k, int64_t n, const void* B,
+                                   int64_t ldb, vabft_bside_t* out, void* stream);
 vabft_status vabft_bside_update(vabft_bside_t h, const void* B, void* stream);
 vabft_status vabft_bside_destroy(vabft_bside_t h);
 
@@ -301,6 +305,12 @@ typedef struct vabft_fused_opts {
      * memory at a reused address) sets workspace_fresh = 1. */
     int32_t workspace_fresh;
     int32_t reserved_v2;
+    /* [v2] Row strides in elements of A (M x K) and C (M x N); 0 = dense.
+     * BF16 / FP16 handles: multiples of 8 (16-byte rows); FP32 / FP64: dense
+     * only. With vabft_bside_create_ld a slice B[:, n0:n1] of a wider weight
+     * and the matching C[:, n0:n1] run without copies (SURVEY §8(e) N-split). */
+    int64_t lda;
+    int64_t ldc;
 } vabft_fused_opts;
 
 /* Workspace bytes for vabft_fused_gemm at this shape. */

@@ -64,7 +64,8 @@ class FusedOpts(C.Structure):
                 ("fault_records", C.c_void_p), ("stages", C.c_int32), ("fault_target", C.c_int32),
                 ("n_operand_faults", C.c_int32), ("correct", C.c_int32), ("operand_faults", C.c_void_p),
                 ("operand_fault_records", C.c_void_p), ("cta_mode", C.c_int32), ("tf32_passes", C.c_int32),
-                ("accum_out", C.c_void_p), ("workspace_fresh", C.c_int32), ("reserved_v2", C.c_int32)]
+                ("accum_out", C.c_void_p), ("workspace_fresh", C.c_int32), ("reserved_v2", C.c_int32),
+                ("lda", C.c_int64), ("ldc", C.c_int64)]
 
 
 _st = C.c_int
@@ -97,6 +98,7 @@ _SIGS = {
     "vabft_verify": (_st, [C.POINTER(Precision), _i32, _i64, _i64, _vp, _vp, _vp, _vp, _d, Verdicts, _vp, _vp]),
     "vabft_inject": (_st, [_i32, _i64, _i64, _vp, C.POINTER(Fault), _i64, C.POINTER(FaultRecord), _vp]),
     "vabft_bside_create": (_st, [_i32, _i32, _i64, _i64, _vp, C.POINTER(_vp), _vp]),
+    "vabft_bside_create_ld": (_st, [_i32, _i32, _i64, _i64, _vp, _i64, C.POINTER(_vp), _vp]),
     "vabft_bside_update": (_st, [_vp, _vp, _vp]),
     "vabft_bside_destroy": (_st, [_vp]),
     "vabft_fused_workspace_size": (_st, [_i64, _i64, _i64, C.POINTER(C.c_size_t)]),

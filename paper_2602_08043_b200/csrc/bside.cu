@@ -112,6 +112,7 @@ template <int F>
 struct BsJob {
     const typename Elem<F>::T* B;
     int64_t K, N, Kp;
+    int64_t ldb;  // row stride of B (elements)
     int nb, ngroups, quantize_br;
     BsideBuffers buf;
     BsPart<F> part;
@@ -129,16 +130,16 @@ __device__ __forceinline__ double bs_add(double a, double b) { return __dadd_rn(
 // starting at row pointer `base` (row stride N elements) into registers: lane l
 // holds word l of every row. Rows at or past `rows` read as zero.
 template <int F>
-__device__ __forceinline__ void bs_load(const typename Elem<F>::T* __restrict__ base, int64_t N, int rows, int64_t c,
-                                        typename BsT<F>::Word (&v)[32]) {
+__device__ __forceinline__ void bs_load(const typename Elem<F>::T* __restrict__ base, int64_t N, int64_t ld, int rows,
+                                        int64_t c, typename BsT<F>::Word (&v)[32]) {
     using Word = typename BsT<F>::Word;
     const int lane = threadIdx.x & 31;
     if constexpr (BsT<F>::k16) {
         const int64_t col = c + 2 * lane;
         const bool in = col < N;
-        if ((N & 1) == 0) {  // rows 4-byte aligned: one 32-bit word per lane and row
+        if ((ld & 1) == 0 && (N & 1) == 0) {  // rows 4-byte aligned: one 32-bit word per lane and row
             const unsigned int* p = reinterpret_cast<const unsigned int*>(base + col);
-            const int64_t st = N >> 1;
+            const int64_t st = ld >> 1;
 #pragma unroll
             for (int rr = 0; rr < 32; ++rr) v[rr] = (rr < rows && in) ? __ldcs(p + rr * st) : 0u;
         } else {  // odd N
@@ -148,8 +149,8 @@ __device__ __forceinline__ void bs_load(const typename Elem<F>::T* __restrict__ 
             for (int rr = 0; rr < 32; ++rr) {
                 uint32_t w = 0;
                 if (rr < rows && in) {
-                    w = __ldcs(p + rr * N);
-                    if (in2) w |= uint32_t(__ldcs(p + rr * N + 1)) << 16;
+                    w = __ldcs(p + rr * ld);
+                    if (in2) w |= uint32_t(__ldcs(p + rr * ld + 1)) << 16;
                 }
                 v[rr] = w;
             }
@@ -162,8 +163,8 @@ __device__ __forceinline__ void bs_load(const typename Elem<F>::T* __restrict__ 
         for (int rr = 0; rr < 32; ++rr) {
             Word w = Word(0);
             if (rr < rows && in) {
-                if constexpr (F == VABFT_FP32) w = __float_as_uint(__ldcs(p + rr * N));
-                else w = __ldcs(p + rr * N);
+                if constexpr (F == VABFT_FP32) w = __float_as_uint(__ldcs(p + rr * ld));
+                else w = __ldcs(p + rr * ld);
             }
             v[rr] = w;
         }
@@ -175,16 +176,16 @@ __device__ __forceinline__ void bs_load(const typename Elem<F>::T* __restrict__ 
 // 4 (l % 8) .. + 3 of row 4 i + l / 8 (8 lanes per 128-byte row segment);
 // stored into the staged tile with 16-byte stores.
 template <int F>
-__device__ __forceinline__ void bs_load_v4(const typename Elem<F>::T* __restrict__ base, int64_t N, int rows, int64_t c,
-                                           uint4 (&v)[8]) {
+__device__ __forceinline__ void bs_load_v4(const typename Elem<F>::T* __restrict__ base, int64_t N, int64_t ld, int rows,
+                                           int64_t c, uint4 (&v)[8]) {
     constexpr int kPerWord = BsT<F>::k16 ? 2 : 1;  // elements per 32-bit word
     const int lane = threadIdx.x & 31;
     const int64_t col = c + int64_t(4 * kPerWord) * (lane & 7);
     const int rs = lane >> 3;
-    const typename Elem<F>::T* p = base + int64_t(rs) * N + col;
+    const typename Elem<F>::T* p = base + int64_t(rs) * ld + col;
 #pragma unroll
     for (int i = 0; i < 8; ++i)
-        v[i] = (4 * i + rs < rows && col < N) ? __ldcs(reinterpret_cast<const uint4*>(p + int64_t(4 * i) * N))
+        v[i] = (4 * i + rs < rows && col < N) ? __ldcs(reinterpret_cast<const uint4*>(p + int64_t(4 * i) * ld))
                                               : make_uint4(0u, 0u, 0u, 0u);
 }
 __device__ __forceinline__ void bs_stage_v4(uint32_t* tile, int stride, const uint4 (&v)[8]) {
@@ -307,13 +308,14 @@ __device__ __forceinline__ void bs_block(const BsJob<F>& j, typename BsT<F>::Wor
     const int64_t c0 = int64_t(b) * 128;
     const int bw = int(N - c0 < 128 ? N - c0 : 128);
     const int nsub = (bw + kCols - 1) / kCols;
-    const typename Elem<F>::T* base = j.B + r0 * N;
+    const int64_t ld = j.ldb;
+    const typename Elem<F>::T* base = j.B + r0 * ld;
 
     BsAcc<F> a;
     Word v[kVec ? 1 : 32];
     uint4 v4[kVec ? 8 : 1];
-    if constexpr (kVec) bs_load_v4<F>(base, N, rows, c0, v4);
-    else bs_load<F>(base, N, rows, c0, v);
+    if constexpr (kVec) bs_load_v4<F>(base, N, ld, rows, c0, v4);
+    else bs_load<F>(base, N, ld, rows, c0, v);
     __syncwarp();
     if constexpr (kVec) {
         bs_stage_v4(reinterpret_cast<uint32_t*>(tile), kStride, v4);
@@ -327,8 +329,8 @@ __device__ __forceinline__ void bs_block(const BsJob<F>& j, typename BsT<F>::Wor
         const int64_t cq = c0 + int64_t(q) * kCols;
         // the next sub-tile's loads are in flight while this one is processed
         if (q + 1 < nsub) {
-            if constexpr (kVec) bs_load_v4<F>(base, N, rows, cq + kCols, v4);
-            else bs_load<F>(base, N, rows, cq + kCols, v);
+            if constexpr (kVec) bs_load_v4<F>(base, N, ld, rows, cq + kCols, v4);
+            else bs_load<F>(base, N, ld, rows, cq + kCols, v);
         }
         const int cnt = int(c0 + bw - cq < kCols ? c0 + bw - cq : kCols);  // warp-uniform
         const float w0 = float(cq + 1);  // weight j + 1 of the sub-tile's first element (exact: N <= 2^24)
@@ -452,7 +454,7 @@ __device__ __forceinline__ void bs_combine(const BsJob<F>& j, int64_t rg, unsign
         const int l = __ffs(slow) - 1;
         slow &= slow - 1;
         double pl;
-        const double hs = warp_neumaier_row<F>(j.B + (rg * 32 + l) * j.N, j.N, BsT<F>::k16 ? &pl : nullptr);
+        const double hs = warp_neumaier_row<F>(j.B + (rg * 32 + l) * j.ldb, j.N, BsT<F>::k16 ? &pl : nullptr);
         if (lane == l) {
             n = Neu{};
             n.s = hs;
@@ -674,13 +676,13 @@ __global__ void __launch_bounds__(kBsThreads, F == VABFT_FP64 ? 1 : 2) bside_ker
 // with an order-free atomic max.
 template <int F>
 __global__ void __launch_bounds__(128) bside_rowsum_kernel(const typename Elem<F>::T* __restrict__ B, int64_t K,
-                                                           int64_t N, double* rowsum_abs, double* summary) {
+                                                           int64_t N, int64_t ld, double* rowsum_abs, double* summary) {
     using T = typename Elem<F>::T;
     __shared__ T stage[4][256];
     const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int64_t k = int64_t(blockIdx.x) * 4 + w;
     if (k >= K) return;
-    const T* row = B + k * N;
+    const T* row = B + k * ld;
     double s = 0.0;
     for (int64_t j0 = 0; j0 < N; j0 += 256) {
         const int cnt = int(N - j0 < 256 ? N - j0 : 256);
@@ -697,8 +699,9 @@ __global__ void __launch_bounds__(128) bside_rowsum_kernel(const typename Elem<F
 }
 
 template <int F>
-void launch_bs(int64_t K, int64_t N, const void* B, int quantize_br, BsideBuffers& buf, cudaStream_t s) {
+void launch_bs(int64_t K, int64_t N, int64_t ld, const void* B, int quantize_br, BsideBuffers& buf, cudaStream_t s) {
     BsJob<F> j;
+    j.ldb = ld;
     j.B = static_cast<const typename Elem<F>::T*>(B);
     j.K = K;
     j.N = N;
@@ -718,7 +721,8 @@ void launch_bs(int64_t K, int64_t N, const void* B, int quantize_br, BsideBuffer
     j.grp_epoch = buf.groups + 2 * j.ngroups;
     constexpr size_t smem = bs_smem<F>();
     // 16-byte loads when rows are 16-byte multiples and B is aligned (4-byte words only)
-    const bool vec = F != VABFT_FP64 && (N * int64_t(sizeof(typename Elem<F>::T))) % 16 == 0 &&
+    const bool vec = F != VABFT_FP64 && (ld * int64_t(sizeof(typename Elem<F>::T))) % 16 == 0 &&
+                     (N * int64_t(sizeof(typename Elem<F>::T))) % 16 == 0 &&
                      reinterpret_cast<uintptr_t>(B) % 16 == 0;
     auto kern = vec ? bside_kernel<F, F != VABFT_FP64> : bside_kernel<F, false>;
     ensure_smem_attr(reinterpret_cast<const void*>(kern), int(smem));
@@ -747,26 +751,30 @@ size_t bside_group_words(int64_t K) { return size_t(2 * ((K + 31) / 32) + 2); }
 int64_t br_storage_floats(int64_t K) { return ((K + 127) / 128) * 128; }
 
 void launch_bside(int fmt, int64_t K, int64_t N, const void* B, int quantize_br, BsideBuffers& buf,
-                  cudaStream_t s) {
+                  cudaStream_t s, int64_t ld) {
+    if (ld == 0) ld = N;
+    if (ld < N) fail(VABFT_INVALID_ARGUMENT, "launch_bside: leading dimension below N");
     if (!buf.work || !buf.groups) fail(VABFT_LOGIC_ERROR, "launch_bside: workspace missing");
     if (N > (int64_t(1) << 24)) fail(VABFT_INVALID_ARGUMENT, "ChecksumVectors: weights exceed exact range");
     switch (fmt) {
-        case VABFT_BF16: launch_bs<VABFT_BF16>(K, N, B, quantize_br, buf, s); break;
-        case VABFT_FP16: launch_bs<VABFT_FP16>(K, N, B, quantize_br, buf, s); break;
-        case VABFT_FP32: launch_bs<VABFT_FP32>(K, N, B, 0, buf, s); break;
-        case VABFT_FP64: launch_bs<VABFT_FP64>(K, N, B, 0, buf, s); break;
+        case VABFT_BF16: launch_bs<VABFT_BF16>(K, N, ld, B, quantize_br, buf, s); break;
+        case VABFT_FP16: launch_bs<VABFT_FP16>(K, N, ld, B, quantize_br, buf, s); break;
+        case VABFT_FP32: launch_bs<VABFT_FP32>(K, N, ld, B, 0, buf, s); break;
+        case VABFT_FP64: launch_bs<VABFT_FP64>(K, N, ld, B, 0, buf, s); break;
         default: fail(VABFT_INVALID_ARGUMENT, "bad format");
     }
 }
 
-void launch_bside_rowsum(int fmt, int64_t K, int64_t N, const void* B, BsideBuffers& buf, cudaStream_t s) {
+void launch_bside_rowsum(int fmt, int64_t K, int64_t N, const void* B, BsideBuffers& buf, cudaStream_t s,
+                         int64_t ld) {
+    if (ld == 0) ld = N;
     check_cuda(cudaMemsetAsync(buf.summary + 3, 0, sizeof(double), s), "memset");
     const unsigned grid = unsigned((K + 3) / 4);
     switch (fmt) {
-        case VABFT_BF16: bside_rowsum_kernel<VABFT_BF16><<<grid, 128, 0, s>>>(static_cast<const uint16_t*>(B), K, N, buf.rowsum_abs, buf.summary); break;
-        case VABFT_FP16: bside_rowsum_kernel<VABFT_FP16><<<grid, 128, 0, s>>>(static_cast<const uint16_t*>(B), K, N, buf.rowsum_abs, buf.summary); break;
-        case VABFT_FP32: bside_rowsum_kernel<VABFT_FP32><<<grid, 128, 0, s>>>(static_cast<const float*>(B), K, N, buf.rowsum_abs, buf.summary); break;
-        case VABFT_FP64: bside_rowsum_kernel<VABFT_FP64><<<grid, 128, 0, s>>>(static_cast<const double*>(B), K, N, buf.rowsum_abs, buf.summary); break;
+        case VABFT_BF16: bside_rowsum_kernel<VABFT_BF16><<<grid, 128, 0, s>>>(static_cast<const uint16_t*>(B), K, N, ld, buf.rowsum_abs, buf.summary); break;
+        case VABFT_FP16: bside_rowsum_kernel<VABFT_FP16><<<grid, 128, 0, s>>>(static_cast<const uint16_t*>(B), K, N, ld, buf.rowsum_abs, buf.summary); break;
+        case VABFT_FP32: bside_rowsum_kernel<VABFT_FP32><<<grid, 128, 0, s>>>(static_cast<const float*>(B), K, N, ld, buf.rowsum_abs, buf.summary); break;
+        case VABFT_FP64: bside_rowsum_kernel<VABFT_FP64><<<grid, 128, 0, s>>>(static_cast<const double*>(B), K, N, ld, buf.rowsum_abs, buf.summary); break;
         default: fail(VABFT_INVALID_ARGUMENT, "bad format");
     }
     check_cuda(cudaGetLastError(), "bside rowsum launch");

@@ -40,6 +40,7 @@ struct vabft_bside {
     int mode;
     int b_kmajor;
     int64_t k, n;
+    int64_t ldb = 0;  // row stride of B (elements): n unless created by vabft_bside_create_ld
     const void* B;  // not owned
     vabft_dev::BsideBuffers buf;
     void* storage;  // one cudaMalloc holding every buffer
@@ -283,7 +284,7 @@ void wide_fused(const vabft_fused_opts* o, vabft_bside* h, int64_t m, const void
     // needs the global max|A| first: stage the statistics, then a tail kernel
     const bool global_y = o->threshold_method == 2;
     if (global_y && !h->rowsum_ready) {  // max_k |sum_j B[k][j]| on first use (bside.cu)
-        launch_bside_rowsum(h->fmt, h->k, h->n, h->B, h->buf, s);
+        launch_bside_rowsum(h->fmt, h->k, h->n, h->B, h->buf, s, h->ldb);
         h->rowsum_ready = true;
     }
     if (claim_workspace(workspace, h, ws.bytes, o->workspace_fresh != 0))
@@ -334,7 +335,16 @@ using namespace vabft_dev;
 
 extern "C" vabft_status vabft_bside_create(int32_t format, int32_t mode, int64_t k, int64_t n,
                                            const void* B, vabft_bside_t* out, void* stream) {
+    return vabft_bside_create_ld(format, mode, k, n, B, 0, out, stream);
+}
+
+extern "C" vabft_status vabft_bside_create_ld(int32_t format, int32_t mode, int64_t k, int64_t n, const void* B,
+                                              int64_t ldb, vabft_bside_t* out, void* stream) {
     return guarded([&] {
+        if (ldb == 0) ldb = n;
+        if (ldb < n) fail(VABFT_INVALID_ARGUMENT, "vabft_bside_create_ld: ldb < n");
+        if (ldb != n && (format == VABFT_FP32 || format == VABFT_FP64))
+            fail(VABFT_UNSUPPORTED, "vabft_bside_create_ld: strided weights are BF16 / FP16 only");
         if (!out) fail(VABFT_INVALID_ARGUMENT, "vabft_bside_create: null handle pointer");
         if (format < VABFT_BF16 || format > VABFT_FP64) fail(VABFT_INVALID_ARGUMENT, "bad format");
         if (mode != VABFT_OFFLINE && mode != VABFT_ONLINE) fail(VABFT_INVALID_ARGUMENT, "bad mode");
@@ -351,6 +361,7 @@ extern "C" vabft_status vabft_bside_create(int32_t format, int32_t mode, int64_t
         h->b_kmajor = 0;
         h->k = k;
         h->n = n;
+        h->ldb = ldb;
         h->B = B;
         const size_t K = size_t(k);
         const size_t KB = size_t(br_storage_floats(k));
@@ -381,7 +392,7 @@ extern "C" vabft_status vabft_bside_create(int32_t format, int32_t mode, int64_t
             }
         }
         if (B) {
-            launch_bside(format, k, n, B, mode == VABFT_OFFLINE ? 1 : 0, h->buf, as_stream(stream));
+            launch_bside(format, k, n, B, mode == VABFT_OFFLINE ? 1 : 0, h->buf, as_stream(stream), ldb);
             if (format == VABFT_FP32) wide_split(h, as_stream(stream));
         }
         *out = hp.release();
@@ -393,7 +404,7 @@ extern "C" vabft_status vabft_bside_update(vabft_bside_t h, const void* B, void*
         if (!h || !B) fail(VABFT_INVALID_ARGUMENT, "vabft_bside_update: null argument");
         h->B = B;
         h->rowsum_ready = false;
-        launch_bside(h->fmt, h->k, h->n, B, h->mode == VABFT_OFFLINE ? 1 : 0, h->buf, as_stream(stream));
+        launch_bside(h->fmt, h->k, h->n, B, h->mode == VABFT_OFFLINE ? 1 : 0, h->buf, as_stream(stream), h->ldb);
         if (h->fmt == VABFT_FP32) wide_split(h, as_stream(stream));
     });
 }
@@ -429,6 +440,10 @@ extern "C" vabft_status vabft_fused_gemm(const vabft_fused_opts* o, vabft_bside_
         if (m > (int64_t(1) << 24)) fail(VABFT_INVALID_ARGUMENT, "ChecksumVectors: weights exceed exact range");
         const int64_t n = h->n, k = h->k;
         if (k % 8 != 0 || n % 8 != 0) fail(VABFT_UNSUPPORTED, "vabft_fused_gemm: K and N must be multiples of 8");
+        const int64_t lda = o->lda ? o->lda : k, ldc = o->ldc ? o->ldc : n;
+        if (lda < k || ldc < n) fail(VABFT_INVALID_ARGUMENT, "vabft_fused_gemm: lda < K or ldc < N");
+        if (is_wide(h->fmt) && (lda != k || ldc != n))
+            fail(VABFT_UNSUPPORTED, "vabft_fused_gemm: strided A / C are BF16 / FP16 only");
         const size_t need = std::max(carve(nullptr, m, n, k).bytes, carve_wide(nullptr, m, n, k).bytes);
         if (!workspace || ws_bytes < need) fail(VABFT_INVALID_ARGUMENT, "vabft_fused_gemm: workspace too small");
         cudaStream_t s = as_stream(stream);
@@ -448,6 +463,8 @@ extern "C" vabft_status vabft_fused_gemm(const vabft_fused_opts* o, vabft_bside_
         a.nblkN = (n + 127) / 128;
         a.nblkK = (k + 127) / 128;
         a.A = static_cast<const uint16_t*>(A);
+        a.lda = lda;
+        a.ldc = ldc;
         a.part1 = ws.part1;
         a.part2 = ws.part2;
         a.sp1 = ws.sp1;
@@ -528,7 +545,7 @@ extern "C" vabft_status vabft_fused_gemm(const vabft_fused_opts* o, vabft_bside_
                     epi.group_cnt = ws.group_cnt;
                 }
             }
-            tc_gemm_launch(h->fmt, o->b_kmajor != 0, m, n, k, A, h->B, C, epi, s);
+            tc_gemm_launch(h->fmt, o->b_kmajor != 0, m, n, k, A, h->B, C, epi, s, lda, h->ldb, ldc);
             return;
         }
         if (!(stages & 4)) return;

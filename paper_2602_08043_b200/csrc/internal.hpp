@@ -43,6 +43,7 @@ size_t elem_size(int fmt);
 // ---- verify tail (tail.cuh): inputs of one fused launch
 struct TailArgs {
     int64_t M, N, K, nblkN, nblkK;
+    int64_t lda = 0, ldc = 0;            // row strides of A and C (elements)
     const uint16_t* A;
     const float *part1, *part2;          // C row partials (part_index, nb = nblkN)
     const float *sp1, *sp2;              // A (B r) partials (nb = nblkK)
@@ -114,8 +115,11 @@ __host__ __device__ inline size_t part_index(int64_t b, int64_t row, int64_t nb)
     return size_t(((row >> 5) * nb + b) * 32 + (row & 31));
 }
 
+// lda / ldb / ldc: row strides in elements (0 = dense); multiples of 8
+// (16-byte TMA strides and C stores)
 void tc_gemm_launch(int fmt, bool b_kmajor, int64_t M, int64_t N, int64_t K, const void* A,
-                    const void* B, void* C, const TcEpilogue& epi, cudaStream_t stream);
+                    const void* B, void* C, const TcEpilogue& epi, cudaStream_t stream, int64_t lda = 0,
+                    int64_t ldb = 0, int64_t ldc = 0);
 bool tc_gemm_supported(int fmt, int64_t M, int64_t N, int64_t K);
 // the kernel-shape decision of tc_gemm_launch (CTA pairs or not)
 bool tc_gemm_uses_pairs(bool b_kmajor, int64_t N, const TcEpilogue& epi);

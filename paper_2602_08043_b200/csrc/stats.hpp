@@ -33,9 +33,11 @@ void launch_row_stats(int fmt, int64_t rows, int64_t cols, const void* X, double
 // The B-side pass (bside.cu). rowsum_abs / summary[3] (A-ABFT computed y)
 // are part of it for BF16 / FP16; the wide formats build them on demand with
 // launch_bside_rowsum.
+// ld: row stride of B in elements (0 = N)
 void launch_bside(int fmt, int64_t K, int64_t N, const void* B, int quantize_br, BsideBuffers& buf,
-                  cudaStream_t s);
-void launch_bside_rowsum(int fmt, int64_t K, int64_t N, const void* B, BsideBuffers& buf, cudaStream_t s);
+                  cudaStream_t s, int64_t ld = 0);
+void launch_bside_rowsum(int fmt, int64_t K, int64_t N, const void* B, BsideBuffers& buf, cudaStream_t s,
+                         int64_t ld = 0);
 void launch_aside(int fmt, int64_t M, int64_t K, int64_t N, const void* A, const BsideBuffers& buf,
                   int quantize_cr, double e_max, double c_sigma, double* T, double* cr1, double* cr2,
                   double* max_abs_a, cudaStream_t s);

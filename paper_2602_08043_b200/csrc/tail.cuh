@@ -166,7 +166,7 @@ __device__ __forceinline__ void row_threshold(const TailArgs& a, int64_t i, bool
         const int l = __ffs(rows) - 1;
         rows &= rows - 1;
         const int64_t il = i - (threadIdx.x & 31) + l;
-        const double hs = warp_neumaier_row<F>(a.A + il * a.K, a.K, nullptr);
+        const double hs = warp_neumaier_row<F>(a.A + il * a.lda, a.K, nullptr);
         if ((threadIdx.x & 31) == l) sum = hs;
     }
     if (!valid) {
@@ -226,7 +226,7 @@ __device__ __forceinline__ void row_verdict(const TailArgs& a, int64_t i, bool v
                     // correct (detect.cpp:57-64) for a confidently located single
                     // error (residual < 0.5 - DetectOptions::residual_margin)
                     if (a.correct && a.C != nullptr && rr < 0.4) {
-                        uint16_t* cij = a.C + i * a.N + j;
+                        uint16_t* cij = a.C + i * a.ldc + j;
                         *cij = quantize16_bits_d<F>(__dsub_rn(double(bits16_to_float<F>(*cij)), d1));
                         corrected = true;
                     }

@@ -84,6 +84,7 @@ struct TcParams {
     int group_m;  // tile raster: groups of group_m row blocks, n-major inside a group
     int pair;     // 1: CTA-pair kernel (tiles of 256 rows, num_m_blk in 256-row blocks)
     uint16_t* C;
+    int64_t ldc;  // row stride of C (elements)
     TcEpilogue epi;
 };
 
@@ -790,7 +791,7 @@ __global__ void __launch_bounds__(kThreadsStats, 1)
                     }
                 }
                 if (row_ok) {
-                    uint16_t* dst = p.C + size_t(row) * p.N + n0 + c;
+                    uint16_t* dst = p.C + size_t(row) * size_t(p.ldc) + n0 + c;
 #pragma unroll
                     for (int g = 0; g < 4; ++g) {
                         if (n0 + c + g * 8 + 8 <= p.N) {
@@ -888,12 +889,13 @@ PFN_cuTensorMapEncodeTiled_v12000 get_encode_fn() {
     return fn;
 }
 
-// 2D row-major tensor [rows][cols] of 16-bit elements, box {box_cols, box_rows}.
-CUtensorMap make_map_2d(int fmt, const void* base, uint64_t rows, uint64_t cols, uint32_t box_cols,
+// 2D row-major tensor [rows][cols] of 16-bit elements, row stride ld
+// elements, box {box_cols, box_rows}.
+CUtensorMap make_map_2d(int fmt, const void* base, uint64_t rows, uint64_t cols, uint64_t ld, uint32_t box_cols,
                         uint32_t box_rows) {
     CUtensorMap m;
     cuuint64_t dims[2] = {cols, rows};
-    cuuint64_t strides[1] = {cols * 2};
+    cuuint64_t strides[1] = {ld * 2};
     cuuint32_t box[2] = {box_cols, box_rows};
     cuuint32_t estr[2] = {1, 1};
     const CUtensorMapDataType dt =
@@ -1036,9 +1038,16 @@ bool tc_gemm_supported(int fmt, int64_t M, int64_t N, int64_t K) {
 }
 
 void tc_gemm_launch(int fmt, bool b_kmajor, int64_t M, int64_t N, int64_t K, const void* A,
-                    const void* B, void* C, const TcEpilogue& epi, cudaStream_t stream) {
+                    const void* B, void* C, const TcEpilogue& epi, cudaStream_t stream, int64_t lda, int64_t ldb,
+                    int64_t ldc) {
     if (!tc_gemm_supported(fmt, M, N, K))
         fail(VABFT_UNSUPPORTED, "tcgen05 GEMM: needs BF16/FP16 with N % 8 == 0 and K % 8 == 0");
+    const int64_t bcols = b_kmajor ? K : N;
+    if (lda == 0) lda = K;
+    if (ldb == 0) ldb = bcols;
+    if (ldc == 0) ldc = N;
+    if (lda < K || ldb < bcols || ldc < N || lda % 8 || ldb % 8 || ldc % 8)
+        fail(VABFT_UNSUPPORTED, "tcgen05 GEMM: leading dimensions must cover the rows and be multiples of 8");
     TcParams p;
     p.M = int(M);
     p.N = int(N);
@@ -1059,6 +1068,7 @@ void tc_gemm_launch(int fmt, bool b_kmajor, int64_t M, int64_t N, int64_t K, con
     const int raster = raster_env ? raster_env : (epi.sp1 != nullptr ? 32 : 8);
     p.group_m = raster <= 0 || raster > p.num_m_blk ? p.num_m_blk : raster;
     p.C = static_cast<uint16_t*>(C);
+    p.ldc = ldc;
     p.epi = epi;
     static unsigned long long* trace_buf = [] {
         unsigned long long* t = nullptr;
@@ -1094,9 +1104,9 @@ void tc_gemm_launch(int fmt, bool b_kmajor, int64_t M, int64_t N, int64_t K, con
         if (split_env && p.num_tiles > pairs && rem > 0 && 2 * rem <= pairs && N > kBN / 2) p.split_from = p.num_tiles - rem;
         p.num_units = p.split_from + 2 * (p.num_tiles - p.split_from);
     }
-    const CUtensorMap ta = make_map_2d(fmt, A, uint64_t(M), uint64_t(K), kBK, kBM);
-    const CUtensorMap tb = b_kmajor ? make_map_2d(fmt, B, uint64_t(N), uint64_t(K), kBK, kBN)
-                                    : make_map_2d(fmt, B, uint64_t(K), uint64_t(N), 64, kBK);
+    const CUtensorMap ta = make_map_2d(fmt, A, uint64_t(M), uint64_t(K), uint64_t(lda), kBK, kBM);
+    const CUtensorMap tb = b_kmajor ? make_map_2d(fmt, B, uint64_t(N), uint64_t(K), uint64_t(ldb), kBK, kBN)
+                                    : make_map_2d(fmt, B, uint64_t(K), uint64_t(N), uint64_t(ldb), 64, kBK);
     if (fmt == VABFT_BF16) {
         if (b_kmajor) dispatch_epi<VABFT_BF16, true>(ta, tb, p, stream);
         else dispatch_epi<VABFT_BF16, false>(ta, tb, p, stream);

@@ -61,7 +61,11 @@ class FusedAbftGemm:
                  tf32_passes: int = 3):
         if B.dtype not in _FMT or not B.is_cuda or B.dim() != 2:
             raise _capi.InvalidArgument("FusedAbftGemm: B must be a 2-D BF16/FP16/FP32/FP64 CUDA tensor")
-        self.B = B.contiguous()
+        # a row-strided view (e.g. a column slice B[:, n0:n1] of a wider
+        # weight) is used in place for BF16 / FP16 (row stride a multiple of 8)
+        strided_ok = B.dtype in (torch.bfloat16, torch.float16) and B.stride(1) == 1 and B.stride(0) % 8 == 0
+        self.B = B if (B.is_contiguous() or strided_ok) else B.contiguous()
+        self.ldb = self.B.stride(0)
         self.fmt = _FMT[B.dtype]
         self.k, self.n = self.B.shape
         self.mode = _capi.ONLINE if mode == "online" else _capi.OFFLINE
@@ -82,8 +86,8 @@ class FusedAbftGemm:
         self.opts.cta_mode = -1
         self.opts.tf32_passes = tf32_passes  # FP32 weights: 3xTF32 (default) or one TF32 pass
         self.h = C.c_void_p()
-        check(lib.vabft_bside_create(self.fmt, self.mode, self.k, self.n, ptr(self.B), C.byref(self.h),
-                                     stream_ptr()))
+        check(lib.vabft_bside_create_ld(self.fmt, self.mode, self.k, self.n, ptr(self.B), self.ldb, C.byref(self.h),
+                                        stream_ptr()))
         self._ws = None
         self._bufs = {}
 
@@ -92,7 +96,9 @@ class FusedAbftGemm:
         return bool(lib.vabft_fused_uses_cta_pairs(C.byref(self.opts), m, self.n, self.k))
 
     def update_weight(self, B: torch.Tensor) -> None:
-        self.B = B.contiguous()
+        if tuple(B.shape) != (self.k, self.n) or B.stride() != self.B.stride():
+            raise _capi.InvalidArgument("update_weight: same shape and strides as the handle's weight")
+        self.B = B
         check(lib.vabft_bside_update(self.h, ptr(self.B), stream_ptr()))
 
     def workspace(self, m: int) -> torch.Tensor:
@@ -116,6 +122,11 @@ class FusedAbftGemm:
         if A.dtype != self.B.dtype or A.dim() != 2 or A.shape[1] != self.k:
             raise _capi.InvalidArgument("FusedAbftGemm: A must be M x K with B's dtype")
         m = A.shape[0]
+        sixteen = A.dtype in (torch.bfloat16, torch.float16)
+        if not (sixteen and A.stride(1) == 1 and A.stride(0) % 8 == 0):
+            A = A.contiguous()
+        if out is not None and not (out.stride(1) == 1 and (out.is_contiguous() or (sixteen and out.stride(0) % 8 == 0))):
+            raise _capi.InvalidArgument("FusedAbftGemm: out must be contiguous (BF16/FP16: or row-strided by a multiple of 8)")
         # output buffers are cached per M (valid until the next call with the
         # same M) so the hot loop allocates nothing
         bufs = self._bufs.get(m)
@@ -166,8 +177,12 @@ class FusedAbftGemm:
                 raise _capi.InvalidArgument("accum_out must be a contiguous M x N float32 tensor")
             opts = _capi.FusedOpts.from_buffer_copy(opts)
             opts.accum_out = ptr(accum_out)
+        if A.stride(0) != self.k or C_.stride(0) != self.n:
+            opts = _capi.FusedOpts.from_buffer_copy(opts)
+            opts.lda = A.stride(0)
+            opts.ldc = C_.stride(0)
         ws = self.workspace(m)
-        check(lib.vabft_fused_gemm(C.byref(opts), self.h, m, ptr(A.contiguous()), ptr(C_), ptr(T), v, ptr(counts),
+        check(lib.vabft_fused_gemm(C.byref(opts), self.h, m, ptr(A), ptr(C_), ptr(T), v, ptr(counts),
                                    ptr(ws), ws.numel(), stream_ptr()))
         return FusedResult(C_, T, d1, d2, det, loc, res, counts, rc1, rc2)
 

@@ -378,3 +378,34 @@ def test_bside_update_replayed_from_a_cuda_graph(env):
         T_ref, _ = O.vabft_thresholds(A.double().cpu().numpy(), Bbuf.double().cpu().numpy(), g.opts.e_max, fmt="bf16")
         assert _same(r.T.cpu().numpy(), T_ref), seed
     g.close()
+
+
+@pytest.mark.parametrize("mode", ["online", "offline"])
+def test_leading_dimensions_match_dense_calls(env, mode):
+    """Row-strided operands (C-ABI v2 lda / ldc, vabft_bside_create_ld):
+    A = a column window of a wider activation, B = a column slice of a wider
+    weight, C written into the matching slice of a wider output — no copies;
+    C, thresholds, checksums and verdicts equal the dense call's bit for bit
+    (and the reference's on the slice, through the dense call's parity)."""
+    torch, O = env
+    from paper_2602_08043_b200.fused import FusedAbftGemm
+    m, k, n, n0 = 1024, 768, 1536, 512
+    Afull, Bfull = _inputs(torch, m, 2 * k, 2 * n, torch.bfloat16, 71)
+    A = Afull[:, 128:128 + k]            # lda = 2K
+    B = Bfull[:k, n0:n0 + n]             # ldb = 2N
+    assert not A.is_contiguous() and not B.is_contiguous()
+    g_s = FusedAbftGemm(B, mode=mode)
+    assert g_s.ldb == 2 * n
+    Cfull = torch.zeros(m, 2 * n, dtype=torch.bfloat16, device="cuda")
+    r_s = g_s(A, out=Cfull[:, n0:n0 + n], checksums=True)
+    torch.cuda.synchronize()
+    got = [x.clone() for x in (r_s.T, r_s.diff1, r_s.detected, r_s.row_check1, r_s.row_check2)]
+    g_d = FusedAbftGemm(B.contiguous(), mode=mode)
+    r_d = g_d(A.contiguous(), checksums=True)
+    torch.cuda.synchronize()
+    assert torch.equal(Cfull[:, n0:n0 + n].view(torch.int16), r_d.C.view(torch.int16))
+    assert torch.equal(Cfull[:, :n0], torch.zeros_like(Cfull[:, :n0]))  # nothing written outside the slice
+    for a, b in zip(got, (r_d.T, r_d.diff1, r_d.detected, r_d.row_check1, r_d.row_check2)):
+        assert torch.equal(a, b)
+    g_s.close()
+    g_d.close()
