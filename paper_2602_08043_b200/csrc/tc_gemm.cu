@@ -942,7 +942,12 @@ void launch_inst(const CUtensorMap& ta, const CUtensorMap& tb, const TcParams& p
                 return n > 0 ? n : 1;
             },
             &cfg);
-        const int pairs = p.num_units < max_clusters ? p.num_units : max_clusters;
+        static const int cap_env = [] {
+            const char* e = std::getenv("VABFT_MAX_PAIRS");  // developer cap (tools/l2_probe.py)
+            return e ? std::atoi(e) : 0;
+        }();
+        const int avail = cap_env > 0 && cap_env < max_clusters ? cap_env : max_clusters;
+        const int pairs = p.num_units < avail ? p.num_units : avail;
         cfg.gridDim = dim3(unsigned(2 * pairs));
         check_cuda(cudaLaunchKernelEx(&cfg, kern, ta, tb, p), "tc_gemm pair launch");
     } else {

@@ -255,3 +255,19 @@ def test_plain_gemm_pair_split_last_wave_matches_one_cta(api):
             out.append(c)
         torch.cuda.synchronize()
         assert torch.equal(out[0].view(torch.int16), out[1].view(torch.int16))
+
+
+def test_aabft_fixed_y_zero_and_negative_keep_reference_semantics(api):
+    """AabftParams::fixed_y = 0 (or negative) is a fixed y in the reference
+    (threshold_aabft.cpp:50-60): y_used = that value, degenerate = (y == 0),
+    thresholds = confidence * sigma(K, t, y); only an empty fixed_y computes y
+    (the C-ABI's NaN sentinel)."""
+    A = np.ones((4, 8))
+    B = np.ones((8, 5))
+    z = api.aabft_threshold(A, B, api.AabftParams(23, 0.0, 3.0), "fp32")
+    assert z.y_used == 0.0 and z.degenerate and np.all(z.per_row == 0.0)
+    neg = api.aabft_threshold(A, B, api.AabftParams(23, -2.0, 3.0), "fp32")
+    assert neg.y_used == -2.0 and not neg.degenerate and np.all(neg.per_row < 0.0)
+    assert neg.per_row[0] == 3.0 * api.aabft_sigma(8, 23, -2.0)
+    comp = api.aabft_threshold(A, B, api.AabftParams(23, None, 3.0), "fp32")
+    assert comp.y_used == 1.0 * 5.0  # max|A| * max_k |sum_j B[k][j]|
