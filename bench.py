@@ -257,6 +257,8 @@ def measure_formats(dev, flush, torch, n=4096, steps=20, warmup=3):
     from paper_2602_08043_b200.fused import FusedAbftGemm
     out = {}
     stream = torch.cuda.current_stream()
+    pp = os.path.join(ROOT, "profiles", "r02_peaks_tf32_fp64.json")
+    wide_peaks = json.load(open(pp)) if os.path.exists(pp) else {}
     for name, dt, passes in (("fp32_3xtf32", torch.float32, 3), ("fp32_1xtf32", torch.float32, 1),
                              ("fp64_dfma", torch.float64, 3)):
         nn = n if dt == torch.float32 else n // 2  # FP64: 2048^3 keeps the run short
@@ -291,7 +293,18 @@ def measure_formats(dev, flush, torch, n=4096, steps=20, warmup=3):
         g(A, out=Cc, counts=counts)
         torch.cuda.synchronize()
         fl = 2.0 * nn ** 3
-        out[name] = {"shape": [nn, nn, nn], "fused_tflops": fl / ms_f / 1e9, "plain_tflops": fl / ms_p / 1e9,
+        fused_tf = fl / ms_f / 1e9
+        # roofline against cuBLAS on this B200 model (tools/peaks_probe.py):
+        # TF32 tensor cores for the TF32 passes (3xTF32 issues 3 passes per
+        # algorithmic flop), DGEMM for FP64
+        pk = wide_peaks.get("fp64_tflops" if dt == torch.float64 else "tf32_tflops")
+        roof = None
+        if pk:
+            work = 3.0 if name == "fp32_3xtf32" else 1.0
+            roof = {"peak_tflops": pk, "peak": "cuBLAS " + ("DGEMM" if dt == torch.float64 else "TF32") + " 8192^3, "
+                    + "profiles/r02_peaks_tf32_fp64.json", "frac_algorithmic": fused_tf / pk,
+                    "frac_issued": work * fused_tf / pk}
+        out[name] = {"shape": [nn, nn, nn], "fused_tflops": fused_tf, "plain_tflops": fl / ms_p / 1e9, "roofline": roof,
                      "abft_overhead_pct": 100.0 * (ms_f / ms_p - 1.0), "e_max": g.opts.e_max,
                      "us_runs": {"fused": [round(x * 1e3, 1) for x in runs_f],
                                  "plain": [round(x * 1e3, 1) for x in runs_p]},

@@ -254,6 +254,46 @@ def test_bside_pass_mixed_scales_bit_exact(env, fmt, shape):
     assert _same(T, T_ref)
 
 
+@pytest.mark.parametrize("k", [700, 4096])
+def test_bside_summary_chain_adversarial(env, k):
+    """BStatsSummary's three sequential FP64 sums (threshold_vabft.cpp:19-24)
+    folded from the published row groups through the summary warps' cp.async
+    ring (bside.cu bs_summary), on terms that stress a sequential sum: leading
+    zero rows, tiny rows (1e-300), runs of ties against the running sum
+    (1 + 2^-52 while the sum is in [2, 4)), binade crossings, huge jumps and
+    random magnitudes, with K not a multiple of the 256-row batch. FP64 rows
+    [v, v] give mean v and var_bound 0; other rows [v, w] give var_bound > 0."""
+    torch, O = env
+    from paper_2602_08043_b200 import api
+    rng = np.random.default_rng(k)
+    v = np.empty(k)
+    w = np.empty(k)
+    i = 0
+    for blk in range(k):
+        kind = (blk * 7919) % 11
+        if blk < 5:
+            x = 0.0
+        elif blk < 9:
+            x = 1e-300 * (blk - 4)
+        elif kind < 4:
+            x = 1.0 + 2.0 ** -52
+        elif kind == 4:
+            x = 2.0 ** int(rng.integers(-40, 40))
+        elif kind == 5:
+            x = float(rng.standard_normal()) * 1e6
+        else:
+            x = float(rng.standard_normal())
+        v[i] = x
+        w[i] = x if kind % 2 == 0 else x + float(rng.standard_normal()) * 2.0 ** -20
+        i += 1
+    B = np.stack([v, w], axis=1)
+    A = rng.standard_normal((64, k))
+    T, summ = api.vabft_thresholds(A, B, api.VabftParams(1e-3, 2.5), "fp64", return_summary=True)
+    T_ref, s_ref = O.vabft_thresholds(A, B, 1e-3, fmt="fp64")
+    assert _same(summ, s_ref), (summ, s_ref)
+    assert _same(T, T_ref)
+
+
 def test_nsplit_slices_match_oracle_on_slices(env):
     """SURVEY §8(e) N-sharding: two column slices of one C4-shaped GEMM
     (8192 x 4096 x 11008 split by shard_columns), each a ColumnShardedGemm
