@@ -244,4 +244,13 @@ __host__ __device__ constexpr uint32_t umma_idesc_f16(uint32_t ab_fmt, bool b_mn
            | ((m >> 4) << 24);                // M >> 4
 }
 
+// Programmatic dependent launch: a primary kernel lets the next kernel on
+// the stream (launched with cudaLaunchAttributeProgrammaticStreamSerialization)
+// start while it is still running; the secondary waits for the primary's
+// completion (and its memory) before consuming its results.
+__device__ __forceinline__ void griddep_launch_dependents() {
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+__device__ __forceinline__ void griddep_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+
 }  // namespace vabft_dev

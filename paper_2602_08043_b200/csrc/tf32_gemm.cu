@@ -133,6 +133,9 @@ __global__ void __launch_bounds__(kThreads, 1)
     __syncthreads();
     tc_fence_after();
     const uint32_t tmem_base = *tmem_slot;
+    // the wide A pass that follows (programmatic launch) may start on SMs this
+    // grid leaves idle; it waits for the grid's completion before reading C
+    griddep_launch_dependents();
 
     if (warp == 0) {
         if (lane == 0) {

@@ -49,6 +49,15 @@ __device__ __forceinline__ void cp_async16(uint32_t dst, const void* src, bool v
     asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(dst), "l"(src), "r"(valid ? 16 : 0)
                  : "memory");
 }
+__device__ __forceinline__ void cp_async16n(uint32_t dst, const void* src, int src_bytes) {  // zero-fills the rest
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(dst), "l"(src), "r"(src_bytes) : "memory");
+}
+template <int kBytes>  // 4 or 8
+__device__ __forceinline__ void cp_async_small(uint32_t dst, const void* src, bool valid) {
+    asm volatile("cp.async.ca.shared.global [%0], [%1], %2, %3;\n" ::"r"(dst), "l"(src), "n"(kBytes),
+                 "r"(valid ? kBytes : 0)
+                 : "memory");
+}
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
 template <int N>
 __device__ __forceinline__ void cp_async_wait() {
@@ -74,6 +83,7 @@ __global__ void __launch_bounds__(kDThreads, 1) dgemm_kernel(const __grid_consta
     const int64_t m0 = int64_t(blockIdx.y) * kDBM, n0 = int64_t(blockIdx.x) * kDBN;
     const int wm = warp & 3, wn = warp >> 2, ty = lane >> 3, tx = lane & 7;
     const int64_t ktiles = (p.K + kDBK - 1) / kDBK;
+    griddep_launch_dependents();  // the A pass may start on SMs this grid's last wave leaves idle
 
     auto load_stage = [&](int64_t kt, int slot) {
         double* As = sm + size_t(slot) * kStage;
@@ -281,43 +291,16 @@ struct ApJob {
 constexpr int kApWarps = 8;
 constexpr int kApLd = 36;  // staged row stride (elements): 16-byte aligned rows, conflict-free 16-byte LDS
 
+// per warp: a 2-slot ring of staged 32 x 32 sub-tiles and a 2-slot ring of
+// block weights [B r1 | B r2] (128 + 128 in the working type W == T)
+template <int F>
+constexpr size_t ap_warp_smem() {
+    using T = typename Elem<F>::T;
+    return 2 * (32 * kApLd * sizeof(T)) + 2 * (2 * 128 * sizeof(T));
+}
 template <int F>
 constexpr size_t ap_smem() {
-    using T = typename Elem<F>::T;
-    return size_t(kApWarps) * (32 * kApLd * sizeof(T) + 2 * 128 * sizeof(T));
-}
-
-template <int F>
-__device__ __forceinline__ void ap_load(const typename Elem<F>::T* __restrict__ A, int64_t M, int64_t K, int64_t r0,
-                                        int64_t c, typename Elem<F>::T (&v)[32]) {
-    using T = typename Elem<F>::T;
-    const int64_t col = c + (threadIdx.x & 31);
-    const T* p = A + r0 * K + col;
-    const int rows = int(M - r0 < 32 ? M - r0 : 32);
-#pragma unroll
-    for (int rr = 0; rr < 32; ++rr) v[rr] = (rr < rows && col < K) ? __ldcs(p + rr * K) : T(0);
-}
-
-// FP32 with K % 4 == 0 and A 16-byte aligned: 16-byte loads, lane l holding
-// row 4 i + l / 8, columns c + 4 (l % 8) .. + 3 of the sub-tile (8 lanes per
-// 128-byte row segment), and 16-byte stores into the staged tile.
-__device__ __forceinline__ void ap_load_v4(const float* __restrict__ A, int64_t M, int64_t K, int64_t r0, int64_t c,
-                                           float4 (&v)[8]) {
-    const int lane = threadIdx.x & 31;
-    const int64_t col = c + 4 * (lane & 7);
-    const int rs = lane >> 3;
-    const float* p = A + (r0 + rs) * K + col;
-    const int rows = int(M - r0 < 32 ? M - r0 : 32);
-#pragma unroll
-    for (int i = 0; i < 8; ++i)
-        v[i] = (4 * i + rs < rows && col < K) ? __ldcs(reinterpret_cast<const float4*>(p + int64_t(4 * i) * K))
-                                              : make_float4(0.f, 0.f, 0.f, 0.f);
-}
-__device__ __forceinline__ void ap_stage_v4(float* tile, const float4 (&v)[8]) {
-    const int lane = threadIdx.x & 31;
-#pragma unroll
-    for (int i = 0; i < 8; ++i)
-        *reinterpret_cast<float4*>(tile + (4 * i + (lane >> 3)) * kApLd + 4 * (lane & 7)) = v[i];
+    return size_t(kApWarps) * ap_warp_smem<F>();
 }
 
 // One element of the FP32 A pass: checksum products (no FMA), the plain FP64
@@ -492,6 +475,9 @@ __device__ __forceinline__ void ap_finish_group(const ApJob<W>& j, int64_t rg) {
         }
         return;
     }
+    // the GEMM's C-row partials (and C for the correction): the A pass may
+    // have started beside the GEMM's last wave (programmatic launch)
+    griddep_wait();
     double r1 = 0.0, r2 = 0.0;
     if (valid) wide_row_sums<W>(a, i, r1, r2);
     wide_verdicts<F>(a, i, valid, r1, r2, mean_i, vb_i, c1, c2);
@@ -503,44 +489,103 @@ __global__ void __launch_bounds__(32 * kApWarps, F == VABFT_FP64 ? 1 : 2)
     using T = typename Elem<F>::T;
     extern __shared__ __align__(16) uint8_t ap_raw[];
     const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    T* tile = reinterpret_cast<T*>(ap_raw + size_t(w) * (32 * kApLd * sizeof(T) + 2 * 128 * sizeof(T)));
-    W* wts = reinterpret_cast<W*>(tile + 32 * kApLd);  // [2][128] weights of the block (W == T)
+    uint8_t* mine = ap_raw + size_t(w) * ap_warp_smem<F>();
+    T* tiles = reinterpret_cast<T*>(mine);                          // [2][32 * kApLd]
+    W* wtsb = reinterpret_cast<W*>(mine + 2 * 32 * kApLd * sizeof(T));  // [2][256]
     const int64_t M = j.t.M, K = j.t.K;
     const int64_t nb = (K + 127) / 128, ngroups = (M + 31) / 32;
     const int64_t tasks = ngroups * nb;
-    for (int64_t t = int64_t(blockIdx.x) * kApWarps + w; t < tasks; t += int64_t(gridDim.x) * kApWarps) {
+    const int64_t nt = int64_t(gridDim.x) * kApWarps;
+    // Every load is a cp.async into the warp's 2-slot rings, one sub-tile
+    // ahead of the fold — across task boundaries too (the next task's first
+    // sub-tile and block weights land while this task's last sub-tile is
+    // folded) — so no register staging and no exposed load at a task start.
+    // A task's arrival (release RMW, whose fence also waits for memory
+    // operations in flight) is deferred to the start of the warp's next task,
+    // when no copy of this warp is pending. (Measured before: long-
+    // scoreboard stalls on register staging and on each task's first loads
+    // and weights, plus the fence, were the top stall reasons.)
+    auto issue = [&](int64_t t, int q, int slot, int wslot) {
+        const int64_t rg = t / nb, b = t - rg * nb;
+        const int64_t r0 = rg * 32, c = b * 128 + int64_t(q) * 32;
+        const int rows = int(M - r0 < 32 ? M - r0 : 32);
+        T* tile = tiles + slot * (32 * kApLd);
+        if constexpr (kVec) {  // FP32, K % 4 == 0, aligned: 16-byte chunks, 8 lanes per 128-byte row segment
+            const int64_t col = c + 4 * (lane & 7);
+            const int rs = lane >> 3;
+#pragma unroll
+            for (int i = 0; i < 8; ++i) {
+                const int r = 4 * i + rs;
+                const bool ok = r < rows && col < K;
+                cp_async16n(smem_u32(tile + r * kApLd + 4 * (lane & 7)), ok ? A + (r0 + r) * K + col : A,
+                            ok ? 16 : 0);
+            }
+        } else {  // lane = column, one element per row
+            const int64_t col = c + lane;
+#pragma unroll
+            for (int r = 0; r < 32; ++r) {
+                const bool ok = r < rows && col < K;
+                cp_async_small<int(sizeof(T))>(smem_u32(tile + r * kApLd + lane), ok ? A + (r0 + r) * K + col : A, ok);
+            }
+        }
+        if (q == 0) {  // the block's weights, 16-byte chunks (zero-filled past K)
+            const int bw = int(K - b * 128 < 128 ? K - b * 128 : 128);
+            constexpr int kPer = int(16 / sizeof(W));  // weights per chunk
+            W* wd = wtsb + wslot * 256;
+            for (int ch = lane; ch < 128 / kPer; ch += 32) {
+                const int e0 = ch * kPer;
+                const int nvalid = bw - e0 < 0 ? 0 : (bw - e0 > kPer ? kPer : bw - e0);
+                const int64_t o = nvalid ? b * 128 + e0 : 0;  // no bytes read for an empty chunk
+                cp_async16n(smem_u32(wd + e0), j.br1 + o, nvalid * int(sizeof(W)));
+                cp_async16n(smem_u32(wd + 128 + e0), j.br2 + o, nvalid * int(sizeof(W)));
+            }
+        }
+    };
+    auto arrive = [&](int64_t rg) {
+        // every lane's partial stores before lane 0's release RMW; the last
+        // arriver then reads all partials through L2 (.cg) after a fence
+        __syncwarp();
+        unsigned old = 0;
+        if (lane == 0) old = atom_add_release_gpu(j.gcnt + rg, 1u);
+        old = __shfl_sync(0xffffffffu, old, 0);
+        if (old == unsigned(nb) - 1u) {
+            __threadfence();
+            if (lane == 0) j.gcnt[rg] = 0u;  // ready for the next launch
+            ap_finish_group<F, W>(j, rg);
+        }
+    };
+    int64_t pending = -1;  // row group of the task whose arrival is deferred
+    int slot = 0, wslot = 0;
+    int64_t t = int64_t(blockIdx.x) * kApWarps + w;
+    if (t < tasks) issue(t, 0, 0, 0);
+    cp_async_commit();
+    for (;; t += nt) {
+        // the task's first sub-tile and weights were issued during the previous
+        // task's last sub-tile; with them landed no copy of ours is in flight
+        // for the deferred arrival's fence
+        cp_async_wait<0>();
+        __syncwarp();
+        if (pending >= 0) {
+            arrive(pending);
+            pending = -1;
+        }
+        if (t >= tasks) break;
         const int64_t rg = t / nb, b = t - rg * nb;
         const int64_t r0 = rg * 32, c0 = b * 128;
         const int bw = int(K - c0 < 128 ? K - c0 : 128);
         const int nsub = (bw + 31) / 32;
-        T v[kVec ? 1 : 32];
-        float4 v4[kVec ? 8 : 1];
-        if constexpr (kVec) ap_load_v4(reinterpret_cast<const float*>(A), M, K, r0, c0, v4);
-        else ap_load<F>(A, M, K, r0, c0, v);
-        __syncwarp();
-#pragma unroll
-        for (int q = 0; q < 4; ++q) {
-            const int jj = q * 32 + lane;
-            wts[jj] = jj < bw ? W(j.br1[c0 + jj]) : W(0);
-            wts[128 + jj] = jj < bw ? W(j.br2[c0 + jj]) : W(0);
-        }
-        if constexpr (kVec) {
-            ap_stage_v4(reinterpret_cast<float*>(tile), v4);
-        } else {
-#pragma unroll
-            for (int rr = 0; rr < 32; ++rr) tile[rr * kApLd + lane] = v[rr];
-        }
-        __syncwarp();
+        const W* wts = wtsb + wslot * 256;
         W p1 = W(0), p2 = W(0);
         double s = 0.0, c = 0.0;
         T sabs = T(0), mx = T(-INFINITY), mn = T(INFINITY);
-        const T* trow = tile + lane * kApLd;
         for (int q = 0; q < nsub; ++q) {
             const int64_t cq = c0 + int64_t(q) * 32;
-            if (q + 1 < nsub) {  // in flight during this sub-tile
-                if constexpr (kVec) ap_load_v4(reinterpret_cast<const float*>(A), M, K, r0, cq + 32, v4);
-                else ap_load<F>(A, M, K, r0, cq + 32, v);
-            }
+            if (q + 1 < nsub) issue(t, q + 1, slot ^ 1, wslot);
+            else if (t + nt < tasks) issue(t + nt, 0, slot ^ 1, wslot ^ 1);
+            cp_async_commit();
+            cp_async_wait<1>();  // this sub-tile (and the task's weights) landed
+            __syncwarp();
+            const T* trow = tiles + slot * (32 * kApLd) + lane * kApLd;
             const int cnt = int(c0 + bw - cq < 32 ? c0 + bw - cq : 32);  // warp-uniform
             const W* w1 = wts + q * 32;
             const W* w2 = wts + 128 + q * 32;
@@ -609,16 +654,8 @@ __global__ void __launch_bounds__(32 * kApWarps, F == VABFT_FP64 ? 1 : 2)
                     mn = x < mn ? x : mn;
                 }
             }
-            if (q + 1 < nsub) {
-                __syncwarp();
-                if constexpr (kVec) {
-                    ap_stage_v4(reinterpret_cast<float*>(tile), v4);
-                } else {
-#pragma unroll
-                    for (int rr = 0; rr < 32; ++rr) tile[rr * kApLd + lane] = v[rr];
-                }
-                __syncwarp();
-            }
+            __syncwarp();  // the slot is refilled two steps later
+            slot ^= 1;
         }
         const int64_t row = r0 + lane;
         if (row < M) {
@@ -632,19 +669,10 @@ __global__ void __launch_bounds__(32 * kApWarps, F == VABFT_FP64 ? 1 : 2)
             j.part.mx[o] = double(mx);
             j.part.mn[o] = double(mn);
         }
-        // arrival: every lane's partial stores before lane 0's release RMW;
-        // the last arriver then reads all partials through L2 (.cg) after a
-        // fence (acquire side)
-        __syncwarp();
-        unsigned old = 0;
-        if (lane == 0) old = atom_add_release_gpu(j.gcnt + rg, 1u);
-        old = __shfl_sync(0xffffffffu, old, 0);
-        if (old == unsigned(nb) - 1u) {
-            __threadfence();
-            if (lane == 0) j.gcnt[rg] = 0u;  // ready for the next launch
-            ap_finish_group<F, W>(j, rg);
-        }
+        pending = rg;
+        wslot ^= 1;
     }
+    griddep_wait();  // never complete before the GEMM this pass may overlap
 }
 
 // Verify tail for thresholds with a global dependency (A-ABFT computed y):
@@ -733,7 +761,20 @@ void launch_wide_aside(const WideTail& t, const void* br1, const void* br2, void
         const int per_sm = cached_occupancy(reinterpret_cast<const void*>(kern), 32 * kApWarps, int(smem));
         const int64_t tasks = (t.M + 31) / 32 * nb;
         const int grid = int(std::min<int64_t>(int64_t(sm_count()) * std::max(per_sm, 1), (tasks + kApWarps - 1) / kApWarps));
-        kern<<<grid, 32 * kApWarps, smem, stream>>>(static_cast<const T*>(t.A), j);
+        // programmatic launch: the pass reads only A and the per-weight B r
+        // until a row group's verdicts (griddep_wait), so its CTAs start on
+        // the SMs the GEMM's last wave leaves idle
+        cudaLaunchConfig_t cfg{};
+        cfg.gridDim = dim3(unsigned(grid));
+        cfg.blockDim = dim3(32 * kApWarps);
+        cfg.dynamicSmemBytes = smem;
+        cfg.stream = stream;
+        cudaLaunchAttribute attr[1];
+        attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+        attr[0].val.programmaticStreamSerializationAllowed = 1;
+        cfg.attrs = attr;
+        cfg.numAttrs = 1;
+        check_cuda(cudaLaunchKernelEx(&cfg, kern, static_cast<const T*>(t.A), j), "wide A-side launch");
     };
     if (t.fmt == VABFT_FP64) run(double{});
     else if (t.fmt == VABFT_FP32) run(float{});
