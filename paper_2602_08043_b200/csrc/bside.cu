@@ -35,6 +35,7 @@
 //    FP64 row sum A-ABFT's computed y needs is built on first use
 //    (launch_bside_rowsum).
 #include <algorithm>
+#include <cstdio>
 #include <cstdlib>
 #include <type_traits>
 
@@ -121,7 +122,18 @@ struct BsJob {
     unsigned* grp_epoch;  // [2] epoch of the last complete launch, chains-done counter (device state, so a
                           // CUDA-graph replay of the launch is a new epoch too)
     int debug;  // developer ablation (VABFT_BSIDE_DEBUG): 1 no summary chains, 2 also no group combine
+    int trace;  // developer timeline (VABFT_BSIDE_TRACE): %globaltimer stamps into g_bs_trace
 };
+
+// developer timeline (VABFT_BSIDE_TRACE=1): [0] first CTA start, [1] last
+// streaming warp done, [2..4] chain 0..2 done, [5] chain 0 first batch
+// start, [6] last group combine done
+__device__ unsigned long long g_bs_trace[8];
+__device__ __forceinline__ unsigned long long bs_now() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
 
 __device__ __forceinline__ float bs_add(float a, float b) { return __fadd_rn(a, b); }
 __device__ __forceinline__ double bs_add(double a, double b) { return __dadd_rn(a, b); }
@@ -547,29 +559,40 @@ __device__ void bs_summary(const BsJob<F>& j, double* buf2 /* 2 x kBatch doubles
         if (lane == 0) j.buf.summary[3] = acc;
         return;  // (warp 3 does not take part in the epoch hand-over)
     }
-    auto stage = [&](const double (&x)[kPer], double* dst) {
+    // Batches land in the warp's double buffer by cp.async (LDGSTS, .cg: L2),
+    // issued one batch ahead: fire-and-forget, so they stay in flight during
+    // the chain. (Measured: register fetches were sunk below the lane-0 chain
+    // by the compiler, every batch then waited on L2 — 12.7 cycles per
+    // element instead of ~8.)
+    auto fetch_async = [&](int64_t k0, double* dst) {
 #pragma unroll
-        for (int e = 0; e < kPer; ++e) dst[e * 32 + lane] = x[e];
-        __syncwarp();
+        for (int ch = lane; ch < kBatch / 2; ch += 32) {  // 16-byte chunks, zero-filled past K
+            const int64_t k = k0 + 2 * ch;
+            const int nv = K - k >= 2 ? 16 : (K - k == 1 ? 8 : 0);
+            cp_async16n(smem_u32(dst + 2 * ch), nv ? src + k : src, nv);
+        }
+        cp_async_commit();
     };
     while (!published(kBatch < K ? kBatch : K)) __nanosleep(64);
-    fetch(0, v);
-    stage(v, buf2);
+    if (j.trace && which == 0 && lane == 0) atomicMax(&g_bs_trace[5], bs_now());
+    fetch_async(0, buf2);
     int cur = 0;
     for (int64_t k0 = 0; k0 < K; k0 += kBatch) {
         const int64_t k1 = k0 + kBatch;
         const bool more = k1 < K;
         const int64_t kend = k1 + kBatch < K ? k1 + kBatch : K;
+        cp_async_wait<0>();  // batch k0 landed (this lane's chunks) ...
+        __syncwarp();        // ... and every lane's
         const bool pre = more && published(kend);
-        if (pre) fetch(k1, v);  // in flight during the chain below
+        if (pre) fetch_async(k1, buf2 + (cur ^ 1) * kBatch);  // in flight during the chain below
         if (lane == 0) {
             const double* x = buf2 + cur * kBatch;
             const int cnt = int(K - k0 < kBatch ? K - k0 : kBatch);
             if (cnt == kBatch) {
                 // 32 values per round loaded into registers before the adds,
                 // so no add waits on a shared-memory load
-#pragma unroll 1
-                for (int e0 = 0; e0 < kBatch; e0 += 32) {
+#pragma unroll
+                for (int e0 = 0; e0 < kBatch; e0 += 32) {  // unrolled: no load bubble at a round start
                     double2 q[16];
 #pragma unroll
                     for (int i = 0; i < 16; ++i) q[i] = reinterpret_cast<const double2*>(x + e0)[i];
@@ -590,16 +613,16 @@ __device__ void bs_summary(const BsJob<F>& j, double* buf2 /* 2 x kBatch doubles
                 }
             }
         }
-        __syncwarp();
+        __syncwarp();  // the buffer half is refilled next round
         if (more) {
             if (!pre) {
                 while (!published(kend)) __nanosleep(64);
-                fetch(k1, v);
+                fetch_async(k1, buf2 + (cur ^ 1) * kBatch);
             }
             cur ^= 1;
-            stage(v, buf2 + cur * kBatch);
         }
     }
+    if (j.trace && lane == 0) atomicMax(&g_bs_trace[2 + which], bs_now());
     if (lane == 0) {
         j.buf.summary[which] = acc;
         // the last of the three chains (every flag read) closes the epoch
@@ -626,6 +649,7 @@ __global__ void __launch_bounds__(kBsThreads, F == VABFT_FP64 ? 1 : 2) bside_ker
     Word* tiles = reinterpret_cast<Word*>(bs_smem_raw);
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const unsigned epoch = *reinterpret_cast<volatile const unsigned*>(j.grp_epoch) + 1u;
+    if (j.trace && threadIdx.x == 0) atomicMin(&g_bs_trace[0], bs_now());
     if (blockIdx.x == 0 && warp < kChains) {  // the warp's tile slice is its double buffer (>= 2 KiB)
         double* b2 = reinterpret_cast<double*>(tiles + size_t(warp) * 32 * kStride);
         if (j.debug == 0 || j.debug == 3 || j.debug == 4 + warp) {
@@ -666,8 +690,10 @@ __global__ void __launch_bounds__(kBsThreads, F == VABFT_FP64 ? 1 : 2) bside_ker
             __threadfence();
             if (lane == 0) j.grp_cnt[rg] = 0u;  // ready for the next launch
             bs_combine<F>(j, rg, epoch);
+            if (j.trace && lane == 0) atomicMax(&g_bs_trace[6], bs_now());
         }
     }
+    if (j.trace && lane == 0) atomicMax(&g_bs_trace[1], bs_now());
 }
 
 // The plain sequential FP64 row sum (threshold_aabft.cpp:42-46) of every B
@@ -718,6 +744,15 @@ void launch_bs(int64_t K, int64_t N, int64_t ld, const void* B, int quantize_br,
         return e ? std::atoi(e) : 0;
     }();
     j.debug = dbg;
+    static const int trc = [] {
+        const char* e = std::getenv("VABFT_BSIDE_TRACE");
+        return e ? std::atoi(e) : 0;
+    }();
+    j.trace = trc;
+    if (trc) {
+        const unsigned long long init[8] = {~0ull, 0, 0, 0, 0, 0, 0, 0};
+        check_cuda(cudaMemcpyToSymbolAsync(g_bs_trace, init, sizeof(init), 0, cudaMemcpyHostToDevice, s), "trace");
+    }
     j.grp_epoch = buf.groups + 2 * j.ngroups;
     constexpr size_t smem = bs_smem<F>();
     // 16-byte loads when rows are 16-byte multiples and B is aligned (4-byte words only)
@@ -729,9 +764,22 @@ void launch_bs(int64_t K, int64_t N, int64_t ld, const void* B, int quantize_br,
     const int per_sm = cached_occupancy(reinterpret_cast<const void*>(kern), kBsThreads, int(smem));
     const int64_t tasks = int64_t(j.ngroups) * j.nb;
     const int64_t want = (tasks + kBsWarps - 1) / kBsWarps + 1;
-    const int grid = int(std::min<int64_t>(int64_t(sm_count()) * std::max(per_sm, 1), want));
+    static const int per_sm_env = [] {  // developer override (VABFT_BSIDE_PERSM)
+        const char* e = std::getenv("VABFT_BSIDE_PERSM");
+        return e ? std::atoi(e) : 0;
+    }();
+    const int use_per_sm = per_sm_env > 0 ? std::min(per_sm_env, std::max(per_sm, 1)) : std::max(per_sm, 1);
+    const int grid = int(std::min<int64_t>(int64_t(sm_count()) * use_per_sm, want));
     kern<<<grid, kBsThreads, smem, s>>>(j);
     check_cuda(cudaGetLastError(), "bside launch");
+    if (trc) {
+        unsigned long long t[8];
+        check_cuda(cudaMemcpyFromSymbolAsync(t, g_bs_trace, sizeof(t), 0, cudaMemcpyDeviceToHost, s), "trace");
+        check_cuda(cudaStreamSynchronize(s), "trace");
+        auto us = [&](int i) { return t[i] ? double(t[i] - t[0]) * 1e-3 : -1.0; };
+        std::fprintf(stderr, "bside trace F=%d K=%lld N=%lld: pass %.2f combine %.2f chain0-start %.2f chains %.2f %.2f %.2f us\n",
+                     F, (long long)K, (long long)N, us(1), us(6), us(5), us(2), us(3), us(4));
+    }
 }
 
 }  // namespace

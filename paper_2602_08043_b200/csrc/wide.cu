@@ -45,25 +45,6 @@ constexpr int kCLd = kDBN + 1;          // epilogue staging stride: row walks ar
 constexpr size_t kDSmem = sizeof(double) * size_t(kDStages) * kStage;
 static_assert(sizeof(double) * kDBM * kCLd <= kDSmem, "epilogue staging reuses the operand ring");
 
-__device__ __forceinline__ void cp_async16(uint32_t dst, const void* src, bool valid) {
-    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(dst), "l"(src), "r"(valid ? 16 : 0)
-                 : "memory");
-}
-__device__ __forceinline__ void cp_async16n(uint32_t dst, const void* src, int src_bytes) {  // zero-fills the rest
-    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(dst), "l"(src), "r"(src_bytes) : "memory");
-}
-template <int kBytes>  // 4 or 8
-__device__ __forceinline__ void cp_async_small(uint32_t dst, const void* src, bool valid) {
-    asm volatile("cp.async.ca.shared.global [%0], [%1], %2, %3;\n" ::"r"(dst), "l"(src), "n"(kBytes),
-                 "r"(valid ? kBytes : 0)
-                 : "memory");
-}
-__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
-template <int N>
-__device__ __forceinline__ void cp_async_wait() {
-    asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory");
-}
-
 struct DgemmParams {
     int64_t M, N, K;
     const double* A;
