@@ -121,6 +121,7 @@ struct BsJob {
     unsigned* grp_flag;  // [ngroups] == this launch's epoch once the group is combined
     unsigned* grp_epoch;  // [2] epoch of the last complete launch, chains-done counter (device state, so a
                           // CUDA-graph replay of the launch is a new epoch too)
+    float *split_hi, *split_lo;  // FP32: the transposed TF32 split written by the pass (or null)
     int debug;  // developer ablation (VABFT_BSIDE_DEBUG): 1 no summary chains, 2 also no group combine
     int trace;  // developer timeline (VABFT_BSIDE_TRACE): %globaltimer stamps into g_bs_trace
 };
@@ -274,6 +275,107 @@ struct BsAcc {
     }
 };
 
+// One 16-bit sub-tile row: cnt (<= 64) elements from weight w0 (= column + 1).
+template <int F>
+__device__ __forceinline__ void bs16_sub(BsAcc<F>& a, const uint32_t* trow, int cnt, float w0) {
+    if (cnt == 64) {  // 16-byte LDS: 8 elements per load
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+            const uint4 q4 = reinterpret_cast<const uint4*>(trow)[u];
+            const float wu = __fadd_rn(w0, float(8 * u));
+            a.pair(q4.x, wu);
+            a.pair(q4.y, __fadd_rn(wu, 2.0f));
+            a.pair(q4.z, __fadd_rn(wu, 4.0f));
+            a.pair(q4.w, __fadd_rn(wu, 6.0f));
+        }
+    } else {
+        const int npair = cnt >> 1;
+        for (int jj = 0; jj < npair; ++jj) a.pair(trow[jj], __fadd_rn(w0, float(2 * jj)));
+        if (cnt & 1) a.single(trow[npair] & 0xFFFFu, __fadd_rn(w0, float(2 * npair)));
+    }
+}
+
+// One FP32 sub-tile row (lane = row, cnt columns from column cq, weights
+// w0 + j): the A pass's scheme (wide.cu, ApF32) — a plain FP64 sum of the
+// sub-tile, exact when 32 max|x| < 2^(53 + lsb(min nonzero |x|)) (else the
+// sub-tile is redone as a TwoSum cascade from the staged row), TwoSum-merged
+// into the block's (s, c) pair; one F2F + one DADD per element instead of a
+// TwoSum per element. With split_hi set, the TF32 split of each element
+// (hi = rna(x), lo = rna(x - hi), lo = 0 for non-finite x; tf32_gemm.cu
+// split_tf32_t_kernel) is stored transposed: element (k, n) at n K + k, so
+// the warp's 32 rows make one coalesced 128-byte segment per column.
+template <bool kSplit>
+__device__ __forceinline__ void bs_fp32_sub(BsAcc<VABFT_FP32>& a, const uint32_t* trow, int cnt, float w0,
+                                            float* hp, int64_t lo_off, int64_t K, bool rowok) {
+    float p1 = a.p1, p2 = a.p2, sabs = a.sabs, mx = a.mx, mn = a.mn;
+    double ps = 0.0;
+    uint32_t amx = 0u, mnz = 0xFFFFFFFFu;
+    auto one = [&](float x, float wt) {
+        const uint32_t mag = __float_as_uint(x) & 0x7FFFFFFFu;
+        amx = max(amx, mag);
+        mnz = min(mnz, mag - 1u);  // 0 wraps to the maximum: ignored
+        ps = __dadd_rn(ps, double(x));
+        p1 = __fadd_rn(p1, x);
+        p2 = __fadd_rn(p2, __fmul_rn(wt, x));
+        sabs = __fadd_rn(sabs, fabsf(x));
+        mx = fmaxf(mx, x);  // finite rows (non-finite ones are flagged and rejected)
+        mn = fminf(mn, x);
+        if constexpr (kSplit) {
+            uint32_t hb, lb;
+            asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(hb) : "f"(x));
+            const float r = mag < 0x7F800000u ? __fsub_rn(x, __uint_as_float(hb)) : 0.0f;
+            asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(lb) : "f"(r));
+            if (rowok) {
+                hp[0] = __uint_as_float(hb);
+                hp[lo_off] = __uint_as_float(lb);
+            }
+            hp += K;
+        }
+    };
+    if (cnt == 32) {  // 16-byte LDS
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+            const uint4 q4 = reinterpret_cast<const uint4*>(trow)[u];
+            const float wu = __fadd_rn(w0, float(4 * u));
+            one(__uint_as_float(q4.x), wu);
+            one(__uint_as_float(q4.y), __fadd_rn(wu, 1.0f));
+            one(__uint_as_float(q4.z), __fadd_rn(wu, 2.0f));
+            one(__uint_as_float(q4.w), __fadd_rn(wu, 3.0f));
+        }
+    } else {
+        for (int jj = 0; jj < cnt; ++jj) one(__uint_as_float(trow[jj]), __fadd_rn(w0, float(jj)));
+    }
+    bool exact = true;
+    if (mnz != 0xFFFFFFFFu && amx < 0x7F800000u) {
+        const int ez = int((mnz + 1u) >> 23);
+        const int lsb = (ez == 0 ? 1 : ez) - 127 - 23;
+        const int top = int(amx >> 23) - 127 + 1 + 6;  // 32 terms < 2^6 max
+        exact = top <= 53 + lsb;
+    }
+    double c = a.c;
+    if (!exact) {  // rare: the sub-tile's exact sum as a TwoSum cascade
+        double hs = 0.0, hc = 0.0;
+        for (int jj = 0; jj < cnt; ++jj) {
+            double tt, ee;
+            two_sum(hs, double(__uint_as_float(trow[jj])), tt, ee);
+            hs = tt;
+            hc = __dadd_rn(hc, ee);
+        }
+        ps = hs;
+        c = __dadd_rn(c, hc);
+    }
+    double tt, ee;
+    two_sum(a.s, ps, tt, ee);
+    a.s = tt;
+    a.c = __dadd_rn(c, ee);
+    a.p1 = p1;
+    a.p2 = p2;
+    a.sabs = sabs;
+    a.mx = mx;
+    a.mn = mn;
+    a.bad = max(a.bad, static_cast<unsigned long long>(amx));
+}
+
 // The block's per-row partials (lane = row) into the group-major arrays.
 template <int F>
 __device__ __forceinline__ void bs_store(const BsJob<F>& j, const BsAcc<F>& a, int64_t rg, int b) {
@@ -347,34 +449,17 @@ __device__ __forceinline__ void bs_block(const BsJob<F>& j, typename BsT<F>::Wor
         const int cnt = int(c0 + bw - cq < kCols ? c0 + bw - cq : kCols);  // warp-uniform
         const float w0 = float(cq + 1);  // weight j + 1 of the sub-tile's first element (exact: N <= 2^24)
         if constexpr (BsT<F>::k16) {
-            if (cnt == kCols) {  // 16-byte LDS: 8 elements per load
-#pragma unroll
-                for (int u = 0; u < kCols / 8; ++u) {
-                    const uint4 q4 = reinterpret_cast<const uint4*>(trow)[u];
-                    const float wu = __fadd_rn(w0, float(8 * u));
-                    a.pair(q4.x, wu);
-                    a.pair(q4.y, __fadd_rn(wu, 2.0f));
-                    a.pair(q4.z, __fadd_rn(wu, 4.0f));
-                    a.pair(q4.w, __fadd_rn(wu, 6.0f));
-                }
+            bs16_sub<F>(a, trow, cnt, w0);
+        } else if constexpr (F == VABFT_FP32) {
+            if (j.split_hi) {
+                bs_fp32_sub<true>(a, trow, cnt, w0, j.split_hi + cq * K + (r0 + lane), j.split_lo - j.split_hi,
+                                         K, lane < rows);
             } else {
-                const int npair = cnt >> 1;
-                for (int jj = 0; jj < npair; ++jj) a.pair(trow[jj], __fadd_rn(w0, float(2 * jj)));
-                if (cnt & 1) a.single(trow[npair] & 0xFFFFu, __fadd_rn(w0, float(2 * npair)));
+                bs_fp32_sub<false>(a, trow, cnt, w0, nullptr, 0, K, false);
             }
         } else {
             if (cnt == kCols) {  // 16-byte LDS
-                if constexpr (F == VABFT_FP32) {
-#pragma unroll
-                    for (int u = 0; u < kCols / 4; ++u) {
-                        const uint4 q4 = reinterpret_cast<const uint4*>(trow)[u];
-                        const float wu = __fadd_rn(w0, float(4 * u));
-                        a.elem(__uint_as_float(q4.x), wu);
-                        a.elem(__uint_as_float(q4.y), __fadd_rn(wu, 1.0f));
-                        a.elem(__uint_as_float(q4.z), __fadd_rn(wu, 2.0f));
-                        a.elem(__uint_as_float(q4.w), __fadd_rn(wu, 3.0f));
-                    }
-                } else {
+                {
 #pragma unroll 4
                     for (int u = 0; u < kCols / 2; ++u) {
                         const double2 q2 = reinterpret_cast<const double2*>(trow)[u];
@@ -384,10 +469,7 @@ __device__ __forceinline__ void bs_block(const BsJob<F>& j, typename BsT<F>::Wor
                     }
                 }
             } else {
-                for (int jj = 0; jj < cnt; ++jj) {
-                    if constexpr (F == VABFT_FP32) a.elem(__uint_as_float(trow[jj]), __fadd_rn(w0, float(jj)));
-                    else a.elem(trow[jj], __fadd_rn(w0, float(jj)));
-                }
+                for (int jj = 0; jj < cnt; ++jj) a.elem(trow[jj], __fadd_rn(w0, float(jj)));
             }
         }
         if (q + 1 < nsub) {
@@ -512,10 +594,10 @@ __device__ __forceinline__ void bs_combine(const BsJob<F>& j, int64_t rg, unsign
 // the kernel's floor, K x 8 cycles. (Measured: a 16-value register prefetch
 // left every batch waiting ~1000 cycles on L2; a data-dependent branch or an
 // fmax in the chain doubled or quadrupled its cost.)
-template <int F, int kWhich>
+template <int F, int kWhich, int kBatch = 256>
 __device__ void bs_summary(const BsJob<F>& j, double* buf2 /* 2 x kBatch doubles */, unsigned epoch) {
     constexpr int which = kWhich;  // compile-time: no branch inside the chain
-    constexpr int kBatch = 256, kPer = kBatch / 32;
+    constexpr int kPer = kBatch / 32;
     const int lane = threadIdx.x & 31;
     const double* src = which == 2 ? j.buf.vb : which == 3 ? j.buf.rowsum_abs : j.buf.mean;
     const int64_t K = j.K;
@@ -591,8 +673,9 @@ __device__ void bs_summary(const BsJob<F>& j, double* buf2 /* 2 x kBatch doubles
             if (cnt == kBatch) {
                 // 32 values per round loaded into registers before the adds,
                 // so no add waits on a shared-memory load
-#pragma unroll
-                for (int e0 = 0; e0 < kBatch; e0 += 32) {  // unrolled: no load bubble at a round start
+#pragma unroll 1
+                for (int e0 = 0; e0 < kBatch; e0 += 32) {  // (unrolled: no faster, and the code size
+                                                           // cost the streaming warps i-cache misses)
                     double2 q[16];
 #pragma unroll
                     for (int i = 0; i < 16; ++i) q[i] = reinterpret_cast<const double2*>(x + e0)[i];
@@ -724,6 +807,16 @@ __global__ void __launch_bounds__(128) bside_rowsum_kernel(const typename Elem<F
     }
 }
 
+void bs_trace_report(int trc, int F, int64_t K, int64_t N, cudaStream_t s) {
+    if (!trc) return;
+    unsigned long long t[8];
+    check_cuda(cudaMemcpyFromSymbolAsync(t, g_bs_trace, sizeof(t), 0, cudaMemcpyDeviceToHost, s), "trace");
+    check_cuda(cudaStreamSynchronize(s), "trace");
+    auto us = [&](int i) { return t[i] ? double(t[i] - t[0]) * 1e-3 : -1.0; };
+    std::fprintf(stderr, "bside trace F=%d K=%lld N=%lld: pass %.2f combine %.2f chain0-start %.2f chains %.2f %.2f %.2f us\n",
+                 F, (long long)K, (long long)N, us(1), us(6), us(5), us(2), us(3), us(4));
+}
+
 template <int F>
 void launch_bs(int64_t K, int64_t N, int64_t ld, const void* B, int quantize_br, BsideBuffers& buf, cudaStream_t s) {
     BsJob<F> j;
@@ -737,6 +830,8 @@ void launch_bs(int64_t K, int64_t N, int64_t ld, const void* B, int quantize_br,
     j.quantize_br = quantize_br;
     j.buf = buf;
     j.part = bs_view<F>(buf.work, j.nb, j.Kp);
+    j.split_hi = F == VABFT_FP32 ? buf.split_hi : nullptr;
+    j.split_lo = F == VABFT_FP32 ? buf.split_lo : nullptr;
     j.grp_cnt = buf.groups;
     j.grp_flag = buf.groups + j.ngroups;
     static const int dbg = [] {
@@ -772,14 +867,7 @@ void launch_bs(int64_t K, int64_t N, int64_t ld, const void* B, int quantize_br,
     const int grid = int(std::min<int64_t>(int64_t(sm_count()) * use_per_sm, want));
     kern<<<grid, kBsThreads, smem, s>>>(j);
     check_cuda(cudaGetLastError(), "bside launch");
-    if (trc) {
-        unsigned long long t[8];
-        check_cuda(cudaMemcpyFromSymbolAsync(t, g_bs_trace, sizeof(t), 0, cudaMemcpyDeviceToHost, s), "trace");
-        check_cuda(cudaStreamSynchronize(s), "trace");
-        auto us = [&](int i) { return t[i] ? double(t[i] - t[0]) * 1e-3 : -1.0; };
-        std::fprintf(stderr, "bside trace F=%d K=%lld N=%lld: pass %.2f combine %.2f chain0-start %.2f chains %.2f %.2f %.2f us\n",
-                     F, (long long)K, (long long)N, us(1), us(6), us(5), us(2), us(3), us(4));
-    }
+    bs_trace_report(trc, F, K, N, s);
 }
 
 }  // namespace

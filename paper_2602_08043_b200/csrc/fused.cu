@@ -194,11 +194,6 @@ WideWs carve_wide(void* base, int64_t M, int64_t N, int64_t K) {
 
 bool is_wide(int fmt) { return fmt == VABFT_FP32 || fmt == VABFT_FP64; }
 
-// FP32 weights: the TF32 hi / lo split, transposed for the kind::tf32 operand.
-// (B r1 / B r2 in the working type come from the B-side pass, buf.brd1/2.)
-void wide_split(vabft_bside* h, cudaStream_t s) {
-    split_tf32_t(static_cast<const float*>(h->B), h->b_split, h->b_split + size_t(h->k) * size_t(h->n), h->k, h->n, s);
-}
 
 // vabft_fused_gemm for FP32 / FP64: the GEMM with the ABFT epilogue, the
 // A-side pass (row statistics and A (B r) block partials, one read of A) and
@@ -389,11 +384,13 @@ extern "C" vabft_status vabft_bside_create_ld(int32_t format, int32_t mode, int6
             h->buf.brd2 = h->brd + K;
             if (format == VABFT_FP32) {
                 check_cuda(cudaMalloc(&h->b_split, 2 * sizeof(float) * K * size_t(n)), "cudaMalloc(B split)");
+                // the B-side pass writes the transposed TF32 split as it streams B
+                h->buf.split_hi = h->b_split;
+                h->buf.split_lo = h->b_split + K * size_t(n);
             }
         }
         if (B) {
             launch_bside(format, k, n, B, mode == VABFT_OFFLINE ? 1 : 0, h->buf, as_stream(stream), ldb);
-            if (format == VABFT_FP32) wide_split(h, as_stream(stream));
         }
         *out = hp.release();
     });
@@ -405,7 +402,6 @@ extern "C" vabft_status vabft_bside_update(vabft_bside_t h, const void* B, void*
         h->B = B;
         h->rowsum_ready = false;
         launch_bside(h->fmt, h->k, h->n, B, h->mode == VABFT_OFFLINE ? 1 : 0, h->buf, as_stream(stream), h->ldb);
-        if (h->fmt == VABFT_FP32) wide_split(h, as_stream(stream));
     });
 }
 

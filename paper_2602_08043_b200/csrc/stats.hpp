@@ -18,6 +18,8 @@ struct BsideBuffers {
     int* nonfinite = nullptr;      // [1] set when B holds NaN/Inf
     double* brd1 = nullptr;        // wide formats (optional): B r1 / B r2 in the working type, as doubles
     double* brd2 = nullptr;
+    float* split_hi = nullptr;     // FP32 (optional): the pass also writes the TF32 split of B, transposed
+    float* split_lo = nullptr;     // ([N][K], K-major: the kind::tf32 B operand), hi = rna(x), lo = rna(x - hi)
     void* work = nullptr;          // bside_work_bytes(): per-(128-column block, row) partials
     unsigned* groups = nullptr;    // bside_group_words(): arrival counters, ready flags and the launch
                                    // epoch, zero-initialised (device state: graph replays stay correct)
