@@ -143,6 +143,121 @@ __device__ __forceinline__ void ordered_sums(const float* x1, const float* x2, i
     }
 }
 
+// The reference's Neumaier row sum of one 16-bit row (a row that failed the
+// exactness guard), by the warp in INTEGER arithmetic: element x = +-M 2^q
+// (M the integer significand, q the exponent of its lsb) adds M << (q - qmin)
+// into a per-lane 128-bit two's-complement accumulator, qmin being the lsb
+// exponent of the row's smallest nonzero magnitude (from the statistics
+// trackers) — no FP64 per element. (Measured: FP64 loops inside the running
+// tcgen05 GEMM took ~90 us per row; 64 such rows made a 4096^3 launch 2.7x
+// slower.) The exact sum E = S 2^qmin is rounded to the nearest double, ties
+// to even, by integer ops.
+//   Why fl(E) is the reference's fl(sum + comp) (stats.cpp:12-24): every
+// running sum s_k, element and Fast2Sum error err_k is a multiple of
+// 2^qmin, and |comp| <= sum_k |err_k| <= K ulp(max |s_k|) / 2 <
+// 2^(ilogb(max|x|) + 2 lg K - 53). When that is below 2^(53 + qmin) —
+// ilogb(max|x|) + 2 lg K - qmin <= 104 — no addition into comp rounds, so
+// comp_K = sum_k err_k = E - s_K exactly and the final fl(s_K + comp_K) =
+// fl(E): including exact ties, which a margin test must give up on (a BF16
+// row of O(1) and ~1e-10 entries lands on a midpoint ~1 time in 7). FP16
+// rows always qualify. Wider rows that still fit 127 bits take the margin
+// test (exact_sum_safe, margin from K max|x| >= sum|x|); false (the caller
+// falls back to warp_neumaier_row) for the rest and for non-finite rows.
+template <int F>
+__device__ __noinline__ bool warp_exact_sum16(const uint16_t* row /* 16-byte aligned */, int64_t K, uint32_t mnz_pat, float amax,
+                                               double* out) {
+    constexpr int kBias = F == VABFT_BF16 ? 134 : 25;  // q = E - kBias for normals, 1 - kBias for subnormals
+    constexpr int kMant = F == VABFT_BF16 ? 7 : 10;
+    const int lane = threadIdx.x & 31;
+    if (mnz_pat >= 0x7FFFu || !isfinite(amax) || amax == 0.0f) return false;
+    const uint32_t pat = mnz_pat + 1;
+    const int ef = int(pat >> kMant);
+    const int qmin = (ef == 0 ? 1 : ef) - kBias;
+    const int lg = 64 - __clzll(static_cast<unsigned long long>(K));
+    const int span = ilogbf(amax) - qmin;
+    if (span + lg + 2 > 126) return false;
+    const bool comp_exact = span + 2 * lg <= 104;
+    unsigned __int128 acc = 0;
+    auto add = [&](uint32_t h) {
+        const uint32_t e = (h >> kMant) & (F == VABFT_BF16 ? 0xFFu : 0x1Fu);
+        const uint32_t m = (h & ((1u << kMant) - 1u)) | (e ? (1u << kMant) : 0u);
+        const int sh = (e ? int(e) : 1) - kBias - qmin;  // >= 0 for every nonzero element
+        unsigned __int128 v = static_cast<unsigned __int128>(m) << (sh > 0 ? sh : 0);
+        if (h & 0x8000u) v = ~v + 1;
+        acc += v;
+    };
+    // the row in 4 KiB rounds of eight independent 16-byte loads per lane (K
+    // % 8 == 0 and 16-byte rows on the fused path): one L2 round trip per
+    // round — a strided one-element-per-iteration loop paid one per element
+    // inside the running GEMM (measured ~90 us per row)
+    const uint4* r4 = reinterpret_cast<const uint4*>(row);
+    const int64_t n4 = K / 8;
+    for (int64_t c0 = 0; c0 < n4; c0 += 32 * 8) {
+        uint4 v[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+            const int64_t idx = c0 + u * 32 + lane;
+            v[u] = idx < n4 ? __ldcg(r4 + idx) : make_uint4(0u, 0u, 0u, 0u);
+        }
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+            const uint32_t w[4] = {v[u].x, v[u].y, v[u].z, v[u].w};
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                add(w[q] & 0xFFFFu);
+                add(w[q] >> 16);
+            }
+        }
+    }
+    for (int64_t j = n4 * 8 + lane; j < K; j += 32) add(row[j]);  // K % 8 tail (other callers)
+#pragma unroll
+    for (int mm = 16; mm >= 1; mm >>= 1) {
+        const unsigned long long lo = static_cast<unsigned long long>(acc);
+        const unsigned long long hi = static_cast<unsigned long long>(acc >> 64);
+        const unsigned long long olo = __shfl_xor_sync(0xffffffffu, lo, mm);
+        const unsigned long long ohi = __shfl_xor_sync(0xffffffffu, hi, mm);
+        acc += (static_cast<unsigned __int128>(ohi) << 64) | olo;
+    }
+    const bool neg = static_cast<long long>(static_cast<unsigned long long>(acc >> 64)) < 0;
+    const unsigned __int128 mag = neg ? ~acc + 1 : acc;
+    if (mag == 0) {
+        if (!comp_exact) return false;
+        *out = 0.0;  // s_K + comp_K == 0 exactly: +0 under round-to-nearest
+        return true;
+    }
+    const unsigned long long mh = static_cast<unsigned long long>(mag >> 64);
+    const unsigned long long ml = static_cast<unsigned long long>(mag);
+    const int nbits = mh ? 128 - __clzll(mh) : 64 - __clzll(ml);
+    const int drop = nbits > 53 ? nbits - 53 : 0;
+    unsigned __int128 m53 = mag >> drop;
+    if (drop > 0) {  // round to nearest, ties to even
+        const unsigned __int128 rem = mag - (m53 << drop);
+        const unsigned __int128 half = static_cast<unsigned __int128>(1) << (drop - 1);
+        if (rem > half || (rem == half && (m53 & 1))) m53 += 1;
+    }
+    if (comp_exact) {
+        const double h = scalbn(__ull2double_rn(static_cast<unsigned long long>(m53)), drop + qmin);
+        *out = neg ? -h : h;
+        return true;
+    }
+    const unsigned __int128 hint = m53 << drop;  // |hi| in units of 2^qmin
+    // lo = E - hi (|lo| <= 2^(drop - 1): rounding it to a double is far below the margin)
+    const bool lneg = mag < hint;
+    const unsigned __int128 r = lneg ? hint - mag : mag - hint;
+    const double rd = __ull2double_rn(static_cast<unsigned long long>(r >> 64)) * 18446744073709551616.0 +
+                      __ull2double_rn(static_cast<unsigned long long>(r));
+    double hi = scalbn(__ull2double_rn(static_cast<unsigned long long>(m53)), drop + qmin);
+    double lo = scalbn(rd, qmin);
+    if (lneg) lo = -lo;
+    if (neg) {
+        hi = -hi;
+        lo = -lo;
+    }
+    return exact_sum_safe(hi, lo, __dmul_ru(double(K), double(amax)), K, out);
+}
+
+__device__ unsigned long long g_tail_dbg[4];  // developer counters: integer-path successes / fallbacks
+
 // ---------------------------------------------------------------- pieces
 // Threshold of row i from its order-independent statistics (which are reset
 // to their identities for the next launch) and the A (B r) checksums from
@@ -166,7 +281,12 @@ __device__ __forceinline__ void row_threshold(const TailArgs& a, int64_t i, bool
         const int l = __ffs(rows) - 1;
         rows &= rows - 1;
         const int64_t il = i - (threadIdx.x & 31) + l;
-        const double hs = warp_neumaier_row<F>(a.A + il * a.lda, a.K, nullptr);
+        const uint32_t mz_l = __shfl_sync(0xffffffffu, mnz, l);
+        const float amax_l = __shfl_sync(0xffffffffu, amax, l);
+        double hs;
+        const bool ok16 = warp_exact_sum16<F>(a.A + il * a.lda, a.K, mz_l, amax_l, &hs);
+        if (!ok16) hs = warp_neumaier_row<F>(a.A + il * a.lda, a.K, nullptr);
+        if ((threadIdx.x & 31) == 0) atomicAdd(&g_tail_dbg[ok16 ? 0 : 1], 1ull);
         if ((threadIdx.x & 31) == l) sum = hs;
     }
     if (!valid) {

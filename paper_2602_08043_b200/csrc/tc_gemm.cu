@@ -1124,6 +1124,15 @@ void tc_gemm_launch(int fmt, bool b_kmajor, int64_t M, int64_t N, int64_t K, con
 }  // namespace vabft_dev
 
 // developer timeline read-back (not part of the C-ABI header)
+extern "C" int vabft_debug_tail(unsigned long long* out4, int reset) {
+    if (cudaMemcpyFromSymbol(out4, vabft_dev::g_tail_dbg, sizeof(unsigned long long) * 4) != cudaSuccess) return 1;
+    if (reset) {
+        const unsigned long long z[4] = {0, 0, 0, 0};
+        if (cudaMemcpyToSymbol(vabft_dev::g_tail_dbg, z, sizeof(z)) != cudaSuccess) return 1;
+    }
+    return 0;
+}
+
 extern "C" int vabft_debug_trace(unsigned long long* out, int n, int reset) {
     if (cudaMemcpyFromSymbol(out, vabft_dev::g_trace, sizeof(unsigned long long) * size_t(n)) != cudaSuccess) return 1;
     if (reset) {

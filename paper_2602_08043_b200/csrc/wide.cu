@@ -23,6 +23,8 @@
 // doubles). Per k pair: 16 LDS.128 for 128 DFMA — the FP64 pipe (64 DFMA /
 // clk / SM) is the bound, not shared memory.
 #include <algorithm>
+#include <cstdio>
+#include <cstdlib>
 #include <type_traits>
 
 #include "devcommon.cuh"
@@ -233,6 +235,16 @@ __global__ void __launch_bounds__(kDThreads, 1) dgemm_kernel(const __grid_consta
 // localization and the optional correction (detect.cpp:9-64): the whole
 // verify tail, in the same kernel. A-ABFT with computed y (global max|A|
 // first) stages the row statistics instead and verifies in wide_tail_kernel.
+// developer timeline (VABFT_APART_TRACE=1): [0] first CTA start, [1] last
+// warp's streaming done, [2] last group finished, [3] first group finished,
+// [4] first warp's streaming done
+__device__ unsigned long long g_ap_trace[8];
+__device__ __forceinline__ unsigned long long ap_now() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+
 template <class W>
 struct APart {  // per (block, row) partial arrays, group-major (ap_index)
     W *p1, *p2;
@@ -266,6 +278,7 @@ struct ApJob {
     APart<W> part;
     unsigned* gcnt;          // [ceil(M/32)] block arrivals per row group (self-resetting)
     int finish;              // 1: verdicts in this kernel; 0: stage the row statistics
+    int trace;               // developer timeline (g_ap_trace)
     double *mean, *vb, *mx, *mn, *cr1, *cr2;  // staging (finish == 0)
 };
 
@@ -533,8 +546,14 @@ __global__ void __launch_bounds__(32 * kApWarps, F == VABFT_FP64 ? 1 : 2)
             __threadfence();
             if (lane == 0) j.gcnt[rg] = 0u;  // ready for the next launch
             ap_finish_group<F, W>(j, rg);
+            if (j.trace && lane == 0) {
+                const unsigned long long t = ap_now();
+                atomicMax(&g_ap_trace[2], t);
+                atomicMin(&g_ap_trace[3], t);
+            }
         }
     };
+    if (j.trace && threadIdx.x == 0) atomicMin(&g_ap_trace[0], ap_now());
     int64_t pending = -1;  // row group of the task whose arrival is deferred
     int slot = 0, wslot = 0;
     int64_t t = int64_t(blockIdx.x) * kApWarps + w;
@@ -546,6 +565,11 @@ __global__ void __launch_bounds__(32 * kApWarps, F == VABFT_FP64 ? 1 : 2)
         // for the deferred arrival's fence
         cp_async_wait<0>();
         __syncwarp();
+        if (t >= tasks && j.trace && lane == 0) {
+            const unsigned long long now = ap_now();
+            atomicMax(&g_ap_trace[1], now);
+            atomicMin(&g_ap_trace[4], now);
+        }
         if (pending >= 0) {
             arrive(pending);
             pending = -1;
@@ -755,7 +779,24 @@ void launch_wide_aside(const WideTail& t, const void* br1, const void* br2, void
         attr[0].val.programmaticStreamSerializationAllowed = 1;
         cfg.attrs = attr;
         cfg.numAttrs = 1;
+        static const int trc = [] {
+            const char* e = std::getenv("VABFT_APART_TRACE");
+            return e ? std::atoi(e) : 0;
+        }();
+        j.trace = trc;
+        if (trc) {
+            const unsigned long long init[8] = {~0ull, 0, 0, ~0ull, ~0ull, 0, 0, 0};
+            check_cuda(cudaMemcpyToSymbolAsync(g_ap_trace, init, sizeof(init), 0, cudaMemcpyHostToDevice, stream), "trace");
+        }
         check_cuda(cudaLaunchKernelEx(&cfg, kern, static_cast<const T*>(t.A), j), "wide A-side launch");
+        if (trc) {
+            unsigned long long tt[8];
+            check_cuda(cudaMemcpyFromSymbolAsync(tt, g_ap_trace, sizeof(tt), 0, cudaMemcpyDeviceToHost, stream), "trace");
+            check_cuda(cudaStreamSynchronize(stream), "trace");
+            auto us = [&](int i) { return double(tt[i] - tt[0]) * 1e-3; };
+            std::fprintf(stderr, "apart trace M=%lld K=%lld grid=%d: first-warp-done %.2f last-warp-done %.2f first-group %.2f last-group %.2f us\n",
+                         (long long)t.M, (long long)t.K, grid, us(4), us(1), us(3), us(2));
+        }
     };
     if (t.fmt == VABFT_FP64) run(double{});
     else if (t.fmt == VABFT_FP32) run(float{});

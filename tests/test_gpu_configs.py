@@ -449,3 +449,42 @@ def test_leading_dimensions_match_dense_calls(env, mode):
         assert torch.equal(a, b)
     g_s.close()
     g_d.close()
+
+
+def test_guard_failing_tie_rows_bit_exact(env):
+    """BF16 rows of O(1) and ~1e-10 entries whose exact sum lies EXACTLY on a
+    rounding midpoint of doubles (about one such row in seven): a margin test
+    cannot decide them, the integer exact sum inside the fused GEMM does
+    (tail.cuh warp_exact_sum16: the reference's Neumaier compensation adds
+    exactly for these rows, so fl(sum + comp) = fl(E), ties to even).
+    Thresholds of the tie rows bit-exact against the reference's
+    vabft_thresholds (stats.cpp:12-24, threshold_vabft.cpp:54-61)."""
+    from fractions import Fraction
+
+    torch, O = env
+    from paper_2602_08043_b200.fused import FusedAbftGemm
+    m, k, n = 512, 4096, 512
+    dA, dB = _inputs(torch, m, k, n, torch.bfloat16, 33)
+    rows = torch.arange(0, m, 4, device="cuda")  # 128 rows
+    g = torch.Generator(device="cuda").manual_seed(34)
+    tiny = torch.rand(len(rows), k, device="cuda", generator=g) < 0.5
+    dA[rows] = torch.where(tiny, dA[rows].float() * 1e-10, dA[rows].float()).bfloat16()
+    hA = dA.float().double().cpu().numpy()
+    ties = []
+    for r in rows.tolist():
+        E = sum((Fraction(float(v)) for v in hA[r] if v != 0.0), Fraction(0))
+        hi = float(E)
+        lo = E - Fraction(hi)
+        if lo != 0 and abs(lo) == abs(Fraction(np.nextafter(hi, np.inf if lo > 0 else -np.inf)) - Fraction(hi)) / 2:
+            ties.append(r)
+    assert len(ties) >= 5, ties
+    h = FusedAbftGemm(dB)
+    counts = torch.zeros(6, dtype=torch.int64, device="cuda")
+    res = h(dA, counts=counts)
+    torch.cuda.synchronize()
+    assert int(counts[4].item()) >= len(rows) // 2, counts.tolist()
+    S = torch.tensor(ties + [1, 2, 3], device="cuda")
+    T_ref, _ = O.vabft_thresholds(dA[S].double().cpu().numpy(), dB.double().cpu().numpy(), h.opts.e_max, fmt="bf16")
+    assert _same(res.T[S].cpu().numpy(), T_ref)
+    assert int(counts[1].item()) == 0
+    h.close()
