@@ -276,7 +276,7 @@ struct ApJob {
     WideTail t;              // verdict arguments (t.apart / t.mean ... unused here)
     const W *br1, *br2;      // B r1 / B r2 in the working type (FP32: the handle's float copies)
     APart<W> part;
-    unsigned* gcnt;          // [ceil(M/32)] block arrivals per row group (self-resetting)
+    unsigned* gcnt;          // [0]: the pass's task counter (zero at rest; the combine kernel resets it)
     int finish;              // 1: verdicts in this kernel; 0: stage the row statistics
     int trace;               // developer timeline (g_ap_trace)
     double *mean, *vb, *mx, *mn, *cr1, *cr2;  // staging (finish == 0)
@@ -404,10 +404,45 @@ __device__ __forceinline__ void wide_row_sums(const WideTail& a, int64_t i, doub
     r2 = double(s2);
 }
 
+// Sources of a row group's partials for ap_finish_group (lane = row i):
+// straight from L2 (ApGlobal), or staged in shared memory by bulk copies
+// (ApStaged: every array of the group lands in one round trip).
+template <class W>
+struct ApGlobal {
+    const APart<W>& part;
+    const WideTail& a;
+    size_t o0;  // ap_index(0, i, nb)
+    int64_t i;
+    __device__ W p1(int64_t b) const { return __ldcg(part.p1 + o0 + size_t(b) * 32); }
+    __device__ W p2(int64_t b) const { return __ldcg(part.p2 + o0 + size_t(b) * 32); }
+    __device__ double s(int64_t b) const { return __ldcg(part.s + o0 + size_t(b) * 32); }
+    __device__ double c(int64_t b) const { return __ldcg(part.c + o0 + size_t(b) * 32); }
+    __device__ double sabs(int64_t b) const { return __ldcg(part.sabs + o0 + size_t(b) * 32); }
+    __device__ double mx(int64_t b) const { return __ldcg(part.mx + o0 + size_t(b) * 32); }
+    __device__ double mn(int64_t b) const { return __ldcg(part.mn + o0 + size_t(b) * 32); }
+    __device__ W cp1(int64_t b) const { return __ldcg(static_cast<const W*>(a.part1) + i + b * a.ld); }
+    __device__ W cp2(int64_t b) const { return __ldcg(static_cast<const W*>(a.part2) + i + b * a.ld); }
+};
+template <class W>
+struct ApStaged {
+    const W *sp1, *sp2, *scp1, *scp2;
+    const double *ss, *sc, *ssabs, *smx, *smn;
+    int lane;
+    __device__ W p1(int64_t b) const { return sp1[b * 32 + lane]; }
+    __device__ W p2(int64_t b) const { return sp2[b * 32 + lane]; }
+    __device__ double s(int64_t b) const { return ss[b * 32 + lane]; }
+    __device__ double c(int64_t b) const { return sc[b * 32 + lane]; }
+    __device__ double sabs(int64_t b) const { return ssabs[b * 32 + lane]; }
+    __device__ double mx(int64_t b) const { return smx[b * 32 + lane]; }
+    __device__ double mn(int64_t b) const { return smn[b * 32 + lane]; }
+    __device__ W cp1(int64_t b) const { return scp1[b * 32 + lane]; }
+    __device__ W cp2(int64_t b) const { return scp2[b * 32 + lane]; }
+};
+
 // Finish a row group (lane = row): A statistics and checksums, then either
 // the verdicts (finish) or the staged statistics.
-template <int F, class W>
-__device__ __forceinline__ void ap_finish_group(const ApJob<W>& j, int64_t rg) {
+template <int F, class W, class Src>
+__device__ __forceinline__ void ap_finish_group(const ApJob<W>& j, int64_t rg, const Src& src) {
     using T = typename Elem<F>::T;
     const WideTail& a = j.t;
     const int lane = threadIdx.x & 31;
@@ -417,18 +452,16 @@ __device__ __forceinline__ void ap_finish_group(const ApJob<W>& j, int64_t rg) {
     W t1 = W(0), t2 = W(0);
     double s = 0.0, c = 0.0, sabs = 0.0, mx = -INFINITY, mn = INFINITY;
     if (valid) {
-        const size_t o0 = ap_index(0, i, nb);
 #pragma unroll 8
         for (int64_t b = 0; b < nb; ++b) {
-            const size_t o = o0 + size_t(b) * 32;
-            t1 = radd(t1, __ldcg(j.part.p1 + o));
-            t2 = radd(t2, __ldcg(j.part.p2 + o));
+            t1 = radd(t1, src.p1(b));
+            t2 = radd(t2, src.p2(b));
             double tt, err;
-            two_sum(s, __ldcg(j.part.s + o), tt, err);
+            two_sum(s, src.s(b), tt, err);
             s = tt;
-            c = __dadd_rn(__dadd_rn(c, __ldcg(j.part.c + o)), err);
-            sabs = __dadd_rn(sabs, __ldcg(j.part.sabs + o));
-            const double bx = __ldcg(j.part.mx + o), bn = __ldcg(j.part.mn + o);
+            c = __dadd_rn(__dadd_rn(c, src.c(b)), err);
+            sabs = __dadd_rn(sabs, src.sabs(b));
+            const double bx = src.mx(b), bn = src.mn(b);
             mx = mx < bx ? bx : mx;
             mn = bn < mn ? bn : mn;
         }
@@ -469,12 +502,96 @@ __device__ __forceinline__ void ap_finish_group(const ApJob<W>& j, int64_t rg) {
         }
         return;
     }
-    // the GEMM's C-row partials (and C for the correction): the A pass may
-    // have started beside the GEMM's last wave (programmatic launch)
-    griddep_wait();
+    // C r1 / C r2: the GEMM epilogue's per-128-column partials in block order (blocked:128)
     double r1 = 0.0, r2 = 0.0;
-    if (valid) wide_row_sums<W>(a, i, r1, r2);
+    if (valid) {
+        W s1 = W(0), s2 = W(0);
+#pragma unroll 8
+        for (int64_t b = 0; b < a.nblk; ++b) {
+            s1 = radd(s1, src.cp1(b));
+            s2 = radd(s2, src.cp2(b));
+        }
+        r1 = double(s1);
+        r2 = double(s2);
+    }
     wide_verdicts<F>(a, i, valid, r1, r2, mean_i, vb_i, c1, c2);
+}
+
+// Bytes of a row group's partials staged by wide_combine_kernel.
+template <class W>
+__host__ __device__ inline size_t ap_stage_bytes(int64_t nbK, int64_t nbN) {
+    return size_t(nbK) * 32 * (2 * sizeof(W) + 5 * sizeof(double)) + size_t(nbN) * 32 * 2 * sizeof(W);
+}
+constexpr size_t kApStageMax = 200 * 1024;
+
+// The per-row-group combine and verify tail of the wide A pass, one warp per
+// row group, after the streaming pass (programmatic launch: scheduled as the
+// pass's CTAs retire; griddepcontrol.wait for its partials). kStaged: lane 0
+// bulk-copies every partial array of the group into shared memory at once —
+// each array's group span is contiguous (group-major layout), the epilogue's
+// C-row partials are 32-row segments — so the combine costs one L2 round
+// trip instead of one per eight blocks. (Measured before: inline combines by
+// the last-arriving streaming warp took 5-8 us each under the streaming load
+// and stalled that warp's next task; the pass ended 8 us after its last
+// task.)
+template <int F, class W, bool kStaged>
+__global__ void __launch_bounds__(32) wide_combine_kernel(const __grid_constant__ ApJob<W> j) {
+    extern __shared__ __align__(16) uint8_t cb[];
+    __shared__ __align__(8) uint64_t bar;
+    const int lane = threadIdx.x & 31;
+    const int64_t rg = blockIdx.x;
+    const WideTail& a = j.t;
+    const int64_t nb = (a.K + 127) / 128;
+    griddep_wait();  // the A pass (which itself waited for the GEMM) complete: partials visible
+    if constexpr (kStaged) {
+        const int64_t nbN = j.finish ? a.nblk : 0;
+        W* sp1 = reinterpret_cast<W*>(cb);
+        W* sp2 = sp1 + nb * 32;
+        double* ss = reinterpret_cast<double*>(sp2 + nb * 32);
+        double* sc = ss + nb * 32;
+        double* ssabs = sc + nb * 32;
+        double* smx = ssabs + nb * 32;
+        double* smn = smx + nb * 32;
+        W* scp1 = reinterpret_cast<W*>(smn + nb * 32);
+        W* scp2 = scp1 + nbN * 32;
+        const uint32_t b0 = smem_u32(&bar);
+        if (lane == 0) {
+            mbar_init(b0, 1);
+            fence_mbar_init();
+        }
+        __syncwarp();
+        if (lane == 0) {
+            const uint32_t wbytes = uint32_t(nb * 32 * sizeof(W)), dbytes = uint32_t(nb * 32 * sizeof(double));
+            mbar_arrive_expect_tx(b0, uint32_t(ap_stage_bytes<W>(nb, nbN)));
+            const size_t o = ap_index(0, rg * 32, nb);
+            bulk_load(smem_u32(sp1), j.part.p1 + o, wbytes, b0);
+            bulk_load(smem_u32(sp2), j.part.p2 + o, wbytes, b0);
+            bulk_load(smem_u32(ss), j.part.s + o, dbytes, b0);
+            bulk_load(smem_u32(sc), j.part.c + o, dbytes, b0);
+            bulk_load(smem_u32(ssabs), j.part.sabs + o, dbytes, b0);
+            bulk_load(smem_u32(smx), j.part.mx + o, dbytes, b0);
+            bulk_load(smem_u32(smn), j.part.mn + o, dbytes, b0);
+        }
+        // the C-row partials: nbN segments of 32 rows per array, 4 copies in flight per lane
+        for (int64_t b = lane; b < nbN; b += 32) {
+            const size_t o = size_t(b) * size_t(a.ld) + size_t(rg) * 32;
+            bulk_load(smem_u32(scp1 + b * 32), static_cast<const W*>(a.part1) + o, uint32_t(32 * sizeof(W)), b0);
+            bulk_load(smem_u32(scp2 + b * 32), static_cast<const W*>(a.part2) + o, uint32_t(32 * sizeof(W)), b0);
+        }
+        mbar_wait(b0, 0);
+        const ApStaged<W> src{sp1, sp2, scp1, scp2, ss, sc, ssabs, smx, smn, lane};
+        ap_finish_group<F, W>(j, rg, src);
+    } else {
+        const int64_t i = rg * 32 + lane;
+        const ApGlobal<W> src{j.part, a, ap_index(0, i, nb), i};
+        ap_finish_group<F, W>(j, rg, src);
+    }
+    if (blockIdx.x == 0 && lane == 0) *j.gcnt = 0u;  // the pass's task counter, for the next launch
+    if (j.trace && lane == 0) {
+        const unsigned long long t = ap_now();
+        atomicMax(&g_ap_trace[2], t);
+        atomicMin(&g_ap_trace[3], t);
+    }
 }
 
 template <int F, class W, bool kVec>
@@ -535,46 +652,25 @@ __global__ void __launch_bounds__(32 * kApWarps, F == VABFT_FP64 ? 1 : 2)
             }
         }
     };
-    auto arrive = [&](int64_t rg) {
-        // every lane's partial stores before lane 0's release RMW; the last
-        // arriver then reads all partials through L2 (.cg) after a fence
-        __syncwarp();
-        unsigned old = 0;
-        if (lane == 0) old = atom_add_release_gpu(j.gcnt + rg, 1u);
-        old = __shfl_sync(0xffffffffu, old, 0);
-        if (old == unsigned(nb) - 1u) {
-            __threadfence();
-            if (lane == 0) j.gcnt[rg] = 0u;  // ready for the next launch
-            ap_finish_group<F, W>(j, rg);
-            if (j.trace && lane == 0) {
-                const unsigned long long t = ap_now();
-                atomicMax(&g_ap_trace[2], t);
-                atomicMin(&g_ap_trace[3], t);
-            }
-        }
-    };
     if (j.trace && threadIdx.x == 0) atomicMin(&g_ap_trace[0], ap_now());
-    int64_t pending = -1;  // row group of the task whose arrival is deferred
+    griddep_launch_dependents();  // the combine kernel's CTAs take the SMs this pass leaves
     int slot = 0, wslot = 0;
-    int64_t t = int64_t(blockIdx.x) * kApWarps + w;
+    // Tasks are claimed in order from a counter (j.gcnt[0], reset by the
+    // combine kernel): the claim goes out two sub-tiles before a task's end
+    // and its result is read at the task's last sub-tile, where the next
+    // task's first loads go out. (Static dealing left 27 % of the warps idle
+    // in the second round of a 4096^2 pass: 4096 tasks over 2368 warps.)
+    auto claim = [&]() {
+        unsigned old = 0;
+        if (lane == 0) old = atomicAdd(j.gcnt, 1u);
+        return old;
+    };
+    int64_t t = int64_t(__shfl_sync(0xffffffffu, claim(), 0));
     if (t < tasks) issue(t, 0, 0, 0);
     cp_async_commit();
-    for (;; t += nt) {
-        // the task's first sub-tile and weights were issued during the previous
-        // task's last sub-tile; with them landed no copy of ours is in flight
-        // for the deferred arrival's fence
-        cp_async_wait<0>();
-        __syncwarp();
-        if (t >= tasks && j.trace && lane == 0) {
-            const unsigned long long now = ap_now();
-            atomicMax(&g_ap_trace[1], now);
-            atomicMin(&g_ap_trace[4], now);
-        }
-        if (pending >= 0) {
-            arrive(pending);
-            pending = -1;
-        }
-        if (t >= tasks) break;
+    while (t < tasks) {
+        unsigned pend = 0;  // the next task's claim, issued two sub-tiles before it is needed
+        int64_t tn = tasks;
         const int64_t rg = t / nb, b = t - rg * nb;
         const int64_t r0 = rg * 32, c0 = b * 128;
         const int bw = int(K - c0 < 128 ? K - c0 : 128);
@@ -585,8 +681,15 @@ __global__ void __launch_bounds__(32 * kApWarps, F == VABFT_FP64 ? 1 : 2)
         T sabs = T(0), mx = T(-INFINITY), mn = T(INFINITY);
         for (int q = 0; q < nsub; ++q) {
             const int64_t cq = c0 + int64_t(q) * 32;
-            if (q + 1 < nsub) issue(t, q + 1, slot ^ 1, wslot);
-            else if (t + nt < tasks) issue(t + nt, 0, slot ^ 1, wslot ^ 1);
+            // (claimed late enough that the claim order follows the warps'
+            // progress — a claim at the task start dealt the tasks statically)
+            if (q == (nsub > 2 ? nsub - 2 : 0)) pend = claim();
+            if (q + 1 < nsub) {
+                issue(t, q + 1, slot ^ 1, wslot);
+            } else {
+                tn = int64_t(__shfl_sync(0xffffffffu, pend, 0));
+                if (tn < tasks) issue(tn, 0, slot ^ 1, wslot ^ 1);
+            }
             cp_async_commit();
             cp_async_wait<1>();  // this sub-tile (and the task's weights) landed
             __syncwarp();
@@ -674,8 +777,14 @@ __global__ void __launch_bounds__(32 * kApWarps, F == VABFT_FP64 ? 1 : 2)
             j.part.mx[o] = double(mx);
             j.part.mn[o] = double(mn);
         }
-        pending = rg;
         wslot ^= 1;
+        t = tn;
+    }
+    cp_async_wait<0>();
+    if (j.trace && lane == 0) {
+        const unsigned long long now = ap_now();
+        atomicMax(&g_ap_trace[1], now);
+        atomicMin(&g_ap_trace[4], now);
     }
     griddep_wait();  // never complete before the GEMM this pass may overlap
 }
@@ -789,6 +898,18 @@ void launch_wide_aside(const WideTail& t, const void* br1, const void* br2, void
             check_cuda(cudaMemcpyToSymbolAsync(g_ap_trace, init, sizeof(init), 0, cudaMemcpyHostToDevice, stream), "trace");
         }
         check_cuda(cudaLaunchKernelEx(&cfg, kern, static_cast<const T*>(t.A), j), "wide A-side launch");
+        // the combine + verify tail: one warp per row group, programmatic launch
+        // after the pass; partials staged in shared memory when they fit
+        const int64_t ngroups = (t.M + 31) / 32;
+        const size_t sbytes = ap_stage_bytes<W>(nb, finish ? t.nblk : 0);
+        const bool staged = sbytes <= kApStageMax;
+        auto ck = staged ? wide_combine_kernel<F, W, true> : wide_combine_kernel<F, W, false>;
+        if (staged) ensure_smem_attr(reinterpret_cast<const void*>(ck), int(sbytes));
+        cudaLaunchConfig_t cc = cfg;
+        cc.gridDim = dim3(unsigned(ngroups));
+        cc.blockDim = dim3(32);
+        cc.dynamicSmemBytes = staged ? sbytes : 0;
+        check_cuda(cudaLaunchKernelEx(&cc, ck, j), "wide combine launch");
         if (trc) {
             unsigned long long tt[8];
             check_cuda(cudaMemcpyFromSymbolAsync(tt, g_ap_trace, sizeof(tt), 0, cudaMemcpyDeviceToHost, stream), "trace");
