@@ -529,8 +529,8 @@ constexpr size_t kApStageMax = 200 * 1024;
 // pass's CTAs retire; griddepcontrol.wait for its partials). kStaged: lane 0
 // bulk-copies every partial array of the group into shared memory at once —
 // each array's group span is contiguous (group-major layout), the epilogue's
-// C-row partials are 32-row segments — so the combine costs one L2 round
-// trip instead of one per eight blocks. (Measured before: inline combines by
+// C-row partials are coalesced 32-row segments loaded alongside — so the
+// combine costs about one L2 round trip instead of one per eight blocks. (Measured before: inline combines by
 // the last-arriving streaming warp took 5-8 us each under the streaming load
 // and stalled that warp's next task; the pass ended 8 us after its last
 // task.)
@@ -562,7 +562,7 @@ __global__ void __launch_bounds__(32) wide_combine_kernel(const __grid_constant_
         __syncwarp();
         if (lane == 0) {
             const uint32_t wbytes = uint32_t(nb * 32 * sizeof(W)), dbytes = uint32_t(nb * 32 * sizeof(double));
-            mbar_arrive_expect_tx(b0, uint32_t(ap_stage_bytes<W>(nb, nbN)));
+            mbar_arrive_expect_tx(b0, uint32_t(ap_stage_bytes<W>(nb, 0)));
             const size_t o = ap_index(0, rg * 32, nb);
             bulk_load(smem_u32(sp1), j.part.p1 + o, wbytes, b0);
             bulk_load(smem_u32(sp2), j.part.p2 + o, wbytes, b0);
@@ -572,11 +572,15 @@ __global__ void __launch_bounds__(32) wide_combine_kernel(const __grid_constant_
             bulk_load(smem_u32(smx), j.part.mx + o, dbytes, b0);
             bulk_load(smem_u32(smn), j.part.mn + o, dbytes, b0);
         }
-        // the C-row partials: nbN segments of 32 rows per array, 4 copies in flight per lane
-        for (int64_t b = lane; b < nbN; b += 32) {
-            const size_t o = size_t(b) * size_t(a.ld) + size_t(rg) * 32;
-            bulk_load(smem_u32(scp1 + b * 32), static_cast<const W*>(a.part1) + o, uint32_t(32 * sizeof(W)), b0);
-            bulk_load(smem_u32(scp2 + b * 32), static_cast<const W*>(a.part2) + o, uint32_t(32 * sizeof(W)), b0);
+        // the C-row partials (32-row segments at stride ld): coalesced loads,
+        // 32 in flight per lane, parked in shared memory (each lane reads back
+        // only its own row) while the bulk copies land. (Per-lane bulk copies
+        // serialise: the compiler loops over the lanes with ELECT / R2UR.)
+#pragma unroll 16
+        for (int64_t b = 0; b < nbN; ++b) {
+            const size_t o = size_t(b) * size_t(a.ld) + size_t(rg) * 32 + size_t(lane);
+            scp1[b * 32 + lane] = __ldcg(static_cast<const W*>(a.part1) + o);
+            scp2[b * 32 + lane] = __ldcg(static_cast<const W*>(a.part2) + o);
         }
         mbar_wait(b0, 0);
         const ApStaged<W> src{sp1, sp2, scp1, scp2, ss, sc, ssabs, smx, smn, lane};
