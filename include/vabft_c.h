@@ -196,6 +196,20 @@ vabft_status vabft_vabft_thresholds(int32_t format, int64_t m, int64_t n, int64_
                                     const void* B, double e_max, double c_sigma, double* T,
                                     double* b_summary_out, void* stream);
 
+/* Block-wise (tile-level) V-ABFT thresholds (PAPER.md "Integration with
+ * Block-wise ABFT"): the composition of vabft_thresholds
+ * (threshold_vabft.cpp:54-61) over slices, T[i][J] = sum over the k-tiles kt,
+ * in order, of the V-ABFT threshold of row i of A[:, kt] against B[kt, J]
+ * with n = |J| and e_max_per_tile[kt] (HOST array of ceil(K / tile_k)
+ * values). T: device array M x ceil(N / tile_n), row-major. lda / ldb: row
+ * strides in elements (0 = dense). Replaces the host loop over slice pairs
+ * (paper_2602_08043_b200/blockwise.py) by three launches. Synchronizes
+ * `stream` to report non-finite input (VABFT_DOMAIN_ERROR). */
+vabft_status vabft_blockwise_thresholds(int32_t format, int64_t m, int64_t n, int64_t k, const void* A,
+                                        int64_t lda, const void* B, int64_t ldb, int64_t tile_k,
+                                        int64_t tile_n, const double* e_max_per_tile, double c_sigma,
+                                        double* T, void* stream);
+
 /* aabft_threshold (threshold_aabft.cpp:50-60): fills M doubles with the
  * row-independent bound confidence_multiplier * aabft_sigma(K, t, y);
  * *y_used / *degenerate (y == 0) are host outputs. fixed_y = NaN selects

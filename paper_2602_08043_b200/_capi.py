@@ -93,6 +93,8 @@ _SIGS = {
     "vabft_row_sums": (_st, [C.POINTER(Precision), _i32, _i64, _i64, _vp, _vp, _vp, _vp]),
     "vabft_row_stats": (_st, [_i32, _i64, _i64, _vp, _vp, _vp, _vp, _vp, _vp]),
     "vabft_vabft_thresholds": (_st, [_i32, _i64, _i64, _i64, _vp, _vp, _d, _d, _vp, _vp, _vp]),
+    "vabft_blockwise_thresholds": (_st, [_i32, _i64, _i64, _i64, _vp, _i64, _vp, _i64, _i64, _i64, _vp, _d, _vp,
+                                         _vp]),
     "vabft_aabft_threshold": (_st, [_i32, _i64, _i64, _i64, _vp, _vp, _i32, _d, _d, _vp, _dp,
                                     C.POINTER(C.c_int32), _vp]),
     "vabft_verify": (_st, [C.POINTER(Precision), _i32, _i64, _i64, _vp, _vp, _vp, _vp, _d, Verdicts, _vp, _vp]),

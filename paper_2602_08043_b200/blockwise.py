@@ -21,8 +21,11 @@ from dataclasses import dataclass
 from typing import List, Optional
 
 import numpy as np
+import torch
 
-from . import api
+from . import _capi, api
+from ._capi import check, lib
+from .device import ptr, stream_ptr, to_device, to_host
 
 
 @dataclass
@@ -43,12 +46,44 @@ def k_tiles(k: int, tile_k: int) -> List[tuple]:
     return [(k0, min(k0 + tile_k, k)) for k0 in range(0, k, tile_k)]
 
 
+def _tile_emax(fmt: str, k: int, tile_k: int, e_max: Optional[float]) -> np.ndarray:
+    return np.array([e_max if e_max is not None else api.resolve_e_max(fmt, k1 - k0) for (k0, k1) in k_tiles(k, tile_k)],
+                    dtype=np.float64)
+
+
+def blockwise_thresholds_device(A: torch.Tensor, B: torch.Tensor, fmt: str, tile_k: int = 1024, tile_n: int = 256,
+                                e_max: Optional[float] = None, c_sigma: float = 2.5) -> torch.Tensor:
+    """T[i, J] for CUDA operands in their storage format (bf16 / fp16 / fp32 /
+    fp64 tensors, row strides honoured): one C-ABI call, three launches
+    (csrc/blockwise.cu) — segment row statistics, the per-(k-tile, block)
+    B summaries as independent chains, the k-tile sums. Returns an M x nJ
+    float64 CUDA tensor."""
+    m, k = A.shape
+    n = B.shape[1]
+    if B.shape[0] != k:
+        raise _capi.InvalidArgument("blockwise_thresholds: inner dimensions disagree")
+    if A.stride(1) != 1 or B.stride(1) != 1:
+        raise _capi.InvalidArgument("blockwise_thresholds: rows must be contiguous")
+    em = _tile_emax(fmt, k, tile_k, e_max)
+    T = torch.empty(m, (n + tile_n - 1) // tile_n, dtype=torch.float64, device=A.device)
+    check(lib.vabft_blockwise_thresholds(api._spec(fmt).code, m, n, k, ptr(A), A.stride(0), ptr(B), B.stride(0),
+                                         tile_k, tile_n, em.ctypes.data, c_sigma, ptr(T), stream_ptr()))
+    return T
+
+
 def blockwise_thresholds(a: np.ndarray, b: np.ndarray, fmt: str, tile_k: int = 1024, tile_n: int = 256,
-                         e_max: Optional[float] = None, c_sigma: float = 2.5) -> np.ndarray:
+                         e_max: Optional[float] = None, c_sigma: float = 2.5, engine: str = "device") -> np.ndarray:
     """T[i, J] = sum_kt vabft_threshold(A[i, kt], B[kt, J], n = |J|), with
-    e_max per k-tile from the format model at dim = |kt| unless given."""
+    e_max per k-tile from the format model at dim = |kt| unless given.
+    engine "device": one call of the block-wise kernels; "slices": the
+    composition slice pair by slice pair through vabft_thresholds (the
+    reference's own function on each slice — the check of the kernels)."""
     a = np.asarray(a, dtype=np.float64)
     b = np.asarray(b, dtype=np.float64)
+    if engine == "device":
+        s = api._spec(fmt)
+        return to_host(blockwise_thresholds_device(to_device(a, s.format), to_device(b, s.format), fmt, tile_k,
+                                                   tile_n, e_max, c_sigma))
     m, k = a.shape
     blocks = col_blocks(b.shape[1], tile_n)
     T = np.zeros((m, len(blocks)))

@@ -254,6 +254,37 @@ extern "C" vabft_status vabft_vabft_thresholds(int32_t format, int64_t m, int64_
     });
 }
 
+extern "C" vabft_status vabft_blockwise_thresholds(int32_t format, int64_t m, int64_t n, int64_t k,
+                                                   const void* A, int64_t lda, const void* B, int64_t ldb,
+                                                   int64_t tile_k, int64_t tile_n, const double* e_max_per_tile,
+                                                   double c_sigma, double* T, void* stream) {
+    return guarded([&] {
+        check_fmt(format);
+        if (!A || !B || !T || !e_max_per_tile) fail(VABFT_INVALID_ARGUMENT, "blockwise_thresholds: null argument");
+        if (m < 1 || n < 1 || k < 1) fail(VABFT_INVALID_ARGUMENT, "dims must be >= 1");
+        if (tile_k < 1 || tile_n < 1) fail(VABFT_INVALID_ARGUMENT, "blockwise_thresholds: tiles must be >= 1");
+        if (lda == 0) lda = k;
+        if (ldb == 0) ldb = n;
+        if (lda < k || ldb < n) fail(VABFT_INVALID_ARGUMENT, "blockwise_thresholds: leading dimension too small");
+        const int64_t nkt = (k + tile_k - 1) / tile_k;
+        for (int64_t t = 0; t < nkt; ++t)  // threshold_row's e_max: the caller's model at dim = |kt|
+            if (!(e_max_per_tile[t] >= 0.0)) fail(VABFT_INVALID_ARGUMENT, "blockwise_thresholds: e_max must be >= 0");
+        cudaStream_t s = as_stream(stream);
+        Tmp tmp(s);
+        double* em = tmp.get<double>(size_t(nkt));
+        check_cuda(cudaMemcpyAsync(em, e_max_per_tile, sizeof(double) * size_t(nkt), cudaMemcpyHostToDevice, s),
+                   "copy");
+        double* work = tmp.get<double>(blockwise_work_doubles(m, n, k, tile_k, tile_n));
+        int* bad = tmp.get<int>(1);
+        check_cuda(cudaMemsetAsync(bad, 0, sizeof(int), s), "memset");
+        launch_blockwise_thresholds(format, m, n, k, A, lda, B, ldb, tile_k, tile_n, em, c_sigma, T, work, bad, s);
+        int h = 0;
+        check_cuda(cudaMemcpyAsync(&h, bad, sizeof(int), cudaMemcpyDeviceToHost, s), "copy");
+        check_cuda(cudaStreamSynchronize(s), "sync");
+        if (h) fail(VABFT_DOMAIN_ERROR, "row_stats: non-finite value");
+    });
+}
+
 extern "C" vabft_status vabft_aabft_threshold(int32_t format, int64_t m, int64_t n, int64_t k,
                                               const void* A, const void* B, int32_t t, double fixed_y,
                                               double conf, double* T, double* y_used,

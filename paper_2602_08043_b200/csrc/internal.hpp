@@ -168,6 +168,11 @@ struct WideTail {
     const void* A = nullptr;  // the A operand (FP32 / FP64), read by the A pass
     int qfmt = -1;            // offline FP32: checksums rounded to the input format
 };
+// blockwise.cu: block-wise V-ABFT thresholds (work: blockwise_work_doubles doubles)
+void launch_blockwise_thresholds(int fmt, int64_t M, int64_t N, int64_t K, const void* A, int64_t lda,
+                                 const void* B, int64_t ldb, int64_t tile_k, int64_t tile_n, const double* e_max,
+                                 double c_sigma, double* T, double* work, int* nonfinite, cudaStream_t s);
+size_t blockwise_work_doubles(int64_t M, int64_t N, int64_t K, int64_t tile_k, int64_t tile_n);
 void launch_wide_tail(const WideTail& t, cudaStream_t stream);
 // A side (wide.cu): one pass over t.A producing the row statistics and the
 // blocked:128 row checksums A (B r) (br1 / br2 in the working type: float

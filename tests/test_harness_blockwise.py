@@ -92,3 +92,29 @@ def test_blockwise_matches_reference_on_slices(ref_or_port):
     e1 = O.encode_and_multiply(A, np.ascontiguousarray(B[:, 8:16]), "bf16", "offline")
     r = O.verify(np.ascontiguousarray(C[:, 8:16]), e1.row_check1, e1.row_check2, T[:, 1], "bf16", "offline")
     assert np.array_equal(v.diff1[:, 1], r["diff1"])
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("fmt", ["bf16", "fp32", "fp16", "fp64"])
+def test_blockwise_device_kernels_equal_slice_composition(fmt):
+    """csrc/blockwise.cu (three launches) equals the slice-by-slice
+    composition of the reference's vabft_thresholds (threshold_vabft.cpp:54-61)
+    bit for bit, with ragged last k-tile and column block, e_max per k-tile
+    from the format model."""
+    import torch
+
+    from paper_2602_08043_b200 import blockwise
+    g = np.random.default_rng(7)
+    m, k, n = 96, 1000, 600
+    A = g.standard_normal((m, k))
+    B = g.standard_normal((k, n)) * 0.05 + 0.01
+    if fmt in ("bf16", "fp16"):
+        dt = torch.bfloat16 if fmt == "bf16" else torch.float16
+        A = torch.from_numpy(A).to(dt).double().numpy()
+        B = torch.from_numpy(B).to(dt).double().numpy()
+    elif fmt == "fp32":
+        A, B = A.astype(np.float32).astype(np.float64), B.astype(np.float32).astype(np.float64)
+    Td = blockwise.blockwise_thresholds(A, B, fmt, tile_k=384, tile_n=128)
+    Ts = blockwise.blockwise_thresholds(A, B, fmt, tile_k=384, tile_n=128, engine="slices")
+    assert Td.shape == (m, 5)
+    assert np.array_equal(Td.view(np.uint64), Ts.view(np.uint64))
