@@ -25,7 +25,7 @@
 extern "C" {
 #endif
 
-#define VABFT_C_API_VERSION 2
+#define VABFT_C_API_VERSION 3
 
 /* Status codes <-> reference exception types (proj/src/*.cpp throw sites). */
 typedef enum vabft_status {
@@ -258,7 +258,8 @@ vabft_status vabft_bside_destroy(vabft_bside_t h);
 /* Options of one fused launch. */
 typedef struct vabft_fused_opts {
     int32_t mode;              /* vabft_verify_mode */
-    int32_t threshold_method;  /* 0 = V-ABFT, 1 = A-ABFT fixed y, 2 = A-ABFT computed y */
+    int32_t threshold_method;  /* 0 = V-ABFT, 1 = A-ABFT fixed y, 2 = A-ABFT computed y,
+                                  3 = [v3] given thresholds t_in (e.g. vabft_blockwise_thresholds) */
     double e_max;              /* V-ABFT e_max (caller-resolved) */
     double c_sigma;            /* 2.5 */
     double floor_scale;        /* DetectOptions::localization_floor_scale, 1e-3 */
@@ -325,6 +326,13 @@ typedef struct vabft_fused_opts {
      * and the matching C[:, n0:n1] run without copies (SURVEY §8(e) N-split). */
     int64_t lda;
     int64_t ldc;
+    /* [v3] threshold_method 3: row i is verified against t_in[i * ldt]
+     * (device doubles, >= 0 — verify's T >= 0 contract, detect.cpp:24-27, is
+     * the caller's; ldt 0 = 1). With vabft_blockwise_thresholds and a column
+     * slice of the weight (vabft_bside_create_ld) each tile_n-column block of
+     * C is verified against its block-wise threshold in the fused kernel. */
+    const double* t_in;
+    int64_t ldt;
 } vabft_fused_opts;
 
 /* Workspace bytes for vabft_fused_gemm at this shape. */

@@ -65,7 +65,7 @@ class FusedOpts(C.Structure):
                 ("n_operand_faults", C.c_int32), ("correct", C.c_int32), ("operand_faults", C.c_void_p),
                 ("operand_fault_records", C.c_void_p), ("cta_mode", C.c_int32), ("tf32_passes", C.c_int32),
                 ("accum_out", C.c_void_p), ("workspace_fresh", C.c_int32), ("reserved_v2", C.c_int32),
-                ("lda", C.c_int64), ("ldc", C.c_int64)]
+                ("lda", C.c_int64), ("ldc", C.c_int64), ("t_in", C.c_void_p), ("ldt", C.c_int64)]
 
 
 _st = C.c_int

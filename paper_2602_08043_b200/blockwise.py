@@ -46,8 +46,15 @@ def k_tiles(k: int, tile_k: int) -> List[tuple]:
     return [(k0, min(k0 + tile_k, k)) for k0 in range(0, k, tile_k)]
 
 
-def _tile_emax(fmt: str, k: int, tile_k: int, e_max: Optional[float]) -> np.ndarray:
-    return np.array([e_max if e_max is not None else api.resolve_e_max(fmt, k1 - k0) for (k0, k1) in k_tiles(k, tile_k)],
+def _tile_emax(fmt: str, k: int, tile_k: int, e_max) -> np.ndarray:
+    """e_max per k-tile: given per tile (a sequence), one value for all, or
+    the format model at dim = |kt| (resolve_e_max)."""
+    tiles = k_tiles(k, tile_k)
+    if e_max is not None and np.ndim(e_max) == 1:
+        if len(e_max) != len(tiles):
+            raise _capi.InvalidArgument("blockwise: one e_max per k-tile")
+        return np.asarray(e_max, dtype=np.float64)
+    return np.array([e_max if e_max is not None else api.resolve_e_max(fmt, k1 - k0) for (k0, k1) in tiles],
                     dtype=np.float64)
 
 
@@ -121,3 +128,88 @@ def blockwise_verify(a: np.ndarray, b: np.ndarray, c: Optional[np.ndarray], fmt:
         first = (loc < 0) & v["detected"] & (v["location"] >= 0)
         loc[first] = v["location"][first] + j0
     return BlockVerdicts(det.any(axis=1), loc, det, d1, T, blocks)
+
+
+@dataclass
+class FusedBlockVerdicts:
+    """Device tensors of blockwise_verify_fused (M x nJ unless noted)."""
+    C: torch.Tensor            # M x N product
+    thresholds: torch.Tensor   # float64
+    block_detected: torch.Tensor  # uint8
+    diff1: torch.Tensor        # float64
+    location: torch.Tensor     # int64, global columns (-1: none)
+    detected: torch.Tensor     # [M] bool: any block of the row flagged
+    col_blocks: List[tuple]
+
+
+class BlockwiseFusedGemm:
+    """Block-wise V-ABFT on the fused path for one weight: per tile_n-column
+    block J a fused handle over B[:, J] (a strided slice for BF16 / FP16 — no
+    copy; the B-side statistics are per weight, built once), and per call the
+    block-wise thresholds from the device kernels, then every block of C
+    computed and verified by the fused tcgen05 kernel as its own ABFT unit
+    (checksum weights local to J, as in the N-split) against T[:, J]
+    (threshold method 3). Located columns are global."""
+
+    def __init__(self, B: torch.Tensor, fmt: str, mode: str = "online", tile_k: int = 1024, tile_n: int = 256,
+                 e_max=None, c_sigma: float = 2.5, **fused_kw):
+        from .fused import FusedAbftGemm
+        self.B, self.fmt, self.mode, self.tile_k, self.tile_n, self.c_sigma = B, fmt, mode, tile_k, tile_n, c_sigma
+        k, n = B.shape
+        if e_max is None:
+            # the device calibration of the engine that accumulates (emax.py:
+            # tcgen05 FP32 accumulation, 3xTF32 / one TF32 pass, DFMA) at each
+            # k-tile's length — the reference's model is the emulator's
+            from .emax import default_e_max
+            name = "tf32" if (fmt == "fp32" and fused_kw.get("tf32_passes", 3) == 1) else fmt
+            e_max = [default_e_max(name, mode, k1 - k0) for (k0, k1) in k_tiles(k, tile_k)]
+        self.e_max = e_max
+        self.blocks = col_blocks(n, tile_n)
+        self.sixteen = B.dtype in (torch.bfloat16, torch.float16)
+        self.handles = []
+        for (j0, j1) in self.blocks:
+            view = self.sixteen and j0 % 8 == 0 and (j1 - j0) % 8 == 0
+            self.handles.append((FusedAbftGemm(B[:, j0:j1] if view else B[:, j0:j1].contiguous(), mode=mode,
+                                               **fused_kw), view))
+
+    def __call__(self, A: torch.Tensor, out: Optional[torch.Tensor] = None,
+                 counts: Optional[torch.Tensor] = None) -> "FusedBlockVerdicts":
+        m = A.shape[0]
+        n = self.B.shape[1]
+        T = blockwise_thresholds_device(A, self.B, self.fmt, self.tile_k, self.tile_n, self.e_max, self.c_sigma)
+        Cm = out if out is not None else torch.empty((m, n), dtype=A.dtype, device=A.device)
+        nJ = len(self.blocks)
+        det = torch.empty((m, nJ), dtype=torch.uint8, device=A.device)
+        d1 = torch.empty((m, nJ), dtype=torch.float64, device=A.device)
+        loc = torch.empty((m, nJ), dtype=torch.int64, device=A.device)
+        for jb, ((j0, j1), (g, view)) in enumerate(zip(self.blocks, self.handles)):
+            o = Cm[:, j0:j1] if view else torch.empty((m, j1 - j0), dtype=A.dtype, device=A.device)
+            r = g(A, out=o, counts=counts, t_in=T[:, jb])
+            if not view:
+                Cm[:, j0:j1] = o
+            det[:, jb] = r.detected
+            d1[:, jb] = r.diff1
+            loc[:, jb] = torch.where(r.location >= 0, r.location + j0, r.location)
+        flagged = det.bool()
+        # the first flagged block with a located column (blockwise_verify's rule)
+        hit = flagged & (loc >= 0)
+        first = hit.int().argmax(dim=1)
+        location = torch.where(hit.any(dim=1), loc.gather(1, first[:, None])[:, 0],
+                               torch.full((m,), -1, dtype=torch.int64, device=A.device))
+        return FusedBlockVerdicts(Cm, T, det, d1, location, flagged.any(dim=1), self.blocks)
+
+    def close(self) -> None:
+        for g, _ in self.handles:
+            g.close()
+        self.handles = []
+
+
+def blockwise_verify_fused(A: torch.Tensor, B: torch.Tensor, fmt: str, mode: str = "online", tile_k: int = 1024,
+                           tile_n: int = 256, e_max=None, c_sigma: float = 2.5,
+                           counts: Optional[torch.Tensor] = None, **fused_kw) -> FusedBlockVerdicts:
+    """One-shot BlockwiseFusedGemm (handles built and released per call)."""
+    g = BlockwiseFusedGemm(B, fmt, mode, tile_k, tile_n, e_max, c_sigma, **fused_kw)
+    try:
+        return g(A, counts=counts)
+    finally:
+        g.close()

@@ -8,15 +8,15 @@
 // every (A[:, kt], B[kt, J]) slice pair and accumulated over the k-tiles —
 // the composition paper_2602_08043_b200/blockwise.py runs slice by slice
 // through the host. Here:
-//   1. seg_stats_kernel: row_stats (stats.cpp:9-32) of every row segment, one
-//      thread per (row, segment) running the reference's sequential Neumaier
-//      loop over its segment — A rows cut into k-tiles, B rows into column
-//      blocks (bit-exact by construction: the same operations in the same
-//      order);
+//   1. seg_stats_kernel: row_stats (stats.cpp:9-32) of every row segment, lane
+//      = row running the reference's sequential Neumaier loop over its
+//      segment from a shared-memory tile — A rows cut into k-tiles, B rows
+//      into column blocks (bit-exact by construction: the same operations in
+//      the same order);
 //   2. seg_summary_kernel: BStatsSummary::from (threshold_vabft.cpp:15-26)
 //      for every (k-tile, column block): three sequential FP64 sums over the
-//      k-tile's rows, one thread per (pair, sum) — independent chains, so
-//      they run side by side instead of one 4096-long chain;
+//      k-tile's rows, one warp per (pair, sum) — independent chains, so they
+//      run side by side instead of one 4096-long chain;
 //   3. blockwise_t_kernel: one thread per (row, column block) adds the
 //      k-tiles' threshold_row totals in k-tile order.
 #include "devcommon.cuh"
@@ -28,55 +28,103 @@ namespace vabft_dev {
 namespace {
 
 // row_stats of X[r][s*seg : min((s+1)*seg, cols)] for every (r, s); out
-// arrays [rows][nseg]. The reference throws on a non-finite value: flagged.
+// arrays [rows][nseg]. A warp takes 32 consecutive rows of one segment: the
+// segment streams through the warp's shared-memory tile in 32 x 32 sub-tiles
+// (lane = column: coalesced row segments; the next sub-tile's loads in
+// registers while this one is folded) and lane = row runs the reference's
+// sequential Neumaier loop over its row's segment — all lanes busy on the
+// FP64 pipe. The reference throws on a non-finite value: flagged.
+constexpr int kSegWarps = 4;
 template <int F>
-__global__ void __launch_bounds__(128) seg_stats_kernel(const typename Elem<F>::T* __restrict__ X, int64_t rows,
-                                                        int64_t cols, int64_t ld, int64_t seg, int64_t nseg,
-                                                        double* mean, double* vb, int* nonfinite) {
-    const int64_t t = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
-    if (t >= rows * nseg) return;
-    const int64_t r = t / nseg, sg = t - r * nseg;
-    const int64_t c0 = sg * seg, c1 = c0 + seg < cols ? c0 + seg : cols;
-    const typename Elem<F>::T* row = X + r * ld;
+__global__ void __launch_bounds__(32 * kSegWarps) seg_stats_kernel(const typename Elem<F>::T* __restrict__ X,
+                                                                   int64_t rows, int64_t cols, int64_t ld,
+                                                                   int64_t seg, int64_t nseg, double* mean,
+                                                                   double* vb, int* nonfinite) {
+    __shared__ double tile[kSegWarps][32][33];
+    const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int64_t ngr = (rows + 31) / 32;
+    const int64_t task = int64_t(blockIdx.x) * kSegWarps + w;  // (row group, segment)
+    if (task >= ngr * nseg) return;
+    const int64_t rg = task / nseg, sg = task - rg * nseg;
+    const int64_t r0 = rg * 32, c0 = sg * seg, c1 = c0 + seg < cols ? c0 + seg : cols;
+    const int nr = int(rows - r0 < 32 ? rows - r0 : 32);
+    const typename Elem<F>::T* base = X + r0 * ld;
+    double v[32];
+    auto load = [&](int64_t cq) {
+        const int64_t c = cq + lane;
+        const bool in = c < c1;
+#pragma unroll
+        for (int rr = 0; rr < 32; ++rr) v[rr] = (rr < nr && in) ? Elem<F>::d(base[rr * ld + c]) : 0.0;
+    };
     Neu n;
-    double mx = Elem<F>::d(row[c0]), mn = mx;
-    bool bad = false;
-    for (int64_t q = c0; q < c1; ++q) {
-        const double x = Elem<F>::d(row[q]);
-        bad |= !isfinite(x);
-        n.add(x);
-        mx = fmax(mx, x);
-        mn = fmin(mn, x);
+    double mx = 0.0, mn = 0.0;
+    bool bad = false, first = true;
+    load(c0);
+    for (int64_t cq = c0; cq < c1; cq += 32) {
+        __syncwarp();
+#pragma unroll
+        for (int rr = 0; rr < 32; ++rr) tile[w][rr][lane] = v[rr];
+        __syncwarp();
+        if (cq + 32 < c1) load(cq + 32);  // in flight during the fold
+        const int cnt = int(c1 - cq < 32 ? c1 - cq : 32);
+        if (first) {
+            mx = mn = tile[w][lane][0];
+            first = false;
+        }
+        for (int e = 0; e < cnt; ++e) {
+            const double x = tile[w][lane][e];
+            bad |= !isfinite(x);
+            n.add(x);
+            mx = fmax(mx, x);
+            mn = fmin(mn, x);
+        }
     }
-    if (bad) atomicExch(nonfinite, 1);
-    double m, v;
-    stats_finish(n, mx, mn, c1 - c0, &m, &v);
-    mean[t] = m;
-    vb[t] = v;
+    if (lane < nr) {
+        if (bad) atomicExch(nonfinite, 1);
+        double m, vv;
+        stats_finish(n, mx, mn, c1 - c0, &m, &vv);
+        const int64_t o = (r0 + lane) * nseg + sg;
+        mean[o] = m;
+        vb[o] = vv;
+    }
 }
 
-// BStatsSummary::from over rows [kt*tile_k, ...) of column block J: thread
-// (kt, J, which) runs sum |mean|, sum mean^2 or sum var_bound in row order.
+// BStatsSummary::from over rows [kt*tile_k, ...) of column block J: one warp
+// per (kt, J, which) — the warp stages the k-tile's values in chunks of 256
+// (coalesced-enough strided loads, all in flight) and lane 0 runs the
+// sequential sum |mean|, sum mean^2 or sum var_bound in row order.
 __global__ void __launch_bounds__(128) seg_summary_kernel(const double* __restrict__ mean,
                                                           const double* __restrict__ vb, int64_t K, int64_t tile_k,
                                                           int64_t nkt, int64_t nJ, double* summary /* [nkt][nJ][3] */) {
-    const int64_t t = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    __shared__ double buf[4][256];
+    const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int64_t t = int64_t(blockIdx.x) * 4 + w;
     if (t >= nkt * nJ * 3) return;
     const int which = int(t % 3);
     const int64_t pair = t / 3, kt = pair / nJ, J = pair - kt * nJ;
     const int64_t k0 = kt * tile_k, k1 = k0 + tile_k < K ? k0 + tile_k : K;
+    const double* src = which == 2 ? vb : mean;
     double acc = 0.0;
-    if (which == 0) {
-        for (int64_t k = k0; k < k1; ++k) acc = __dadd_rn(acc, fabs(mean[k * nJ + J]));
-    } else if (which == 1) {
-        for (int64_t k = k0; k < k1; ++k) {
-            const double x = mean[k * nJ + J];
-            acc = __dadd_rn(acc, __dmul_rn(x, x));
+    for (int64_t c = k0; c < k1; c += 256) {
+        const int cnt = int(k1 - c < 256 ? k1 - c : 256);
+        __syncwarp();
+#pragma unroll
+        for (int e = 0; e < 8; ++e) {
+            const int q = e * 32 + lane;
+            buf[w][q] = q < cnt ? src[(c + q) * nJ + J] : 0.0;
         }
-    } else {
-        for (int64_t k = k0; k < k1; ++k) acc = __dadd_rn(acc, vb[k * nJ + J]);
+        __syncwarp();
+        if (lane == 0) {
+            if (which == 0) {
+                for (int q = 0; q < cnt; ++q) acc = __dadd_rn(acc, fabs(buf[w][q]));
+            } else if (which == 1) {
+                for (int q = 0; q < cnt; ++q) acc = __dadd_rn(acc, __dmul_rn(buf[w][q], buf[w][q]));
+            } else {
+                for (int q = 0; q < cnt; ++q) acc = __dadd_rn(acc, buf[w][q]);
+            }
+        }
     }
-    summary[pair * 3 + which] = acc;
+    if (lane == 0) summary[pair * 3 + which] = acc;
 }
 
 __global__ void __launch_bounds__(256) blockwise_t_kernel(int64_t M, int64_t N, int64_t tile_n, int64_t nkt,
@@ -102,9 +150,9 @@ template <int F>
 void seg_stats(const void* X, int64_t rows, int64_t cols, int64_t ld, int64_t seg, double* mean, double* vb,
                int* nonfinite, cudaStream_t s) {
     const int64_t nseg = (cols + seg - 1) / seg;
-    const int64_t n = rows * nseg;
-    seg_stats_kernel<F><<<unsigned((n + 127) / 128), 128, 0, s>>>(static_cast<const typename Elem<F>::T*>(X), rows,
-                                                                  cols, ld, seg, nseg, mean, vb, nonfinite);
+    const int64_t tasks = (rows + 31) / 32 * nseg;
+    seg_stats_kernel<F><<<unsigned((tasks + kSegWarps - 1) / kSegWarps), 32 * kSegWarps, 0, s>>>(
+        static_cast<const typename Elem<F>::T*>(X), rows, cols, ld, seg, nseg, mean, vb, nonfinite);
 }
 
 }  // namespace
@@ -131,7 +179,7 @@ void launch_blockwise_thresholds(int fmt, int64_t M, int64_t N, int64_t K, const
         default: fail(VABFT_INVALID_ARGUMENT, "bad format");
     }
     const int64_t nch = nkt * nJ * 3;
-    seg_summary_kernel<<<unsigned((nch + 127) / 128), 128, 0, s>>>(bmean, bvb, K, tile_k, nkt, nJ, summary);
+    seg_summary_kernel<<<unsigned((nch + 3) / 4), 128, 0, s>>>(bmean, bvb, K, tile_k, nkt, nJ, summary);
     const int64_t nt = M * nJ;
     blockwise_t_kernel<<<unsigned((nt + 255) / 256), 256, 0, s>>>(M, N, tile_n, nkt, nJ, amean, avb, summary, e_max,
                                                                   c_sigma, T);

@@ -300,6 +300,8 @@ void wide_fused(const vabft_fused_opts* o, vabft_bside* h, int64_t m, const void
     t.bsum = h->buf.summary;
     t.max_abs_a = ws.max_abs_a;
     t.method = o->threshold_method;
+    t.t_in = o->t_in;
+    t.ldt = o->ldt ? o->ldt : 1;
     t.aabft_t = o->aabft_mantissa_bits > 0 ? o->aabft_mantissa_bits : (h->fmt == VABFT_FP64 ? 53 : 23);
     t.e_max = o->e_max;
     t.c_sigma = o->c_sigma;
@@ -429,7 +431,8 @@ extern "C" vabft_status vabft_fused_gemm(const vabft_fused_opts* o, vabft_bside_
     return guarded([&] {
         if (!o || !h || !A || !C || !h->B) fail(VABFT_INVALID_ARGUMENT, "vabft_fused_gemm: null argument");
         if (o->mode != h->mode) fail(VABFT_INVALID_ARGUMENT, "vabft_fused_gemm: mode differs from the B-side handle");
-        if (o->threshold_method < 0 || o->threshold_method > 2) fail(VABFT_INVALID_ARGUMENT, "bad threshold method");
+        if (o->threshold_method < 0 || o->threshold_method > 3) fail(VABFT_INVALID_ARGUMENT, "bad threshold method");
+        if (o->threshold_method == 3 && !o->t_in) fail(VABFT_INVALID_ARGUMENT, "threshold method 3 needs t_in");
         if (o->b_kmajor != h->b_kmajor)
             fail(VABFT_UNSUPPORTED, "vabft_fused_gemm: B layout differs from the B-side handle");
         if (m < 1) fail(VABFT_INVALID_ARGUMENT, "dims must be >= 1");
@@ -486,6 +489,8 @@ extern "C" vabft_status vabft_fused_gemm(const vabft_fused_opts* o, vabft_bside_
         a.Tv = ws.Tv;
         a.max_abs_a = ws.max_abs_a;
         a.method = o->threshold_method;
+        a.t_in = o->t_in;
+        a.ldt = o->ldt ? o->ldt : 1;
         a.aabft_t = o->aabft_mantissa_bits > 0 ? o->aabft_mantissa_bits : (h->fmt == VABFT_BF16 ? 8 : 11);
         a.quantize_cr = offline ? 1 : 0;
         a.e_max = o->e_max;

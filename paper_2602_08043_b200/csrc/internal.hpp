@@ -58,6 +58,8 @@ struct TailArgs {
     int method, aabft_t, quantize_cr;
     double e_max, c_sigma, aabft_fixed_y, aabft_conf, floor_scale;
     double* T_out;
+    const double* t_in = nullptr;  // threshold_method 3: given thresholds t_in[i * ldt]
+    int64_t ldt = 1;
     vabft_verdicts v;
     int64_t* counts;
     // in-kernel correction (detect.cpp:57-64): C[i][j] = quantize(C[i][j] - diff1)
@@ -158,6 +160,8 @@ struct WideTail {
     const double *cr1, *cr2;               // row checksums A (B r), staged
     const double* bsum;                    // B summary (4)
     const double* max_abs_a;               // A-ABFT computed y
+    const double* t_in = nullptr;          // threshold_method 3: given thresholds t_in[i * ldt]
+    int64_t ldt = 1;
     int method, aabft_t;
     double e_max, c_sigma, aabft_fixed_y, aabft_conf, floor_scale;
     double* T_out;

@@ -322,6 +322,8 @@ __device__ __forceinline__ void row_verdict(const TailArgs& a, int64_t i, bool v
         double t;
         if (a.method == 0) {
             t = tv;
+        } else if (a.method == 3) {
+            t = a.t_in[i * a.ldt];
         } else {
             const double y = a.method == 1 ? a.aabft_fixed_y : __dmul_rn(*a.max_abs_a, a.bsum[3]);
             t = aabft_total(a.K, a.aabft_t, y, a.aabft_conf);

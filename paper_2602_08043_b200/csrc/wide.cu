@@ -327,6 +327,8 @@ __device__ __forceinline__ void wide_verdicts(const WideTail& a, int64_t i, bool
         double t;
         if (a.method == 0) {
             t = vabft_threshold_total(mean_i, vb_i, a.bsum[0], a.bsum[1], a.bsum[2], a.N, a.e_max, a.c_sigma);
+        } else if (a.method == 3) {
+            t = a.t_in[i * a.ldt];
         } else {
             const double y = a.method == 1 ? a.aabft_fixed_y : __dmul_rn(*a.max_abs_a, a.bsum[3]);
             t = aabft_total(a.K, a.aabft_t, y, a.aabft_conf);

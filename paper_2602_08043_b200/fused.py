@@ -111,14 +111,17 @@ class FusedAbftGemm:
     def __call__(self, A: torch.Tensor, out: Optional[torch.Tensor] = None, *, verdicts: bool = True,
                  thresholds: bool = True, counts: Optional[torch.Tensor] = None,
                  faults: Optional[dict] = None, stages: int = 0, checksums: bool = False,
-                 correct: bool = False, accum_out: Optional[torch.Tensor] = None) -> FusedResult:
+                 correct: bool = False, accum_out: Optional[torch.Tensor] = None,
+                 t_in: Optional[torch.Tensor] = None) -> FusedResult:
         """faults: {"target": "output" | "A" | "B", ...}. output / A: per-row
         int32 tensors "col" (output column, or the k index of A[i][k]; < 0 =
         none), "bit", "dir" and optional "records" (M x 24-byte records). B:
         "operand" = operand_faults(...) and optional "records" (per fault).
         correct: in-kernel correction of located single errors.
         accum_out: M x N FP32 tensor receiving the (post-injection) FP32
-        accumulator that online verification reads (BF16 / FP16 weights)."""
+        accumulator that online verification reads (BF16 / FP16 weights).
+        t_in: given thresholds (threshold method 3) — a float64 CUDA vector of
+        M values, any stride (e.g. a column of blockwise_thresholds_device)."""
         if A.dtype != self.B.dtype or A.dim() != 2 or A.shape[1] != self.k:
             raise _capi.InvalidArgument("FusedAbftGemm: A must be M x K with B's dtype")
         m = A.shape[0]
@@ -177,6 +180,13 @@ class FusedAbftGemm:
                 raise _capi.InvalidArgument("accum_out must be a contiguous M x N float32 tensor")
             opts = _capi.FusedOpts.from_buffer_copy(opts)
             opts.accum_out = ptr(accum_out)
+        if t_in is not None:
+            if t_in.dtype != torch.float64 or t_in.dim() != 1 or t_in.shape[0] != m or not t_in.is_cuda:
+                raise _capi.InvalidArgument("t_in must be an M-vector of float64 on the device")
+            opts = _capi.FusedOpts.from_buffer_copy(opts)
+            opts.threshold_method = 3
+            opts.t_in = ptr(t_in)
+            opts.ldt = t_in.stride(0)
         if A.stride(0) != self.k or C_.stride(0) != self.n:
             opts = _capi.FusedOpts.from_buffer_copy(opts)
             opts.lda = A.stride(0)

@@ -31,7 +31,7 @@ def test_library_exports_every_header_symbol(capi):
     for n in names:
         assert hasattr(capi.lib, n), f"missing export {n}"
     assert set(capi.EXPORTED) == set(names)
-    assert capi.lib.vabft_api_version() == 2
+    assert capi.lib.vabft_api_version() == 3
 
 
 def test_product_does_not_link_the_oracle():

@@ -118,3 +118,51 @@ def test_blockwise_device_kernels_equal_slice_composition(fmt):
     Ts = blockwise.blockwise_thresholds(A, B, fmt, tile_k=384, tile_n=128, engine="slices")
     assert Td.shape == (m, 5)
     assert np.array_equal(Td.view(np.uint64), Ts.view(np.uint64))
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("fmt", ["bf16", "fp32"])
+def test_fused_kernel_verifies_against_given_blockwise_thresholds(ref_or_port, fmt):
+    """Threshold method 3 (vabft_fused_opts.t_in): the fused kernel verifies
+    a column block of C against the block-wise thresholds T[:, J]; its
+    verdicts, differences and located column equal the reference's verify
+    (detect.cpp:19-55) on the device's own accumulator with the same T, and a
+    planted accumulator fault is located. blockwise_verify_fused runs all
+    blocks: clean rows give no detections."""
+    import torch
+
+    from paper_2602_08043_b200 import blockwise
+    from paper_2602_08043_b200.fused import FusedAbftGemm
+    O = ref_or_port
+    m, k, n, tk, tn = 256, 2048, 512, 1024, 256
+    dt = torch.bfloat16 if fmt == "bf16" else torch.float32
+    g0 = torch.Generator(device="cuda").manual_seed(11)
+    A = torch.randn(m, k, device="cuda", generator=g0).to(dt)
+    B = torch.randn(k, n, device="cuda", generator=g0).to(dt)
+    T = blockwise.blockwise_thresholds_device(A, B, fmt, tile_k=tk, tile_n=tn)
+    Ts = blockwise.blockwise_thresholds(A.double().cpu().numpy(), B.double().cpu().numpy(), fmt, tk, tn,
+                                        engine="slices")
+    assert np.array_equal(T.cpu().numpy().view(np.uint64), Ts.view(np.uint64))
+    jb, j0, j1 = 1, 256, 512
+    bj = B[:, j0:j1] if fmt == "bf16" else B[:, j0:j1].contiguous()
+    g = FusedAbftGemm(bj, mode="online")
+    col = torch.full((m,), -1, dtype=torch.int32, device="cuda")
+    bit = torch.zeros(m, dtype=torch.int32, device="cuda")
+    col[9], bit[9] = 77, 29
+    acc = torch.empty(m, j1 - j0, dtype=torch.float32, device="cuda") if fmt == "bf16" else None
+    r = g(A, t_in=T[:, jb], checksums=True, accum_out=acc,
+          faults={"col": col, "bit": bit, "dir": torch.zeros(m, dtype=torch.int32, device="cuda")})
+    torch.cuda.synchronize()
+    assert np.array_equal(r.T.cpu().numpy(), T[:, jb].cpu().numpy())
+    src = (acc if fmt == "bf16" else r.C).double().cpu().numpy()
+    v = O.verify(src, r.row_check1.cpu().numpy(), r.row_check2.cpu().numpy(), T[:, jb].cpu().numpy(),
+                 "fp32" if fmt == "bf16" else fmt, "offline" if fmt == "bf16" else "online", accum=(2, 128))
+    assert np.array_equal(v["detected"], r.detected.cpu().numpy().astype(bool))
+    assert np.array_equal(v["diff1"].view(np.uint64), r.diff1.cpu().numpy().view(np.uint64))
+    assert np.array_equal(v["location"], r.location.cpu().numpy())
+    assert bool(r.detected[9].item()) and int(r.location[9].item()) == 77
+    g.close()
+    fv = blockwise.blockwise_verify_fused(A, B, fmt, "online", tile_k=tk, tile_n=tn)
+    torch.cuda.synchronize()
+    assert not bool(fv.detected.any().item())
+    assert int((fv.location >= 0).sum().item()) == 0
