@@ -166,6 +166,9 @@ class BlockwiseFusedGemm:
         self.e_max = e_max
         self.blocks = col_blocks(n, tile_n)
         self.sixteen = B.dtype in (torch.bfloat16, torch.float16)
+        # one stream per column block: a 256-column block's GEMM fills only
+        # 2 x ceil(M / 256) SMs, so the blocks run side by side
+        self.streams = [torch.cuda.Stream(device=B.device) for _ in self.blocks]
         self.handles = []
         for (j0, j1) in self.blocks:
             view = self.sixteen and j0 % 8 == 0 and (j1 - j0) % 8 == 0
@@ -182,14 +185,23 @@ class BlockwiseFusedGemm:
         det = torch.empty((m, nJ), dtype=torch.uint8, device=A.device)
         d1 = torch.empty((m, nJ), dtype=torch.float64, device=A.device)
         loc = torch.empty((m, nJ), dtype=torch.int64, device=A.device)
+        main = torch.cuda.current_stream(A.device)
+        cbs = torch.zeros((len(self.blocks), 6), dtype=torch.int64, device=A.device) if counts is not None else None
+        for st in self.streams:
+            st.wait_stream(main)  # T, the output buffers and the counters are ready
         for jb, ((j0, j1), (g, view)) in enumerate(zip(self.blocks, self.handles)):
-            o = Cm[:, j0:j1] if view else torch.empty((m, j1 - j0), dtype=A.dtype, device=A.device)
-            r = g(A, out=o, counts=counts, t_in=T[:, jb])
-            if not view:
-                Cm[:, j0:j1] = o
-            det[:, jb] = r.detected
-            d1[:, jb] = r.diff1
-            loc[:, jb] = torch.where(r.location >= 0, r.location + j0, r.location)
+            with torch.cuda.stream(self.streams[jb]):
+                o = Cm[:, j0:j1] if view else torch.empty((m, j1 - j0), dtype=A.dtype, device=A.device)
+                r = g(A, out=o, counts=cbs[jb] if cbs is not None else None, t_in=T[:, jb])
+                if not view:
+                    Cm[:, j0:j1] = o
+                det[:, jb] = r.detected
+                d1[:, jb] = r.diff1
+                loc[:, jb] = torch.where(r.location >= 0, r.location + j0, r.location)
+        for st in self.streams:
+            main.wait_stream(st)
+        if counts is not None:
+            counts += cbs.sum(dim=0)
         flagged = det.bool()
         # the first flagged block with a located column (blockwise_verify's rule)
         hit = flagged & (loc >= 0)
