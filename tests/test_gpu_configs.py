@@ -488,3 +488,34 @@ def test_guard_failing_tie_rows_bit_exact(env):
     assert _same(res.T[S].cpu().numpy(), T_ref)
     assert int(counts[1].item()) == 0
     h.close()
+
+
+def test_fp16_guard_failing_rows_integer_path(env):
+    """FP16 rows that fail the exactness guard (|x| ~ 2^15.9 next to
+    subnormals ~2^-24 at K = 8192): the fused kernel's integer exact sum (always exact
+    for FP16: its whole range fits the 128-bit accumulator with the
+    compensation provably exact) gives thresholds bit-exact against the
+    reference's vabft_thresholds."""
+    torch, O = env
+    from paper_2602_08043_b200.fused import FusedAbftGemm
+    m, k, n = 128, 8192, 512
+    g = torch.Generator(device="cuda").manual_seed(41)
+    A = torch.randn(m, k, device="cuda", generator=g)
+    B = torch.randn(k, n, device="cuda", generator=g)
+    rows = torch.arange(0, m, 5, device="cuda")
+    big = torch.rand(len(rows), k, device="cuda", generator=g) < 0.02
+    tiny = torch.rand(len(rows), k, device="cuda", generator=g) < 0.3
+    Ar = A[rows]
+    Ar = torch.where(big, Ar.sign() * 60000.0, Ar)
+    Ar = torch.where(tiny, Ar.sign() * 6e-8 * torch.randint(1, 4, Ar.shape, device="cuda", generator=g), Ar)
+    A[rows] = Ar
+    dA, dB = A.half(), B.half()
+    h = FusedAbftGemm(dB, e_max=1e-3)
+    counts = torch.zeros(6, dtype=torch.int64, device="cuda")
+    r = h(dA, counts=counts)
+    torch.cuda.synchronize()
+    assert int(counts[4].item()) >= len(rows) // 2, counts.tolist()
+    S = torch.cat([rows[:20], torch.tensor([1, 2, 3], device="cuda")])
+    T_ref, _ = O.vabft_thresholds(dA[S].double().cpu().numpy(), dB.double().cpu().numpy(), 1e-3, fmt="fp16")
+    assert _same(r.T[S].cpu().numpy(), T_ref)
+    h.close()
