@@ -428,7 +428,17 @@ extern "C" vabft_status vabft_fused_gemm(const vabft_fused_opts* o, vabft_bside_
                                          const void* A, void* C, double* T, vabft_verdicts verdicts,
                                          int64_t* counts, void* workspace, size_t ws_bytes,
                                          void* stream) {
-    return guarded([&] {
+    // a launch that fails after the workspace was claimed may leave its
+    // counters (per-row atomics, arrival counters, the A pass's task counter)
+    // mid-flight: forget the claim so the next call resets them
+    struct ReleaseOnError {
+        const void* ws;
+        bool armed = true;
+        ~ReleaseOnError() {
+            if (armed) release_workspace(ws);
+        }
+    } on_error{workspace};
+    const vabft_status st = guarded([&] {
         if (!o || !h || !A || !C || !h->B) fail(VABFT_INVALID_ARGUMENT, "vabft_fused_gemm: null argument");
         if (o->mode != h->mode) fail(VABFT_INVALID_ARGUMENT, "vabft_fused_gemm: mode differs from the B-side handle");
         if (o->threshold_method < 0 || o->threshold_method > 3) fail(VABFT_INVALID_ARGUMENT, "bad threshold method");
@@ -565,6 +575,8 @@ extern "C" vabft_status vabft_fused_gemm(const vabft_fused_opts* o, vabft_bside_
         else run(fused_tail_kernel<VABFT_FP16>);
         check_cuda(cudaGetLastError(), "fused tail launch");
     });
+    if (st == VABFT_OK) on_error.armed = false;
+    return st;
 }
 
 extern "C" int32_t vabft_fused_uses_cta_pairs(const vabft_fused_opts* o, int64_t m, int64_t n, int64_t k) {
