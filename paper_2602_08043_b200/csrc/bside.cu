@@ -78,6 +78,13 @@ struct BsPart {
     V *sabs, *mx, *mn;
     uint32_t* flags;  // 16-bit: min nonzero magnitude pattern - 1 (0x7FFF: none);
                       // wide: 1 if the block holds a non-finite element
+    // 16-bit: per-row accumulators of the order-free statistics, folded by
+    // every block task with atomics (the exact row sum under the guard is
+    // order-free; max / min / min-nonzero as order-preserving keys), reset
+    // by the group combine — so a combine reads only the ordered checksum
+    // partials p1 / p2 of its blocks
+    double* rsum;
+    uint32_t *rmax, *rmin, *rmnz;
 };
 
 __host__ __device__ inline size_t bs_index(int64_t b, int64_t k, int64_t nb) {
@@ -98,7 +105,11 @@ __host__ __device__ inline BsPart<F> bs_view(void* base, int64_t nb, int64_t kp)
     v.sabs = reinterpret_cast<V*>(p); p += sizeof(V) * n;
     v.mx = reinterpret_cast<V*>(p); p += sizeof(V) * n;
     v.mn = reinterpret_cast<V*>(p); p += sizeof(V) * n;
-    v.flags = reinterpret_cast<uint32_t*>(p);
+    v.flags = reinterpret_cast<uint32_t*>(p); p += 4 * n;
+    v.rsum = reinterpret_cast<double*>(p); p += 8 * size_t(kp);
+    v.rmax = reinterpret_cast<uint32_t*>(p); p += 4 * size_t(kp);
+    v.rmin = reinterpret_cast<uint32_t*>(p); p += 4 * size_t(kp);
+    v.rmnz = reinterpret_cast<uint32_t*>(p);
     return v;
 }
 
@@ -106,7 +117,7 @@ template <int F>
 size_t bs_bytes(int64_t nb, int64_t kp) {
     using W = typename BsT<F>::W;
     using V = typename BsT<F>::V;
-    return size_t(nb) * size_t(kp) * (16 + 2 * sizeof(W) + 3 * sizeof(V) + 4) + 256;
+    return size_t(nb) * size_t(kp) * (16 + 2 * sizeof(W) + 3 * sizeof(V) + 4) + size_t(kp) * 20 + 256;
 }
 
 template <int F>
@@ -401,10 +412,18 @@ __device__ __forceinline__ void bs_store(const BsJob<F>& j, const BsAcc<F>& a, i
         }
         j.part.p1[o] = a.p1;
         j.part.p2[o] = a.p2;
-        j.part.s[o] = a.s;
-        j.part.mx[o] = mx;
-        j.part.mn[o] = mn;
-        j.part.flags[o] = flg;
+        if constexpr (BsT<F>::k16) {
+            const int64_t k = r0 + lane;
+            atomicAdd(j.part.rsum + k, a.s);  // exact in any order under the guard (else the row is redone)
+            atomicMax(j.part.rmax + k, fkey(mx));
+            atomicMin(j.part.rmin + k, fkey(mn));
+            atomicMin(j.part.rmnz + k, flg);
+        } else {
+            j.part.s[o] = a.s;
+            j.part.mx[o] = mx;
+            j.part.mn[o] = mn;
+            j.part.flags[o] = flg;
+        }
     }
 }
 
@@ -499,8 +518,41 @@ __device__ __forceinline__ void bs_combine(const BsJob<F>& j, int64_t rg, unsign
     V mx = V(-INFINITY), mn = V(INFINITY);
     uint32_t mz = 0x7FFFu, bad = 0u;
     const size_t o0 = bs_index(0, k, nb);
+    if constexpr (BsT<F>::k16) {
+        // the ordered checksum partials, 16 blocks of loads in flight per
+        // round; the order-free statistics from the per-row accumulators
+        // (loaded alongside), reset for the next launch
+        if (k < j.K) {
+            s = __ldcg(j.part.rsum + k);
+            mx = fkey_decode(__ldcg(j.part.rmax + k));
+            mn = fkey_decode(__ldcg(j.part.rmin + k));
+            mz = __ldcg(j.part.rmnz + k);
+        }
+        for (int b0 = 0; b0 < nb; b0 += 16) {
+            W v1[16], v2[16];
+#pragma unroll
+            for (int q = 0; q < 16; ++q) {
+                const bool in = b0 + q < nb;
+                v1[q] = in ? __ldcg(j.part.p1 + o0 + size_t(b0 + q) * 32) : W(0);
+                v2[q] = in ? __ldcg(j.part.p2 + o0 + size_t(b0 + q) * 32) : W(0);
+            }
+#pragma unroll
+            for (int q = 0; q < 16; ++q) {
+                if (b0 + q < nb) {  // block order: the blocked:128 combination
+                    t1 = bs_add(t1, v1[q]);
+                    t2 = bs_add(t2, v2[q]);
+                }
+            }
+        }
+        if (k < j.K) {
+            j.part.rsum[k] = 0.0;
+            j.part.rmax[k] = 0u;
+            j.part.rmin[k] = 0xFFFFFFFFu;
+            j.part.rmnz[k] = 0xFFFFFFFFu;
+        }
+    }
 #pragma unroll 8
-    for (int b = 0; b < nb; ++b) {  // block order: the blocked:128 combination
+    for (int b = 0; b < (BsT<F>::k16 ? 0 : nb); ++b) {  // block order: the blocked:128 combination
         const size_t o = o0 + size_t(b) * 32;
         t1 = bs_add(t1, __ldcg(j.part.p1 + o));
         t2 = bs_add(t2, __ldcg(j.part.p2 + o));
@@ -883,6 +935,15 @@ size_t bside_work_bytes(int fmt, int64_t K, int64_t N) {
 }
 
 size_t bside_group_words(int64_t K) { return size_t(2 * ((K + 31) / 32) + 2); }
+
+void bside_init_work(int fmt, int64_t K, int64_t N, void* work, cudaStream_t s) {
+    if (fmt != VABFT_BF16 && fmt != VABFT_FP16) return;
+    const int64_t kp = (K + 31) / 32 * 32, nb = (N + 127) / 128;
+    const BsPart<VABFT_BF16> v = bs_view<VABFT_BF16>(work, nb, kp);  // same layout for FP16
+    // per-row accumulators at their identities: sum 0 and max key 0, then min keys all ones
+    check_cuda(cudaMemsetAsync(v.rsum, 0, size_t(kp) * 12, s), "memset");
+    check_cuda(cudaMemsetAsync(v.rmin, 0xFF, size_t(kp) * 8, s), "memset");
+}
 
 int64_t br_storage_floats(int64_t K) { return ((K + 127) / 128) * 128; }
 

@@ -66,6 +66,7 @@ BsideBuffers tmp_bside(Tmp& tmp, int fmt, int64_t k, int64_t n, cudaStream_t s) 
     buf.work = tmp.get<char>(bside_work_bytes(fmt, k, n));
     check_cuda(cudaMemsetAsync(buf.nonfinite, 0, sizeof(int), s), "memset");
     check_cuda(cudaMemsetAsync(buf.groups, 0, sizeof(unsigned) * bside_group_words(k), s), "memset");
+    bside_init_work(fmt, k, n, buf.work, s);
     return buf;
 }
 

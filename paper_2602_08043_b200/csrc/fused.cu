@@ -380,6 +380,8 @@ extern "C" vabft_status vabft_bside_create_ld(int32_t format, int32_t mode, int6
         // grid barrier, B-side group counters / flags and the non-finite flag start at zero
         check_cuda(cudaMemset(h->buf.nonfinite, 0, size_t(p - reinterpret_cast<char*>(h->buf.nonfinite))),
                    "memset(bside state)");
+        bside_init_work(format, k, n, h->buf.work, nullptr);
+        check_cuda(cudaDeviceSynchronize(), "bside init");
         if (is_wide(format)) {
             check_cuda(cudaMalloc(&h->brd, 2 * sizeof(double) * K), "cudaMalloc(bside B r)");
             h->buf.brd1 = h->brd;

@@ -29,6 +29,8 @@ struct BsideBuffers {
 int64_t br_storage_floats(int64_t K);
 size_t bside_work_bytes(int fmt, int64_t K, int64_t N);
 size_t bside_group_words(int64_t K);
+// identities of the 16-bit pass's per-row accumulators in a fresh work buffer
+void bside_init_work(int fmt, int64_t K, int64_t N, void* work, cudaStream_t s);
 
 void launch_row_stats(int fmt, int64_t rows, int64_t cols, const void* X, double* mean, double* mx,
                       double* mn, double* vb, int* nonfinite, cudaStream_t s);
