@@ -139,7 +139,7 @@ struct BsJob {
 
 // developer timeline (VABFT_BSIDE_TRACE=1): [0] first CTA start, [1] last
 // streaming warp done, [2..4] chain 0..2 done, [5] chain 0 first batch
-// start, [6] last group combine done
+// start, [6] last group combine done, [7] chain 0's duration in SM cycles
 __device__ unsigned long long g_bs_trace[8];
 __device__ __forceinline__ unsigned long long bs_now() {
     unsigned long long t;
@@ -708,7 +708,10 @@ __device__ void bs_summary(const BsJob<F>& j, double* buf2 /* 2 x kBatch doubles
         cp_async_commit();
     };
     while (!published(kBatch < K ? kBatch : K)) __nanosleep(64);
-    if (j.trace && which == 0 && lane == 0) atomicMax(&g_bs_trace[5], bs_now());
+    if (j.trace && which == 0 && lane == 0) {
+        atomicMax(&g_bs_trace[5], bs_now());
+        g_bs_trace[7] = static_cast<unsigned long long>(clock64());  // chain 0's start, SM cycles
+    }
     fetch_async(0, buf2);
     int cur = 0;
     for (int64_t k0 = 0; k0 < K; k0 += kBatch) {
@@ -758,6 +761,8 @@ __device__ void bs_summary(const BsJob<F>& j, double* buf2 /* 2 x kBatch doubles
         }
     }
     if (j.trace && lane == 0) atomicMax(&g_bs_trace[2 + which], bs_now());
+    if (j.trace && which == 0 && lane == 0)
+        g_bs_trace[7] = static_cast<unsigned long long>(clock64()) - g_bs_trace[7];  // chain 0's SM cycles
     if (lane == 0) {
         j.buf.summary[which] = acc;
         // the last of the three chains (every flag read) closes the epoch
@@ -865,8 +870,10 @@ void bs_trace_report(int trc, int F, int64_t K, int64_t N, cudaStream_t s) {
     check_cuda(cudaMemcpyFromSymbolAsync(t, g_bs_trace, sizeof(t), 0, cudaMemcpyDeviceToHost, s), "trace");
     check_cuda(cudaStreamSynchronize(s), "trace");
     auto us = [&](int i) { return t[i] ? double(t[i] - t[0]) * 1e-3 : -1.0; };
-    std::fprintf(stderr, "bside trace F=%d K=%lld N=%lld: pass %.2f combine %.2f chain0-start %.2f chains %.2f %.2f %.2f us\n",
-                 F, (long long)K, (long long)N, us(1), us(6), us(5), us(2), us(3), us(4));
+    const double c0us = t[2] && t[5] ? double(t[2] - t[5]) * 1e-3 : 0.0;
+    std::fprintf(stderr, "bside trace F=%d K=%lld N=%lld: pass %.2f combine %.2f chain0-start %.2f chains %.2f %.2f %.2f us"
+                 " (chain 0: %llu SM cycles, %.0f MHz)\n", F, (long long)K, (long long)N, us(1), us(6), us(5), us(2), us(3),
+                 us(4), t[7], c0us > 0 ? double(t[7]) / c0us : 0.0);
 }
 
 template <int F>
