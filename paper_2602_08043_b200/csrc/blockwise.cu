@@ -89,6 +89,73 @@ __global__ void __launch_bounds__(32 * kSegWarps) seg_stats_kernel(const typenam
     }
 }
 
+// 16-bit variant with 16-byte row-segment loads: a sub-tile is 32 rows x 64
+// elements, loaded as 8 x 16 bytes per lane (8 lanes per 128-byte row
+// segment, coalesced) into registers one sub-tile ahead of the fold, staged
+// raw (padded rows: conflict-free 16-byte reads), and lane = row converts
+// while it runs the reference's Neumaier loop. Needs 16-byte aligned rows
+// and segment starts (ld, seg multiples of 8; X 16-byte aligned).
+template <int F>
+__global__ void __launch_bounds__(32 * kSegWarps) seg_stats16_kernel(const uint16_t* __restrict__ X, int64_t rows,
+                                                                     int64_t cols, int64_t ld, int64_t seg,
+                                                                     int64_t nseg, double* mean, double* vb,
+                                                                     int* nonfinite) {
+    constexpr int kLd = 36;  // words per staged row (64 elements + pad)
+    __shared__ __align__(16) uint32_t tile[kSegWarps][32 * kLd];
+    const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int64_t ngr = (rows + 31) / 32;
+    const int64_t task = int64_t(blockIdx.x) * kSegWarps + w;
+    if (task >= ngr * nseg) return;
+    const int64_t rg = task / nseg, sg = task - rg * nseg;
+    const int64_t r0 = rg * 32, c0 = sg * seg, c1 = c0 + seg < cols ? c0 + seg : cols;
+    const int nr = int(rows - r0 < 32 ? rows - r0 : 32);
+    const int rs = lane >> 3, ch = lane & 7;  // this lane loads rows 4 i + rs, chunk ch (8 elements)
+    uint4 v[8];
+    auto load = [&](int64_t cq) {
+        const int64_t c = cq + ch * 8;
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+            const int rr = 4 * i + rs;
+            v[i] = (rr < nr && c < c1) ? __ldcs(reinterpret_cast<const uint4*>(X + (r0 + rr) * ld + c))
+                                       : make_uint4(0u, 0u, 0u, 0u);
+        }
+    };
+    Neu n;
+    float mx = 0.0f, mn = 0.0f;
+    bool bad = false, first = true;
+    uint32_t* mine = tile[w];
+    load(c0);
+    for (int64_t cq = c0; cq < c1; cq += 64) {
+        __syncwarp();
+#pragma unroll
+        for (int i = 0; i < 8; ++i) *reinterpret_cast<uint4*>(mine + (4 * i + rs) * kLd + ch * 4) = v[i];
+        __syncwarp();
+        if (cq + 64 < c1) load(cq + 64);  // in flight during the fold
+        const int cnt = int(c1 - cq < 64 ? c1 - cq : 64);
+        const uint32_t* trow = mine + lane * kLd;
+        if (first) {
+            mx = mn = bits16_to_float<F>(uint16_t(trow[0] & 0xFFFFu));
+            first = false;
+        }
+        for (int e = 0; e < cnt; ++e) {
+            const uint32_t wd = trow[e >> 1];
+            const float xf = bits16_to_float<F>(uint16_t((e & 1) ? (wd >> 16) : (wd & 0xFFFFu)));
+            bad |= !isfinite(xf);
+            n.add(double(xf));
+            mx = fmaxf(mx, xf);
+            mn = fminf(mn, xf);
+        }
+    }
+    if (lane < nr) {
+        if (bad) atomicExch(nonfinite, 1);
+        double m, vv;
+        stats_finish(n, double(mx), double(mn), c1 - c0, &m, &vv);
+        const int64_t o = (r0 + lane) * nseg + sg;
+        mean[o] = m;
+        vb[o] = vv;
+    }
+}
+
 // BStatsSummary::from over rows [kt*tile_k, ...) of column block J: one warp
 // per (kt, J, which) — the warp stages the k-tile's values in chunks of 256
 // (coalesced-enough strided loads, all in flight) and lane 0 runs the
@@ -151,6 +218,13 @@ void seg_stats(const void* X, int64_t rows, int64_t cols, int64_t ld, int64_t se
                int* nonfinite, cudaStream_t s) {
     const int64_t nseg = (cols + seg - 1) / seg;
     const int64_t tasks = (rows + 31) / 32 * nseg;
+    if constexpr (F == VABFT_BF16 || F == VABFT_FP16) {
+        if (ld % 8 == 0 && seg % 8 == 0 && reinterpret_cast<uintptr_t>(X) % 16 == 0) {
+            seg_stats16_kernel<F><<<unsigned((tasks + kSegWarps - 1) / kSegWarps), 32 * kSegWarps, 0, s>>>(
+                static_cast<const uint16_t*>(X), rows, cols, ld, seg, nseg, mean, vb, nonfinite);
+            return;
+        }
+    }
     seg_stats_kernel<F><<<unsigned((tasks + kSegWarps - 1) / kSegWarps), 32 * kSegWarps, 0, s>>>(
         static_cast<const typename Elem<F>::T*>(X), rows, cols, ld, seg, nseg, mean, vb, nonfinite);
 }

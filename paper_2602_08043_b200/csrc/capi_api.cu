@@ -5,6 +5,7 @@
 // reference throws (non-finite stats, negative thresholds, A-ABFT y) wait on
 // the stream.
 #include <cmath>
+#include <mutex>
 #include <vector>
 
 #include "devcommon.cuh"
@@ -17,10 +18,30 @@ using namespace vabft_dev;
 
 namespace {
 
+// The stream-ordered pool keeps up to 1 GiB of freed temporaries mapped
+// (default release threshold 0: every synchronising entry point handed its
+// pages back and the next call re-mapped them — measured ~0.3-2.5 ms of host
+// time per block-wise threshold call). Once per device.
+void keep_pool_mapped() {
+    static std::mutex mu;
+    static std::vector<bool> done;
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess) return;
+    std::lock_guard<std::mutex> lk(mu);
+    if (size_t(dev) >= done.size()) done.resize(size_t(dev) + 1, false);
+    if (done[size_t(dev)]) return;
+    done[size_t(dev)] = true;
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+        uint64_t keep = uint64_t(1) << 30;
+        cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+    }
+}
+
 struct Tmp {
     cudaStream_t s;
     std::vector<void*> ptrs;
-    explicit Tmp(cudaStream_t st) : s(st) {}
+    explicit Tmp(cudaStream_t st) : s(st) { keep_pool_mapped(); }
     template <class T>
     T* get(size_t count) {
         void* p = nullptr;
