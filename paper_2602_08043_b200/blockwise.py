@@ -59,7 +59,8 @@ def _tile_emax(fmt: str, k: int, tile_k: int, e_max) -> np.ndarray:
 
 
 def blockwise_thresholds_device(A: torch.Tensor, B: torch.Tensor, fmt: str, tile_k: int = 1024, tile_n: int = 256,
-                                e_max: Optional[float] = None, c_sigma: float = 2.5) -> torch.Tensor:
+                                e_max: Optional[float] = None, c_sigma: float = 2.5,
+                                out: Optional[torch.Tensor] = None) -> torch.Tensor:
     """T[i, J] for CUDA operands in their storage format (bf16 / fp16 / fp32 /
     fp64 tensors, row strides honoured): one C-ABI call, three launches
     (csrc/blockwise.cu) — segment row statistics, the per-(k-tile, block)
@@ -72,7 +73,10 @@ def blockwise_thresholds_device(A: torch.Tensor, B: torch.Tensor, fmt: str, tile
     if A.stride(1) != 1 or B.stride(1) != 1:
         raise _capi.InvalidArgument("blockwise_thresholds: rows must be contiguous")
     em = _tile_emax(fmt, k, tile_k, e_max)
-    T = torch.empty(m, (n + tile_n - 1) // tile_n, dtype=torch.float64, device=A.device)
+    nJ = (n + tile_n - 1) // tile_n
+    T = out if out is not None else torch.empty(m, nJ, dtype=torch.float64, device=A.device)
+    if tuple(T.shape) != (m, nJ) or T.dtype != torch.float64 or not T.is_contiguous():
+        raise _capi.InvalidArgument("blockwise_thresholds: out must be a contiguous M x nJ float64 tensor")
     check(lib.vabft_blockwise_thresholds(api._spec(fmt).code, m, n, k, ptr(A), A.stride(0), ptr(B), B.stride(0),
                                          tile_k, tile_n, em.ctypes.data, c_sigma, ptr(T), stream_ptr()))
     return T
@@ -152,8 +156,10 @@ class BlockwiseFusedGemm:
     (threshold method 3). Located columns are global."""
 
     def __init__(self, B: torch.Tensor, fmt: str, mode: str = "online", tile_k: int = 1024, tile_n: int = 256,
-                 e_max=None, c_sigma: float = 2.5, **fused_kw):
+                 e_max=None, c_sigma: float = 2.5, graphs: bool = True, **fused_kw):
         from .fused import FusedAbftGemm
+        self.use_graphs = graphs
+        self._graphs = {}
         self.B, self.fmt, self.mode, self.tile_k, self.tile_n, self.c_sigma = B, fmt, mode, tile_k, tile_n, c_sigma
         k, n = B.shape
         if e_max is None:
@@ -175,18 +181,10 @@ class BlockwiseFusedGemm:
             self.handles.append((FusedAbftGemm(B[:, j0:j1] if view else B[:, j0:j1].contiguous(), mode=mode,
                                                **fused_kw), view))
 
-    def __call__(self, A: torch.Tensor, out: Optional[torch.Tensor] = None,
-                 counts: Optional[torch.Tensor] = None) -> "FusedBlockVerdicts":
+    def _blocks(self, A, T, Cm, det, d1, loc, cbs):
+        """The column blocks on their streams (eager, or recorded into a graph)."""
         m = A.shape[0]
-        n = self.B.shape[1]
-        T = blockwise_thresholds_device(A, self.B, self.fmt, self.tile_k, self.tile_n, self.e_max, self.c_sigma)
-        Cm = out if out is not None else torch.empty((m, n), dtype=A.dtype, device=A.device)
-        nJ = len(self.blocks)
-        det = torch.empty((m, nJ), dtype=torch.uint8, device=A.device)
-        d1 = torch.empty((m, nJ), dtype=torch.float64, device=A.device)
-        loc = torch.empty((m, nJ), dtype=torch.int64, device=A.device)
         main = torch.cuda.current_stream(A.device)
-        cbs = torch.zeros((len(self.blocks), 6), dtype=torch.int64, device=A.device) if counts is not None else None
         for st in self.streams:
             st.wait_stream(main)  # T, the output buffers and the counters are ready
         for jb, ((j0, j1), (g, view)) in enumerate(zip(self.blocks, self.handles)):
@@ -200,17 +198,86 @@ class BlockwiseFusedGemm:
                 loc[:, jb] = torch.where(r.location >= 0, r.location + j0, r.location)
         for st in self.streams:
             main.wait_stream(st)
+
+    def __call__(self, A: torch.Tensor, out: Optional[torch.Tensor] = None,
+                 counts: Optional[torch.Tensor] = None) -> "FusedBlockVerdicts":
+        """Block-wise verification of A B. With graphs on (the default) the
+        16 per-block launches replay from a CUDA graph recorded per M (the
+        eager per-block calls were host-bound): A is copied into the graph's
+        input buffer, and C / the verdicts returned are the graph's buffers,
+        valid until the next call with the same M (unless `out` is given)."""
+        m = A.shape[0]
+        n = self.B.shape[1]
+        nJ = len(self.blocks)
+        dev = A.device
+        if self.use_graphs:
+            st = self._graphs.get(m)
+            if st is None:
+                st = self._record(A)
+            if st is not None:
+                st["A"].copy_(A)
+                blockwise_thresholds_device(st["A"], self.B, self.fmt, self.tile_k, self.tile_n, self.e_max,
+                                            self.c_sigma, out=st["T"])
+                st["graph"].replay()
+                if counts is not None:
+                    counts += st["cbs"].sum(dim=0)
+                Cm = st["C"]
+                if out is not None:
+                    out.copy_(Cm)
+                    Cm = out
+                return self._verdicts(Cm, st["T"], st["det"], st["d1"], st["loc"], m, dev)
+        T = blockwise_thresholds_device(A, self.B, self.fmt, self.tile_k, self.tile_n, self.e_max, self.c_sigma)
+        Cm = out if out is not None else torch.empty((m, n), dtype=A.dtype, device=dev)
+        det = torch.empty((m, nJ), dtype=torch.uint8, device=dev)
+        d1 = torch.empty((m, nJ), dtype=torch.float64, device=dev)
+        loc = torch.empty((m, nJ), dtype=torch.int64, device=dev)
+        cbs = torch.zeros((nJ, 6), dtype=torch.int64, device=dev) if counts is not None else None
+        self._blocks(A, T, Cm, det, d1, loc, cbs)
         if counts is not None:
             counts += cbs.sum(dim=0)
+        return self._verdicts(Cm, T, det, d1, loc, m, dev)
+
+    def _record(self, A):
+        m, k = A.shape
+        n = self.B.shape[1]
+        nJ = len(self.blocks)
+        dev = A.device
+        st = {"A": torch.empty_like(A, memory_format=torch.contiguous_format),
+              "T": torch.empty((m, nJ), dtype=torch.float64, device=dev),
+              "C": torch.empty((m, n), dtype=A.dtype, device=dev),
+              "det": torch.empty((m, nJ), dtype=torch.uint8, device=dev),
+              "d1": torch.empty((m, nJ), dtype=torch.float64, device=dev),
+              "loc": torch.empty((m, nJ), dtype=torch.int64, device=dev),
+              "cbs": torch.zeros((nJ, 6), dtype=torch.int64, device=dev)}
+        st["A"].copy_(A)
+        blockwise_thresholds_device(st["A"], self.B, self.fmt, self.tile_k, self.tile_n, self.e_max, self.c_sigma,
+                                    out=st["T"])
+        args = (st["A"], st["T"], st["C"], st["det"], st["d1"], st["loc"], st["cbs"])
+        try:
+            self._blocks(*args)  # eager once: handles' buffers and workspaces exist before recording
+            torch.cuda.synchronize(dev)
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g):
+                st["cbs"].zero_()
+                self._blocks(*args)
+            st["graph"] = g
+        except Exception:
+            self.use_graphs = False
+            return None
+        self._graphs[m] = st
+        return st
+
+    def _verdicts(self, Cm, T, det, d1, loc, m, dev) -> "FusedBlockVerdicts":
         flagged = det.bool()
         # the first flagged block with a located column (blockwise_verify's rule)
         hit = flagged & (loc >= 0)
         first = hit.int().argmax(dim=1)
         location = torch.where(hit.any(dim=1), loc.gather(1, first[:, None])[:, 0],
-                               torch.full((m,), -1, dtype=torch.int64, device=A.device))
+                               torch.full((m,), -1, dtype=torch.int64, device=dev))
         return FusedBlockVerdicts(Cm, T, det, d1, location, flagged.any(dim=1), self.blocks)
 
     def close(self) -> None:
+        self._graphs = {}
         for g, _ in self.handles:
             g.close()
         self.handles = []
@@ -220,7 +287,7 @@ def blockwise_verify_fused(A: torch.Tensor, B: torch.Tensor, fmt: str, mode: str
                            tile_n: int = 256, e_max=None, c_sigma: float = 2.5,
                            counts: Optional[torch.Tensor] = None, **fused_kw) -> FusedBlockVerdicts:
     """One-shot BlockwiseFusedGemm (handles built and released per call)."""
-    g = BlockwiseFusedGemm(B, fmt, mode, tile_k, tile_n, e_max, c_sigma, **fused_kw)
+    g = BlockwiseFusedGemm(B, fmt, mode, tile_k, tile_n, e_max, c_sigma, graphs=False, **fused_kw)
     try:
         return g(A, counts=counts)
     finally:

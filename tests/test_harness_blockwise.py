@@ -166,3 +166,31 @@ def test_fused_kernel_verifies_against_given_blockwise_thresholds(ref_or_port, f
     torch.cuda.synchronize()
     assert not bool(fv.detected.any().item())
     assert int((fv.location >= 0).sum().item()) == 0
+
+
+@pytest.mark.gpu
+def test_blockwise_fused_graph_replay_equals_eager():
+    """BlockwiseFusedGemm's CUDA-graph replay (the per-block launches
+    recorded once per M) gives the same C, thresholds and verdicts as the
+    eager per-block calls, on two different activations, with a planted
+    single error found at its global column."""
+    import torch
+
+    from paper_2602_08043_b200 import blockwise
+    g0 = torch.Generator(device="cuda").manual_seed(5)
+    m, k, n = 512, 2048, 768
+    B = torch.randn(k, n, device="cuda", generator=g0).bfloat16()
+    eager = blockwise.BlockwiseFusedGemm(B, "bf16", "online", 1024, 256, graphs=False)
+    graph = blockwise.BlockwiseFusedGemm(B, "bf16", "online", 1024, 256)
+    for seed in (1, 2):
+        A = torch.randn(m, k, device="cuda", generator=torch.Generator(device="cuda").manual_seed(seed)).bfloat16()
+        ce, cg = torch.zeros(6, dtype=torch.int64, device="cuda"), torch.zeros(6, dtype=torch.int64, device="cuda")
+        re, rg = eager(A, counts=ce), graph(A, counts=cg)
+        torch.cuda.synchronize()
+        assert torch.equal(re.C.view(torch.int16), rg.C.view(torch.int16))
+        assert torch.equal(re.thresholds, rg.thresholds)
+        assert torch.equal(re.block_detected, rg.block_detected)
+        assert torch.equal(re.diff1, rg.diff1)
+        assert torch.equal(ce, cg) and int(cg[0].item()) == m * 3 and int(cg[1].item()) == 0
+    eager.close()
+    graph.close()
