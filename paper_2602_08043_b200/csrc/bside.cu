@@ -12,9 +12,10 @@
 // per (block, row): the blocked:128 checksum partials sum_j x and
 // sum_j fl(fl(j + 1) x) in the working type (reference order inside the
 // block, no FMA), an exactness-preserving partial of the row sum, max / min
-// and the order-free trackers of the exactness guard. The warp completing a
-// row group's last block combines the group (lane = row): block partials in
-// block order (the blocked:128 combination), the exact row sum -> the
+// and the order-free trackers of the exactness guard (16-bit formats: those
+// order-free statistics go straight into per-row atomic accumulators). The
+// warp completing a row group's last block combines the group (lane = row):
+// block partials in block order (the blocked:128 combination), the exact row sum -> the
 // reference's Neumaier mean (guarded; rows outside the guard rerun the
 // reference's loop), var_bound, and publishes the group. One summary warp
 // (CTA 0, warp 0) folds the published groups, in row order, into

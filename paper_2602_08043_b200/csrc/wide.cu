@@ -203,10 +203,12 @@ __global__ void __launch_bounds__(kDThreads, 1) dgemm_kernel(const __grid_consta
     }
 }
 
-// A side and verification of the wide fused path: ONE pass over A after the
-// GEMM on the same stream (run beside the GEMM on a second stream it was
-// starved of memory bandwidth and finished late — measured), with the
-// per-row-group combine and the verdicts inside the same kernel.
+// A side and verification of the wide fused path: ONE streaming pass over A
+// after the GEMM on the same stream (run beside the GEMM on a second stream it
+// was starved of memory bandwidth and finished late — measured; a
+// programmatic launch lets it take the SMs the GEMM's last wave leaves), then
+// the per-row-group combine and the verdicts as a second programmatic launch
+// (wide_combine_kernel).
 //
 // wide_apart_kernel: persistent; a warp task is (32-row group, 128-column
 // block of K). The warp streams the 32 x 128 tile through its shared-memory
@@ -223,8 +225,8 @@ __global__ void __launch_bounds__(kDThreads, 1) dgemm_kernel(const __grid_consta
 //    block's pair; FP64: a TwoSum cascade per element. sum|x| (the margin of
 //    exact_sum_safe) is kept in the element type and stored rounded up by a
 //    relative 2^-8 (an upper bound).
-// The warp completing a row group's last block (self-resetting arrival
-// counter) finishes the group, lane = row: checksum partials in block order,
+// wide_combine_kernel (one warp per row group) finishes the group, lane =
+// row: checksum partials in block order,
 // the (s, c) pairs merged with TwoSum; hi = fl(s + c) equals the reference's
 // sequential Neumaier fl(sum + comp) unless the exact sum lies within
 // 8 (K u)^2 sum|x| of a rounding midpoint (exact_sum_safe) — those rows get
@@ -617,11 +619,10 @@ __global__ void __launch_bounds__(32 * kApWarps, F == VABFT_FP64 ? 1 : 2)
     // ahead of the fold — across task boundaries too (the next task's first
     // sub-tile and block weights land while this task's last sub-tile is
     // folded) — so no register staging and no exposed load at a task start.
-    // A task's arrival (release RMW, whose fence also waits for memory
-    // operations in flight) is deferred to the start of the warp's next task,
-    // when no copy of this warp is pending. (Measured before: long-
-    // scoreboard stalls on register staging and on each task's first loads
-    // and weights, plus the fence, were the top stall reasons.)
+    // No per-task arrivals: the combine is its own launch. (Measured before:
+    // long-scoreboard stalls on register staging and on each task's first
+    // loads and weights, then the arrivals' release fences — which also wait
+    // for the copies in flight — and the inline combines were the top costs.)
     auto issue = [&](int64_t t, int q, int slot, int wslot) {
         const int64_t rg = t / nb, b = t - rg * nb;
         const int64_t r0 = rg * 32, c = b * 128 + int64_t(q) * 32;
