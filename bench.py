@@ -259,9 +259,10 @@ def measure_formats(dev, flush, torch, n=4096, steps=20, warmup=3):
     stream = torch.cuda.current_stream()
     pp = os.path.join(ROOT, "profiles", "r02_peaks_tf32_fp64.json")
     wide_peaks = json.load(open(pp)) if os.path.exists(pp) else {}
-    for name, dt, passes in (("fp32_3xtf32", torch.float32, 3), ("fp32_1xtf32", torch.float32, 1),
-                             ("fp64_dfma", torch.float64, 3)):
-        nn = n if dt == torch.float32 else n // 2  # FP64: 2048^3 keeps the run short
+    # FP64 at 2048^3 (256 tiles of 128 x 128 over 148 SMs: 1.73 waves, the
+    # tile quantization shows) and at 4096^3 (6.9 waves)
+    for name, dt, passes, nn in (("fp32_3xtf32", torch.float32, 3, n), ("fp32_1xtf32", torch.float32, 1, n),
+                                 ("fp64_dfma", torch.float64, 3, n // 2), ("fp64_dfma_4096", torch.float64, 3, n)):
         torch.manual_seed(0)  # fixed draws: a midpoint (sequential-fallback) row costs extra
         A = torch.randn(nn, nn, device=dev, dtype=dt)
         B = torch.randn(nn, nn, device=dev, dtype=dt)
