@@ -34,11 +34,18 @@
 #include "reducers.cuh"
 #include "tail.cuh"
 
+#ifndef VABFT_DBK
+#define VABFT_DBK 32
+#endif
+#ifndef VABFT_DSTAGES
+#define VABFT_DSTAGES 3
+#endif
+
 namespace vabft_dev {
 
 namespace {
 
-constexpr int kDBM = 128, kDBN = 128, kDBK = 16, kDStages = 4, kDThreads = 256;
+constexpr int kDBM = 128, kDBN = 128, kDBK = VABFT_DBK, kDStages = VABFT_DSTAGES, kDThreads = 256;
 constexpr int kALd = kDBK + 2;          // doubles per staged A row (16-byte aligned, conflict-free)
 constexpr int kAStage = kDBM * kALd;    // doubles
 constexpr int kBStage = kDBK * kDBN;
@@ -72,16 +79,17 @@ __global__ void __launch_bounds__(kDThreads, 1) dgemm_kernel(const __grid_consta
         double* As = sm + size_t(slot) * kStage;
         double* Bs = As + kAStage;
         const int64_t k0 = kt * kDBK;
+        constexpr int kAChunks = kDBK / 2;  // 16-byte chunks per staged A row
 #pragma unroll
-        for (int q = 0; q < 4; ++q) {  // A: 128 rows x 8 chunks of 2 doubles
+        for (int q = 0; q < kDBM * kAChunks / kDThreads; ++q) {  // A: 128 rows x kDBK / 2 chunks of 2 doubles
             const int c = tid + q * kDThreads;
-            const int r = c >> 3, part = c & 7;
+            const int r = c / kAChunks, part = c % kAChunks;
             const int64_t gr = m0 + r, gk = k0 + part * 2;
             const bool ok = gr < p.M && gk < p.K;
             cp_async16(smem_u32(As + r * kALd + part * 2), ok ? p.A + gr * p.K + gk : p.A, ok);
         }
 #pragma unroll
-        for (int q = 0; q < 4; ++q) {  // B: 16 rows x 64 chunks
+        for (int q = 0; q < kDBK * 64 / kDThreads; ++q) {  // B: kDBK rows x 64 chunks
             const int c = tid + q * kDThreads;
             const int r = c >> 6, part = c & 63;
             const int64_t gk = k0 + r, gc = n0 + part * 2;
