@@ -312,6 +312,53 @@ def measure_formats(dev, flush, torch, n=4096, steps=20, warmup=3):
                      "fpr": {"false_positive_rows": int(counts[1].item()), "rows_checked": int(counts[0].item())},
                      "sequential_fallback_rows": int(counts[4].item())}
         g.close()
+    # FP16 (the BF16 kernel family, kind::f16 with FP16 operands): fused vs the
+    # same tcgen05 kernel shape with ABFT compiled out
+    from paper_2602_08043_b200.fused import plain_gemm
+    torch.manual_seed(0)
+    A = torch.randn(n, n, device=dev).half()
+    B = torch.randn(n, n, device=dev).half()
+    g = FusedAbftGemm(B)
+    Cc = torch.empty(n, n, device=dev, dtype=torch.float16)
+    counts = torch.zeros(6, dtype=torch.int64, device=dev)
+    md = 1 if g.uses_cta_pairs(n) else 0
+
+    def run16(fn):
+        for _ in range(warmup):
+            flush.zero_()
+            fn()
+        torch.cuda.synchronize()
+        gr = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(gr):
+            fn()
+        ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(steps)]
+        torch.cuda.synchronize()
+        for s, e in ev:
+            flush.zero_()
+            s.record(stream)
+            gr.replay()
+            e.record(stream)
+        torch.cuda.synchronize()
+        return sum(s.elapsed_time(e) for s, e in ev) / steps
+    fused_fn = lambda: g(A, out=Cc, counts=counts)  # noqa: E731
+    plain_fn = lambda: plain_gemm(A, B, out=Cc, cta_mode=md)  # noqa: E731
+    runs_f = [run16(fused_fn), run16(fused_fn)]
+    runs_p = [run16(plain_fn), run16(plain_fn)]
+    ms_f, ms_p = min(runs_f), min(runs_p)
+    counts.zero_()
+    g(A, out=Cc, counts=counts)
+    torch.cuda.synchronize()
+    fl = 2.0 * n ** 3
+    burst = load_peaks()[0]
+    out["fp16"] = {"shape": [n, n, n], "fused_tflops": fl / ms_f / 1e9, "plain_tflops": fl / ms_p / 1e9,
+                   "roofline": {"peak_tflops": burst, "peak": "measured bf16_tflops (MEASURED_PEAKS.json; FP16 runs "
+                                "at the same tcgen05 kind::f16 rate)", "frac_algorithmic": fl / ms_f / 1e9 / burst,
+                                "frac_issued": fl / ms_f / 1e9 / burst},
+                   "abft_overhead_pct": 100.0 * (ms_f / ms_p - 1.0), "e_max": g.opts.e_max,
+                   "us_runs": {"fused": [round(x * 1e3, 1) for x in runs_f], "plain": [round(x * 1e3, 1) for x in runs_p]},
+                   "fpr": {"false_positive_rows": int(counts[1].item()), "rows_checked": int(counts[0].item())},
+                   "sequential_fallback_rows": int(counts[4].item())}
+    g.close()
     return out
 
 
