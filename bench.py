@@ -96,6 +96,7 @@ def make_config(args, world: int):
             "gemms_per_step": len(shapes), "distinct_shapes_mkn": sorted({tuple(s) for s in shapes}),
             "flop_per_step": sum(2.0 * m * k * n for (m, k, n) in shapes),
             "e_max": e_max, "c_sigma": 2.5, "threshold": "V-ABFT (threshold_vabft.cpp:54-61)",
+            "l2": "GPU arm: L2 flushed between timed steps (512 MiB write, untimed)",
             "parallelism": (f"{world} rank(s); " + {"c2": "one independent GEMM per rank",
                                                     "llama": "plan_gemm_batch LPT over ranks",
                                                     "nsplit": "shard_columns N-slices"}[args.config]
