@@ -219,7 +219,8 @@ void seg_stats(const void* X, int64_t rows, int64_t cols, int64_t ld, int64_t se
     const int64_t nseg = (cols + seg - 1) / seg;
     const int64_t tasks = (rows + 31) / 32 * nseg;
     if constexpr (F == VABFT_BF16 || F == VABFT_FP16) {
-        if (ld % 8 == 0 && seg % 8 == 0 && reinterpret_cast<uintptr_t>(X) % 16 == 0) {
+        // 16-byte chunks never cross a segment end or the matrix end
+        if (ld % 8 == 0 && seg % 8 == 0 && cols % 8 == 0 && reinterpret_cast<uintptr_t>(X) % 16 == 0) {
             seg_stats16_kernel<F><<<unsigned((tasks + kSegWarps - 1) / kSegWarps), 32 * kSegWarps, 0, s>>>(
                 static_cast<const uint16_t*>(X), rows, cols, ld, seg, nseg, mean, vb, nonfinite);
             return;
