@@ -194,3 +194,15 @@ def test_blockwise_fused_graph_replay_equals_eager():
         assert torch.equal(ce, cg) and int(cg[0].item()) == m * 3 and int(cg[1].item()) == 0
     eager.close()
     graph.close()
+
+
+def test_tile_emax_forms():
+    """e_max per k-tile: one value for all tiles, one per tile (checked
+    against the tile count), or the format model at dim = |kt|."""
+    from paper_2602_08043_b200 import _capi, blockwise
+    assert blockwise._tile_emax("bf16", 1000, 384, 1e-3).tolist() == [1e-3] * 3
+    assert blockwise._tile_emax("bf16", 1000, 384, [1e-3, 2e-3, 3e-3]).tolist() == [1e-3, 2e-3, 3e-3]
+    with pytest.raises(_capi.InvalidArgument):
+        blockwise._tile_emax("bf16", 1000, 384, [1e-3, 2e-3])
+    em = blockwise._tile_emax("fp32", 1000, 384, None)
+    assert em.shape == (3,) and (em > 0).all()
