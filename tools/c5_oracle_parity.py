@@ -12,7 +12,7 @@ post-injection accumulator / output. Per trial the applicability, the
 verdict and the located column must agree bit for bit; the line per
 (shape, mode, bit) records the counts and the agreement.
 
-  python tools/c5_oracle_parity.py [--sample 96] > profiles/r02_c5_oracle_parity.jsonl
+  python tools/c5_oracle_parity.py [--sample 96] [--fmt bf16|fp16|fp32|fp64] [--shapes ...]
 """
 import argparse
 import json
@@ -44,7 +44,13 @@ def main():
     ap.add_argument("--sample", type=int, default=96, help="trials per launch re-verified by the reference")
     ap.add_argument("--shapes", default=",".join(SHAPES))
     ap.add_argument("--dist", default="normal:1e-6,1")
+    ap.add_argument("--fmt", default="bf16", choices=["bf16", "fp16", "fp32", "fp64"],
+                    help="operand format: 16-bit — FP32-accumulator bits online, output bits offline; "
+                         "FP32 / FP64 — the bits of C (the accumulator), online")
     args = ap.parse_args()
+    fmt = args.fmt
+    dt = {"bf16": torch.bfloat16, "fp16": torch.float16, "fp32": torch.float32, "fp64": torch.float64}[fmt]
+    sixteen = fmt in ("bf16", "fp16")
     R = oracle.ref() if oracle.have_ref() else oracle.port()
     dev = torch.device("cuda", 0)
     pool = ThreadPoolExecutor(max_workers=os.cpu_count() or 4)
@@ -52,11 +58,13 @@ def main():
     for name in args.shapes.split(","):
         m, k, n = SHAPES[name]
         gen = torch.Generator(device=dev).manual_seed(zlib.crc32(name.encode()))
-        A = sample_matrix((m, k), args.dist, gen, dev)
-        B = sample_matrix((k, n), args.dist, gen, dev)
+        A = sample_matrix((m, k), args.dist, gen, dev, dtype=dt)
+        B = sample_matrix((k, n), args.dist, gen, dev, dtype=dt)
         B_h = B.double().cpu().numpy()
         rng = np.random.default_rng(len(name) * 7919 + m)
-        for mode, bits in (("online", range(32)), ("offline", range(16))):
+        plan = ((("online", range(32)), ("offline", range(16))) if sixteen else
+                (("online", range(32 if fmt == "fp32" else 64)),))
+        for mode, bits in plan:
             g = FusedAbftGemm(B, mode=mode)
             S = np.sort(rng.choice(m, size=min(args.sample, m), replace=False))
             Sd = torch.from_numpy(S).to(dev)
@@ -64,12 +72,12 @@ def main():
             # reference thresholds / checksums of the sampled rows, once per (shape, mode):
             # row slices are exact sub-problems; chunks run in parallel
             chunks = np.array_split(np.arange(len(S)), min(len(S), os.cpu_count() or 4))
-            th = list(pool.map(lambda c: R.vabft_thresholds(A_s[c], B_h, g.opts.e_max, fmt="bf16")[0], chunks))
-            cs = list(pool.map(lambda c: R.blocked_row_checksums(A_s[c], B_h, "bf16", mode), chunks))
+            th = list(pool.map(lambda c: R.vabft_thresholds(A_s[c], B_h, g.opts.e_max, fmt=fmt)[0], chunks))
+            cs = list(pool.map(lambda c: R.blocked_row_checksums(A_s[c], B_h, fmt, mode), chunks))
             T_ref = np.concatenate(th)
             rc1 = np.concatenate([c[0] for c in cs])
             rc2 = np.concatenate([c[1] for c in cs])
-            acc = torch.empty(m, n, dtype=torch.float32, device=dev) if mode == "online" else None
+            acc = torch.empty(m, n, dtype=torch.float32, device=dev) if (sixteen and mode == "online") else None
             rec = torch.empty(m * 24, dtype=torch.uint8, device=dev)
             for bit in bits:
                 t0 = time.time()
@@ -80,8 +88,11 @@ def main():
                 r = g(A, faults=f, counts=counts, accum_out=acc)
                 torch.cuda.synchronize()
                 applied = rec.view(m, 24)[:, 16:20].contiguous().view(torch.int32).view(m).cpu().numpy() != 0
-                src = (acc[Sd] if mode == "online" else r.C[Sd]).double().cpu().numpy()
-                v = R.verify(src, rc1, rc2, T_ref, "fp32", "offline", accum=(2, 128))
+                src = (acc[Sd] if acc is not None else r.C[Sd]).double().cpu().numpy()
+                if sixteen:
+                    v = R.verify(src, rc1, rc2, T_ref, "fp32", "offline", accum=(2, 128))
+                else:  # C is the accumulator; checksum precision = the format, blocked:128
+                    v = R.verify(src, rc1, rc2, T_ref, fmt, "online", accum=(2, 128))
                 det = r.detected[Sd].cpu().numpy().astype(bool)
                 loc = r.location[Sd].cpu().numpy()
                 T_dev = r.T[Sd].cpu().numpy()
@@ -90,7 +101,9 @@ def main():
                 cols = col[Sd].cpu().numpy()
                 app = applied[S]
                 line = {"shape": name, "mkn": [m, k, n], "mode": mode, "bit": bit,
-                        "target": "fp32_accumulator" if mode == "online" else "bf16_output",
+                        "fmt": fmt,
+                        "target": (("fp32_accumulator" if mode == "online" else fmt + "_output") if sixteen
+                                   else fmt + "_C"),
                         "device_trials": m, "device_applicable": int(applied.sum()),
                         "device_detected": int(counts[1].item()),
                         "compared": int(len(S)), "applicable_compared": int(app.sum()),
@@ -104,7 +117,7 @@ def main():
                 grand["agree"] += int(agree.sum())
                 print(json.dumps(line), flush=True)
             g.close()
-    print(json.dumps({"summary": grand, "reference": R.name}), flush=True)
+    print(json.dumps({"summary": grand, "fmt": fmt, "reference": R.name}), flush=True)
 
 
 if __name__ == "__main__":
