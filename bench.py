@@ -563,6 +563,16 @@ def run_ours(args):
     nb = max(3, args.steps // 4)
     ms_best, _ = timed(g_best, nb, args.warmup)
     del g_best
+    # cuBLAS (torch.matmul, library GEMM) on the same shapes and protocol: the
+    # context of roofline.peak, which is cuBLAS at 8192^3 (MEASURED_PEAKS.json)
+    cub_out = [torch.empty_like(Cc) for (A, B, Cc, h) in gl]
+
+    def step_cublas():
+        for (A, B, Cc, h), o in zip(gl, cub_out):
+            torch.matmul(A, B, out=o)
+    g_cub = capture(step_cublas)
+    ms_cub, _ = timed(g_cub, nb, args.warmup)
+    del g_cub, cub_out
 
     # FPR over one clean step (all ranks)
     counts.zero_()
@@ -734,6 +744,7 @@ def run_ours(args):
                            "interleaved (4 rounds), same L2 flush",
         "kernel_shape": sorted({"cta_pair" if md else "one_cta" for md in modes}),
         "best_plain_gemm_tflops": best_tf,
+        "cublas_same_shape_tflops": total_flops / (ms_cub / nb / 1e3) / 1e12,
         "overhead_vs_best_plain_pct": 100.0 * (best_tf / fused_int_tf - 1.0),
         "offline_tflops": off_tf,
         "fpr": {"false_positive_rows": fp_rows, "rows_checked": rows_checked, "sequential_fallback_rows": slow_rows},
