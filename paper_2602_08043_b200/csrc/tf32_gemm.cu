@@ -23,6 +23,7 @@
 #include <cuda.h>
 #include <cudaTypedefs.h>
 
+#include <cstdlib>
 #include <mutex>
 
 #include "internal.hpp"
@@ -53,6 +54,7 @@ static_assert(TfCfg<true>::kStage == 49152 && TfCfg<false>::kStage == 49152, "st
 struct Tf32Params {
     int M, N, K;
     int num_m, num_n, num_k, num_tiles;
+    int group;  // row blocks per raster group
     float* C;
     WideEpilogue epi;
 };
@@ -80,9 +82,10 @@ __device__ __forceinline__ void umma_tf32(uint32_t tmem_d, uint64_t adesc, uint6
 // grouped raster: 8 row blocks per group, so concurrently running tiles share
 // A row panels and B column panels in L2
 __device__ __forceinline__ void tile_mn(const Tf32Params& p, int t, int& m, int& n) {
-    const int gsz = 8 * p.num_n;
-    const int g = t / gsz, first = g * 8;
-    const int gm = p.num_m - first < 8 ? p.num_m - first : 8;
+    const int G = p.group;
+    const int gsz = G * p.num_n;
+    const int g = t / gsz, first = g * G;
+    const int gm = p.num_m - first < G ? p.num_m - first : G;
     const int r = t % gsz;
     m = first + r % gm;
     n = r / gm;
@@ -430,6 +433,11 @@ void tf32_gemm_launch(int64_t M, int64_t N, int64_t K, const float* a_hi, const 
     const CUtensorMapSwizzle sw = split ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_128B;
     p.num_k = int((K + bk - 1) / bk);
     p.num_tiles = p.num_m * p.num_n;
+    static const int grp_env = [] {  // developer override (VABFT_TF32_GROUP)
+        const char* e = std::getenv("VABFT_TF32_GROUP");
+        return e ? std::atoi(e) : 0;
+    }();
+    p.group = grp_env > 0 ? grp_env : 8;
     p.C = C;
     p.epi = epi;
     const CUtensorMap ah = map_f32(a_hi, M, K, bk, kBM, sw);
