@@ -16,11 +16,11 @@
 //                     rule, localization and optional correction
 //                     (detect.cpp:9-64), counters.
 //
-// DGEMM mapping: 128 x 128 x 16 CTA tiles, 256 threads (8 warps as 4 x 2),
+// DGEMM mapping: 128 x 128 x kDBK (32) CTA tiles, 256 threads (8 warps as 4 x 2),
 // an 8 x 8 register tile per thread (rows wm*32 + 8j + 2ty + {0,1}, columns
 // wn*64 + 16j + 2tx + {0,1}) so that every shared-memory fragment read is a
-// conflict-free 16-byte access; a 4-stage cp.async ring (A rows padded to 18
-// doubles). Per k pair: 16 LDS.128 for 128 DFMA — the FP64 pipe (64 DFMA /
+// conflict-free 16-byte access; a 3-stage cp.async ring (A rows padded to
+// kDBK + 2 doubles; 16-deep tiles with 4 stages measured ~2 % slower). Per k pair: 16 LDS.128 for 128 DFMA — the FP64 pipe (64 DFMA /
 // clk / SM) is the bound, not shared memory.
 #include <algorithm>
 #include <cstdio>
