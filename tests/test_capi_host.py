@@ -121,3 +121,24 @@ def test_bits_every_pattern(capi, golden, fmt):
         assert np.float64(d.value).view(np.uint64) == dec[p].view(np.uint64)
         capi.check(capi.lib.vabft_encode_bits(d.value, code, C.byref(u)))
         assert u.value == rt[p]
+
+
+def test_blockwise_thresholds_validates_before_device_work(capi):
+    """vabft_blockwise_thresholds (C-ABI v3) rejects bad arguments on the host
+    with the reference's invalid_argument status, before touching the device."""
+    lib = capi.lib
+    em = (C.c_double * 4)(1e-3, 1e-3, 1e-3, 1e-3)
+    fake = C.c_void_p(16)
+    bad_cases = [
+        (0, 8, 8, 8, None, 0, fake, 0, 4, 4, em, 2.5, fake),     # null A
+        (0, 8, 8, 8, fake, 0, fake, 0, 0, 4, em, 2.5, fake),     # tile_k = 0
+        (0, 8, 8, 8, fake, 0, fake, 0, 4, 4, None, 2.5, fake),   # null e_max
+        (0, 0, 8, 8, fake, 0, fake, 0, 4, 4, em, 2.5, fake),     # m = 0
+        (0, 8, 8, 8, fake, 4, fake, 0, 4, 4, em, 2.5, fake),     # lda < k
+        (9, 8, 8, 8, fake, 0, fake, 0, 4, 4, em, 2.5, fake),     # bad format
+    ]
+    for args in bad_cases:
+        assert lib.vabft_blockwise_thresholds(*args, None) == capi.INVALID_ARGUMENT, args
+    neg = (C.c_double * 2)(1e-3, -1.0)  # e_max < 0 on the second k-tile
+    assert lib.vabft_blockwise_thresholds(0, 8, 8, 8, fake, 0, fake, 0, 4, 4, neg, 2.5, fake,
+                                          None) == capi.INVALID_ARGUMENT
