@@ -410,7 +410,7 @@ __device__ __forceinline__ void stats_producer(const TcParams& p, const CUtensor
                 // [B r1 | B r2] segments; the br arrays are padded to 128 entries
                 const uint32_t adst = smem_u32(smS + slot * kABytes);
                 const uint32_t bdst = smem_u32(smS + 2 * kABytes + slot * (2 * kBK * 4));
-                if (p.epi.debug == 1) {  // ablation: no statistics loads
+                if (p.epi.debug == 1 || p.epi.debug == 10) {  // ablation: no statistics loads (10: nor math)
                     mbar_arrive(sb);
                     continue;
                 }
@@ -445,7 +445,7 @@ __device__ __forceinline__ void stats_warps(const TcParams& p, const uint8_t* sm
                 const float* sbr2 = sbr1 + kBK;
                 const int kbase = kb * kBK;
                 const int ng = (p.K - kbase) >= kBK ? 8 : (p.K - kbase) / 8;  // K % 8 == 0: whole granules
-                if (p.epi.debug != 2) {  // 2: ablation, no math
+                if (p.epi.debug != 2 && p.epi.debug != 10) {  // 2 / 10: ablation, no math
                     if (ng == 8) {  // whole stage: one shared-memory pass into registers
                         uint4 v[8];
 #pragma unroll
