@@ -53,7 +53,14 @@ constexpr int kBK = 64;
 #endif
 constexpr int kStages = VABFT_STAGES;
 constexpr int kThreads = 192;       // TMA, MMA, 4 epilogue warps
-constexpr int kThreadsStats = 352;  // + 4 A-statistics warps + 1 statistics producer
+#ifndef VABFT_STATS_REMAP
+#define VABFT_STATS_REMAP 0
+#endif
+// + 4 A-statistics warps + 1 statistics producer; with VABFT_STATS_REMAP the
+// statistics warps are 6, 7, 8, 10 and the producer 11 (warp 9 idle), so the
+// MMA issuer's SM sub-partition (warp % 4 == 1) hosts no statistics warp
+constexpr int kThreadsStats = VABFT_STATS_REMAP ? 384 : 352;
+constexpr int kStatsProducerWarp = VABFT_STATS_REMAP ? 11 : 10;
 constexpr uint32_t kABytes = kBM * kBK * 2;  // 16 KiB
 constexpr uint32_t kBBytes = kBN * kBK * 2;  // 32 KiB
 constexpr uint32_t kStageBytes = kABytes + kBBytes;
@@ -670,12 +677,16 @@ __global__ void __launch_bounds__(kThreadsStats, 1)
             }
             if (p.epi.trace && lane == 0) p.epi.trace[blockIdx.x * 8 + 1] = gtime();
         }
-    } else if (warp == 10) {
+    } else if (warp == kStatsProducerWarp) {
         if constexpr (kStats) {
             if (lane == 0) stats_producer(p, &tmA, smS, sfull_bar, sempty_bar);
         }
     } else if (warp >= 6) {
-        if constexpr (kStats) stats_warps<kFmt>(p, smS, sfull_bar, sempty_bar, warp - 6, lane);
+        if constexpr (kStats) {
+            if (!VABFT_STATS_REMAP || warp != 9)
+                stats_warps<kFmt>(p, smS, sfull_bar, sempty_bar, (VABFT_STATS_REMAP && warp == 10) ? 3 : warp - 6,
+                                  lane);
+        }
     } else {
         // ------------------------------------------------------- epilogue
         const int quad = warp & 3;  // TMEM lanes [32*quad, 32*quad+32) are addressable by this warp
